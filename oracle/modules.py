@@ -1,0 +1,66 @@
+"""TEST INFRASTRUCTURE ONLY -- oracle arithmetic behind the PipelineModules boundary.
+
+``cpu_modules(lexicon, cfg)`` returns a :class:`PipelineModules` whose
+encoder / decoder / vocoder callables are the numpy Tier-S oracle
+(``oracle/tier_s.py``), i.e. a CPU restatement of the reference's
+``build_modules`` (``pkg/src/incrtts/scheduler.py:266-282``).  Used by the
+parity tests (schedules, batch transparency) and by ``bench.py``'s
+reference arm.  Never imported by the product package.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from paper_2211_13939_b200.domain import AudioChunk, MelChunk, PipelineConfig
+from paper_2211_13939_b200.scheduler import PipelineModules, frontend_module
+
+from . import tier_s
+
+
+@dataclass(frozen=True)
+class Encoded:
+    rows: np.ndarray
+
+    @property
+    def seq_len(self) -> int:
+        return int(self.rows.shape[0])
+
+
+@dataclass(frozen=True)
+class DecodeResult:
+    mel: MelChunk
+    stop: bool
+    state: tier_s.DecState
+
+
+def cpu_modules(lexicon, cfg: PipelineConfig) -> PipelineModules:
+    dim = cfg.feature_dim
+
+    def encoder(fos):
+        out = []
+        for fo in fos:
+            rows = tier_s.encode_rows(fo.phonemes, fo.pw, fo.pph, fo.iph, dim)
+            out.append((Encoded(rows), tier_s.init_state(rows.shape[0], dim, cfg.frames_per_phoneme)))
+        return out
+
+    def decoder(pairs):
+        out = []
+        for state, enc in pairs:
+            mel, stop, new = tier_s.decode_chunk(state, enc.rows, cfg.chunk_frames,
+                                                 cfg.attention_penalty, cfg.stop_threshold)
+            out.append(DecodeResult(MelChunk(mel), stop, new))
+        return out
+
+    def vocoder(triples):
+        out = []
+        for state, mel, is_last in triples:
+            st = tier_s.VocState(state.mel_tail, state.held_tail, state.emitted_samples)
+            samples, off, new = tier_s.vocode_chunk(st, mel.frames, is_last, cfg.overlap_frames,
+                                                    cfg.hop_samples)
+            out.append((AudioChunk(samples, off), new))
+        return out
+
+    return PipelineModules(frontend_module(lexicon), encoder, decoder, vocoder)
