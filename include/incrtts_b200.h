@@ -1,0 +1,102 @@
+/*
+ * incrtts_b200 -- C ABI of the B200-native incremental-TTS serving path.
+ *
+ * The reference (`incrtts`, pure Python) binds its models through the
+ * PipelineModules plugin boundary (pkg/src/incrtts/scheduler.py:249-263),
+ * four batched Python callables built by build_modules (:266-282).  The
+ * drop-in replacement keeps that boundary in Python
+ * (paper_2211_13939_b200/modules.py) and reaches the GPU only through the
+ * functions below, loaded with ctypes.
+ *
+ * Conventions
+ *   - Every function returns int: 0 on success, a cudaError_t value on a
+ *     CUDA failure, or an ITTS_E* code for an argument error detected before
+ *     anything is enqueued.  Nothing throws across this boundary.
+ *   - All pointers are device pointers unless named host_*; `stream` is a
+ *     cudaStream_t passed as void*.  Calls only enqueue work on `stream`.
+ *   - Per-item addressing uses a device int64 "plan": one fixed-width row
+ *     per batch item holding absolute device addresses and sizes, built by
+ *     the host in batch order (= IterationReport.decoder_ids order).  The
+ *     library never frees or retains caller memory.
+ */
+#ifndef INCRTTS_B200_H
+#define INCRTTS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ITTS_OK 0
+#define ITTS_EINVAL 10001
+#define ITTS_EALIGN 10002
+#define ITTS_EUNSUPPORTED 10003
+
+int itts_version(void);
+
+/* ---- K1: slot gather / scatter --------------------------------------
+ * Replaces the per-item gather `[(item.dec_state, item.enc) for item in
+ * dec_items]` and scatter `item.dec_state = out.state`
+ * (scheduler.py:452-468, :485) for device-resident state: row i of the
+ * contiguous batch buffer <-> the state row at src_ptrs[i] / dst_ptrs[i].
+ * row_bytes and the contiguous buffer must be 16-byte aligned (128-bit
+ * vector moves). */
+int itts_gather_rows(void* dst, const int64_t* src_ptrs, int32_t n_rows, int64_t row_bytes,
+                     void* stream);
+int itts_scatter_rows(const int64_t* dst_ptrs, const void* src, int32_t n_rows, int64_t row_bytes,
+                      void* stream);
+
+/* ---- Tier S: the reference stand-in models in fp64 ------------------- */
+
+/* K2. Replaces encode_batch + init_decoder_state (acoustic.py:222-231,
+ * :118-133; scheduler.py:272-274).  tok4 = int32 [4][total_tokens]
+ * (phoneme, pw, pph, iph streams of FrontendOutput, items concatenated);
+ * plan = int64 [n_items][4] {tok_off, L, feat_ptr (double[L][dim]),
+ * state_ptr (double[6*dim + 2L], zeroed)}; scratch = double[2*total*dim]. */
+int itts_s_encode(const int32_t* tok4, int64_t total_tokens, const int64_t* plan, int32_t n_items,
+                  int64_t max_len, int32_t dim, double* scratch, void* stream);
+
+/* K3. Replaces decode_chunk_batch (acoustic.py:234-238, :204-219).
+ * plan = int64 [n_items][6] {feat_ptr, L, src_state_ptr, dst_state_ptr,
+ * steps, mel_ptr (double[steps][dim])}.  `steps` = min(chunk_frames,
+ * target - emitted) is the reference's counter stop (acoustic.py:174-175,
+ * :213-218), decided on the host.  src is read, dst written (value
+ * semantics: the old state stays valid). */
+int itts_s_decode_chunk(const int64_t* plan, int32_t n_items, int32_t dim, double penalty,
+                        void* stream);
+
+/* K4. Replaces vocode_batch (vocoder.py:139-143, :92-136) with the
+ * stand-in generator (vocoder.py:52-60).  plan = int64 [n_items][7]
+ * {mel_ptr, m, flags (1 = has tail, 2 = is_last), src_vs_ptr, dst_vs_ptr,
+ * out_off, 0}; vocoder state = double[overlap*dim + overlap*hop]
+ * (mel tail, held samples).  fade = double[2][overlap*hop] (sin, cos
+ * ramps); audio = packed output, item i at audio[out_off]. */
+int itts_s_vocode_chunk(const int64_t* plan, int32_t n_items, int32_t dim, int32_t overlap_frames,
+                        int32_t hop, int64_t max_samples, const double* fade, double* audio,
+                        void* stream);
+
+/* ---- Tier R: Tacotron2 + HiFi-GAN V1 ---------------------------------- */
+
+/* K7 core: one 1-D convolution layer as a tcgen05 implicit GEMM (bf16
+ * operands, fp32 TMEM accumulation).  Replaces the per-layer work of the
+ * vocoder G inside vocode_chunk (vocoder.py:107/:124 `generate`; HiFi-GAN
+ * V1 conv_pre / ConvTranspose / MRF convs).
+ *   x      bf16 [rows][c_in] channels-last, items packed with zero halos
+ *   w      bf16 [n_taps][n_total][c_in]; host_tap_off[n_taps] row offsets
+ *   out    n_total = phases * c_out columns; row_out[r] = output row of input
+ *          row r (phase p goes to row_out[r] + p), -1 for halo rows
+ *   epilogue: v = acc + bias; (+resid_in); -> resid_out; acc_mode 1 store,
+ *          2 add, 3 finalize v = (acc + v) / 3; act_out = bf16(lrelu(v, slope));
+ *          zero_halo writes zeros to act_out halo rows.
+ * c_in must be a multiple of 32, c_out a multiple of 32. */
+int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, const void* w, int32_t n_total,
+                   int32_t n_taps, const int32_t* host_tap_off, const float* bias, int32_t c_out,
+                   const int32_t* row_out, const float* resid_in, float* resid_out, float* acc,
+                   int32_t acc_mode, void* act_out, float slope, int32_t zero_halo, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* INCRTTS_B200_H */

@@ -1,0 +1,106 @@
+"""Ragged device arena: per-request state regions inside one HBM tensor.
+
+Every live request owns a handful of variable-length regions (encoder
+memory, two ping-pong decoder-state buffers, two vocoder-state buffers).
+They are carved out of a single growable torch tensor by a first-fit
+allocator with coalescing, so kernels address them with plain base+offset
+pointers and no per-request cudaMalloc ever happens on the serving path.
+
+Offsets are in elements and 128-byte aligned.  Growth reallocates and
+copies on the owning stream; callers keep offsets (never raw pointers)
+across calls and rebuild pointers from :attr:`base_ptr` per call.
+"""
+
+from __future__ import annotations
+
+import bisect
+import threading
+
+import torch
+
+_ALIGN_BYTES = 128
+
+
+class RaggedArena:
+    def __init__(self, dtype: torch.dtype, device: torch.device, capacity: int, stream=None):
+        self.dtype = dtype
+        self.device = device
+        self.itemsize = torch.tensor([], dtype=dtype).element_size()
+        self.align = max(1, _ALIGN_BYTES // self.itemsize)
+        self.stream = stream
+        self._lock = threading.Lock()
+        cap = self._round(capacity)
+        self.tensor = torch.empty(cap, dtype=dtype, device=device)
+        self._free_starts = [0]
+        self._free_sizes = {0: cap}
+        self.used = 0
+        self.peak = 0
+
+    def _round(self, n: int) -> int:
+        return max(self.align, -(-int(n) // self.align) * self.align)
+
+    @property
+    def capacity(self) -> int:
+        return self.tensor.numel()
+
+    @property
+    def base_ptr(self) -> int:
+        return self.tensor.data_ptr()
+
+    def ptr(self, off: int) -> int:
+        return self.tensor.data_ptr() + off * self.itemsize
+
+    def alloc(self, n: int) -> int:
+        size = self._round(n)
+        with self._lock:
+            for i, start in enumerate(self._free_starts):
+                have = self._free_sizes[start]
+                if have >= size:
+                    del self._free_sizes[start]
+                    self._free_starts.pop(i)
+                    if have > size:
+                        self._insert_free(start + size, have - size)
+                    self.used += size
+                    self.peak = max(self.peak, self.used)
+                    return start
+            self._grow(size)
+        return self.alloc(n)
+
+    def free(self, off: int, n: int) -> None:
+        size = self._round(n)
+        with self._lock:
+            self.used -= size
+            self._insert_free(off, size)
+
+    def _insert_free(self, start: int, size: int) -> None:
+        i = bisect.bisect_left(self._free_starts, start)
+        # coalesce with right neighbour
+        if i < len(self._free_starts) and start + size == self._free_starts[i]:
+            size += self._free_sizes.pop(self._free_starts.pop(i))
+        # coalesce with left neighbour
+        if i > 0:
+            left = self._free_starts[i - 1]
+            if left + self._free_sizes[left] == start:
+                self._free_sizes[left] += size
+                return
+        self._free_starts.insert(i, start)
+        self._free_sizes[start] = size
+
+    def _grow(self, need: int) -> None:
+        old = self.tensor
+        cap = old.numel()
+        new_cap = self._round(max(2 * cap, cap + need))
+        ctx = torch.cuda.stream(self.stream) if self.stream is not None else _nullctx()
+        with ctx:
+            new = torch.empty(new_cap, dtype=self.dtype, device=self.device)
+            new[:cap].copy_(old)
+        self.tensor = new
+        self._insert_free(cap, new_cap - cap)
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False

@@ -1,0 +1,53 @@
+// Shared helpers for the incrtts_b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define ITTS_API extern "C" __attribute__((visibility("default")))
+
+// Status codes (ITTS_OK / ITTS_E*) come from the public header: 0 = success,
+// a positive cudaError_t for CUDA failures, ITTS_E* for argument errors
+// detected before any launch (so nothing is enqueued on failure).
+#include "incrtts_b200.h"
+
+#define ITTS_RETURN_LAUNCH()                        \
+  do {                                              \
+    cudaError_t _e = cudaGetLastError();            \
+    return _e == cudaSuccess ? ITTS_OK : (int)_e;   \
+  } while (0)
+
+namespace itts {
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide reduction; `scratch` holds >= 32 T.  Result broadcast to all.
+template <typename T, bool IsMax>
+__device__ __forceinline__ T block_reduce(T v, T* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = IsMax ? warp_max(v) : warp_sum(v);
+  __syncthreads();  // scratch reuse guard
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    T x = lane < nw ? scratch[lane] : (IsMax ? -INFINITY : T(0));
+    x = IsMax ? warp_max(x) : warp_sum(x);
+    if (lane == 0) scratch[0] = x;
+  }
+  __syncthreads();
+  return scratch[0];
+}
+
+}  // namespace itts

@@ -1,0 +1,365 @@
+// K7 core: implicit-GEMM 1-D convolution on the 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+// out[r, n] = epilogue( sum_j sum_ci X[r + off_j, ci] * Wt[j, n, ci] + bias[n % C_out] )
+//
+//   X   : bf16 activations, channels-last [R][C_in] (a packed batch of items,
+//         each with a zero halo of >= max|off_j| rows on both sides, so the
+//         shifted taps read zeros at every item edge = 'same' zero padding).
+//   Wt  : bf16 weights [taps][N][C_in] (K-major B operand).
+//   taps: regular conv -> off_j = dil*(j - (k-1)/2); ConvTranspose(stride u,
+//         kernel 2u) -> 3 taps {-1,0,+1} over N = u*C_out phase-major
+//         columns (see hifigan.py: the transpose conv is a 3-tap conv whose
+//         output row q of width u*C_out is u consecutive output rows).
+//
+// CTA tile 128 x BN, fp32 accumulator in TMEM; K loop over (tap, 64- or 32-
+// channel chunk).  Warp roles (192 threads, 1 CTA/SM):
+//   warp 0   TMA producer (one elected lane): A box {KT,128} at row m0+off_j,
+//            B box {KT,BN}; STAGES-deep smem ring, mbarrier full/empty.
+//   warp 1   TMEM allocator + MMA issuer (one lane): KT/16 x
+//            tcgen05.mma.cta_group::1.kind::f16 per stage, tcgen05.commit
+//            frees the stage; a final commit signals the epilogue.
+//   warps 2-5 epilogue: tcgen05.ld 32x32b.x32 -> +bias -> residual / MRF
+//            accumulate / leaky-ReLU -> global (fp32 and bf16 outputs).
+//
+// Used by the HiFi-GAN V1 chunk vocoder (MRF resblock convs, the transposed
+// upsampling convs, conv_pre) and the Tacotron2 encoder conv stack.
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kBlockM = 128;
+constexpr int kThreads = 192;
+constexpr int kMaxTaps = 16;
+
+struct Taps {
+  int n;
+  int off[kMaxTaps];
+};
+
+struct Epi {
+  const float* bias;          // [C_out]
+  const int32_t* row_out;     // [rows_pad]: output row for input row r, or -1 (halo)
+  const float* resid_in;      // fp32 [out_rows][C_out] or null
+  float* resid_out;           // fp32 [out_rows][C_out] or null
+  float* acc;                 // fp32 [out_rows][C_out] or null
+  __nv_bfloat16* act_out;     // bf16 [out_rows][C_out] or null
+  int64_t rows;               // input rows R (tiles beyond are skipped)
+  int c_out;                  // output row width; N = phases * c_out
+  int acc_mode;               // 0 none, 1 store, 2 add, 3 finalize: y = (acc + y) / 3
+  float slope;                // leaky-ReLU slope for act_out (1.0 = identity)
+  int zero_halo;              // write zeros into act_out for halo rows (CONV mode only)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes));
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, swizzle SWZ bytes (128 or 64):
+// 8-row atoms of SWZ-byte rows, SBO = 8*SWZ, LBO unused (1), version 1.
+template <int SWZ>
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
+  constexpr uint64_t layout = SWZ == 128 ? 2ull : 4ull;
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                               // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(((8 * SWZ) >> 4) & 0x3FFF) << 32;     // SBO
+  d |= (uint64_t)1 << 46;                               // version (sm100)
+  d |= layout << 61;
+  return d;
+}
+
+// Instruction descriptor: kind::f16, A/B bf16, D fp32, K-major both, M=128, N=BN.
+template <int BN>
+__device__ __forceinline__ uint32_t make_idesc() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kBlockM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float lrelu(float x, float s) { return x >= 0.f ? x : x * s; }
+
+template <int BN, int SWZ, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_conv_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, Taps taps,
+              int kchunks, int n_total, Epi epi) {
+  constexpr int KT = SWZ / 2;                   // bf16 channels per smem row
+  constexpr uint32_t A_BYTES = kBlockM * SWZ;
+  constexpr uint32_t B_BYTES = BN * SWZ;
+  constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* done = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * kBlockM;
+  const int n0 = blockIdx.y * BN;
+  const int iters = taps.n * kchunks;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int it = 0; it < iters; ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        const int j = it / kchunks, kc = it - j * kchunks;
+        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+        tma_load_2d(sA + s * A_BYTES, &mapA, &full[s], kc * KT, m0 + taps.off[j]);
+        tma_load_2d(sB + s * B_BYTES, &mapB, &full[s], kc * KT, j * n_total + n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc<BN>();
+      for (int it = 0; it < iters; ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t da = make_desc<SWZ>(smem_u32(sA + s * A_BYTES));
+        const uint64_t db = make_desc<SWZ>(smem_u32(sB + s * B_BYTES));
+#pragma unroll
+        for (int kk = 0; kk < KT / 16; ++kk)  // +32 bytes per K=16 step inside the swizzle row
+          umma_bf16(tmem, da + 2 * kk, db + 2 * kk, idesc, (it | kk) != 0);
+        umma_commit(&empty[s]);
+      }
+      umma_commit(done);
+    }
+  } else {
+    // Epilogue: warp w owns TMEM lanes [32*(w%4), +32) = tile rows.
+    const int quarter = warp & 3;
+    const int64_t r = (int64_t)m0 + quarter * 32 + lane;
+    mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const bool in_range = r < epi.rows;
+    const int out_row = in_range ? epi.row_out[r] : -1;
+    const int C = epi.c_out;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + c0, v);
+      if (!in_range) continue;
+      const int n = n0 + c0;        // first global column of this 32-chunk
+      const int phase = n / C, co = n - phase * C;
+      if (out_row < 0) {
+        if (epi.zero_halo && epi.act_out) {
+          uint4* dst = reinterpret_cast<uint4*>(epi.act_out + (int64_t)r * C + co);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dst[q] = make_uint4(0, 0, 0, 0);
+        }
+        continue;
+      }
+      const int64_t o = ((int64_t)out_row + phase) * C + co;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += __ldg(epi.bias + co + i);
+      if (epi.resid_in) {
+        const float4* src = reinterpret_cast<const float4*>(epi.resid_in + o);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 t = src[q];
+          v[4 * q] += t.x; v[4 * q + 1] += t.y; v[4 * q + 2] += t.z; v[4 * q + 3] += t.w;
+        }
+      }
+      if (epi.resid_out) {
+        float4* dst = reinterpret_cast<float4*>(epi.resid_out + o);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+      if (epi.acc_mode) {
+        float4* a = reinterpret_cast<float4*>(epi.acc + o);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (epi.acc_mode == 1) {
+            a[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          } else {
+            const float4 t = a[q];
+            float4 s = make_float4(t.x + v[4 * q], t.y + v[4 * q + 1], t.z + v[4 * q + 2], t.w + v[4 * q + 3]);
+            if (epi.acc_mode == 2) {
+              a[q] = s;
+            } else {  // finalize: x = (rb0 + rb1 + rb2) / 3
+              v[4 * q] = s.x / 3.0f; v[4 * q + 1] = s.y / 3.0f; v[4 * q + 2] = s.z / 3.0f; v[4 * q + 3] = s.w / 3.0f;
+            }
+          }
+        }
+      }
+      if (epi.act_out) {
+        uint4* dst = reinterpret_cast<uint4*>(epi.act_out + o);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t p[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(lrelu(v[8 * q + 2 * e], epi.slope),
+                                                      lrelu(v[8 * q + 2 * e + 1], epi.slope));
+            p[e] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          dst[q] = make_uint4(p[0], p[1], p[2], p[3]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+bool encode_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+               uint32_t box_outer, int swz) {
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, int SWZ, int STAGES>
+int launch(const void* x, int64_t rows, int c_in, const void* w, int n_total, const Taps& taps, const Epi& epi,
+           cudaStream_t st) {
+  constexpr int KT = SWZ / 2;
+  CUtensorMap ma, mb;
+  if (!encode_2d(&ma, x, (uint64_t)c_in, (uint64_t)rows, KT, kBlockM, SWZ)) return ITTS_EINVAL;
+  if (!encode_2d(&mb, w, (uint64_t)c_in, (uint64_t)taps.n * n_total, KT, BN, SWZ)) return ITTS_EINVAL;
+  const size_t smem = 1024 + STAGES * (kBlockM + BN) * SWZ + (2 * STAGES + 1) * 8 + 16;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_conv_tc<BN, SWZ, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  dim3 grid((unsigned)((rows + kBlockM - 1) / kBlockM), (unsigned)(n_total / BN));
+  k_conv_tc<BN, SWZ, STAGES><<<grid, kThreads, smem, st>>>(ma, mb, taps, c_in / KT, n_total, epi);
+  ITTS_RETURN_LAUNCH();
+}
+
+}  // namespace
+
+ITTS_API int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, const void* w, int32_t n_total,
+                            int32_t n_taps, const int32_t* host_tap_off, const float* bias, int32_t c_out,
+                            const int32_t* row_out, const float* resid_in, float* resid_out, float* acc,
+                            int32_t acc_mode, void* act_out, float slope, int32_t zero_halo, void* stream) {
+  if (!x || !w || !bias || !row_out || !host_tap_off || rows <= 0) return ITTS_EINVAL;
+  if (n_taps < 1 || n_taps > kMaxTaps || c_out <= 0 || n_total % c_out) return ITTS_EINVAL;
+  if (c_out % 32 || (acc_mode && !acc) || acc_mode < 0 || acc_mode > 3) return ITTS_EINVAL;
+  if (((uintptr_t)x | (uintptr_t)w) & 15) return ITTS_EALIGN;
+  Taps taps{};
+  taps.n = n_taps;
+  for (int i = 0; i < n_taps; ++i) taps.off[i] = host_tap_off[i];
+  Epi epi{bias, row_out, resid_in, resid_out, acc, (__nv_bfloat16*)act_out, rows, c_out, acc_mode, slope, zero_halo};
+  cudaStream_t st = (cudaStream_t)stream;
+  const int swz = (c_in % 64 == 0) ? 128 : (c_in % 32 == 0 ? 64 : 0);
+  if (!swz) return ITTS_EUNSUPPORTED;
+  if (swz == 128) {
+    if (n_total % 256 == 0) return launch<256, 128, 4>(x, rows, c_in, w, n_total, taps, epi, st);
+    if (n_total % 128 == 0) return launch<128, 128, 6>(x, rows, c_in, w, n_total, taps, epi, st);
+    if (n_total % 64 == 0) return launch<64, 128, 8>(x, rows, c_in, w, n_total, taps, epi, st);
+    if (n_total % 32 == 0) return launch<32, 128, 8>(x, rows, c_in, w, n_total, taps, epi, st);
+  } else {
+    if (n_total % 64 == 0) return launch<64, 64, 8>(x, rows, c_in, w, n_total, taps, epi, st);
+    if (n_total % 32 == 0) return launch<32, 64, 8>(x, rows, c_in, w, n_total, taps, epi, st);
+  }
+  return ITTS_EUNSUPPORTED;
+}

@@ -1,0 +1,61 @@
+"""Host wrappers for the tcgen05 implicit-GEMM conv (``csrc/tc_conv.cu``).
+
+Weight re-layout helpers turn PyTorch-layout conv / transposed-conv weights
+into the kernel's K-major ``Wt[tap][n][c_in]`` bf16 form, and
+:func:`conv1d_tc` launches one layer through the C ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+
+ACC_NONE, ACC_STORE, ACC_ADD, ACC_FINAL = 0, 1, 2, 3
+
+
+def conv_weights(w: torch.Tensor, dilation: int = 1, c_in_pad: int | None = None):
+    """Conv1d weight [C_out][C_in][k] -> (Wt [k][C_out][C_in'] bf16, tap offsets)."""
+    c_out, c_in, k = w.shape
+    cp = c_in_pad or c_in
+    wt = torch.zeros(k, c_out, cp, dtype=torch.float32, device=w.device)
+    wt[:, :, :c_in] = w.permute(2, 0, 1)
+    offs = [dilation * (j - (k - 1) // 2) for j in range(k)]
+    return wt.to(torch.bfloat16).contiguous(), offs
+
+
+def convt_weights(w: torch.Tensor, stride: int):
+    """ConvTranspose1d weight [C_in][C_out][2u], padding u/2 -> 3-tap phase conv.
+
+    out[u*q + r] = sum_s X[q + s] . W[:, :, r + p - u*s]  (s in -1, 0, 1) ->
+    Wp[s+1][r*C_out + co][ci]; zero where the kernel index leaves [0, 2u).
+    """
+    c_in, c_out, k = w.shape
+    u = stride
+    assert k == 2 * u, "HiFi-GAN V1 upsampling uses kernel = 2 * stride"
+    p = (k - u) // 2
+    wp = torch.zeros(3, u * c_out, c_in, dtype=torch.float32, device=w.device)
+    for s in (-1, 0, 1):
+        for r in range(u):
+            kk = r + p - u * s
+            if 0 <= kk < k:
+                wp[s + 1, r * c_out:(r + 1) * c_out, :] = w[:, :, kk].T
+    return wp.to(torch.bfloat16).contiguous(), [-1, 0, 1]
+
+
+def conv1d_tc(x: torch.Tensor, wt: torch.Tensor, offs, bias: torch.Tensor, c_out: int,
+              row_out: torch.Tensor, *, resid_in=None, resid_out=None, acc=None, acc_mode=ACC_NONE,
+              act_out=None, slope: float = 1.0, zero_halo: bool = True, stream=None) -> None:
+    """One conv layer: x bf16 [R][C_in] -> epilogue outputs (see tc_conv.cu)."""
+    rows, c_in = x.shape
+    taps, n_total, c_in_w = wt.shape
+    assert c_in_w == c_in and len(offs) == taps
+    offs_arr = (ctypes.c_int32 * len(offs))(*offs)
+    ptr = lambda t: 0 if t is None else t.data_ptr()
+    st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    _native.call("itts_conv1d_tc", x.data_ptr(), rows, c_in, wt.data_ptr(), n_total, taps, offs_arr,
+                 bias.data_ptr(), c_out, row_out.data_ptr(), ptr(resid_in), ptr(resid_out), ptr(acc),
+                 acc_mode, ptr(act_out), float(slope), int(zero_halo), st)
