@@ -89,11 +89,56 @@ int itts_s_vocode_chunk(const int64_t* plan, int32_t n_items, int32_t dim, int32
  *   epilogue: v = acc + bias; (+resid_in); -> resid_out; acc_mode 1 store,
  *          2 add, 3 finalize v = (acc + v) / 3; act_out = bf16(lrelu(v, slope));
  *          zero_halo writes zeros to act_out halo rows.
- * c_in must be a multiple of 32, c_out a multiple of 32. */
-int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, const void* w, int32_t n_total,
-                   int32_t n_taps, const int32_t* host_tap_off, const float* bias, int32_t c_out,
-                   const int32_t* row_out, const float* resid_in, float* resid_out, float* acc,
-                   int32_t acc_mode, void* act_out, float slope, int32_t zero_halo, void* stream);
+ * c_in must be a multiple of 32, c_out a multiple of 32; x rows are x_ld
+ * elements apart (x_ld >= c_in, so a GEMM operand can be a column slice);
+ * bn = N tile (32/64/128/256) or 0 for automatic. */
+int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, const void* w,
+                   int32_t n_total, int32_t n_taps, const int32_t* host_tap_off, const float* bias,
+                   int32_t c_out, const int32_t* row_out, const float* resid_in, float* resid_out,
+                   float* acc, int32_t acc_mode, void* act_out, float slope, int32_t zero_halo,
+                   int32_t bn, void* stream);
+
+/* K6 decoder-step chain (replaces decode_chunk_batch, acoustic.py:234-238,
+ * with the Tacotron2 decoder, paper Eq. 2).  `state` = fp32 [B][4944] rows
+ * gathered by itts_gather_rows: [p 256 | ctx 512 | att_h 1024 | dec_h 1024 |
+ * att_c 1024 | dec_c 1024 | last_frame 80]; `xb` = bf16 [B][2816] operand
+ * mirror of the first 2816 floats.  plan = int64 [B][8] {memory_ptr,
+ * processed_memory_ptr, L, w_src_ptr (W|W_acc), w_dst_ptr, steps, mel_ptr,
+ * gate_ptr}; items with step >= steps are left untouched (stop divergence).
+ * The gate GEMMs between these calls are itts_conv1d_tc with one tap. */
+int itts_r_dec_prepare(const float* state, void* xb, int32_t B, void* stream);
+int itts_r_prenet(float* state, void* xb, const float* W0T, const float* W1T, const int64_t* plan,
+                  int32_t B, int32_t step, void* stream);
+int itts_r_lstm_cell(const float* gates, float* state, void* xb, int32_t h_off, int32_t c_off,
+                     const int64_t* plan, int32_t B, int32_t step, void* stream);
+int itts_r_attention(float* state, void* xb, const int64_t* plan, int32_t B, int32_t max_len,
+                     const float* WqT, const float* Wloc, const float* WdT, const float* v, int32_t step,
+                     void* stream);
+int itts_r_proj(float* state, const int64_t* plan, int32_t B, const float* WpT, const float* bp,
+                int32_t step, void* stream);
+
+/* K5 encoder (replaces encode_batch + init_decoder_state, acoustic.py:222-231,
+ * :118-133, with the Tacotron2 encoder, paper Eq. 1).  plan = int64 [n][6]
+ * {tok_off, L, first_row, memory_ptr (fp32 [L][512]), pm_ptr (fp32 [L][128]),
+ * 0}; X = bf16 [rows][512] zero-haloed conv input; PRE = fp32 [rows][2048]
+ * BiLSTM input projections (both directions, biases folded). */
+int itts_r_enc_embed(const int32_t* tok4, int64_t total, const int64_t* plan, int32_t n,
+                     int64_t max_len, const float* Eph, const float* Epw, const float* Epph,
+                     const float* Eiph, void* X, void* stream);
+int itts_r_bilstm(const float* PRE, const int64_t* plan, int32_t n, const float* WhhT, void* stream);
+int itts_r_pmem(const int64_t* plan, int32_t n, int64_t max_len, const float* WmT, void* stream);
+
+/* K7 helpers around the HiFi-GAN conv stack (replaces vocode_batch,
+ * vocoder.py:92-143): spliced-mel assembly, per-stage row maps, halo
+ * re-zeroing, and conv_post + tanh fused with the Eq.-3 cross-fade /
+ * hold-back epilogue writing the packed fp32 audio. */
+int itts_r_mel_assemble(const int64_t* plan, int32_t n, int64_t max_rows, void* X0, int32_t ld,
+                        void* stream);
+int itts_r_rowmap(const int64_t* plan, int32_t n, int64_t max_span, int32_t* row_out, void* stream);
+int itts_r_zero_halo(const int64_t* plan, int32_t n, int64_t max_halo, void* X, int32_t C, void* stream);
+int itts_r_post_splice(const void* X4, const int64_t* plan, int32_t n, int64_t max_g, const float* wpost,
+                       float bpost, const float* fade, int32_t overlap_frames, int32_t overlap_samples,
+                       float* audio, void* stream);
 
 #ifdef __cplusplus
 }

@@ -302,12 +302,12 @@ EncodeFn get_encode() {
   return fn;
 }
 
-bool encode_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
-               uint32_t box_outer, int swz) {
+bool encode_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+               uint32_t box_inner, uint32_t box_outer, int swz) {
   EncodeFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {inner * 2};
+  cuuint64_t strides[1] = {ld * 2};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
@@ -318,12 +318,13 @@ bool encode_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t oute
 }
 
 template <int BN, int SWZ, int STAGES>
-int launch(const void* x, int64_t rows, int c_in, const void* w, int n_total, const Taps& taps, const Epi& epi,
-           cudaStream_t st) {
+int launch(const void* x, int64_t rows, int c_in, int64_t x_ld, const void* w, int n_total, const Taps& taps,
+           const Epi& epi, cudaStream_t st) {
   constexpr int KT = SWZ / 2;
   CUtensorMap ma, mb;
-  if (!encode_2d(&ma, x, (uint64_t)c_in, (uint64_t)rows, KT, kBlockM, SWZ)) return ITTS_EINVAL;
-  if (!encode_2d(&mb, w, (uint64_t)c_in, (uint64_t)taps.n * n_total, KT, BN, SWZ)) return ITTS_EINVAL;
+  if (!encode_2d(&ma, x, (uint64_t)c_in, (uint64_t)rows, (uint64_t)x_ld, KT, kBlockM, SWZ)) return ITTS_EINVAL;
+  if (!encode_2d(&mb, w, (uint64_t)c_in, (uint64_t)taps.n * n_total, (uint64_t)c_in, KT, BN, SWZ))
+    return ITTS_EINVAL;
   const size_t smem = 1024 + STAGES * (kBlockM + BN) * SWZ + (2 * STAGES + 1) * 8 + 16;
   static bool attr_set = false;
   if (!attr_set) {
@@ -337,13 +338,15 @@ int launch(const void* x, int64_t rows, int c_in, const void* w, int n_total, co
 
 }  // namespace
 
-ITTS_API int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, const void* w, int32_t n_total,
-                            int32_t n_taps, const int32_t* host_tap_off, const float* bias, int32_t c_out,
-                            const int32_t* row_out, const float* resid_in, float* resid_out, float* acc,
-                            int32_t acc_mode, void* act_out, float slope, int32_t zero_halo, void* stream) {
+ITTS_API int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, const void* w,
+                            int32_t n_total, int32_t n_taps, const int32_t* host_tap_off, const float* bias,
+                            int32_t c_out, const int32_t* row_out, const float* resid_in, float* resid_out,
+                            float* acc, int32_t acc_mode, void* act_out, float slope, int32_t zero_halo,
+                            int32_t bn, void* stream) {
   if (!x || !w || !bias || !row_out || !host_tap_off || rows <= 0) return ITTS_EINVAL;
   if (n_taps < 1 || n_taps > kMaxTaps || c_out <= 0 || n_total % c_out) return ITTS_EINVAL;
   if (c_out % 32 || (acc_mode && !acc) || acc_mode < 0 || acc_mode > 3) return ITTS_EINVAL;
+  if (x_ld < c_in || (x_ld * 2) % 16) return ITTS_EINVAL;
   if (((uintptr_t)x | (uintptr_t)w) & 15) return ITTS_EALIGN;
   Taps taps{};
   taps.n = n_taps;
@@ -352,14 +355,20 @@ ITTS_API int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, const voi
   cudaStream_t st = (cudaStream_t)stream;
   const int swz = (c_in % 64 == 0) ? 128 : (c_in % 32 == 0 ? 64 : 0);
   if (!swz) return ITTS_EUNSUPPORTED;
+  if (bn == 0) bn = n_total % 256 == 0 ? 256 : n_total % 128 == 0 ? 128 : n_total % 64 == 0 ? 64 : 32;
+  if (n_total % bn) return ITTS_EINVAL;
   if (swz == 128) {
-    if (n_total % 256 == 0) return launch<256, 128, 4>(x, rows, c_in, w, n_total, taps, epi, st);
-    if (n_total % 128 == 0) return launch<128, 128, 6>(x, rows, c_in, w, n_total, taps, epi, st);
-    if (n_total % 64 == 0) return launch<64, 128, 8>(x, rows, c_in, w, n_total, taps, epi, st);
-    if (n_total % 32 == 0) return launch<32, 128, 8>(x, rows, c_in, w, n_total, taps, epi, st);
+    switch (bn) {
+      case 256: return launch<256, 128, 4>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
+      case 128: return launch<128, 128, 6>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
+      case 64: return launch<64, 128, 8>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
+      case 32: return launch<32, 128, 8>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
+    }
   } else {
-    if (n_total % 64 == 0) return launch<64, 64, 8>(x, rows, c_in, w, n_total, taps, epi, st);
-    if (n_total % 32 == 0) return launch<32, 64, 8>(x, rows, c_in, w, n_total, taps, epi, st);
+    switch (bn) {
+      case 64: return launch<64, 64, 8>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
+      case 32: return launch<32, 64, 8>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
+    }
   }
   return ITTS_EUNSUPPORTED;
 }

@@ -1,0 +1,446 @@
+"""Tier R GPU modules: random-init Tacotron2 + HiFi-GAN V1 behind PipelineModules.
+
+Same three callables and the same handle/value semantics as Tier S
+(``tier_s.py``), with the reference's stand-in arithmetic replaced by the
+real networks (paper Eq. 1-3):
+
+encoder_batch   K5: embedding sum -> 3 x tcgen05 conv(k5)+ReLU -> tcgen05
+                BiLSTM input GEMM -> cluster BiLSTM recurrence -> memory,
+                processed memory (FFMA).
+decoder_batch   K1 gather of the fixed state rows -> K6 x steps: prenet,
+                tcgen05 attention-LSTM gate GEMM (bf16, swap-free: batch rows
+                x 4096 gates), cell, location-sensitive attention, tcgen05
+                decoder-LSTM gate GEMM, cell, mel/gate projection -> K1
+                scatter into the request's next state buffer.
+vocoder_batch   K7: [mel_tail; mel] -> conv_pre -> 4 x (transposed conv as a
+                3-tap phase GEMM, 3 MRF resblocks = 18 convs with fused
+                bias / residual / MRF-average / leaky-ReLU epilogues) ->
+                conv_post + tanh + cross-fade / hold-back (Eq. 3).
+
+Stop is the reference's frame counter (``acoustic.py:174-175``): chunk
+lengths, stop steps and sample offsets are decided on the host exactly as
+in Tier S; the gate logit is computed and returned but not used.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native
+from . import tc
+from . import weights as W
+from .arena import RaggedArena
+from .audio import cached_curve
+from .domain import AudioChunk, PipelineConfig, validate_config
+from .handles import (DecodeChunkResult, DeviceDecoderState, DeviceEncodedFeatures, DeviceMelChunk,
+                      DeviceRequest, DeviceVocoderState)
+
+# decoder state row layout (floats) -- must match csrc/tier_r.cu
+P_OFF, CTX_OFF, ATTH_OFF, DECH_OFF, ATTC_OFF, DECC_OFF, LAST_OFF, ROW = 0, 256, 768, 1792, 2816, 3840, 4864, 4944
+XB_ROW = 2816
+ENC_HALO = 2        # conv k5
+MEL_HALO = 3        # conv_pre k7
+MRF_HALO = 25       # k11 dilation 5
+UPS = (8, 8, 2, 2)
+STAGE_C = (256, 128, 64, 32)
+
+
+def _h2d(arr: np.ndarray, device) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(arr)).pin_memory().to(device, non_blocking=True)
+
+
+class _Layout:
+    """Packed rows of one activation stage: item i at [base_i, base_i + 2*halo + rows_i)."""
+
+    def __init__(self, rows: list[int], halo: int):
+        self.rows, self.halo = rows, halo
+        spans = np.array(rows, dtype=np.int64) + 2 * halo
+        self.base = np.concatenate([[0], np.cumsum(spans)[:-1]]).astype(np.int64)
+        self.total = int(spans.sum())
+        self.first = self.base + halo   # first valid row per item
+
+
+class TierREngine:
+    dtype = torch.float32
+
+    def __init__(self, cfg: PipelineConfig, device=None, seed: int = 0, weights: dict | None = None):
+        self.cfg = validate_config(cfg)
+        if cfg.hop_samples != 256:
+            raise ValueError("HiFi-GAN V1 upsamples by 256: hop_samples must be 256")
+        self.device = torch.device(device if device is not None else "cuda")
+        if self.device.type != "cuda":
+            raise RuntimeError("Tier-R GPU modules need a CUDA device (no CPU fallback)")
+        _native.lib()
+        self.stream = torch.cuda.Stream(self.device)
+        w = weights if weights is not None else W.tier_r_weights(seed)
+        with torch.cuda.stream(self.stream):
+            self._prepare_weights(w)
+            self.arena = RaggedArena(self.dtype, self.device, 1 << 24, self.stream)
+            curve = cached_curve(cfg.overlap_samples)
+            self.fade = torch.from_numpy(np.concatenate([curve.fade_in, curve.fade_out])).float().to(self.device)
+            self.iota = torch.arange(1 << 16, dtype=torch.int32, device=self.device)
+        self.stream.synchronize()
+        self.launches = 0
+
+    # ------------------------------------------------------------ weights
+    def _prepare_weights(self, w: dict) -> None:
+        d = self.device
+        f32 = lambda t: t.detach().float().contiguous().to(d)
+        self.E = [f32(w[f"emb.{k}"]) for k in ("phoneme", "pw", "pph", "iph")]
+        self.enc_conv = []
+        for i in range(3):
+            wt, offs = tc.conv_weights(f32(w[f"enc.conv{i}.w"]))
+            self.enc_conv.append((wt, offs, f32(w[f"enc.conv{i}.b"])))
+        wih = torch.cat([w["enc.lstm_fwd.w_ih"], w["enc.lstm_bwd.w_ih"]], 0)          # [2048][512]
+        self.enc_ih = (wih.to(d).to(torch.bfloat16)[None].contiguous(), [0],
+                       f32(torch.cat([w["enc.lstm_fwd.b_ih"] + w["enc.lstm_fwd.b_hh"],
+                                      w["enc.lstm_bwd.b_ih"] + w["enc.lstm_bwd.b_hh"]])))
+        self.enc_whhT = f32(torch.stack([w["enc.lstm_fwd.w_hh"].T, w["enc.lstm_bwd.w_hh"].T]))  # [2][256][1024]
+        self.WmT = f32(w["att.memory_layer"].T)                                          # [512][128]
+        # decoder
+        self.W0T, self.W1T = f32(w["prenet.0"].T), f32(w["prenet.1"].T)
+        wa = torch.cat([w["att_rnn.w_ih"], w["att_rnn.w_hh"]], 1)                       # [p|ctx|att_h]
+        self.att_gemm = (wa.to(d).to(torch.bfloat16)[None].contiguous(), [0],
+                         f32(w["att_rnn.b_ih"] + w["att_rnn.b_hh"]))
+        wih = w["dec_rnn.w_ih"]                                                          # cols [att_h | ctx]
+        wd = torch.cat([wih[:, 1024:], wih[:, :1024], w["dec_rnn.w_hh"]], 1)             # [ctx|att_h|dec_h]
+        self.dec_gemm = (wd.to(d).to(torch.bfloat16)[None].contiguous(), [0],
+                         f32(w["dec_rnn.b_ih"] + w["dec_rnn.b_hh"]))
+        self.WqT = f32(w["att.query_layer"].T)                                           # [1024][128]
+        self.Wloc = f32(w["att.location_conv"])                                          # [32][2][31]
+        self.WdT = f32(w["att.location_dense"].T)                                        # [32][128]
+        self.v = f32(w["att.v"][0])
+        self.WpT = f32(torch.cat([w["proj.w"], w["gate.w"]], 0).T)                      # [1536][81]
+        self.bp = f32(torch.cat([w["proj.b"], w["gate.b"]]))
+        # HiFi-GAN
+        wt, offs = tc.conv_weights(f32(w["hg.conv_pre.w"]), 1, c_in_pad=128)
+        self.conv_pre = (wt, offs, f32(w["hg.conv_pre.b"]))
+        self.ups, self.res = [], []
+        for i, u in enumerate(UPS):
+            wp, offs = tc.convt_weights(f32(w[f"hg.up{i}.w"]), u)
+            self.ups.append((wp, offs, f32(w[f"hg.up{i}.b"])))
+            blocks = []
+            for j, k in enumerate(W.HG_RES_KERNELS):
+                layers = []
+                for m, dil in enumerate(W.HG_RES_DILATIONS):
+                    key = f"hg.res{i}.{j}"
+                    c1 = tc.conv_weights(f32(w[f"{key}.c1{m}.w"]), dil) + (f32(w[f"{key}.c1{m}.b"]),)
+                    c2 = tc.conv_weights(f32(w[f"{key}.c2{m}.w"]), 1) + (f32(w[f"{key}.c2{m}.b"]),)
+                    layers.append((c1, c2))
+                blocks.append(layers)
+            self.res.append(blocks)
+        self.wpost = f32(w["hg.conv_post.w"][0])                                        # [32][7]
+        self.bpost = float(w["hg.conv_post.b"][0])
+
+    # ------------------------------------------------------------ helpers
+    def _st(self) -> int:
+        return self.stream.cuda_stream
+
+    def _call(self, name: str, *args) -> None:
+        _native.call(name, *args)
+        self.launches += 1
+
+    def _conv(self, x, layer, c_out, row_out, **kw) -> None:
+        wt, offs, bias = layer
+        tc.conv1d_tc(x, wt, offs, bias, c_out, row_out, stream=self._st(), **kw)
+        self.launches += 1
+
+    def _iota(self, n: int) -> torch.Tensor:
+        if n > self.iota.numel():
+            self.iota = torch.arange(2 * n, dtype=torch.int32, device=self.device)
+        return self.iota[:n]
+
+    def _rowmap(self, layout: _Layout, out_first: np.ndarray, up: int) -> torch.Tensor:
+        n = len(layout.rows)
+        plan = np.stack([layout.base, np.array(layout.rows, np.int64), np.full(n, layout.halo, np.int64),
+                         out_first.astype(np.int64), np.full(n, up, np.int64)], 1)
+        rm = torch.empty(layout.total, dtype=torch.int32, device=self.device)
+        self._call("itts_r_rowmap", _h2d(plan, self.device).data_ptr(), n,
+                   int(max(layout.rows)) + 2 * layout.halo, rm.data_ptr(), self._st())
+        return rm
+
+    def state_size(self, L: int) -> int:
+        return ROW + 2 * L
+
+    def voc_size(self) -> int:
+        return self.cfg.overlap_frames * W.N_MEL + self.cfg.overlap_samples
+
+    # ------------------------------------------------------------ encoder
+    def encoder_batch(self, fos) -> list:
+        n = len(fos)
+        if n == 0:
+            return []
+        lens = [fo.seq_len for fo in fos]
+        if min(lens) < 1:
+            raise ValueError("frontend output needs at least one phoneme")
+        for fo in fos:
+            if max(fo.phonemes) >= W.N_SYMBOLS or min(fo.phonemes) < 0:
+                raise ValueError("phoneme id outside the embedding table")
+            if max(max(fo.pw), max(fo.pph), max(fo.iph)) > 1 or min(min(fo.pw), min(fo.pph), min(fo.iph)) < 0:
+                raise ValueError("prosody tokens must be 0/1")
+        total = sum(lens)
+        tok = np.empty((4, total), dtype=np.int32)
+        pos = 0
+        for fo, L in zip(fos, lens):
+            tok[:, pos:pos + L] = (fo.phonemes, fo.pw, fo.pph, fo.iph)
+            pos += L
+        lay = _Layout(lens, ENC_HALO)
+        reqs = []
+        for L in lens:
+            req = DeviceRequest(self, L)
+            req.extra["mem_off"] = req.add_region(L * W.EMB)
+            req.extra["pm_off"] = req.add_region(L * W.ATT_DIM)
+            buf = req.claim(req.state_bufs, self.state_size(L), set())
+            reqs.append((req, buf))
+        a = self.arena
+        tok_off = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+        plan = np.zeros((n, 6), dtype=np.int64)
+        for i, (req, _) in enumerate(reqs):
+            plan[i] = (tok_off[i], lens[i], lay.first[i], a.ptr(req.extra["mem_off"]),
+                       a.ptr(req.extra["pm_off"]), 0)
+        st = self._st()
+        with torch.cuda.stream(self.stream):
+            d_tok, d_plan = _h2d(tok, self.device), _h2d(plan, self.device)
+            xa = torch.zeros(lay.total, W.EMB, dtype=torch.bfloat16, device=self.device)
+            xb = torch.empty_like(xa)
+            self._call("itts_r_enc_embed", d_tok.data_ptr(), total, d_plan.data_ptr(), n, max(lens),
+                       *[e.data_ptr() for e in self.E], xa.data_ptr(), st)
+            rm = self._rowmap(lay, lay.first, 1)
+            for i, layer in enumerate(self.enc_conv):
+                src, dst = (xa, xb) if i % 2 == 0 else (xb, xa)
+                self._conv(src, layer, W.EMB, rm, act_out=dst, slope=0.0)
+            pre = torch.empty(lay.total, 2048, dtype=torch.float32, device=self.device)
+            self._conv(xb, self.enc_ih, 2048, rm, resid_out=pre, bn=128)
+            self._call("itts_r_bilstm", pre.data_ptr(), d_plan.data_ptr(), n, self.enc_whhT.data_ptr(), st)
+            self._call("itts_r_pmem", d_plan.data_ptr(), n, max(lens), self.WmT.data_ptr(), st)
+            for req, buf in reqs:
+                a.tensor[buf.off:buf.off + self.state_size(req.seq_len)].zero_()
+        fpp = self.cfg.frames_per_phoneme
+        return [(DeviceEncodedFeatures(req), DeviceDecoderState(req, buf, 0, fpp * req.seq_len))
+                for req, buf in reqs]
+
+    # ------------------------------------------------------------ decoder
+    def decoder_batch(self, pairs) -> list:
+        n = len(pairs)
+        if n == 0:
+            return []
+        C = self.cfg.chunk_frames
+        steps, taken, dsts = [], set(), []
+        for state, enc in pairs:
+            if not isinstance(state, DeviceDecoderState) or not isinstance(enc, DeviceEncodedFeatures):
+                raise TypeError("Tier-R GPU decoder needs handles produced by its own encoder")
+            if state.req is not enc.req or state.req.engine is not self:
+                raise ValueError("decoder state does not match encoded features")
+            if state.frames_emitted >= state.target_frames:
+                raise ValueError("decode past stop")
+            steps.append(min(C, state.target_frames - state.frames_emitted))
+        for state, _ in pairs:
+            dsts.append(state.req.claim(state.req.state_bufs, self.state_size(state.req.seq_len), taken))
+        a = self.arena
+        mel_off = np.concatenate([[0], np.cumsum(steps)]).astype(np.int64)
+        max_L = max(s.req.seq_len for s, _ in pairs)
+        st = self._st()
+        with torch.cuda.stream(self.stream):
+            mel = torch.empty(int(mel_off[-1]), W.N_MEL, dtype=torch.float32, device=self.device)
+            gate = torch.empty(int(mel_off[-1]), dtype=torch.float32, device=self.device)
+            plan = np.zeros((n, 8), dtype=np.int64)
+            src = np.zeros(n, dtype=np.int64)
+            dstp = np.zeros(n, dtype=np.int64)
+            for i, ((state, enc), dst) in enumerate(zip(pairs, dsts)):
+                req = state.req
+                src[i], dstp[i] = a.ptr(state.buf.off), a.ptr(dst.off)
+                plan[i] = (a.ptr(req.extra["mem_off"]), a.ptr(req.extra["pm_off"]), req.seq_len,
+                           src[i] + 4 * ROW, dstp[i] + 4 * ROW, steps[i],
+                           mel.data_ptr() + 4 * W.N_MEL * int(mel_off[i]), gate.data_ptr() + 4 * int(mel_off[i]))
+            packed = _h2d(np.concatenate([plan.reshape(-1), src, dstp]), self.device)
+            d_plan, d_src, d_dst = packed[:8 * n], packed[8 * n:9 * n], packed[9 * n:]
+            work = torch.empty(n, ROW, dtype=torch.float32, device=self.device)
+            xbm = torch.empty(n, XB_ROW, dtype=torch.bfloat16, device=self.device)
+            G = torch.empty(n, 4096, dtype=torch.float32, device=self.device)
+            self._call("itts_gather_rows", work.data_ptr(), d_src.data_ptr(), n, 4 * ROW, st)
+            self._call("itts_r_dec_prepare", work.data_ptr(), xbm.data_ptr(), n, st)
+            rows = self._iota(n)
+            x_att, x_dec = xbm[:, :1792], xbm[:, 256:]
+            for step in range(max(steps)):
+                self._call("itts_r_prenet", work.data_ptr(), xbm.data_ptr(), self.W0T.data_ptr(),
+                           self.W1T.data_ptr(), d_plan.data_ptr(), n, step, st)
+                self._conv(x_att, self.att_gemm, 4096, rows, resid_out=G, bn=64)
+                self._call("itts_r_lstm_cell", G.data_ptr(), work.data_ptr(), xbm.data_ptr(), ATTH_OFF,
+                           ATTC_OFF, d_plan.data_ptr(), n, step, st)
+                self._call("itts_r_attention", work.data_ptr(), xbm.data_ptr(), d_plan.data_ptr(), n, max_L,
+                           self.WqT.data_ptr(), self.Wloc.data_ptr(), self.WdT.data_ptr(), self.v.data_ptr(),
+                           step, st)
+                self._conv(x_dec, self.dec_gemm, 4096, rows, resid_out=G, bn=64)
+                self._call("itts_r_lstm_cell", G.data_ptr(), work.data_ptr(), xbm.data_ptr(), DECH_OFF,
+                           DECC_OFF, d_plan.data_ptr(), n, step, st)
+                self._call("itts_r_proj", work.data_ptr(), d_plan.data_ptr(), n, self.WpT.data_ptr(),
+                           self.bp.data_ptr(), step, st)
+            self._call("itts_scatter_rows", d_dst.data_ptr(), work.data_ptr(), n, 4 * ROW, st)
+        out = []
+        for i, ((state, enc), dst) in enumerate(zip(pairs, dsts)):
+            emitted = state.frames_emitted + steps[i]
+            mh = DeviceMelChunk(mel[int(mel_off[i]):int(mel_off[i + 1])], state.req)
+            res = DecodeChunkResult(mh, emitted >= state.target_frames,
+                                    DeviceDecoderState(state.req, dst, emitted, state.target_frames))
+            object.__setattr__(res, "gate_logits", gate[int(mel_off[i]):int(mel_off[i + 1])])
+            out.append(res)
+        return out
+
+    # ------------------------------------------------------------ vocoder
+    def vocoder_batch(self, triples) -> list:
+        n = len(triples)
+        if n == 0:
+            return []
+        O, H, S = self.cfg.overlap_frames, self.cfg.hop_samples, self.cfg.overlap_samples
+        metas, host_mels = [], []
+        for vstate, mel, is_last in triples:
+            m = int(mel.frame_count)
+            if not is_last and m < O:
+                raise ValueError("non-final chunk shorter than the overlap window")
+            has_tail = (vstate.has_tail if isinstance(vstate, DeviceVocoderState)
+                        else vstate.mel_tail is not None)
+            if not has_tail and not is_last and m * H <= S:
+                raise ValueError("non-final chunk shorter than the overlap window")
+            if isinstance(mel, DeviceMelChunk):
+                if mel.data.shape[1] != W.N_MEL:
+                    raise ValueError("mel chunk width must be 80")
+            else:
+                frames = np.asarray(mel.frames, dtype=np.float32)
+                if frames.ndim != 2 or frames.shape[1] != W.N_MEL:
+                    raise ValueError("mel chunk width must be 80")
+                host_mels.append(frames)
+            T = (O if has_tail else 0) + m
+            metas.append((m, has_tail, bool(is_last), T, T * H, T * H if is_last else T * H - S))
+        counts = [mt[5] for mt in metas]
+        out_off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        Ts = [mt[3] for mt in metas]
+        a, st, dev = self.arena, self._st(), self.device
+        keep, taken, results = [], set(), []
+        with torch.cuda.stream(self.stream):
+            if host_mels:
+                hm = _h2d(np.concatenate([f.reshape(-1) for f in host_mels]), dev)
+            hpos = 0
+            lay0 = _Layout(Ts, MEL_HALO)
+            mplan = np.zeros((n, 5), dtype=np.int64)
+            pplan = np.zeros((n, 8), dtype=np.int64)
+            stage4 = _Layout([T * 256 for T in Ts], MRF_HALO)
+            owners = self._claim_voc(triples, [mt[2] for mt in metas], taken)  # before any a.ptr()
+            for i, ((vstate, mel, is_last), (m, has_tail, last, T, G, cnt)) in enumerate(zip(triples, metas)):
+                req, dst = owners[i]
+                if isinstance(mel, DeviceMelChunk):
+                    mel_ptr = mel.data.data_ptr()
+                else:
+                    mel_ptr = hm.data_ptr() + 4 * hpos
+                    hpos += m * W.N_MEL
+                tail_ptr = 0
+                if has_tail:
+                    if isinstance(vstate, DeviceVocoderState):
+                        tail_ptr = a.ptr(vstate.buf.off)
+                    else:
+                        t = _h2d(np.concatenate([np.asarray(vstate.mel_tail, np.float32).reshape(-1),
+                                                 np.asarray(vstate.held_tail, np.float32).reshape(-1)]), dev)
+                        keep.append(t)
+                        tail_ptr = t.data_ptr()
+                mplan[i] = (tail_ptr, mel_ptr, m, O if has_tail else 0, lay0.first[i])
+                pplan[i] = (stage4.first[i], G, int(has_tail) | 2 * int(last),
+                            tail_ptr + 4 * O * W.N_MEL if has_tail else 0,
+                            0 if dst is None else a.ptr(dst.off), out_off[i], mel_ptr, m)
+                results.append((req, dst, int(vstate.emitted_samples)))
+            d_mplan = _h2d(mplan, dev)
+            d_pplan = _h2d(pplan, dev)
+            audio = torch.empty(max(int(out_off[-1]), 1), dtype=torch.float32, device=dev)
+            x4 = self._hifigan(Ts, lay0, d_mplan)
+            self._call("itts_r_post_splice", x4.data_ptr(), d_pplan.data_ptr(), n, max(mt[4] for mt in metas),
+                       self.wpost.data_ptr(), self.bpost, self.fade.data_ptr(), O, S, audio.data_ptr(), st)
+            host = torch.empty(audio.numel(), dtype=torch.float32, pin_memory=True)
+            host.copy_(audio, non_blocking=True)
+        self.stream.synchronize()
+        flat = host.numpy()
+        if not np.isfinite(flat[:out_off[-1]]).all():
+            raise ValueError("array contains non-finite values")
+        out = []
+        for i, (req, dst, emitted) in enumerate(results):
+            out.append((AudioChunk.trusted(flat[out_off[i]:out_off[i + 1]], emitted),
+                        DeviceVocoderState(req, dst, emitted + counts[i])))
+        return out
+
+    def _hifigan(self, Ts: list[int], lay0: _Layout, d_mplan: torch.Tensor) -> torch.Tensor:
+        """HiFi-GAN V1 over a packed batch of spliced chunks -> stage-4 bf16 act (lrelu 0.01 applied)."""
+        dev, st, n = self.device, self._st(), len(Ts)
+        x0 = torch.zeros(lay0.total, 128, dtype=torch.bfloat16, device=dev)
+        self._call("itts_r_mel_assemble", d_mplan.data_ptr(), n, max(Ts), x0.data_ptr(), 128, st)
+        rm0 = self._rowmap(lay0, lay0.first, 1)
+        act_in = torch.empty(lay0.total, 512, dtype=torch.bfloat16, device=dev)
+        self._conv(x0, self.conv_pre, 512, rm0, act_out=act_in, slope=0.1)
+        prev, mult, layouts = lay0, 1, []
+        for u in UPS:
+            mult *= u
+            layouts.append(_Layout([T * mult for T in Ts], MRF_HALO))
+        biggest = max(l.total * c for l, c in zip(layouts, STAGE_C))
+        f32 = [torch.empty(biggest, dtype=torch.float32, device=dev) for _ in range(3)]     # x, y, acc
+        b16 = [torch.empty(biggest, dtype=torch.bfloat16, device=dev) for _ in range(5)]   # xa, ya, tb, oa x2
+        for s, (u, lay) in enumerate(zip(UPS, layouts)):
+            C = STAGE_C[s]
+            view = lambda t: t[:lay.total * C].view(lay.total, C)
+            X, Y, ACC = (view(t) for t in f32)
+            XA, YA, TB = (view(t) for t in b16[:3])
+            OA_next = view(b16[3 + s % 2])
+            # transposed conv: each input row of the previous stage -> u output rows
+            rmT = self._rowmap(prev, lay.first, u)
+            self._conv(act_in, self.ups[s], C, rmT, resid_out=X, act_out=XA, slope=0.1, zero_halo=False)
+            zplan = np.stack([lay.base, np.array(lay.rows, np.int64), np.full(n, lay.halo, np.int64)], 1)
+            self._call("itts_r_zero_halo", _h2d(zplan, dev).data_ptr(), n, lay.halo, XA.data_ptr(), C, st)
+            rm = self._rowmap(lay, lay.first, 1)
+            slope_out = 0.1 if s < 3 else 0.01
+            for j, layers in enumerate(self.res[s]):
+                for m, (c1, c2) in enumerate(layers):
+                    self._conv(XA if m == 0 else YA, c1, C, rm, act_out=TB, slope=0.1)
+                    if m < 2:
+                        self._conv(TB, c2, C, rm, resid_in=X if m == 0 else Y, resid_out=Y, act_out=YA,
+                                   slope=0.1)
+                    else:
+                        mode = (tc.ACC_STORE, tc.ACC_ADD, tc.ACC_FINAL)[j]
+                        self._conv(TB, c2, C, rm, resid_in=Y, acc=ACC, acc_mode=mode,
+                                   act_out=OA_next if j == 2 else None, slope=slope_out)
+            prev, act_in = lay, OA_next
+        return act_in
+
+    def _claim_voc(self, triples, lasts, taken) -> list:
+        """(owning request, next vocoder-state buffer or None) per item; allocates up front."""
+        owners = []
+        for (vstate, mel, _), last in zip(triples, lasts):
+            req = mel.req if isinstance(mel, DeviceMelChunk) else None
+            if req is None:
+                req = vstate.req if isinstance(vstate, DeviceVocoderState) else DeviceRequest(self, 0)
+            owners.append((req, None if last else req.claim(req.voc_bufs, self.voc_size(), taken)))
+        return owners
+
+    # ------------------------------------------------------------ lazy reads (tests/debug)
+    def _read(self, off: int, size: int) -> np.ndarray:
+        self.stream.synchronize()
+        return self.arena.tensor[off:off + size].to("cpu").numpy().copy()
+
+    def read_features(self, req) -> np.ndarray:
+        arr = self._read(req.extra["mem_off"], req.seq_len * W.EMB).reshape(req.seq_len, W.EMB)
+        arr.setflags(write=False)
+        return arr
+
+    def read_processed_memory(self, req) -> np.ndarray:
+        return self._read(req.extra["pm_off"], req.seq_len * W.ATT_DIM).reshape(req.seq_len, W.ATT_DIM)
+
+    def read_state(self, req, buf) -> dict:
+        L = req.seq_len
+        raw = self._read(buf.off, self.state_size(L))
+        out = {"last_frame": raw[LAST_OFF:LAST_OFF + 80], "attn_context": raw[CTX_OFF:CTX_OFF + 512],
+               "attn_hidden": raw[ATTH_OFF:ATTH_OFF + 1024], "attn_cell": raw[ATTC_OFF:ATTC_OFF + 1024],
+               "dec_hidden": raw[DECH_OFF:DECH_OFF + 1024], "dec_cell": raw[DECC_OFF:DECC_OFF + 1024],
+               "attn_weights": raw[ROW:ROW + L], "attn_weights_sum": raw[ROW + L:ROW + 2 * L]}
+        for v in out.values():
+            v.setflags(write=False)
+        return out
+
+    def read_voc_state(self, req, buf):
+        O = self.cfg.overlap_frames
+        raw = self._read(buf.off, self.voc_size())
+        return raw[:O * W.N_MEL].reshape(O, W.N_MEL), raw[O * W.N_MEL:]

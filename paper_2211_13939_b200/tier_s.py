@@ -171,11 +171,13 @@ class TierSEngine:
                 hm = _h2d(np.concatenate([f.reshape(-1) for f in host_mels]), self.device)
                 keep.append(hm)
             hpos = 0
+            owners = self._claim_voc(triples, [mt[2] for mt in metas], taken)  # before any a.ptr()
             for i, ((vstate, mel, is_last), (m, has_tail, last, cnt)) in enumerate(zip(triples, metas)):
+                req, dst = owners[i]
                 if isinstance(mel, DeviceMelChunk):
-                    mel_ptr, req = mel.data.data_ptr(), mel.req
+                    mel_ptr = mel.data.data_ptr()
                 else:
-                    mel_ptr, req = hm.data_ptr() + 8 * hpos, None
+                    mel_ptr = hm.data_ptr() + 8 * hpos
                     hpos += m * self.dim
                 src_ptr = 0
                 if has_tail:
@@ -187,9 +189,6 @@ class TierSEngine:
                                  self.device)
                         keep.append(t)
                         src_ptr = t.data_ptr()
-                if req is None:
-                    req = vstate.req if isinstance(vstate, DeviceVocoderState) else DeviceRequest(self, 0)
-                dst = None if last else req.claim(req.voc_bufs, self.voc_size(), taken)
                 plan[i] = (mel_ptr, m, int(has_tail) | (2 * int(last)), src_ptr,
                            0 if dst is None else a.ptr(dst.off), out_off[i], 0)
                 results_state.append((req, dst, int(vstate.emitted_samples)))
@@ -211,6 +210,16 @@ class TierSEngine:
             out.append((AudioChunk.trusted(samples, emitted),
                         DeviceVocoderState(req, dst, emitted + counts[i])))
         return out
+
+    def _claim_voc(self, triples, lasts, taken) -> list:
+        """(owning request, next vocoder-state buffer or None) per item; allocates up front."""
+        owners = []
+        for (vstate, mel, _), last in zip(triples, lasts):
+            req = mel.req if isinstance(mel, DeviceMelChunk) else None
+            if req is None:
+                req = vstate.req if isinstance(vstate, DeviceVocoderState) else DeviceRequest(self, 0)
+            owners.append((req, None if last else req.claim(req.voc_bufs, self.voc_size(), taken)))
+        return owners
 
     # ------------------------------------------------------------ lazy reads (tests/debug)
     def _read(self, off: int, size: int) -> np.ndarray:

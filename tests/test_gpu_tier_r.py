@@ -1,0 +1,156 @@
+"""Tier-R parity on the B200: Tacotron2 + HiFi-GAN V1 CUDA path vs the torch-CPU fp32 oracle.
+
+Tolerances (stated in north_star): mel max-abs <= 1e-3, waveform SNR >= 40 dB,
+chunk offsets / counts / stop steps / IterationReports exact.  The oracle
+is the builder's restatement (the reference has no networks), so these
+pins are "parity unpinned by the reference" -- see DESIGN.md.
+"""
+
+import math
+import random
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import tier_r as orc
+from oracle import tier_s as orc_s
+from paper_2211_13939_b200.audio import VocoderState
+from paper_2211_13939_b200.domain import MelChunk, PipelineConfig
+from paper_2211_13939_b200.frontend import run_frontend
+from paper_2211_13939_b200.scheduler import CostModel, RequestPool, run_iteration
+from paper_2211_13939_b200.weights import tier_r_weights
+
+pytestmark = pytest.mark.gpu
+MEL_TOL = 1e-3
+SNR_DB = 40.0
+
+
+@pytest.fixture(scope="module")
+def weights():
+    return tier_r_weights(0)
+
+
+@pytest.fixture(scope="module")
+def engine(weights):
+    from paper_2211_13939_b200.tier_r import TierREngine
+    return TierREngine(PipelineConfig(), "cuda:0", weights=weights)
+
+
+def random_texts(lexicon, count, seed, lo, hi):
+    singles = sorted(c for c in lexicon.phrase_to_pinyin if len(c) == 1)
+    rng = random.Random(seed)
+    return ["".join(rng.choice(singles) for _ in range(rng.randint(lo, hi))) for _ in range(count)]
+
+
+def run_direct(engine, fos, max_chunks=None):
+    """Module calls in batch (all items together), like run_iteration without admission."""
+    encs = engine.encoder_batch(fos)
+    live = [(i, enc, st, VocoderState.initial()) for i, (enc, st) in enumerate(encs)]
+    mels = [[] for _ in fos]
+    audio = [[] for _ in fos]
+    rounds = 0
+    while live:
+        res = engine.decoder_batch([(st, enc) for _, enc, st, _ in live])
+        outs = engine.vocoder_batch([(vs, r.mel, r.stop) for (_, _, _, vs), r in zip(live, res)])
+        nxt = []
+        for (i, enc, _, _), r, (a, vs) in zip(live, res, outs):
+            mels[i].append(r.mel.frames)
+            audio[i].append((a.samples.copy(), a.sample_offset))
+            if not r.stop:
+                nxt.append((i, enc, r.state, vs))
+        live = nxt
+        rounds += 1
+        if max_chunks and rounds >= max_chunks:
+            break
+    return mels, audio
+
+
+def test_encoder_matches_oracle(engine, weights, lexicon):
+    texts = ["欢迎收听今天新闻。", "你们好"] + random_texts(lexicon, 3, 5, 20, 60)
+    fos = [run_frontend(t, lexicon) for t in texts]
+    encs = engine.encoder_batch(fos)
+    for fo, (enc, st) in zip(fos, encs):
+        mem, pm = orc.encode(weights, fo.phonemes, fo.pw, fo.pph, fo.iph)
+        got = enc.rows
+        assert got.shape == tuple(mem.shape)
+        assert np.abs(got - mem.numpy()).max() <= 5e-3, np.abs(got - mem.numpy()).max()
+        gpm = engine.read_processed_memory(enc.req)
+        assert np.abs(gpm - pm.numpy()).max() <= 5e-3
+        assert st.frames_emitted == 0 and st.target_frames == 8 * fo.seq_len
+
+
+def test_vocoder_chunks_match_oracle(engine, weights):
+    rng = np.random.default_rng(3)
+    for lens, last_short in (((32, 32, 8), False), ((16,), False), ((32, 2), True)):
+        mels = [rng.uniform(-0.1, 0.1, size=(m, 80)) for m in lens]
+        st_g, st_o = VocoderState.initial(), orc_s.VocState(None, None, 0)
+        for k, m in enumerate(mels):
+            last = k == len(mels) - 1
+            (a, st_g), = engine.vocoder_batch([(st_g, MelChunk(m), last)])
+            want, off, st_o = orc.vocode_chunk(weights, st_o, m, last, 4)
+            assert a.sample_offset == off and a.sample_count == want.size
+            assert orc.snr_db(want, a.samples) >= SNR_DB, orc.snr_db(want, a.samples)
+
+
+def test_batched_vocoder_equals_solo(engine):
+    rng = np.random.default_rng(4)
+    triples = [(VocoderState.initial(), MelChunk(rng.uniform(-0.1, 0.1, (m, 80))), last)
+               for m, last in ((32, False), (20, True), (32, False), (7, True))]
+    batched = engine.vocoder_batch(triples)
+    for t, (a, _) in zip(triples, batched):
+        (solo, _), = engine.vocoder_batch([t])
+        assert np.array_equal(a.samples, solo.samples)  # batch invariance: same kernels, same order
+
+
+def test_end_to_end_mel_and_audio(engine, weights, lexicon):
+    texts = ["欢迎收听今天新闻。", "你们好", "欢迎大家收听今天下午新闻播报"]
+    fos = [run_frontend(t, lexicon) for t in texts]
+    mels, audio = run_direct(engine, fos)
+    for fo, m, au in zip(fos, mels, audio):
+        chunks, mel_ref, _ = orc.synthesize(weights, fo.phonemes, fo.pw, fo.pph, fo.iph)
+        got = np.concatenate(m)
+        assert got.shape == mel_ref.shape
+        err = np.abs(got - mel_ref).max()
+        assert err <= MEL_TOL, err
+        assert [o for _, o in au] == [o for _, o in chunks]
+        assert [s.size for s, _ in au] == [s.size for s, _ in chunks]
+        snr = orc.snr_db(np.concatenate([s for s, _ in chunks]), np.concatenate([s for s, _ in au]))
+        assert snr >= SNR_DB, snr
+
+
+def test_schedule_identical_to_reference(engine, golden_schedules, lexicon):
+    from paper_2211_13939_b200.modules import modules_for
+    mods = modules_for(engine, lexicon)
+    cfg = PipelineConfig()
+    pool, reps = RequestPool(), []
+    step = lambda: reps.append(run_iteration(pool, mods, CostModel.zero(), cfg, step_index=len(reps)))
+    four, five = "欢迎收听新闻播报", "欢迎收听今天新闻。"
+    pool.submit(four); step(); step()
+    pool.submit(four); pool.submit(five)
+    for _ in range(4):
+        step()
+    pool.submit(four); step()
+    while pool.pending():
+        step()
+    table = [[list(r.frontend_ids), list(r.encoder_ids), list(r.decoder_ids), list(r.vocoder_ids),
+              list(r.completed_ids), list(r.failed_ids)] for r in reps]
+    assert table == golden_schedules["fig2_ol4"]
+
+
+def test_stream_conservation_ragged_pool(engine, lexicon):
+    from paper_2211_13939_b200.modules import modules_for
+    mods = modules_for(engine, lexicon)
+    cfg = PipelineConfig()
+    texts = random_texts(lexicon, 40, 11, 1, 40)
+    pool = RequestPool()
+    streams = [(t, pool.submit(t)[1]) for t in texts]
+    while pool.pending():
+        run_iteration(pool, mods, CostModel.zero(), cfg)
+    for text, stream in streams:
+        target = 8 * run_frontend(text, lexicon).seq_len
+        chunks, off = list(stream), 0
+        for c in chunks:
+            assert c.sample_offset == off
+            off += c.sample_count
+        assert off == target * 256 and len(chunks) == math.ceil(target / 32)
