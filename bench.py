@@ -1,0 +1,337 @@
+"""Serving benchmark: first-chunk latency (FCL) p50/p99 under Poisson load (BASELINE config C3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--qps Q] [--impl ours|reference]
+
+Workload (``config.workload``): Poisson arrivals at ``--qps`` per GPU (default
+100, weak scaling), texts of U{20..200} characters drawn from the bundled
+lexicon's single-character entries (seeded), random-init Tacotron2 (512
+enc, 1024 LSTM) + HiFi-GAN V1 at 22.05 kHz, chunk 32 frames, overlap 4,
+through this package's request pool + module-wise dynamic batching loop
+and its GPU modules (``build_modules(..., tier="r")``).
+
+A "step" is one scheduler iteration (one pass of F/E/D/V over the pooled
+batch).  After max(W iterations, ``--warmup-seconds``) of load, exactly K
+iterations are timed; every request sent inside that window is measured:
+
+* ``value``  p99 FCL in ms at the server boundary: submit() to the first
+  AudioChunk becoming visible on the request's ChunkStream.
+* ``e2e``    the same p99 measured by a client thread receiving the chunk
+  through the public ``SchedulerLoop.submit`` / ``ChunkStream`` API (text in,
+  host float32 audio out; H2D of tokens/plans and D2H of audio inside).
+
+Under torchrun (N > 1) every rank serves its own Poisson stream on its own
+GPU (request-sharded pools, no collectives on the data path); rank 0 prints
+p50/p99 over all ranks' requests and the max-over-ranks window length.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "first-chunk latency p50/p99 (ms) and max QPS at <80ms p99, 1/2/4/8 B200"
+
+
+def _peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return {**json.loads(p.read_text()), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed window."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.proc = gpu, None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[4:8]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _percentiles(values):
+    from paper_2211_13939_b200.harness import nearest_rank
+    return (nearest_rank(values, 50), nearest_rank(values, 99)) if values else (None, None)
+
+
+def cpu_serving_baseline(qps: float, seconds: float, seed: int, max_iters: int | None = None) -> dict:
+    """The oracle CPU implementation (torch-CPU fp32 Tacotron2 + HiFi-GAN behind the same
+    scheduler) on a bounded sample of the same Poisson workload.  Requests that have no first
+    chunk when the budget ends are counted with a censored FCL (= budget end - send)."""
+    import threading
+
+    import torch
+
+    from oracle.modules import cpu_modules_r
+    from paper_2211_13939_b200.domain import PipelineConfig
+    from paper_2211_13939_b200.frontend import default_lexicon
+    from paper_2211_13939_b200.harness import poisson_trace
+    from paper_2211_13939_b200.scheduler import CostModel, RequestPool, run_iteration
+    from paper_2211_13939_b200.weights import tier_r_weights
+
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    torch.set_num_threads(cores)
+    cfg, lex = PipelineConfig(), default_lexicon()
+    weights = tier_r_weights(0)
+    trace = poisson_trace(qps, seconds, seed=seed + 999)
+    pool, first, sent = RequestPool(), {}, {}
+    origin = time.perf_counter()
+    mods = cpu_modules_r(lex, cfg, weights, deadline=origin + seconds)
+    it, nxt = 0, 0
+    while True:
+        now = time.perf_counter() - origin
+        while nxt < len(trace) and trace[nxt].send_at <= now:
+            rid, stream = pool.submit(trace[nxt].text)
+            sent[rid] = origin + trace[nxt].send_at
+            push = stream._push
+            stream._push = (lambda c, _p=push, _r=rid: (first.setdefault(_r, time.perf_counter()), _p(c)))
+            nxt += 1
+        if now >= seconds or (max_iters is not None and it >= max_iters):
+            break
+        if pool.pending():
+            run_iteration(pool, mods, CostModel.zero(), cfg, step_index=it)
+            it += 1
+        else:
+            time.sleep(0.001)
+    end = time.perf_counter()
+    fcl = [1e3 * ((first.get(r, end)) - t) for r, t in sent.items()]
+    p50, p99 = _percentiles(fcl)
+    return {"value": p99, "p50": p50, "unit": "ms", "cores": cores, "kind": "port",
+            "iterations": it, "requests": len(sent), "served_first_chunk": len(first),
+            "sample": f"{seconds:.0f} s of Poisson {qps:g} QPS U{{20..200}}-char arrivals through the "
+                      "oracle CPU modules (torch fp32, all host threads) behind the same scheduler; "
+                      "requests without a first chunk at the end are censored at the budget end"}
+
+
+def run_reference(args) -> None:
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    t0 = time.perf_counter()
+    res = cpu_serving_baseline(args.qps, args.cpu_seconds, args.seed, max_iters=args.steps + args.warmup)
+    wall = time.perf_counter() - t0
+    line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "ms", "n_gpus": args.gpus,
+            "steps": res["iterations"], "warmup": 0,
+            "ms_per_step": round(1e3 * wall / max(res["iterations"], 1), 3), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"C3: Poisson {args.qps:g} QPS, U{{20..200}} chars, Tacotron2+HiFi-GAN V1 "
+                                   "(random init), chunk 32, overlap 4", "qps_per_gpu": args.qps},
+            "p50_ms": res["p50"], "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": res["value"], "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "requests": res["requests"], "served_first_chunk": res["served_first_chunk"]}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args) -> None:
+    import torch
+
+    from paper_2211_13939_b200.domain import PipelineConfig
+    from paper_2211_13939_b200.frontend import default_lexicon
+    from paper_2211_13939_b200.harness import poisson_trace, serve
+    from paper_2211_13939_b200.modules import build_engine, modules_for
+
+    world, rank, local = _dist()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    device = f"cuda:{local}"
+    torch.cuda.set_device(local)
+    cfg, lex = PipelineConfig(), default_lexicon()
+    engine = build_engine(cfg, args.tier, device)
+    mods = modules_for(engine, lex)
+
+    # untimed warm-up of every code path (tensor maps, smem attributes, allocator pools)
+    warm = serve(mods, cfg, poisson_trace(50, 1.0, seed=args.seed + 7, lexicon=lex), warmup_iters=0,
+                 timed_iters=2, drain_seconds=0.0)
+    del warm
+    torch.cuda.synchronize()
+
+    peaks = _peaks()
+    sampler = ClockSampler(local)
+    marks = {}
+
+    def on_window(kind, idx):
+        if kind == "start":
+            torch.cuda.synchronize()
+            engine.timers = []
+            marks["start"] = (engine.launches, engine.h2d_bytes, engine.d2h_bytes)
+            sampler.start()
+        else:
+            marks["clocks"] = sampler.stop()
+            marks["end"] = (engine.launches, engine.h2d_bytes, engine.d2h_bytes)
+            marks["timers"], engine.timers = engine.timers, None
+
+    if dist is not None:
+        dist.barrier()
+    trace = poisson_trace(args.qps, 3600.0, seed=args.seed + 1000 * rank, lexicon=lex)
+    run = serve(mods, cfg, trace, warmup_iters=args.warmup, warmup_seconds=args.warmup_seconds,
+                timed_iters=args.steps, on_window=on_window, drain_seconds=args.drain_seconds)
+    torch.cuda.synchronize()
+    t0, t1 = run.window
+    inside = [r for r in run.timings if t0 <= r.send_time < t1]
+    fcl = [1e3 * r.fcl for r in inside if r.fcl is not None]
+    fcl_c = [1e3 * r.fcl_client for r in inside if r.fcl_client is not None]
+    lcl = [1e3 * r.lcl for r in inside if r.lcl is not None and r.error is None]
+    rtf = [r.lcl / (r.samples / cfg.sample_rate) for r in inside
+           if r.lcl is not None and r.error is None and r.samples]
+    missing = sum(1 for r in inside if r.fcl is None)
+    window_s = t1 - t0
+    steps_in = [rep for rep in run.reports[-(len(run.reports)):]]
+    batch_sizes = [len(rep.decoder_ids) for rep in run.reports]
+
+    timers = marks.get("timers") or []
+    agg = {}
+    for kind, e0, e1, units in timers:
+        ms = e0.elapsed_time(e1)
+        a = agg.setdefault(kind, [0.0, 0.0, 0])
+        a[0] += ms
+        a[1] += units
+        a[2] += 1
+    l0, h0, d0 = marks["start"]
+    l1, h1, d1 = marks["end"]
+
+    if dist is not None:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, {"fcl": fcl, "fcl_c": fcl_c, "lcl": lcl, "rtf": rtf, "window": window_s,
+                                          "missing": missing, "agg": agg, "clocks": marks["clocks"],
+                                          "launch": l1 - l0, "h2d": h1 - h0, "d2h": d1 - d0})
+        if rank != 0:
+            dist.barrier()
+            dist.destroy_process_group()
+            return
+        fcl = [x for g in gathered for x in g["fcl"]]
+        fcl_c = [x for g in gathered for x in g["fcl_c"]]
+        lcl = [x for g in gathered for x in g["lcl"]]
+        rtf = [x for g in gathered for x in g["rtf"]]
+        window_s = max(g["window"] for g in gathered)
+        missing = sum(g["missing"] for g in gathered)
+    p50, p99 = _percentiles(fcl)
+    c50, c99 = _percentiles(fcl_c)
+    l50, l99 = _percentiles(lcl)
+
+    voc = agg.get("vocoder", [0.0, 0.0, 0])
+    dec = agg.get("decoder", [0.0, 0.0, 0])
+    enc = agg.get("encoder", [0.0, 0.0, 0])
+    voc_tflops = voc[1] / (voc[0] * 1e-3) / 1e12 if voc[0] else None
+    dec_gbs = dec[1] / (dec[0] * 1e-3) / 1e9 if dec[0] else None
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("hifigan_conv_dram_bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": round(p99, 3) if p99 is not None else None, "unit": "ms",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * window_s / args.steps, 3), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"C3: Poisson {args.qps:g} QPS per GPU, U{{20..200}} chars (seeded, bundled "
+                               "lexicon), random-init Tacotron2 (512 enc, 1024 LSTM) + HiFi-GAN V1 22.05 kHz, "
+                               "chunk 32, overlap 4, tier r",
+                   "qps_per_gpu": args.qps, "qps_total": args.qps * world, "parallelism": f"pool-per-gpu x{world}",
+                   "l2": "inputs larger than L2 (vocoder activations > 1 GB per iteration)",
+                   "warmup_seconds": args.warmup_seconds, "requests_measured": len(fcl),
+                   "requests_missing_first_chunk": missing},
+        "p50_ms": round(p50, 3) if p50 is not None else None,
+        "lcl_p50_ms": l50, "lcl_p99_ms": l99,
+        "rtf_mean": (sum(rtf) / len(rtf)) if rtf else None,
+        "pooled_batch_mean": round(sum(batch_sizes) / max(len(batch_sizes), 1), 1),
+        "pooled_batch_max": max(batch_sizes) if batch_sizes else 0,
+        "module_device_ms_per_step": {k: round(v[0] / args.steps, 3) for k, v in agg.items()},
+        "roofline": {"kernel": "k_conv_tc (HiFi-GAN conv stack, tcgen05 bf16)", "bound": "tensor",
+                     "achieved": round(voc_tflops, 2) if voc_tflops else None,
+                     "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                     "frac": round(voc_tflops / peaks["bf16_tflops_sustained"], 4) if voc_tflops else None,
+                     "traffic": traffic, "peak_source": peaks["source"] + " sustained bf16",
+                     "algorithmic": "2 x 307,052,544 MAC per spliced mel frame"},
+        "roofline_decoder": {"kernel": "decoder-step chain", "bound": "hbm",
+                             "achieved": round(dec_gbs, 1) if dec_gbs else None, "peak": peaks["hbm_gbs"],
+                             "unit": "GB/s", "frac": round(dec_gbs / peaks["hbm_gbs"], 4) if dec_gbs else None,
+                             "algorithmic": "37.04 MB weights per step + per-item state/memory reads"},
+        "e2e": {"value": round(c99, 3) if c99 is not None else None, "p50": c50, "unit": "ms",
+                "h2d_bytes_per_step": int((h1 - h0) / args.steps), "d2h_bytes_per_step": int((d1 - d0) / args.steps)},
+        "gpu_launches": int(l1 - l0),
+        "clocks": marks.get("clocks"),
+    }
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = {k: v for k, v in cpu_serving_baseline(args.qps, args.cpu_seconds, args.seed).items()
+                                if k in ("value", "unit", "cores", "kind", "sample", "p50", "served_first_chunk",
+                                         "requests")}
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--warmup-seconds", type=float, default=5.0)
+    ap.add_argument("--drain-seconds", type=float, default=20.0)
+    ap.add_argument("--qps", type=float, default=100.0)
+    ap.add_argument("--tier", default="r", choices=("r", "s"))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    random.seed(args.seed)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

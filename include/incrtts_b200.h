@@ -111,8 +111,9 @@ int itts_r_prenet(float* state, void* xb, const float* W0T, const float* W1T, co
                   int32_t B, int32_t step, void* stream);
 int itts_r_lstm_cell(const float* gates, float* state, void* xb, int32_t h_off, int32_t c_off,
                      const int64_t* plan, int32_t B, int32_t step, void* stream);
+int itts_r_query(const float* state, const float* WqT, float* Q, int32_t B, void* stream);
 int itts_r_attention(float* state, void* xb, const int64_t* plan, int32_t B, int32_t max_len,
-                     const float* WqT, const float* Wloc, const float* WdT, const float* v, int32_t step,
+                     const float* Q, const float* Wloc, const float* WdT, const float* v, int32_t step,
                      void* stream);
 int itts_r_proj(float* state, const int64_t* plan, int32_t B, const float* WpT, const float* bp,
                 int32_t step, void* stream);

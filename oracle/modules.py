@@ -64,3 +64,56 @@ def cpu_modules(lexicon, cfg: PipelineConfig) -> PipelineModules:
         return out
 
     return PipelineModules(frontend_module(lexicon), encoder, decoder, vocoder)
+
+
+def cpu_modules_r(lexicon, cfg: PipelineConfig, weights, deadline: float | None = None) -> PipelineModules:
+    """Tier-R oracle (torch-CPU fp32 Tacotron2 + HiFi-GAN) behind the same boundary.
+
+    Batched calls are plain per-item loops, like the reference's
+    ``encode_batch`` / ``decode_chunk_batch`` / ``vocode_batch``.
+    """
+    import time
+
+    from . import tier_r
+
+    def check():
+        if deadline is not None and time.perf_counter() > deadline:
+            raise TimeoutError("cpu baseline time budget exhausted")
+
+    def encoder(fos):
+        out = []
+        for fo in fos:
+            check()
+            mem, pm = tier_r.encode(weights, fo.phonemes, fo.pw, fo.pph, fo.iph)
+            out.append((EncodedR(mem, pm), tier_r.init_state(mem.shape[0], cfg.frames_per_phoneme)))
+        return out
+
+    def decoder(pairs):
+        out = []
+        for state, enc in pairs:
+            check()
+            mel, stop, new, _ = tier_r.decode_chunk(weights, state, enc.memory, enc.pm, cfg.chunk_frames)
+            out.append(DecodeResult(MelChunk(mel.numpy()), stop, new))
+        return out
+
+    def vocoder(triples):
+        out = []
+        for state, mel, is_last in triples:
+            check()
+            st = tier_s.VocState(state.mel_tail, state.held_tail, state.emitted_samples)
+            samples, off, new = tier_r.vocode_chunk(weights, st, mel.frames, is_last, cfg.overlap_frames,
+                                                    cfg.hop_samples)
+            out.append((AudioChunk(samples, off), new))
+        return out
+
+    return PipelineModules(frontend_module(lexicon), encoder, decoder, vocoder)
+
+
+@dataclass(frozen=True)
+class EncodedR:
+    memory: object
+    pm: object
+
+    @property
+    def seq_len(self) -> int:
+        return int(self.memory.shape[0])

@@ -327,8 +327,9 @@ int launch(const void* x, int64_t rows, int c_in, int64_t x_ld, const void* w, i
     return ITTS_EINVAL;
   const size_t smem = 1024 + STAGES * (kBlockM + BN) * SWZ + (2 * STAGES + 1) * 8 + 16;
   static bool attr_set = false;
-  if (!attr_set) {
+  if (!attr_set) {  // max carveout so 2-3 CTAs co-reside and one CTA's epilogue overlaps another's MMAs
     cudaFuncSetAttribute(k_conv_tc<BN, SWZ, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_conv_tc<BN, SWZ, STAGES>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr_set = true;
   }
   dim3 grid((unsigned)((rows + kBlockM - 1) / kBlockM), (unsigned)(n_total / BN));
@@ -355,19 +356,20 @@ ITTS_API int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, int64_t x
   cudaStream_t st = (cudaStream_t)stream;
   const int swz = (c_in % 64 == 0) ? 128 : (c_in % 32 == 0 ? 64 : 0);
   if (!swz) return ITTS_EUNSUPPORTED;
-  if (bn == 0) bn = n_total % 256 == 0 ? 256 : n_total % 128 == 0 ? 128 : n_total % 64 == 0 ? 64 : 32;
+  // Stage counts keep smem <= ~100 KB so two CTAs share an SM (BN=256 is 1 CTA/SM).
+  if (bn == 0) bn = n_total % 128 == 0 ? 128 : n_total % 64 == 0 ? 64 : 32;
   if (n_total % bn) return ITTS_EINVAL;
   if (swz == 128) {
     switch (bn) {
-      case 256: return launch<256, 128, 4>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
-      case 128: return launch<128, 128, 6>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
-      case 64: return launch<64, 128, 8>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
-      case 32: return launch<32, 128, 8>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
+      case 256: return launch<256, 128, 3>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
+      case 128: return launch<128, 128, 3>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
+      case 64: return launch<64, 128, 4>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
+      case 32: return launch<32, 128, 4>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
     }
   } else {
     switch (bn) {
-      case 64: return launch<64, 64, 8>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
-      case 32: return launch<32, 64, 8>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
+      case 64: return launch<64, 64, 6>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
+      case 32: return launch<32, 64, 6>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
     }
   }
   return ITTS_EUNSUPPORTED;

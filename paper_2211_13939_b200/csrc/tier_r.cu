@@ -16,7 +16,8 @@
 //   K6  k_dec_prepare    bf16 operand mirror of the gathered state rows
 //       k_prenet         2 x (linear + ReLU), dropout off
 //       k_lstm_cell      gates -> (h, c) for the attention / decoder LSTMCell
-//       k_attention      location-sensitive attention: query, location conv,
+//       k_query          attention query q = Wq . att_h (item-tiled)
+//       k_attention      location-sensitive attention: location conv,
 //                        energies, masked softmax, context, W_acc += W
 //       k_proj           mel / gate projection, writes the chunk's frame
 //   K7  k_mel_assemble   [mel_tail; mel] -> zero-haloed bf16 conv_pre input
@@ -54,25 +55,68 @@ __global__ void k_dec_prepare(const float* __restrict__ state, __nv_bfloat16* __
   for (int i = threadIdx.x; i < XB_ROW; i += blockDim.x) x[i] = __float2bfloat16_rn(s[i]);
 }
 
+// Item-tiled small GEMVs: each CTA serves IT items so every weight matrix is
+// read once per IT items instead of once per item (per-SM L2 bandwidth, not
+// FLOPs, bounds these at large pooled batch).
+constexpr int IT = 8;
+
 // W0T [80][256], W1T [256][256] (input-major so threads read coalesced).
 __global__ void __launch_bounds__(256) k_prenet(float* __restrict__ state, __nv_bfloat16* __restrict__ xb,
                                                 const float* __restrict__ W0T, const float* __restrict__ W1T,
-                                                const int64_t* __restrict__ plan, int step) {
-  const int b = blockIdx.x, j = threadIdx.x;
-  if (step >= plan[b * DPLAN + 5]) return;
-  __shared__ float x[NMEL], h1[PRE];
-  float* s = state + (int64_t)b * ROW;
-  if (j < NMEL) x[j] = s[LAST_OFF + j];
+                                                const int64_t* __restrict__ plan, int step, int B) {
+  const int b0 = blockIdx.x * IT, j = threadIdx.x;
+  const int nb = min(IT, B - b0);
+  __shared__ float x[IT][NMEL], h1[IT][PRE];
+  for (int i = j; i < nb * NMEL; i += 256) x[i / NMEL][i % NMEL] = state[(int64_t)(b0 + i / NMEL) * ROW + LAST_OFF + i % NMEL];
   __syncthreads();
-  float a = 0.f;
-  for (int k = 0; k < NMEL; ++k) a = fmaf(W0T[k * PRE + j], x[k], a);
-  h1[j] = fmaxf(a, 0.f);
+  float a[IT];
+#pragma unroll
+  for (int i = 0; i < IT; ++i) a[i] = 0.f;
+  for (int k = 0; k < NMEL; ++k) {
+    const float w = W0T[k * PRE + j];
+#pragma unroll
+    for (int i = 0; i < IT; ++i) a[i] = fmaf(w, x[i][k], a[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < IT; ++i) h1[i][j] = fmaxf(a[i], 0.f);
   __syncthreads();
-  a = 0.f;
-  for (int k = 0; k < PRE; ++k) a = fmaf(W1T[k * PRE + j], h1[k], a);
-  a = fmaxf(a, 0.f);
-  s[P_OFF + j] = a;
-  xb[(int64_t)b * XB_ROW + P_OFF + j] = __float2bfloat16_rn(a);
+#pragma unroll
+  for (int i = 0; i < IT; ++i) a[i] = 0.f;
+  for (int k = 0; k < PRE; ++k) {
+    const float w = W1T[k * PRE + j];
+#pragma unroll
+    for (int i = 0; i < IT; ++i) a[i] = fmaf(w, h1[i][k], a[i]);
+  }
+  for (int i = 0; i < nb; ++i) {
+    const int b = b0 + i;
+    if (step >= plan[b * DPLAN + 5]) continue;
+    const float v = fmaxf(a[i], 0.f);
+    state[(int64_t)b * ROW + P_OFF + j] = v;
+    xb[(int64_t)b * XB_ROW + P_OFF + j] = __float2bfloat16_rn(v);
+  }
+}
+
+// q[b] = Wq . att_h[b] for IT items per CTA; WqT [1024][128].  256 threads:
+// thread = (output a, item half).
+__global__ void __launch_bounds__(256) k_query(const float* __restrict__ state, const float* __restrict__ WqT,
+                                               float* __restrict__ Q, int B) {
+  const int b0 = blockIdx.x * IT, tid = threadIdx.x;
+  const int nb = min(IT, B - b0);
+  extern __shared__ float hs[];  // [IT][1024]
+  for (int i = tid; i < nb * HID; i += 256) hs[i] = state[(int64_t)(b0 + i / HID) * ROW + ATTH_OFF + i % HID];
+  __syncthreads();
+  const int a = tid & (ATT - 1), ih = tid >> 7;  // items ih*4 .. ih*4+3
+  float acc[IT / 2] = {0.f, 0.f, 0.f, 0.f};
+  for (int k = 0; k < HID; ++k) {
+    const float w = WqT[k * ATT + a];
+#pragma unroll
+    for (int i = 0; i < IT / 2; ++i) acc[i] = fmaf(w, hs[(ih * (IT / 2) + i) * HID + k], acc[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < IT / 2; ++i) {
+    const int it = ih * (IT / 2) + i;
+    if (it < nb) Q[(int64_t)(b0 + it) * ATT + a] = acc[i];
+  }
 }
 
 // G [B][4096] gate pre-activations (bias included), PyTorch order i, f, g, o.
@@ -95,7 +139,7 @@ __global__ void __launch_bounds__(256) k_lstm_cell(const float* __restrict__ G, 
 // Dynamic smem: 3*L floats (W_prev, W_acc, energies).
 __global__ void __launch_bounds__(256) k_attention(float* __restrict__ state, __nv_bfloat16* __restrict__ xb,
                                                    const int64_t* __restrict__ plan,
-                                                   const float* __restrict__ WqT, const float* __restrict__ Wloc,
+                                                   const float* __restrict__ Q, const float* __restrict__ Wloc,
                                                    const float* __restrict__ WdT, const float* __restrict__ v,
                                                    int step) {
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -112,26 +156,19 @@ __global__ void __launch_bounds__(256) k_attention(float* __restrict__ state, __
   float* w_prev = dyn;
   float* w_acc = dyn + L;
   float* e = dyn + 2 * L;
-  __shared__ float h[HID], q[ATT], qpart[ATT], sWloc[NF * 2 * KLOC], sWd[NF * ATT], sv[ATT], red[32];
+  __shared__ float q[ATT], sWloc[NF * 2 * KLOC], sWd[NF * ATT], sv[ATT], red[32];
+  __shared__ float4 cpart[8][EMB / 4];
 
   for (int i = tid; i < L; i += 256) {
     w_prev[i] = wsrc[i];
     w_acc[i] = wsrc[L + i];
   }
-  for (int i = tid; i < HID; i += 256) h[i] = s[ATTH_OFF + i];
+  if (tid < ATT) q[tid] = Q[(int64_t)b * ATT + tid];
   for (int i = tid; i < NF * 2 * KLOC; i += 256) sWloc[i] = Wloc[i];
   for (int i = tid; i < NF * ATT; i += 256) sWd[i] = WdT[i];
   if (tid < ATT) sv[tid] = v[tid];
   __syncthreads();
-  {  // query: q = Wq . att_h, two K halves per output
-    const int a = tid & (ATT - 1), half = tid >> 7;
-    float acc = 0.f;
-    for (int k = half * 512; k < half * 512 + 512; ++k) acc = fmaf(WqT[k * ATT + a], h[k], acc);
-    if (half) qpart[a] = acc;
-    __syncthreads();
-    if (!half) q[a] = acc + qpart[a];
-    __syncthreads();
-  }
+
   // energies: one warp per text position; lane = location filter, then 4 attention dims per lane
   for (int t = warp; t < L; t += 8) {
     float conv = 0.f;
@@ -175,42 +212,76 @@ __global__ void __launch_bounds__(256) k_attention(float* __restrict__ state, __
     wdst[L + t] = w_acc[t] + a;
   }
   __syncthreads();
-  float c0 = 0.f, c1 = 0.f;
-  for (int t = 0; t < L; ++t) {
+  // context = sum_t a_t * memory[t]: warp w takes rows t = w (mod 8), lane holds 16 dims as
+  // 4 float4 (coalesced 512 B per row per j), then a cross-warp reduction through smem.
+  float4 acc[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4* mem4 = reinterpret_cast<const float4*>(mem);
+#pragma unroll 2
+  for (int t = warp; t < L; t += 8) {
     const float a = e[t];
-    c0 = fmaf(a, mem[(int64_t)t * EMB + tid], c0);
-    c1 = fmaf(a, mem[(int64_t)t * EMB + 256 + tid], c1);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 m4 = mem4[(int64_t)t * (EMB / 4) + lane + 32 * j];
+      acc[j].x = fmaf(a, m4.x, acc[j].x);
+      acc[j].y = fmaf(a, m4.y, acc[j].y);
+      acc[j].z = fmaf(a, m4.z, acc[j].z);
+      acc[j].w = fmaf(a, m4.w, acc[j].w);
+    }
   }
-  s[CTX_OFF + tid] = c0;
-  s[CTX_OFF + 256 + tid] = c1;
-  xb[(int64_t)b * XB_ROW + CTX_OFF + tid] = __float2bfloat16_rn(c0);
-  xb[(int64_t)b * XB_ROW + CTX_OFF + 256 + tid] = __float2bfloat16_rn(c1);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) cpart[warp][lane + 32 * j] = acc[j];
+  __syncthreads();
+  const float* cp = reinterpret_cast<const float*>(cpart);
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int d = tid + 256 * r;
+    float c = cp[d];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) c += cp[w * EMB + d];
+    s[CTX_OFF + d] = c;
+    xb[(int64_t)b * XB_ROW + CTX_OFF + d] = __float2bfloat16_rn(c);
+  }
 }
 
-// WpT [1536][81] (80 mel rows + gate row), bp [81].  hc = [dec_h, ctx].
+// WpT [1536][81] (80 mel rows + gate row), bp [81].  hc = [dec_h, ctx]; IT items per CTA.
 __global__ void __launch_bounds__(256) k_proj(float* __restrict__ state, const int64_t* __restrict__ plan,
                                               const float* __restrict__ WpT, const float* __restrict__ bp,
-                                              int step) {
-  const int b = blockIdx.x, tid = threadIdx.x;
-  const int64_t* p = plan + b * DPLAN;
-  if (step >= p[5]) return;
-  float* s = state + (int64_t)b * ROW;
-  __shared__ float hc[1536], part[3][81];
-  for (int i = tid; i < HID; i += 256) hc[i] = s[DECH_OFF + i];
-  for (int i = tid; i < EMB; i += 256) hc[HID + i] = s[CTX_OFF + i];
+                                              int step, int B) {
+  const int b0 = blockIdx.x * IT, tid = threadIdx.x;
+  const int nb = min(IT, B - b0);
+  extern __shared__ float hcs[];  // [IT][1536] then part [3][IT][81]
+  float* part = hcs + IT * 1536;
+  for (int i = tid; i < nb * 1536; i += 256) {
+    const int it = i / 1536, k = i % 1536;
+    const float* s = state + (int64_t)(b0 + it) * ROW;
+    hcs[i] = k < HID ? s[DECH_OFF + k] : s[CTX_OFF + k - HID];
+  }
+  for (int i = nb * 1536 + tid; i < IT * 1536; i += 256) hcs[i] = 0.f;
   __syncthreads();
   const int g = tid / 81, n = tid % 81;
   if (g < 3) {
-    float a = 0.f;
-    for (int k = g * 512; k < g * 512 + 512; ++k) a = fmaf(WpT[k * 81 + n], hc[k], a);
-    part[g][n] = a;
+    float a[IT];
+#pragma unroll
+    for (int i = 0; i < IT; ++i) a[i] = 0.f;
+    for (int k = g * 512; k < g * 512 + 512; ++k) {
+      const float w = WpT[k * 81 + n];
+#pragma unroll
+      for (int i = 0; i < IT; ++i) a[i] = fmaf(w, hcs[i * 1536 + k], a[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < IT; ++i) part[(g * IT + i) * 81 + n] = a[i];
   }
   __syncthreads();
-  if (tid < 81) {
-    const float out = bp[tid] + ((part[0][tid] + part[1][tid]) + part[2][tid]);
-    if (tid < NMEL) {
-      s[LAST_OFF + tid] = out;
-      reinterpret_cast<float*>(p[6])[step * NMEL + tid] = out;
+  for (int i = tid; i < nb * 81; i += 256) {
+    const int it = i / 81, o = i % 81, b = b0 + it;
+    const int64_t* p = plan + b * DPLAN;
+    if (step >= p[5]) continue;
+    const float out = bp[o] + ((part[(0 * IT + it) * 81 + o] + part[(1 * IT + it) * 81 + o]) + part[(2 * IT + it) * 81 + o]);
+    if (o < NMEL) {
+      state[(int64_t)b * ROW + LAST_OFF + o] = out;
+      reinterpret_cast<float*>(p[6])[step * NMEL + o] = out;
     } else {
       reinterpret_cast<float*>(p[7])[step] = out;
     }
@@ -422,7 +493,18 @@ ITTS_API int itts_r_dec_prepare(const float* state, void* xb, int32_t B, void* s
 ITTS_API int itts_r_prenet(float* state, void* xb, const float* W0T, const float* W1T, const int64_t* plan,
                            int32_t B, int32_t step, void* stream) {
   if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
-  k_prenet<<<B, 256, 0, (cudaStream_t)stream>>>(state, (__nv_bfloat16*)xb, W0T, W1T, plan, step);
+  k_prenet<<<(B + IT - 1) / IT, 256, 0, (cudaStream_t)stream>>>(state, (__nv_bfloat16*)xb, W0T, W1T, plan, step, B);
+  ITTS_RETURN_LAUNCH();
+}
+
+ITTS_API int itts_r_query(const float* state, const float* WqT, float* Q, int32_t B, void* stream) {
+  if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_query, cudaFuncAttributeMaxDynamicSharedMemorySize, IT * HID * 4);
+    configured = true;
+  }
+  k_query<<<(B + IT - 1) / IT, 256, IT * HID * 4, (cudaStream_t)stream>>>(state, WqT, Q, B);
   ITTS_RETURN_LAUNCH();
 }
 
@@ -435,7 +517,7 @@ ITTS_API int itts_r_lstm_cell(const float* G, float* state, void* xb, int32_t h_
 }
 
 ITTS_API int itts_r_attention(float* state, void* xb, const int64_t* plan, int32_t B, int32_t max_len,
-                              const float* WqT, const float* Wloc, const float* WdT, const float* v,
+                              const float* Q, const float* Wloc, const float* WdT, const float* v,
                               int32_t step, void* stream) {
   if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
   const size_t smem = (size_t)3 * max_len * sizeof(float);
@@ -445,15 +527,20 @@ ITTS_API int itts_r_attention(float* state, void* xb, const int64_t* plan, int32
     cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     configured = true;
   }
-  k_attention<<<B, 256, smem, (cudaStream_t)stream>>>(state, (__nv_bfloat16*)xb, plan, WqT, Wloc, WdT, v,
-                                                      step);
+  k_attention<<<B, 256, smem, (cudaStream_t)stream>>>(state, (__nv_bfloat16*)xb, plan, Q, Wloc, WdT, v, step);
   ITTS_RETURN_LAUNCH();
 }
 
 ITTS_API int itts_r_proj(float* state, const int64_t* plan, int32_t B, const float* WpT, const float* bp,
                          int32_t step, void* stream) {
   if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
-  k_proj<<<B, 256, 0, (cudaStream_t)stream>>>(state, plan, WpT, bp, step);
+  constexpr int smem = (IT * 1536 + 3 * IT * 81) * 4;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_proj, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  k_proj<<<(B + IT - 1) / IT, 256, smem, (cudaStream_t)stream>>>(state, plan, WpT, bp, step, B);
   ITTS_RETURN_LAUNCH();
 }
 

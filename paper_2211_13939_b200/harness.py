@@ -1,0 +1,179 @@
+"""Load harness: traces, a timed serving run, latency records and percentiles.
+
+Mirrors the reference harness (``pkg/src/incrtts/harness.py``): evenly
+spaced traces (``make_trace``, ``:97-118``), client-side FCL / LCL / RTF
+(``LatencyRecord``, ``:121-152``), nearest-rank percentiles (``:267-275``)
+-- and adds what the B200 measurement needs: Poisson
+arrivals, per-request timestamps taken both where the chunk becomes
+visible on the stream (server boundary) and where a client thread
+receives it, and an iteration-indexed timing window so a bench can time
+exactly K scheduler iterations after W warm-up iterations.
+"""
+
+from __future__ import annotations
+
+import math
+import random
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+
+from .frontend import Lexicon, default_lexicon, default_texts
+from .scheduler import CostModel, IterationReport, PipelineModules, SchedulerLoop, _wait_until
+
+
+@dataclass(frozen=True)
+class TimedRequest:
+    send_at: float
+    text: str
+    text_class: str = "random"
+
+
+def make_trace(qps: int, duration_seconds: float, text_class: str = "mixed", seed: int = 0,
+               fixtures: dict | None = None) -> list[TimedRequest]:
+    """Evenly spaced trace, request i at i/qps (reference ``make_trace``)."""
+    fixtures = default_texts() if fixtures is None else fixtures
+    classes = ("short", "medium", "long") if text_class == "mixed" else (text_class,)
+    rng = random.Random(seed)
+    out = []
+    for i in range(int(qps * duration_seconds)):
+        cls = rng.choice(classes) if text_class == "mixed" else text_class
+        texts = fixtures[cls]
+        out.append(TimedRequest(i / qps, texts[i % len(texts)], cls))
+    return out
+
+
+def random_text(rng: random.Random, lo: int, hi: int, lexicon: Lexicon | None = None) -> str:
+    """U{lo..hi} characters drawn from the single-character lexicon entries."""
+    lex = lexicon or default_lexicon()
+    singles = sorted(c for c in lex.phrase_to_pinyin if len(c) == 1)
+    return "".join(rng.choice(singles) for _ in range(rng.randint(lo, hi)))
+
+
+def poisson_trace(qps: float, duration_seconds: float, lo: int = 20, hi: int = 200, seed: int = 0,
+                  lexicon: Lexicon | None = None) -> list[TimedRequest]:
+    """Exponential inter-arrivals at rate ``qps``; lengths U{lo..hi} chars."""
+    rng = random.Random(seed)
+    t, out = 0.0, []
+    while True:
+        t += rng.expovariate(qps)
+        if t >= duration_seconds:
+            return out
+        out.append(TimedRequest(t, random_text(rng, lo, hi, lexicon)))
+
+
+@dataclass
+class RequestTiming:
+    request_id: int
+    text: str
+    send_time: float
+    first_push: float | None = None      # chunk visible on the ChunkStream (server boundary)
+    first_recv: float | None = None      # client thread received it
+    last_recv: float | None = None
+    samples: int = 0
+    chunks: int = 0
+    error: str | None = None
+
+    @property
+    def fcl(self) -> float | None:
+        return None if self.first_push is None else self.first_push - self.send_time
+
+    @property
+    def fcl_client(self) -> float | None:
+        return None if self.first_recv is None else self.first_recv - self.send_time
+
+    @property
+    def lcl(self) -> float | None:
+        return None if self.last_recv is None else self.last_recv - self.send_time
+
+
+def nearest_rank(values, percentile: float) -> float:
+    if not values:
+        raise ValueError("no values")
+    ordered = sorted(values)
+    return ordered[max(1, math.ceil(percentile / 100.0 * len(ordered))) - 1]
+
+
+@dataclass
+class ServeRun:
+    """Result of :func:`serve`: per-request timings plus per-iteration end times."""
+
+    timings: list[RequestTiming]
+    iteration_end: list[float] = field(default_factory=list)
+    reports: list[IterationReport] = field(default_factory=list)
+    window: tuple[float, float] | None = None
+
+
+def serve(modules: PipelineModules, cfg, trace: list[TimedRequest], *, warmup_iters: int = 3,
+          warmup_seconds: float = 0.0, timed_iters: int | None = None, drain_seconds: float = 30.0,
+          on_window=None, max_clients: int = 4096, sample_rate: int = 22050) -> ServeRun:
+    """Plays ``trace`` against a fresh SchedulerLoop and records every request.
+
+    The timed window is iterations ``[w, w + timed_iters)`` where ``w`` is the
+    first iteration index >= ``warmup_iters`` that starts after
+    ``warmup_seconds``.  ``on_window(kind, iteration_index)`` is called from
+    the loop thread at the window's start and end (bench hooks: CUDA events,
+    clock sampling).  Submissions continue until every request sent inside
+    the window has finished (or ``drain_seconds`` passed), so the load seen
+    by the measured requests stays at the trace rate.
+    """
+    run = ServeRun(timings=[])
+    lock = threading.Lock()
+    state = {"start_idx": None, "end_idx": None}
+    origin = time.perf_counter()
+
+    def sink(rep: IterationReport) -> None:
+        now = time.perf_counter()
+        run.iteration_end.append(now)
+        run.reports.append(rep)
+        i = len(run.iteration_end)  # iterations completed so far == index of the next iteration
+        if state["start_idx"] is None and i >= warmup_iters and now - origin >= warmup_seconds:
+            state["start_idx"] = i
+            run.window = (now, None)
+            if on_window:
+                on_window("start", i)
+        elif (state["start_idx"] is not None and state["end_idx"] is None and timed_iters is not None
+              and i >= state["start_idx"] + timed_iters):
+            state["end_idx"] = i
+            run.window = (run.window[0], now)
+            if on_window:
+                on_window("end", i)
+
+    loop = SchedulerLoop(modules, CostModel.zero(), cfg, report_sink=sink)
+
+    def consume(rec: RequestTiming, stream) -> None:
+        try:
+            for chunk in stream:
+                now = time.perf_counter()
+                if rec.first_recv is None:
+                    rec.first_recv = now
+                rec.last_recv = now
+                rec.samples += chunk.sample_count
+                rec.chunks += 1
+        except Exception as exc:  # noqa: BLE001 -- recorded, reported by the caller
+            rec.error = str(exc)
+
+    with loop, ThreadPoolExecutor(max_workers=max_clients, thread_name_prefix="client") as clients:
+        origin = time.perf_counter()
+        for req in trace:
+            _wait_until(origin + req.send_at)
+            now = time.perf_counter()
+            if run.window is not None and run.window[1] is not None:
+                inside = [r for r in run.timings if run.window[0] <= r.send_time < run.window[1]]
+                if all(r.last_recv is not None or r.error for r in inside) or now - run.window[1] > drain_seconds:
+                    break
+            rid, stream = loop.submit(req.text)
+            rec = RequestTiming(rid, req.text, time.perf_counter())
+            push = stream._push
+
+            def timed_push(chunk, _push=push, _rec=rec):
+                if _rec.first_push is None:
+                    _rec.first_push = time.perf_counter()
+                _push(chunk)
+
+            stream._push = timed_push
+            with lock:
+                run.timings.append(rec)
+            clients.submit(consume, rec, stream)
+    return run

@@ -46,6 +46,22 @@ UPS = (8, 8, 2, 2)
 STAGE_C = (256, 128, 64, 32)
 
 
+def _hifigan_macs_per_frame() -> int:
+    """Algorithmic MACs of HiFi-GAN V1 per input mel frame (307,052,544)."""
+    macs, rate, ch = W.N_MEL * W.HG_CH0 * 7, 1, W.HG_CH0
+    for u, k in zip(W.HG_UP_RATES, W.HG_UP_KERNELS):
+        macs += ch * (ch // 2) * k * rate      # transposed conv: every input sample hits k outputs
+        rate, ch = rate * u, ch // 2
+        macs += rate * 6 * ch * ch * sum(W.HG_RES_KERNELS)
+    return macs + rate * ch * 7
+
+
+HIFIGAN_MACS_PER_FRAME = _hifigan_macs_per_frame()
+# Decoder-step weight bytes as stored here (bf16 gate GEMMs, fp32 elsewhere).
+DEC_WEIGHT_BYTES = (4096 * 1792 + 4096 * 2560) * 2 + (80 * 256 + 256 * 256 + 1024 * 128 + 32 * 62 + 32 * 128
+                                                      + 128 + 1536 * 81 + 81) * 4
+
+
 def _h2d(arr: np.ndarray, device) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(arr)).pin_memory().to(device, non_blocking=True)
 
@@ -82,6 +98,33 @@ class TierREngine:
             self.iota = torch.arange(1 << 16, dtype=torch.int32, device=self.device)
         self.stream.synchronize()
         self.launches = 0
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+        self.timers: list | None = None  # set to [] to record (kind, ev0, ev1, units) per module call
+
+    def _mark(self, kind: str, units: float):
+        """Context manager recording CUDA events on the engine stream around a region."""
+        engine = self
+
+        class _M:
+            def __enter__(self):
+                if engine.timers is not None:
+                    self.e0 = torch.cuda.Event(enable_timing=True)
+                    self.e0.record(engine.stream)
+                return self
+
+            def __exit__(self, *exc):
+                if engine.timers is not None and exc[0] is None:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(engine.stream)
+                    engine.timers.append((kind, self.e0, e1, units))
+                return False
+
+        return _M()
+
+    def _up(self, arr: np.ndarray) -> torch.Tensor:
+        self.h2d_bytes += arr.nbytes
+        return _h2d(arr, self.device)
 
     # ------------------------------------------------------------ weights
     def _prepare_weights(self, w: dict) -> None:
@@ -156,7 +199,7 @@ class TierREngine:
         plan = np.stack([layout.base, np.array(layout.rows, np.int64), np.full(n, layout.halo, np.int64),
                          out_first.astype(np.int64), np.full(n, up, np.int64)], 1)
         rm = torch.empty(layout.total, dtype=torch.int32, device=self.device)
-        self._call("itts_r_rowmap", _h2d(plan, self.device).data_ptr(), n,
+        self._call("itts_r_rowmap", self._up(plan).data_ptr(), n,
                    int(max(layout.rows)) + 2 * layout.halo, rm.data_ptr(), self._st())
         return rm
 
@@ -201,7 +244,9 @@ class TierREngine:
                        a.ptr(req.extra["pm_off"]), 0)
         st = self._st()
         with torch.cuda.stream(self.stream):
-            d_tok, d_plan = _h2d(tok, self.device), _h2d(plan, self.device)
+            d_tok, d_plan = self._up(tok), self._up(plan)
+            mark = self._mark("encoder", total)
+            mark.__enter__()
             xa = torch.zeros(lay.total, W.EMB, dtype=torch.bfloat16, device=self.device)
             xb = torch.empty_like(xa)
             self._call("itts_r_enc_embed", d_tok.data_ptr(), total, d_plan.data_ptr(), n, max(lens),
@@ -216,6 +261,7 @@ class TierREngine:
             self._call("itts_r_pmem", d_plan.data_ptr(), n, max(lens), self.WmT.data_ptr(), st)
             for req, buf in reqs:
                 a.tensor[buf.off:buf.off + self.state_size(req.seq_len)].zero_()
+            mark.__exit__(None, None, None)
         fpp = self.cfg.frames_per_phoneme
         return [(DeviceEncodedFeatures(req), DeviceDecoderState(req, buf, 0, fpp * req.seq_len))
                 for req, buf in reqs]
@@ -253,11 +299,17 @@ class TierREngine:
                 plan[i] = (a.ptr(req.extra["mem_off"]), a.ptr(req.extra["pm_off"]), req.seq_len,
                            src[i] + 4 * ROW, dstp[i] + 4 * ROW, steps[i],
                            mel.data_ptr() + 4 * W.N_MEL * int(mel_off[i]), gate.data_ptr() + 4 * int(mel_off[i]))
-            packed = _h2d(np.concatenate([plan.reshape(-1), src, dstp]), self.device)
+            packed = self._up(np.concatenate([plan.reshape(-1), src, dstp]))
             d_plan, d_src, d_dst = packed[:8 * n], packed[8 * n:9 * n], packed[9 * n:]
             work = torch.empty(n, ROW, dtype=torch.float32, device=self.device)
             xbm = torch.empty(n, XB_ROW, dtype=torch.bfloat16, device=self.device)
             G = torch.empty(n, 4096, dtype=torch.float32, device=self.device)
+            Q = torch.empty(n, 128, dtype=torch.float32, device=self.device)
+            dec_bytes = max(steps) * DEC_WEIGHT_BYTES + sum(
+                k * (2 * 4 * ROW + s.req.seq_len * (4 * 512 + 4 * 128 + 16) + 4 * 81)
+                for k, (s, _) in zip(steps, pairs))
+            mark = self._mark("decoder", dec_bytes)
+            mark.__enter__()
             self._call("itts_gather_rows", work.data_ptr(), d_src.data_ptr(), n, 4 * ROW, st)
             self._call("itts_r_dec_prepare", work.data_ptr(), xbm.data_ptr(), n, st)
             rows = self._iota(n)
@@ -268,8 +320,9 @@ class TierREngine:
                 self._conv(x_att, self.att_gemm, 4096, rows, resid_out=G, bn=64)
                 self._call("itts_r_lstm_cell", G.data_ptr(), work.data_ptr(), xbm.data_ptr(), ATTH_OFF,
                            ATTC_OFF, d_plan.data_ptr(), n, step, st)
+                self._call("itts_r_query", work.data_ptr(), self.WqT.data_ptr(), Q.data_ptr(), n, st)
                 self._call("itts_r_attention", work.data_ptr(), xbm.data_ptr(), d_plan.data_ptr(), n, max_L,
-                           self.WqT.data_ptr(), self.Wloc.data_ptr(), self.WdT.data_ptr(), self.v.data_ptr(),
+                           Q.data_ptr(), self.Wloc.data_ptr(), self.WdT.data_ptr(), self.v.data_ptr(),
                            step, st)
                 self._conv(x_dec, self.dec_gemm, 4096, rows, resid_out=G, bn=64)
                 self._call("itts_r_lstm_cell", G.data_ptr(), work.data_ptr(), xbm.data_ptr(), DECH_OFF,
@@ -277,6 +330,7 @@ class TierREngine:
                 self._call("itts_r_proj", work.data_ptr(), d_plan.data_ptr(), n, self.WpT.data_ptr(),
                            self.bp.data_ptr(), step, st)
             self._call("itts_scatter_rows", d_dst.data_ptr(), work.data_ptr(), n, 4 * ROW, st)
+            mark.__exit__(None, None, None)
         out = []
         for i, ((state, enc), dst) in enumerate(zip(pairs, dsts)):
             emitted = state.frames_emitted + steps[i]
@@ -319,7 +373,7 @@ class TierREngine:
         keep, taken, results = [], set(), []
         with torch.cuda.stream(self.stream):
             if host_mels:
-                hm = _h2d(np.concatenate([f.reshape(-1) for f in host_mels]), dev)
+                hm = self._up(np.concatenate([f.reshape(-1) for f in host_mels]))
             hpos = 0
             lay0 = _Layout(Ts, MEL_HALO)
             mplan = np.zeros((n, 5), dtype=np.int64)
@@ -338,8 +392,8 @@ class TierREngine:
                     if isinstance(vstate, DeviceVocoderState):
                         tail_ptr = a.ptr(vstate.buf.off)
                     else:
-                        t = _h2d(np.concatenate([np.asarray(vstate.mel_tail, np.float32).reshape(-1),
-                                                 np.asarray(vstate.held_tail, np.float32).reshape(-1)]), dev)
+                        t = self._up(np.concatenate([np.asarray(vstate.mel_tail, np.float32).reshape(-1),
+                                                     np.asarray(vstate.held_tail, np.float32).reshape(-1)]))
                         keep.append(t)
                         tail_ptr = t.data_ptr()
                 mplan[i] = (tail_ptr, mel_ptr, m, O if has_tail else 0, lay0.first[i])
@@ -347,15 +401,17 @@ class TierREngine:
                             tail_ptr + 4 * O * W.N_MEL if has_tail else 0,
                             0 if dst is None else a.ptr(dst.off), out_off[i], mel_ptr, m)
                 results.append((req, dst, int(vstate.emitted_samples)))
-            d_mplan = _h2d(mplan, dev)
-            d_pplan = _h2d(pplan, dev)
+            d_mplan = self._up(mplan)
+            d_pplan = self._up(pplan)
             audio = torch.empty(max(int(out_off[-1]), 1), dtype=torch.float32, device=dev)
-            x4 = self._hifigan(Ts, lay0, d_mplan)
+            with self._mark("vocoder", 2.0 * HIFIGAN_MACS_PER_FRAME * sum(Ts)):
+                x4 = self._hifigan(Ts, lay0, d_mplan)
             self._call("itts_r_post_splice", x4.data_ptr(), d_pplan.data_ptr(), n, max(mt[4] for mt in metas),
                        self.wpost.data_ptr(), self.bpost, self.fade.data_ptr(), O, S, audio.data_ptr(), st)
             host = torch.empty(audio.numel(), dtype=torch.float32, pin_memory=True)
             host.copy_(audio, non_blocking=True)
         self.stream.synchronize()
+        self.d2h_bytes += 4 * int(out_off[-1])
         flat = host.numpy()
         if not np.isfinite(flat[:out_off[-1]]).all():
             raise ValueError("array contains non-finite values")
@@ -390,7 +446,7 @@ class TierREngine:
             rmT = self._rowmap(prev, lay.first, u)
             self._conv(act_in, self.ups[s], C, rmT, resid_out=X, act_out=XA, slope=0.1, zero_halo=False)
             zplan = np.stack([lay.base, np.array(lay.rows, np.int64), np.full(n, lay.halo, np.int64)], 1)
-            self._call("itts_r_zero_halo", _h2d(zplan, dev).data_ptr(), n, lay.halo, XA.data_ptr(), C, st)
+            self._call("itts_r_zero_halo", self._up(zplan).data_ptr(), n, lay.halo, XA.data_ptr(), C, st)
             rm = self._rowmap(lay, lay.first, 1)
             slope_out = 0.1 if s < 3 else 0.01
             for j, layers in enumerate(self.res[s]):
