@@ -187,6 +187,8 @@ def run_ours(args) -> None:
     torch.cuda.set_device(local)
     cfg, lex = PipelineConfig(), default_lexicon()
     engine = build_engine(cfg, args.tier, device)
+    if hasattr(engine, "prepare_graphs"):
+        engine.prepare_graphs(max_batch=512)
     mods = modules_for(engine, lex)
 
     # untimed warm-up of every code path (tensor maps, smem attributes, allocator pools)

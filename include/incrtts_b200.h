@@ -78,25 +78,28 @@ int itts_s_vocode_chunk(const int64_t* plan, int32_t n_items, int32_t dim, int32
 
 /* ---- Tier R: Tacotron2 + HiFi-GAN V1 ---------------------------------- */
 
-/* K7 core: one 1-D convolution layer as a tcgen05 implicit GEMM (bf16
- * operands, fp32 TMEM accumulation).  Replaces the per-layer work of the
- * vocoder G inside vocode_chunk (vocoder.py:107/:124 `generate`; HiFi-GAN
- * V1 conv_pre / ConvTranspose / MRF convs).
- *   x      bf16 [rows][c_in] channels-last, items packed with zero halos
+/* K7 core: one 1-D convolution layer as a persistent tcgen05 implicit GEMM
+ * (bf16 operands, fp32 TMEM accumulation, TMA-fed).  Replaces the per-layer
+ * work of the vocoder G inside vocode_chunk (vocoder.py:107/:124 `generate`;
+ * HiFi-GAN V1 conv_pre / ConvTranspose / MRF convs) and
+ * serves as the tensor-core GEMM of the encoder and the decoder gates.
+ *   x      bf16 [rows][c_in] channels-last (row stride x_ld >= c_in), items
+ *          packed with zero halos
  *   w      bf16 [n_taps][n_total][c_in]; host_tap_off[n_taps] row offsets
  *   out    n_total = phases * c_out columns; row_out[r] = output row of input
  *          row r (phase p goes to row_out[r] + p), -1 for halo rows
- *   epilogue: v = acc + bias; (+resid_in); -> resid_out; acc_mode 1 store,
- *          2 add, 3 finalize v = (acc + v) / 3; act_out = bf16(lrelu(v, slope));
- *          zero_halo writes zeros to act_out halo rows.
- * c_in must be a multiple of 32, c_out a multiple of 32; x rows are x_ld
- * elements apart (x_ld >= c_in, so a GEMM operand can be a column slice);
- * bn = N tile (32/64/128/256) or 0 for automatic. */
+ *   epilogue: v = acc + bias (+ inv_lrelu(res_in, res_slope));
+ *          f32_out = v (raw fp32; with ksplit > 1 each K slice z writes its
+ *          partial at f32_out + z*rows*c_out and only slice 0 adds the bias);
+ *          acc_mode 1 store / 2 add / 3 finalize v = (acc + v) / 3 on the bf16
+ *          MRF accumulator; act_out = bf16(lrelu(v, slope)); zero_halo writes
+ *          zeros into act_out halo rows.
+ * c_in and c_out must be multiples of 32; bn = N tile (32/64/128/256) or 0. */
 int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, const void* w,
                    int32_t n_total, int32_t n_taps, const int32_t* host_tap_off, const float* bias,
-                   int32_t c_out, const int32_t* row_out, const float* resid_in, float* resid_out,
-                   float* acc, int32_t acc_mode, void* act_out, float slope, int32_t zero_halo,
-                   int32_t bn, void* stream);
+                   int32_t c_out, const int32_t* row_out, const void* res_in, float res_slope,
+                   float* f32_out, int32_t ksplit, void* acc, int32_t acc_mode, void* act_out,
+                   float slope, int32_t zero_halo, int32_t bn, void* stream);
 
 /* K6 decoder-step chain (replaces decode_chunk_batch, acoustic.py:234-238,
  * with the Tacotron2 decoder, paper Eq. 2).  `state` = fp32 [B][4944] rows
@@ -108,9 +111,10 @@ int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, cons
  * The gate GEMMs between these calls are itts_conv1d_tc with one tap. */
 int itts_r_dec_prepare(const float* state, void* xb, int32_t B, void* stream);
 int itts_r_prenet(float* state, void* xb, const float* W0T, const float* W1T, const int64_t* plan,
-                  int32_t B, int32_t step, void* stream);
-int itts_r_lstm_cell(const float* gates, float* state, void* xb, int32_t h_off, int32_t c_off,
-                     const int64_t* plan, int32_t B, int32_t step, void* stream);
+                  float* H1, int32_t B, int32_t step, void* stream);
+int itts_r_lstm_cell(const float* gates, int32_t nsplit, const float* bias, float* state, void* xb,
+                     int32_t h_off, int32_t c_off, const int64_t* plan, int32_t B, int32_t step,
+                     void* stream);
 int itts_r_query(const float* state, const float* WqT, float* Q, int32_t B, void* stream);
 int itts_r_attention(float* state, void* xb, const int64_t* plan, int32_t B, int32_t max_len,
                      const float* Q, const float* Wloc, const float* WdT, const float* v, int32_t step,

@@ -28,11 +28,11 @@ SIGNATURES: dict[str, list] = {
     "itts_s_encode": [_p, _i64, _p, _i32, _i64, _i32, _p, _p],
     "itts_s_decode_chunk": [_p, _i32, _i32, _f64, _p],
     "itts_s_vocode_chunk": [_p, _i32, _i32, _i32, _i32, _i64, _p, _p, _p],
-    "itts_conv1d_tc": [_p, _i64, _i32, _i64, _p, _i32, _i32, _p, _p, _i32, _p, _p, _p, _p, _i32, _p,
-                       ctypes.c_float, _i32, _i32, _p],
+    "itts_conv1d_tc": [_p, _i64, _i32, _i64, _p, _i32, _i32, _p, _p, _i32, _p, _p, ctypes.c_float, _p, _i32,
+                       _p, _i32, _p, ctypes.c_float, _i32, _i32, _p],
     "itts_r_dec_prepare": [_p, _p, _i32, _p],
-    "itts_r_prenet": [_p, _p, _p, _p, _p, _i32, _i32, _p],
-    "itts_r_lstm_cell": [_p, _p, _p, _i32, _i32, _p, _i32, _i32, _p],
+    "itts_r_prenet": [_p, _p, _p, _p, _p, _p, _i32, _i32, _p],
+    "itts_r_lstm_cell": [_p, _i32, _p, _p, _p, _i32, _i32, _p, _i32, _i32, _p],
     "itts_r_query": [_p, _p, _p, _i32, _p],
     "itts_r_attention": [_p, _p, _p, _i32, _i32, _p, _p, _p, _p, _i32, _p],
     "itts_r_proj": [_p, _p, _i32, _p, _p, _i32, _p],

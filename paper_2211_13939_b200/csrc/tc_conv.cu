@@ -11,15 +11,19 @@
 //         columns (see hifigan.py: the transpose conv is a 3-tap conv whose
 //         output row q of width u*C_out is u consecutive output rows).
 //
-// CTA tile 128 x BN, fp32 accumulator in TMEM; K loop over (tap, 64- or 32-
-// channel chunk).  Warp roles (192 threads, 1 CTA/SM):
-//   warp 0   TMA producer (one elected lane): A box {KT,128} at row m0+off_j,
-//            B box {KT,BN}; STAGES-deep smem ring, mbarrier full/empty.
+// Persistent kernel, one CTA per SM, static round-robin over output tiles
+// 128 x BN (x K-split).  fp32 accumulators in TMEM, double-buffered (2 x BN
+// columns) so the epilogue of tile i overlaps the MMAs of tile i+1 and the
+// TMA ring runs ahead across tile boundaries.  Warp roles (192 threads):
+//   warp 0   TMA producer (one lane): A box {KT,128} at row m0+off_j, B box
+//            {KT,BN}; STAGES-deep smem ring (mbarrier full/empty).
 //   warp 1   TMEM allocator + MMA issuer (one lane): KT/16 x
-//            tcgen05.mma.cta_group::1.kind::f16 per stage, tcgen05.commit
-//            frees the stage; a final commit signals the epilogue.
-//   warps 2-5 epilogue: tcgen05.ld 32x32b.x32 -> +bias -> residual / MRF
-//            accumulate / leaky-ReLU -> global (fp32 and bf16 outputs).
+//            tcgen05.mma.cta_group::1.kind::f16 per stage; tcgen05.commit frees
+//            the stage / publishes the accumulator (tmem_full[b]).
+//   warps 2-5 epilogue: tcgen05.ld 32x32b.x32 -> +bias -> residual (bf16,
+//            stored as lrelu(y) and inverted on load) / MRF accumulate (bf16) /
+//            leaky-ReLU -> bf16 act, or raw fp32 (GEMM outputs, K-split
+//            partials); then tmem_empty[b].
 //
 // Used by the HiFi-GAN V1 chunk vocoder (MRF resblock convs, the transposed
 // upsampling convs, conv_pre) and the Tacotron2 encoder conv stack.
@@ -41,16 +45,18 @@ struct Taps {
 };
 
 struct Epi {
-  const float* bias;          // [C_out]
-  const int32_t* row_out;     // [rows_pad]: output row for input row r, or -1 (halo)
-  const float* resid_in;      // fp32 [out_rows][C_out] or null
-  float* resid_out;           // fp32 [out_rows][C_out] or null
-  float* acc;                 // fp32 [out_rows][C_out] or null
-  __nv_bfloat16* act_out;     // bf16 [out_rows][C_out] or null
-  int64_t rows;               // input rows R (tiles beyond are skipped)
+  const float* bias;          // [C_out] (added by split 0 only)
+  const int32_t* row_out;     // [rows]: output row for input row r (phase p -> +p), -1 = halo
+  const __nv_bfloat16* res_in;  // bf16 [out_rows][C_out] residual y stored as lrelu(y, res_slope), or null
+  float res_slope;            // inverse leaky-ReLU applied to res_in (1.0 = stored raw)
+  float* f32_out;             // fp32 [out_rows][C_out] raw output (per K-split slice), or null
+  int64_t f32_split_stride;   // elements between K-split slices of f32_out
+  __nv_bfloat16* acc;         // bf16 MRF accumulator [out_rows][C_out] (raw), or null
+  __nv_bfloat16* act_out;     // bf16 [out_rows][C_out] = lrelu(y, slope), or null
+  int64_t rows;               // input rows R
   int c_out;                  // output row width; N = phases * c_out
   int acc_mode;               // 0 none, 1 store, 2 add, 3 finalize: y = (acc + y) / 3
-  float slope;                // leaky-ReLU slope for act_out (1.0 = identity)
+  float slope;                // leaky-ReLU slope for act_out (1.0 = identity, 0.0 = ReLU)
   int zero_halo;              // write zeros into act_out for halo rows (CONV mode only)
 };
 
@@ -132,14 +138,59 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 
 __device__ __forceinline__ float lrelu(float x, float s) { return x >= 0.f ? x : x * s; }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ float inv_lrelu(float a, float s) { return a >= 0.f ? a : a / s; }
+
+__device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* p, float (&v)[32]) {
+  const uint4* src = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 u = src[q];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+      v[8 * q + 2 * e] = f.x;
+      v[8 * q + 2 * e + 1] = f.y;
+    }
+  }
+}
+
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* p, const float (&v)[32], float slope) {
+  uint4* dst = reinterpret_cast<uint4*>(p);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      __nv_bfloat162 b2 = __floats2bfloat162_rn(lrelu(v[8 * q + 2 * e], slope), lrelu(v[8 * q + 2 * e + 1], slope));
+      w[e] = *reinterpret_cast<uint32_t*>(&b2);
+    }
+    dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+struct TileSched {
+  int n_tiles, ksplit, iters_per_split;
+  __device__ __forceinline__ void decode(int t, int& mt, int& nt, int& z) const {
+    z = t % ksplit;
+    const int mn = t / ksplit;
+    nt = mn % n_tiles;
+    mt = mn / n_tiles;
+  }
+};
+
 template <int BN, int SWZ, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, Taps taps,
-              int kchunks, int n_total, Epi epi) {
+              int kchunks, int n_total, int num_tiles, TileSched sched, Epi epi) {
   constexpr int KT = SWZ / 2;                   // bf16 channels per smem row
   constexpr uint32_t A_BYTES = kBlockM * SWZ;
   constexpr uint32_t B_BYTES = BN * SWZ;
-  constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -147,20 +198,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sB = smem + STAGES * A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* tfull = empty + STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * kBlockM;
-  const int n0 = blockIdx.y * BN;
-  const int iters = taps.n * kchunks;
+  const int iters = sched.iters_per_split;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
@@ -177,104 +230,109 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int it = 0; it < iters; ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        const int j = it / kchunks, kc = it - j * kchunks;
-        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-        tma_load_2d(sA + s * A_BYTES, &mapA, &full[s], kc * KT, m0 + taps.off[j]);
-        tma_load_2d(sB + s * B_BYTES, &mapB, &full[s], kc * KT, j * n_total + n0);
+      uint32_t g = 0;  // running stage counter across tiles
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mt, nt, z;
+        sched.decode(t, mt, nt, z);
+        const int m0 = mt * kBlockM, n0 = nt * BN;
+        for (int it = z * iters; it < (z + 1) * iters; ++it, ++g) {
+          const uint32_t s = g % STAGES, ph = (g / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          const int j = it / kchunks, kc = it - j * kchunks;
+          mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+          tma_load_2d(sA + s * A_BYTES, &mapA, &full[s], kc * KT, m0 + taps.off[j]);
+          tma_load_2d(sB + s * B_BYTES, &mapB, &full[s], kc * KT, j * n_total + n0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = make_idesc<BN>();
-      for (int it = 0; it < iters; ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      uint32_t g = 0, lt = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+        const uint32_t b = lt & 1, tph = (lt >> 1) & 1;
+        mbar_wait(&tempty[b], tph ^ 1);  // epilogue drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t da = make_desc<SWZ>(smem_u32(sA + s * A_BYTES));
-        const uint64_t db = make_desc<SWZ>(smem_u32(sB + s * B_BYTES));
+        const uint32_t d = tmem + b * BN;
+        for (int it = 0; it < iters; ++it, ++g) {
+          const uint32_t s = g % STAGES, ph = (g / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = make_desc<SWZ>(smem_u32(sA + s * A_BYTES));
+          const uint64_t db = make_desc<SWZ>(smem_u32(sB + s * B_BYTES));
 #pragma unroll
-        for (int kk = 0; kk < KT / 16; ++kk)  // +32 bytes per K=16 step inside the swizzle row
-          umma_bf16(tmem, da + 2 * kk, db + 2 * kk, idesc, (it | kk) != 0);
-        umma_commit(&empty[s]);
+          for (int kk = 0; kk < KT / 16; ++kk)  // +32 bytes per K=16 step inside the swizzle row
+            umma_bf16(d, da + 2 * kk, db + 2 * kk, idesc, (it | kk) != 0);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[b]);
       }
-      umma_commit(done);
     }
   } else {
     // Epilogue: warp w owns TMEM lanes [32*(w%4), +32) = tile rows.
     const int quarter = warp & 3;
-    const int64_t r = (int64_t)m0 + quarter * 32 + lane;
-    mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const bool in_range = r < epi.rows;
-    const int out_row = in_range ? epi.row_out[r] : -1;
     const int C = epi.c_out;
+    uint32_t lt = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+      int mt, nt, z;
+      sched.decode(t, mt, nt, z);
+      const uint32_t b = lt & 1, tph = (lt >> 1) & 1;
+      const int64_t r = (int64_t)mt * kBlockM + quarter * 32 + lane;
+      const bool in_range = r < epi.rows;
+      const int out_row = in_range ? __ldg(epi.row_out + r) : -1;
+      mbar_wait(&tfull[b], tph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + c0, v);
-      if (!in_range) continue;
-      const int n = n0 + c0;        // first global column of this 32-chunk
-      const int phase = n / C, co = n - phase * C;
-      if (out_row < 0) {
-        if (epi.zero_halo && epi.act_out) {
-          uint4* dst = reinterpret_cast<uint4*>(epi.act_out + (int64_t)r * C + co);
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + b * BN + ((uint32_t)(quarter * 32) << 16) + c0, v);
+        if (!in_range) continue;
+        const int n = nt * BN + c0;   // first global column of this 32-chunk
+        const int phase = n / C, co = n - phase * C;
+        if (out_row < 0) {
+          if (epi.zero_halo && epi.act_out) {
+            uint4* dst = reinterpret_cast<uint4*>(epi.act_out + r * C + co);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) dst[q] = make_uint4(0, 0, 0, 0);
+            for (int q = 0; q < 4; ++q) dst[q] = make_uint4(0, 0, 0, 0);
+          }
+          continue;
         }
-        continue;
-      }
-      const int64_t o = ((int64_t)out_row + phase) * C + co;
+        const int64_t o = ((int64_t)out_row + phase) * C + co;
+        if (z == 0) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] += __ldg(epi.bias + co + i);
-      if (epi.resid_in) {
-        const float4* src = reinterpret_cast<const float4*>(epi.resid_in + o);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 t = src[q];
-          v[4 * q] += t.x; v[4 * q + 1] += t.y; v[4 * q + 2] += t.z; v[4 * q + 3] += t.w;
+          for (int i = 0; i < 32; ++i) v[i] += __ldg(epi.bias + co + i);
         }
-      }
-      if (epi.resid_out) {
-        float4* dst = reinterpret_cast<float4*>(epi.resid_out + o);
+        if (epi.f32_out) {
+          float4* dst = reinterpret_cast<float4*>(epi.f32_out + z * epi.f32_split_stride + o);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-      }
-      if (epi.acc_mode) {
-        float4* a = reinterpret_cast<float4*>(epi.acc + o);
+          for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+        if (epi.res_in) {
+          float y[32];
+          load_bf16x32(epi.res_in + o, y);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+          for (int i = 0; i < 32; ++i) v[i] += inv_lrelu(y[i], epi.res_slope);
+        }
+        if (epi.acc_mode) {
           if (epi.acc_mode == 1) {
-            a[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            store_bf16x32(epi.acc + o, v, 1.0f);
           } else {
-            const float4 t = a[q];
-            float4 s = make_float4(t.x + v[4 * q], t.y + v[4 * q + 1], t.z + v[4 * q + 2], t.w + v[4 * q + 3]);
+            float a[32];
+            load_bf16x32(epi.acc + o, a);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) a[i] += v[i];
             if (epi.acc_mode == 2) {
-              a[q] = s;
+              store_bf16x32(epi.acc + o, a, 1.0f);
             } else {  // finalize: x = (rb0 + rb1 + rb2) / 3
-              v[4 * q] = s.x / 3.0f; v[4 * q + 1] = s.y / 3.0f; v[4 * q + 2] = s.z / 3.0f; v[4 * q + 3] = s.w / 3.0f;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = a[i] / 3.0f;
             }
           }
         }
+        if (epi.act_out) store_bf16x32(epi.act_out + o, v, epi.slope);
       }
-      if (epi.act_out) {
-        uint4* dst = reinterpret_cast<uint4*>(epi.act_out + o);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint32_t p[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(lrelu(v[8 * q + 2 * e], epi.slope),
-                                                      lrelu(v[8 * q + 2 * e + 1], epi.slope));
-            p[e] = *reinterpret_cast<uint32_t*>(&b2);
-          }
-          dst[q] = make_uint4(p[0], p[1], p[2], p[3]);
-        }
-      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&tempty[b]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -317,23 +375,39 @@ bool encode_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t oute
   return r == CUDA_SUCCESS;
 }
 
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 template <int BN, int SWZ, int STAGES>
 int launch(const void* x, int64_t rows, int c_in, int64_t x_ld, const void* w, int n_total, const Taps& taps,
-           const Epi& epi, cudaStream_t st) {
+           int ksplit, const Epi& epi, cudaStream_t st) {
   constexpr int KT = SWZ / 2;
   CUtensorMap ma, mb;
   if (!encode_2d(&ma, x, (uint64_t)c_in, (uint64_t)rows, (uint64_t)x_ld, KT, kBlockM, SWZ)) return ITTS_EINVAL;
   if (!encode_2d(&mb, w, (uint64_t)c_in, (uint64_t)taps.n * n_total, (uint64_t)c_in, KT, BN, SWZ))
     return ITTS_EINVAL;
-  const size_t smem = 1024 + STAGES * (kBlockM + BN) * SWZ + (2 * STAGES + 1) * 8 + 16;
+  const int kchunks = c_in / KT;
+  const int total_iters = taps.n * kchunks;
+  if (ksplit < 1 || total_iters % ksplit) return ITTS_EINVAL;
+  const size_t smem = 1024 + STAGES * (kBlockM + BN) * SWZ + (2 * STAGES + 4) * 8 + 16;
   static bool attr_set = false;
-  if (!attr_set) {  // max carveout so 2-3 CTAs co-reside and one CTA's epilogue overlaps another's MMAs
+  if (!attr_set) {
     cudaFuncSetAttribute(k_conv_tc<BN, SWZ, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_conv_tc<BN, SWZ, STAGES>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr_set = true;
   }
-  dim3 grid((unsigned)((rows + kBlockM - 1) / kBlockM), (unsigned)(n_total / BN));
-  k_conv_tc<BN, SWZ, STAGES><<<grid, kThreads, smem, st>>>(ma, mb, taps, c_in / KT, n_total, epi);
+  TileSched sched{n_total / BN, ksplit, total_iters / ksplit};
+  const int m_tiles = (int)((rows + kBlockM - 1) / kBlockM);
+  const int tiles = m_tiles * sched.n_tiles * ksplit;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  k_conv_tc<BN, SWZ, STAGES><<<grid, kThreads, smem, st>>>(ma, mb, taps, kchunks, n_total, tiles, sched, epi);
   ITTS_RETURN_LAUNCH();
 }
 
@@ -341,35 +415,37 @@ int launch(const void* x, int64_t rows, int c_in, int64_t x_ld, const void* w, i
 
 ITTS_API int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, const void* w,
                             int32_t n_total, int32_t n_taps, const int32_t* host_tap_off, const float* bias,
-                            int32_t c_out, const int32_t* row_out, const float* resid_in, float* resid_out,
-                            float* acc, int32_t acc_mode, void* act_out, float slope, int32_t zero_halo,
-                            int32_t bn, void* stream) {
+                            int32_t c_out, const int32_t* row_out, const void* res_in, float res_slope,
+                            float* f32_out, int32_t ksplit, void* acc, int32_t acc_mode, void* act_out,
+                            float slope, int32_t zero_halo, int32_t bn, void* stream) {
   if (!x || !w || !bias || !row_out || !host_tap_off || rows <= 0) return ITTS_EINVAL;
   if (n_taps < 1 || n_taps > kMaxTaps || c_out <= 0 || n_total % c_out) return ITTS_EINVAL;
   if (c_out % 32 || (acc_mode && !acc) || acc_mode < 0 || acc_mode > 3) return ITTS_EINVAL;
-  if (x_ld < c_in || (x_ld * 2) % 16) return ITTS_EINVAL;
+  if (x_ld < c_in || (x_ld * 2) % 16 || res_slope <= 0.f) return ITTS_EINVAL;
+  if (ksplit > 1 && (!f32_out || res_in || acc_mode || act_out)) return ITTS_EINVAL;  // partials are raw fp32
   if (((uintptr_t)x | (uintptr_t)w) & 15) return ITTS_EALIGN;
   Taps taps{};
   taps.n = n_taps;
   for (int i = 0; i < n_taps; ++i) taps.off[i] = host_tap_off[i];
-  Epi epi{bias, row_out, resid_in, resid_out, acc, (__nv_bfloat16*)act_out, rows, c_out, acc_mode, slope, zero_halo};
+  Epi epi{bias, row_out, (const __nv_bfloat16*)res_in, res_slope, f32_out, rows * (int64_t)c_out,
+          (__nv_bfloat16*)acc, (__nv_bfloat16*)act_out, rows, c_out, acc_mode, slope, zero_halo};
+  if (ksplit < 1) ksplit = 1;
   cudaStream_t st = (cudaStream_t)stream;
   const int swz = (c_in % 64 == 0) ? 128 : (c_in % 32 == 0 ? 64 : 0);
   if (!swz) return ITTS_EUNSUPPORTED;
-  // Stage counts keep smem <= ~100 KB so two CTAs share an SM (BN=256 is 1 CTA/SM).
   if (bn == 0) bn = n_total % 128 == 0 ? 128 : n_total % 64 == 0 ? 64 : 32;
   if (n_total % bn) return ITTS_EINVAL;
   if (swz == 128) {
     switch (bn) {
-      case 256: return launch<256, 128, 3>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
-      case 128: return launch<128, 128, 3>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
-      case 64: return launch<64, 128, 4>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
-      case 32: return launch<32, 128, 4>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
+      case 256: return launch<256, 128, 4>(x, rows, c_in, x_ld, w, n_total, taps, ksplit, epi, st);
+      case 128: return launch<128, 128, 6>(x, rows, c_in, x_ld, w, n_total, taps, ksplit, epi, st);
+      case 64: return launch<64, 128, 8>(x, rows, c_in, x_ld, w, n_total, taps, ksplit, epi, st);
+      case 32: return launch<32, 128, 8>(x, rows, c_in, x_ld, w, n_total, taps, ksplit, epi, st);
     }
   } else {
     switch (bn) {
-      case 64: return launch<64, 64, 6>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
-      case 32: return launch<32, 64, 6>(x, rows, c_in, x_ld, w, n_total, taps, epi, st);
+      case 64: return launch<64, 64, 8>(x, rows, c_in, x_ld, w, n_total, taps, ksplit, epi, st);
+      case 32: return launch<32, 64, 8>(x, rows, c_in, x_ld, w, n_total, taps, ksplit, epi, st);
     }
   }
   return ITTS_EUNSUPPORTED;

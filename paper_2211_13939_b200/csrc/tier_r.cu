@@ -55,93 +55,145 @@ __global__ void k_dec_prepare(const float* __restrict__ state, __nv_bfloat16* __
   for (int i = threadIdx.x; i < XB_ROW; i += blockDim.x) x[i] = __float2bfloat16_rn(s[i]);
 }
 
-// Item-tiled small GEMVs: each CTA serves IT items so every weight matrix is
-// read once per IT items instead of once per item (per-SM L2 bandwidth, not
-// FLOPs, bounds these at large pooled batch).
+// Small batched GEMVs (prenet, attention query, mel/gate projection):
+// Y[b][n] = sum_k X[b][k] W^T[k][n].  A CTA serves IT items (weights read
+// once per IT items) with its 8 warps splitting K (each warp streams a
+// contiguous K slice, lanes cover N with NPL outputs each, several weight
+// loads in flight per iteration); partials are reduced across warps in a
+// fixed order, so results do not depend on the batch composition.
 constexpr int IT = 8;
+constexpr int GW = 8;  // warps per CTA
 
-// W0T [80][256], W1T [256][256] (input-major so threads read coalesced).
-__global__ void __launch_bounds__(256) k_prenet(float* __restrict__ state, __nv_bfloat16* __restrict__ xb,
-                                                const float* __restrict__ W0T, const float* __restrict__ W1T,
-                                                const int64_t* __restrict__ plan, int step, int B) {
-  const int b0 = blockIdx.x * IT, j = threadIdx.x;
+struct GemvIO {
+  const float* x;   // rows of the input, x_ld floats apart
+  int x_ld, off0, len0, off1, len1;  // up to two input segments (K = len0 + len1)
+  const float* wT;  // [K][N]
+  int N;
+  // epilogue targets
+  float* y; int y_ld, y_off;          // fp32 output rows (may alias the state rows)
+  __nv_bfloat16* yb; int yb_ld;       // optional bf16 mirror (same column offset)
+  const float* bias;                  // optional
+  int relu;
+  const int64_t* plan; int step;      // proj mode: plan rows + step (mel / gate outputs)
+};
+
+template <int NPL, int MODE>  // MODE 0 generic, 1 mel/gate projection
+__global__ void __launch_bounds__(GW * 32) k_gemv(GemvIO io, int B) {
+  const int b0 = blockIdx.x * IT, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nb = min(IT, B - b0);
-  __shared__ float x[IT][NMEL], h1[IT][PRE];
-  for (int i = j; i < nb * NMEL; i += 256) x[i / NMEL][i % NMEL] = state[(int64_t)(b0 + i / NMEL) * ROW + LAST_OFF + i % NMEL];
+  const int K = io.len0 + io.len1;
+  extern __shared__ float sm[];
+  float* xs = sm;                       // [IT][K]
+  float* part = sm + IT * K;            // [GW][IT][NPL*32]
+  for (int i = tid; i < IT * K; i += GW * 32) {
+    const int it = i / K, k = i % K;
+    float v = 0.f;
+    if (it < nb) {
+      const float* row = io.x + (int64_t)(b0 + it) * io.x_ld;
+      v = k < io.len0 ? row[io.off0 + k] : row[io.off1 + k - io.len0];
+    }
+    xs[i] = v;
+  }
   __syncthreads();
-  float a[IT];
+  const int kw = (K + GW - 1) / GW, k0 = warp * kw, k1 = min(K, k0 + kw);
+  float acc[IT][NPL];
 #pragma unroll
-  for (int i = 0; i < IT; ++i) a[i] = 0.f;
-  for (int k = 0; k < NMEL; ++k) {
-    const float w = W0T[k * PRE + j];
+  for (int i = 0; i < IT; ++i)
 #pragma unroll
-    for (int i = 0; i < IT; ++i) a[i] = fmaf(w, x[i][k], a[i]);
+    for (int j = 0; j < NPL; ++j) acc[i][j] = 0.f;
+#pragma unroll 2
+  for (int k = k0; k < k1; ++k) {
+    float w[NPL];
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      const int n = lane + 32 * j;
+      w[j] = n < io.N ? __ldg(io.wT + (int64_t)k * io.N + n) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      const float xv = xs[i * K + k];
+#pragma unroll
+      for (int j = 0; j < NPL; ++j) acc[i][j] = fmaf(w[j], xv, acc[i][j]);
+    }
   }
 #pragma unroll
-  for (int i = 0; i < IT; ++i) h1[i][j] = fmaxf(a[i], 0.f);
+  for (int i = 0; i < IT; ++i)
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) part[(warp * IT + i) * (NPL * 32) + lane + 32 * j] = acc[i][j];
   __syncthreads();
+  for (int e = tid; e < nb * io.N; e += GW * 32) {
+    const int it = e / io.N, n = e % io.N, b = b0 + it;
+    float v = part[it * (NPL * 32) + n];
 #pragma unroll
-  for (int i = 0; i < IT; ++i) a[i] = 0.f;
-  for (int k = 0; k < PRE; ++k) {
-    const float w = W1T[k * PRE + j];
-#pragma unroll
-    for (int i = 0; i < IT; ++i) a[i] = fmaf(w, h1[i][k], a[i]);
-  }
-  for (int i = 0; i < nb; ++i) {
-    const int b = b0 + i;
-    if (step >= plan[b * DPLAN + 5]) continue;
-    const float v = fmaxf(a[i], 0.f);
-    state[(int64_t)b * ROW + P_OFF + j] = v;
-    xb[(int64_t)b * XB_ROW + P_OFF + j] = __float2bfloat16_rn(v);
+    for (int w = 1; w < GW; ++w) v += part[(w * IT + it) * (NPL * 32) + n];
+    if (io.bias) v += io.bias[n];
+    if (MODE == 0) {
+      if (io.plan && io.step >= io.plan[b * DPLAN + 5]) continue;
+      if (io.relu) v = fmaxf(v, 0.f);
+      io.y[(int64_t)b * io.y_ld + io.y_off + n] = v;
+      if (io.yb) io.yb[(int64_t)b * io.yb_ld + io.y_off + n] = __float2bfloat16_rn(v);
+    } else {
+      const int64_t* p = io.plan + b * DPLAN;
+      if (io.step >= p[5]) continue;
+      if (n < NMEL) {
+        io.y[(int64_t)b * io.y_ld + LAST_OFF + n] = v;
+        reinterpret_cast<float*>(p[6])[io.step * NMEL + n] = v;
+      } else {
+        reinterpret_cast<float*>(p[7])[io.step] = v;
+      }
+    }
   }
 }
 
-// q[b] = Wq . att_h[b] for IT items per CTA; WqT [1024][128].  256 threads:
-// thread = (output a, item half).
-__global__ void __launch_bounds__(256) k_query(const float* __restrict__ state, const float* __restrict__ WqT,
-                                               float* __restrict__ Q, int B) {
-  const int b0 = blockIdx.x * IT, tid = threadIdx.x;
-  const int nb = min(IT, B - b0);
-  extern __shared__ float hs[];  // [IT][1024]
-  for (int i = tid; i < nb * HID; i += 256) hs[i] = state[(int64_t)(b0 + i / HID) * ROW + ATTH_OFF + i % HID];
-  __syncthreads();
-  const int a = tid & (ATT - 1), ih = tid >> 7;  // items ih*4 .. ih*4+3
-  float acc[IT / 2] = {0.f, 0.f, 0.f, 0.f};
-  for (int k = 0; k < HID; ++k) {
-    const float w = WqT[k * ATT + a];
-#pragma unroll
-    for (int i = 0; i < IT / 2; ++i) acc[i] = fmaf(w, hs[(ih * (IT / 2) + i) * HID + k], acc[i]);
+template <int NPL, int MODE>
+int launch_gemv(const GemvIO& io, int B, cudaStream_t st) {
+  const int K = io.len0 + io.len1;
+  const size_t smem = (size_t)(IT * K + GW * IT * NPL * 32) * 4;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaFuncSetAttribute(k_gemv<NPL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = 200 * 1024;
   }
-#pragma unroll
-  for (int i = 0; i < IT / 2; ++i) {
-    const int it = ih * (IT / 2) + i;
-    if (it < nb) Q[(int64_t)(b0 + it) * ATT + a] = acc[i];
-  }
+  k_gemv<NPL, MODE><<<(B + IT - 1) / IT, GW * 32, smem, st>>>(io, B);
+  ITTS_RETURN_LAUNCH();
 }
 
-// G [B][4096] gate pre-activations (bias included), PyTorch order i, f, g, o.
-__global__ void __launch_bounds__(256) k_lstm_cell(const float* __restrict__ G, float* __restrict__ state,
+// G = nsplit K-split partial slices [nsplit][B][4096], summed in fixed order (+ bias).
+__global__ void __launch_bounds__(256) k_lstm_cell(const float* __restrict__ G, int nsplit,
+                                                   const float* __restrict__ bias, float* __restrict__ state,
                                                    __nv_bfloat16* __restrict__ xb, int h_off, int c_off,
                                                    const int64_t* __restrict__ plan, int step, int B) {
   const int idx = blockIdx.x * 256 + threadIdx.x;
   const int b = idx / HID, j = idx % HID;
   if (b >= B || step >= plan[b * DPLAN + 5]) return;
-  const float* g = G + (int64_t)b * 4 * HID;
+  float gate[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float a = G[(int64_t)b * 4 * HID + q * HID + j];
+    for (int z = 1; z < nsplit; ++z) a += G[((int64_t)z * B + b) * 4 * HID + q * HID + j];
+    gate[q] = a + bias[q * HID + j];
+  }
   float* s = state + (int64_t)b * ROW;
-  const float c = sigm(g[HID + j]) * s[c_off + j] + sigm(g[j]) * tanhf(g[2 * HID + j]);
-  const float h = sigm(g[3 * HID + j]) * tanhf(c);
+  const float c = sigm(gate[1]) * s[c_off + j] + sigm(gate[0]) * tanhf(gate[2]);
+  const float h = sigm(gate[3]) * tanhf(c);
   s[c_off + j] = c;
   s[h_off + j] = h;
   xb[(int64_t)b * XB_ROW + h_off + j] = __float2bfloat16_rn(h);
 }
 
-// One CTA per item.  WqT [1024][128], Wloc [32][2][31], WdT [32][128], v [128].
-// Dynamic smem: 3*L floats (W_prev, W_acc, energies).
-__global__ void __launch_bounds__(256) k_attention(float* __restrict__ state, __nv_bfloat16* __restrict__ xb,
-                                                   const int64_t* __restrict__ plan,
-                                                   const float* __restrict__ Q, const float* __restrict__ Wloc,
-                                                   const float* __restrict__ WdT, const float* __restrict__ v,
-                                                   int step) {
+// One CTA (16 warps) per item.  Q [B][128] (query, from k_gemv), Wloc [32][2][31],
+// WdT [32][128], v [128].  Dynamic smem: W_prev, W_acc, energies (3L) + location
+// features [L][33].
+constexpr int AT_WARPS = 16;
+constexpr int LT = 256;  // positions per location-feature tile
+
+__global__ void __launch_bounds__(AT_WARPS * 32) k_attention(float* __restrict__ state, __nv_bfloat16* __restrict__ xb,
+                                                             const int64_t* __restrict__ plan,
+                                                             const float* __restrict__ Q,
+                                                             const float* __restrict__ Wloc,
+                                                             const float* __restrict__ WdT,
+                                                             const float* __restrict__ v, int step) {
+  constexpr int NT = AT_WARPS * 32;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t* p = plan + b * DPLAN;
   if (step >= p[5]) return;
@@ -156,70 +208,82 @@ __global__ void __launch_bounds__(256) k_attention(float* __restrict__ state, __
   float* w_prev = dyn;
   float* w_acc = dyn + L;
   float* e = dyn + 2 * L;
+  float* locf = dyn + ((3 * L + 3) & ~3);  // [LT][33]; later reused for the context partials
   __shared__ float q[ATT], sWloc[NF * 2 * KLOC], sWd[NF * ATT], sv[ATT], red[32];
-  __shared__ float4 cpart[8][EMB / 4];
+  float4 (*cpart)[EMB / 4] = reinterpret_cast<float4 (*)[EMB / 4]>(locf);  // [AT_WARPS][128]
 
-  for (int i = tid; i < L; i += 256) {
+  for (int i = tid; i < L; i += NT) {
     w_prev[i] = wsrc[i];
     w_acc[i] = wsrc[L + i];
   }
-  if (tid < ATT) q[tid] = Q[(int64_t)b * ATT + tid];
-  for (int i = tid; i < NF * 2 * KLOC; i += 256) sWloc[i] = Wloc[i];
-  for (int i = tid; i < NF * ATT; i += 256) sWd[i] = WdT[i];
-  if (tid < ATT) sv[tid] = v[tid];
-  __syncthreads();
-
-  // energies: one warp per text position; lane = location filter, then 4 attention dims per lane
-  for (int t = warp; t < L; t += 8) {
-    float conv = 0.f;
-    const float* wf = sWloc + lane * 2 * KLOC;
-#pragma unroll
-    for (int k = 0; k < KLOC; ++k) {
-      const int u = t + k - (KLOC - 1) / 2;
-      if (u >= 0 && u < L) conv = fmaf(wf[k], w_prev[u], fmaf(wf[KLOC + k], w_acc[u], conv));
-    }
-    float loc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 8
-    for (int f = 0; f < NF; ++f) {
-      const float cf = __shfl_sync(0xffffffffu, conv, f);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) loc[i] = fmaf(sWd[f * ATT + lane + 32 * i], cf, loc[i]);
-    }
-    float en = 0.f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int a = lane + 32 * i;
-      en = fmaf(sv[a], tanhf((q[a] + loc[i]) + pm[(int64_t)t * ATT + a]), en);
-    }
-    en = itts::warp_sum(en);
-    if (lane == 0) e[t] = en;
+  if (tid < ATT) {
+    q[tid] = Q[(int64_t)b * ATT + tid];
+    sv[tid] = v[tid];
   }
+  for (int i = tid; i < NF * 2 * KLOC; i += NT) sWloc[i] = Wloc[i];
+  for (int i = tid; i < NF * ATT; i += NT) sWd[i] = WdT[i];
   __syncthreads();
+  // Tiles of LT positions: location features (conv1d over [W_prev, W_acc], 2 -> 32
+  // filters, k 31, pad 15; one (t, f) per thread) then energies
+  // e_t = v . tanh(q + W_d loc_t + pm_t) (one warp per position, 4 dims per lane).
+  for (int t0 = 0; t0 < L; t0 += LT) {
+    const int nt = min(LT, L - t0);
+    for (int i = tid; i < nt * NF; i += NT) {
+      const int t = t0 + i / NF, f = i % NF;
+      const float* wf = sWloc + f * 2 * KLOC;
+      float c = 0.f;
+      const int k_lo = max(0, (KLOC - 1) / 2 - t), k_hi = min(KLOC, L + (KLOC - 1) / 2 - t);
+      for (int k = k_lo; k < k_hi; ++k) {
+        const int u = t + k - (KLOC - 1) / 2;
+        c = fmaf(wf[k], w_prev[u], fmaf(wf[KLOC + k], w_acc[u], c));
+      }
+      locf[(i / NF) * (NF + 1) + f] = c;
+    }
+    __syncthreads();
+    for (int tt = warp; tt < nt; tt += AT_WARPS) {
+      float loc[4] = {0.f, 0.f, 0.f, 0.f};
+      const float* lf = locf + tt * (NF + 1);
+#pragma unroll 8
+      for (int f = 0; f < NF; ++f) {
+        const float cf = lf[f];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) loc[i] = fmaf(sWd[f * ATT + lane + 32 * i], cf, loc[i]);
+      }
+      float en = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int a = lane + 32 * i;
+        en = fmaf(sv[a], tanhf((q[a] + loc[i]) + pm[(int64_t)(t0 + tt) * ATT + a]), en);
+      }
+      en = itts::warp_sum(en);
+      if (lane == 0) e[t0 + tt] = en;
+    }
+    __syncthreads();
+  }
   float lmax = -INFINITY;
-  for (int t = tid; t < L; t += 256) lmax = fmaxf(lmax, e[t]);
+  for (int t = tid; t < L; t += NT) lmax = fmaxf(lmax, e[t]);
   const float M = itts::block_reduce<float, true>(lmax, red);
   float lsum = 0.f;
-  for (int t = tid; t < L; t += 256) {
+  for (int t = tid; t < L; t += NT) {
     const float x = expf(e[t] - M);
     e[t] = x;
     lsum += x;
   }
   const float Z = itts::block_reduce<float, false>(lsum, red);
-  for (int t = tid; t < L; t += 256) {
+  for (int t = tid; t < L; t += NT) {
     const float a = e[t] / Z;
     e[t] = a;
     wdst[t] = a;
     wdst[L + t] = w_acc[t] + a;
   }
   __syncthreads();
-  // context = sum_t a_t * memory[t]: warp w takes rows t = w (mod 8), lane holds 16 dims as
-  // 4 float4 (coalesced 512 B per row per j), then a cross-warp reduction through smem.
+  // context = sum_t a_t memory[t]: warp w takes rows t = w (mod 16), lane holds 16 dims (4 float4)
   float4 acc[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
   const float4* mem4 = reinterpret_cast<const float4*>(mem);
 #pragma unroll 2
-  for (int t = warp; t < L; t += 8) {
+  for (int t = warp; t < L; t += AT_WARPS) {
     const float a = e[t];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -234,57 +298,12 @@ __global__ void __launch_bounds__(256) k_attention(float* __restrict__ state, __
   for (int j = 0; j < 4; ++j) cpart[warp][lane + 32 * j] = acc[j];
   __syncthreads();
   const float* cp = reinterpret_cast<const float*>(cpart);
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int d = tid + 256 * r;
+  for (int d = tid; d < EMB; d += NT) {
     float c = cp[d];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) c += cp[w * EMB + d];
+    for (int w = 1; w < AT_WARPS; ++w) c += cp[w * EMB + d];
     s[CTX_OFF + d] = c;
     xb[(int64_t)b * XB_ROW + CTX_OFF + d] = __float2bfloat16_rn(c);
-  }
-}
-
-// WpT [1536][81] (80 mel rows + gate row), bp [81].  hc = [dec_h, ctx]; IT items per CTA.
-__global__ void __launch_bounds__(256) k_proj(float* __restrict__ state, const int64_t* __restrict__ plan,
-                                              const float* __restrict__ WpT, const float* __restrict__ bp,
-                                              int step, int B) {
-  const int b0 = blockIdx.x * IT, tid = threadIdx.x;
-  const int nb = min(IT, B - b0);
-  extern __shared__ float hcs[];  // [IT][1536] then part [3][IT][81]
-  float* part = hcs + IT * 1536;
-  for (int i = tid; i < nb * 1536; i += 256) {
-    const int it = i / 1536, k = i % 1536;
-    const float* s = state + (int64_t)(b0 + it) * ROW;
-    hcs[i] = k < HID ? s[DECH_OFF + k] : s[CTX_OFF + k - HID];
-  }
-  for (int i = nb * 1536 + tid; i < IT * 1536; i += 256) hcs[i] = 0.f;
-  __syncthreads();
-  const int g = tid / 81, n = tid % 81;
-  if (g < 3) {
-    float a[IT];
-#pragma unroll
-    for (int i = 0; i < IT; ++i) a[i] = 0.f;
-    for (int k = g * 512; k < g * 512 + 512; ++k) {
-      const float w = WpT[k * 81 + n];
-#pragma unroll
-      for (int i = 0; i < IT; ++i) a[i] = fmaf(w, hcs[i * 1536 + k], a[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < IT; ++i) part[(g * IT + i) * 81 + n] = a[i];
-  }
-  __syncthreads();
-  for (int i = tid; i < nb * 81; i += 256) {
-    const int it = i / 81, o = i % 81, b = b0 + it;
-    const int64_t* p = plan + b * DPLAN;
-    if (step >= p[5]) continue;
-    const float out = bp[o] + ((part[(0 * IT + it) * 81 + o] + part[(1 * IT + it) * 81 + o]) + part[(2 * IT + it) * 81 + o]);
-    if (o < NMEL) {
-      state[(int64_t)b * ROW + LAST_OFF + o] = out;
-      reinterpret_cast<float*>(p[6])[step * NMEL + o] = out;
-    } else {
-      reinterpret_cast<float*>(p[7])[step] = out;
-    }
   }
 }
 
@@ -490,29 +509,31 @@ ITTS_API int itts_r_dec_prepare(const float* state, void* xb, int32_t B, void* s
   ITTS_RETURN_LAUNCH();
 }
 
+// Prenet: H1 = relu(last . W0^T) ; p = relu(H1 . W1^T) -> state p + bf16 mirror.  H1 = fp32 [B][256] scratch.
 ITTS_API int itts_r_prenet(float* state, void* xb, const float* W0T, const float* W1T, const int64_t* plan,
-                           int32_t B, int32_t step, void* stream) {
+                           float* H1, int32_t B, int32_t step, void* stream) {
   if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
-  k_prenet<<<(B + IT - 1) / IT, 256, 0, (cudaStream_t)stream>>>(state, (__nv_bfloat16*)xb, W0T, W1T, plan, step, B);
-  ITTS_RETURN_LAUNCH();
+  cudaStream_t st = (cudaStream_t)stream;
+  GemvIO a{state, ROW, LAST_OFF, NMEL, 0, 0, W0T, PRE, H1, PRE, 0, nullptr, 0, nullptr, 1, nullptr, step};
+  int r = launch_gemv<8, 0>(a, B, st);
+  if (r) return r;
+  GemvIO c{H1, PRE, 0, PRE, 0, 0, W1T, PRE, state, ROW, P_OFF, (__nv_bfloat16*)xb, XB_ROW, nullptr, 1, plan, step};
+  return launch_gemv<8, 0>(c, B, st);
 }
 
 ITTS_API int itts_r_query(const float* state, const float* WqT, float* Q, int32_t B, void* stream) {
   if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_query, cudaFuncAttributeMaxDynamicSharedMemorySize, IT * HID * 4);
-    configured = true;
-  }
-  k_query<<<(B + IT - 1) / IT, 256, IT * HID * 4, (cudaStream_t)stream>>>(state, WqT, Q, B);
-  ITTS_RETURN_LAUNCH();
+  GemvIO io{state, ROW, ATTH_OFF, HID, 0, 0, WqT, ATT, Q, ATT, 0, nullptr, 0, nullptr, 0, nullptr, 0};
+  return launch_gemv<4, 0>(io, B, (cudaStream_t)stream);
 }
 
-ITTS_API int itts_r_lstm_cell(const float* G, float* state, void* xb, int32_t h_off, int32_t c_off,
-                              const int64_t* plan, int32_t B, int32_t step, void* stream) {
+ITTS_API int itts_r_lstm_cell(const float* G, int32_t nsplit, const float* bias, float* state, void* xb,
+                              int32_t h_off, int32_t c_off, const int64_t* plan, int32_t B, int32_t step,
+                              void* stream) {
   if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
-  k_lstm_cell<<<(B * HID + 255) / 256, 256, 0, (cudaStream_t)stream>>>(G, state, (__nv_bfloat16*)xb, h_off,
-                                                                       c_off, plan, step, B);
+  if (nsplit < 1 || !bias) return ITTS_EINVAL;
+  k_lstm_cell<<<(B * HID + 255) / 256, 256, 0, (cudaStream_t)stream>>>(G, nsplit, bias, state, (__nv_bfloat16*)xb,
+                                                                       h_off, c_off, plan, step, B);
   ITTS_RETURN_LAUNCH();
 }
 
@@ -520,28 +541,24 @@ ITTS_API int itts_r_attention(float* state, void* xb, const int64_t* plan, int32
                               const float* Q, const float* Wloc, const float* WdT, const float* v,
                               int32_t step, void* stream) {
   if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
-  const size_t smem = (size_t)3 * max_len * sizeof(float);
-  if (smem > 160 * 1024) return ITTS_EUNSUPPORTED;  // L <= 13653 phonemes
+  static_assert(LT * (NF + 1) >= AT_WARPS * EMB, "context partials alias the location tile");
+  const size_t smem = ((size_t)3 * max_len + 4 + (size_t)LT * (NF + 1)) * sizeof(float);
+  if (smem > 160 * 1024) return ITTS_EUNSUPPORTED;  // L <= ~10,900 phonemes per request
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     configured = true;
   }
-  k_attention<<<B, 256, smem, (cudaStream_t)stream>>>(state, (__nv_bfloat16*)xb, plan, Q, Wloc, WdT, v, step);
+  k_attention<<<B, AT_WARPS * 32, smem, (cudaStream_t)stream>>>(state, (__nv_bfloat16*)xb, plan, Q, Wloc, WdT, v,
+                                                                step);
   ITTS_RETURN_LAUNCH();
 }
 
 ITTS_API int itts_r_proj(float* state, const int64_t* plan, int32_t B, const float* WpT, const float* bp,
                          int32_t step, void* stream) {
   if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
-  constexpr int smem = (IT * 1536 + 3 * IT * 81) * 4;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_proj, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    configured = true;
-  }
-  k_proj<<<(B + IT - 1) / IT, 256, smem, (cudaStream_t)stream>>>(state, plan, WpT, bp, step, B);
-  ITTS_RETURN_LAUNCH();
+  GemvIO io{state, ROW, DECH_OFF, HID, CTX_OFF, EMB, WpT, NMEL + 1, state, ROW, 0, nullptr, 0, bp, 0, plan, step};
+  return launch_gemv<3, 1>(io, B, (cudaStream_t)stream);
 }
 
 ITTS_API int itts_r_enc_embed(const int32_t* tok4, int64_t total, const int64_t* plan, int32_t n,

@@ -47,10 +47,15 @@ def convt_weights(w: torch.Tensor, stride: int):
 
 
 def conv1d_tc(x: torch.Tensor, wt: torch.Tensor, offs, bias: torch.Tensor, c_out: int,
-              row_out: torch.Tensor, *, resid_in=None, resid_out=None, acc=None, acc_mode=ACC_NONE,
-              act_out=None, slope: float = 1.0, zero_halo: bool = True, bn: int = 0,
-              stream=None) -> None:
-    """One conv layer: x bf16 [R][C_in] (row stride x.stride(0)) -> epilogue outputs (tc_conv.cu)."""
+              row_out: torch.Tensor, *, res_in=None, res_slope: float = 1.0, f32_out=None, ksplit: int = 1,
+              acc=None, acc_mode=ACC_NONE, act_out=None, slope: float = 1.0, zero_halo: bool = True,
+              bn: int = 0, stream=None) -> None:
+    """One conv layer: x bf16 [R][C_in] (row stride x.stride(0)) -> epilogue outputs (tc_conv.cu).
+
+    res_in / acc / act_out are bf16; res_in holds lrelu(y, res_slope) and is
+    inverted on load.  f32_out receives the raw fp32 result (K-split partial
+    slices when ksplit > 1).
+    """
     rows, c_in = x.shape
     assert x.stride(1) == 1
     taps, n_total, c_in_w = wt.shape
@@ -59,5 +64,6 @@ def conv1d_tc(x: torch.Tensor, wt: torch.Tensor, offs, bias: torch.Tensor, c_out
     ptr = lambda t: 0 if t is None else t.data_ptr()
     st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
     _native.call("itts_conv1d_tc", x.data_ptr(), rows, c_in, x.stride(0), wt.data_ptr(), n_total, taps,
-                 offs_arr, bias.data_ptr(), c_out, row_out.data_ptr(), ptr(resid_in), ptr(resid_out),
-                 ptr(acc), acc_mode, ptr(act_out), float(slope), int(zero_halo), int(bn), st)
+                 offs_arr, bias.data_ptr(), c_out, row_out.data_ptr(), ptr(res_in), float(res_slope),
+                 ptr(f32_out), int(ksplit), ptr(acc), acc_mode, ptr(act_out), float(slope), int(zero_halo),
+                 int(bn), st)

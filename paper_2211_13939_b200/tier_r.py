@@ -44,6 +44,8 @@ MEL_HALO = 3        # conv_pre k7
 MRF_HALO = 25       # k11 dilation 5
 UPS = (8, 8, 2, 2)
 STAGE_C = (256, 128, 64, 32)
+DEC_KSPLIT = 4      # K-split of the decoder gate GEMMs (partials summed in fixed order by the cell kernel)
+GRAPH_MAX_L = 4096  # attention smem is sized for this in captured graphs; longer texts run eagerly
 
 
 def _hifigan_macs_per_frame() -> int:
@@ -101,6 +103,9 @@ class TierREngine:
         self.h2d_bytes = 0
         self.d2h_bytes = 0
         self.timers: list | None = None  # set to [] to record (kind, ev0, ev1, units) per module call
+        self.use_graphs = True           # CUDA-graph the 32-step decoder chunk per (batch, L) bucket
+        self._dec_buckets: dict = {}
+        self._graph_warm = False
 
     def _mark(self, kind: str, units: float):
         """Context manager recording CUDA events on the engine stream around a region."""
@@ -144,12 +149,13 @@ class TierREngine:
         # decoder
         self.W0T, self.W1T = f32(w["prenet.0"].T), f32(w["prenet.1"].T)
         wa = torch.cat([w["att_rnn.w_ih"], w["att_rnn.w_hh"]], 1)                       # [p|ctx|att_h]
-        self.att_gemm = (wa.to(d).to(torch.bfloat16)[None].contiguous(), [0],
-                         f32(w["att_rnn.b_ih"] + w["att_rnn.b_hh"]))
+        zeros = torch.zeros(4096, device=d)   # gate bias is added (once) by the cell kernel
+        self.att_bias = f32(w["att_rnn.b_ih"] + w["att_rnn.b_hh"])
+        self.att_gemm = (wa.to(d).to(torch.bfloat16)[None].contiguous(), [0], zeros)
         wih = w["dec_rnn.w_ih"]                                                          # cols [att_h | ctx]
         wd = torch.cat([wih[:, 1024:], wih[:, :1024], w["dec_rnn.w_hh"]], 1)             # [ctx|att_h|dec_h]
-        self.dec_gemm = (wd.to(d).to(torch.bfloat16)[None].contiguous(), [0],
-                         f32(w["dec_rnn.b_ih"] + w["dec_rnn.b_hh"]))
+        self.dec_bias = f32(w["dec_rnn.b_ih"] + w["dec_rnn.b_hh"])
+        self.dec_gemm = (wd.to(d).to(torch.bfloat16)[None].contiguous(), [0], zeros)
         self.WqT = f32(w["att.query_layer"].T)                                           # [1024][128]
         self.Wloc = f32(w["att.location_conv"])                                          # [32][2][31]
         self.WdT = f32(w["att.location_dense"].T)                                        # [32][128]
@@ -256,7 +262,7 @@ class TierREngine:
                 src, dst = (xa, xb) if i % 2 == 0 else (xb, xa)
                 self._conv(src, layer, W.EMB, rm, act_out=dst, slope=0.0)
             pre = torch.empty(lay.total, 2048, dtype=torch.float32, device=self.device)
-            self._conv(xb, self.enc_ih, 2048, rm, resid_out=pre, bn=128)
+            self._conv(xb, self.enc_ih, 2048, rm, f32_out=pre, bn=128)
             self._call("itts_r_bilstm", pre.data_ptr(), d_plan.data_ptr(), n, self.enc_whhT.data_ptr(), st)
             self._call("itts_r_pmem", d_plan.data_ptr(), n, max(lens), self.WmT.data_ptr(), st)
             for req, buf in reqs:
@@ -284,62 +290,99 @@ class TierREngine:
         for state, _ in pairs:
             dsts.append(state.req.claim(state.req.state_bufs, self.state_size(state.req.seq_len), taken))
         a = self.arena
-        mel_off = np.concatenate([[0], np.cumsum(steps)]).astype(np.int64)
         max_L = max(s.req.seq_len for s, _ in pairs)
-        st = self._st()
+        dec_bytes = max(steps) * DEC_WEIGHT_BYTES + sum(
+            k * (2 * 4 * ROW + s.req.seq_len * (4 * 512 + 4 * 128 + 16) + 4 * 81) for k, (s, _) in zip(steps, pairs))
+        src = np.array([a.ptr(st_.buf.off) for st_, _ in pairs], dtype=np.int64)
+        dstp = np.array([a.ptr(d.off) for d in dsts], dtype=np.int64)
         with torch.cuda.stream(self.stream):
-            mel = torch.empty(int(mel_off[-1]), W.N_MEL, dtype=torch.float32, device=self.device)
-            gate = torch.empty(int(mel_off[-1]), dtype=torch.float32, device=self.device)
-            plan = np.zeros((n, 8), dtype=np.int64)
-            src = np.zeros(n, dtype=np.int64)
-            dstp = np.zeros(n, dtype=np.int64)
-            for i, ((state, enc), dst) in enumerate(zip(pairs, dsts)):
-                req = state.req
-                src[i], dstp[i] = a.ptr(state.buf.off), a.ptr(dst.off)
-                plan[i] = (a.ptr(req.extra["mem_off"]), a.ptr(req.extra["pm_off"]), req.seq_len,
-                           src[i] + 4 * ROW, dstp[i] + 4 * ROW, steps[i],
-                           mel.data_ptr() + 4 * W.N_MEL * int(mel_off[i]), gate.data_ptr() + 4 * int(mel_off[i]))
-            packed = self._up(np.concatenate([plan.reshape(-1), src, dstp]))
-            d_plan, d_src, d_dst = packed[:8 * n], packed[8 * n:9 * n], packed[9 * n:]
-            work = torch.empty(n, ROW, dtype=torch.float32, device=self.device)
-            xbm = torch.empty(n, XB_ROW, dtype=torch.bfloat16, device=self.device)
-            G = torch.empty(n, 4096, dtype=torch.float32, device=self.device)
-            Q = torch.empty(n, 128, dtype=torch.float32, device=self.device)
-            dec_bytes = max(steps) * DEC_WEIGHT_BYTES + sum(
-                k * (2 * 4 * ROW + s.req.seq_len * (4 * 512 + 4 * 128 + 16) + 4 * 81)
-                for k, (s, _) in zip(steps, pairs))
-            mark = self._mark("decoder", dec_bytes)
-            mark.__enter__()
-            self._call("itts_gather_rows", work.data_ptr(), d_src.data_ptr(), n, 4 * ROW, st)
-            self._call("itts_r_dec_prepare", work.data_ptr(), xbm.data_ptr(), n, st)
-            rows = self._iota(n)
-            x_att, x_dec = xbm[:, :1792], xbm[:, 256:]
-            for step in range(max(steps)):
-                self._call("itts_r_prenet", work.data_ptr(), xbm.data_ptr(), self.W0T.data_ptr(),
-                           self.W1T.data_ptr(), d_plan.data_ptr(), n, step, st)
-                self._conv(x_att, self.att_gemm, 4096, rows, resid_out=G, bn=64)
-                self._call("itts_r_lstm_cell", G.data_ptr(), work.data_ptr(), xbm.data_ptr(), ATTH_OFF,
-                           ATTC_OFF, d_plan.data_ptr(), n, step, st)
-                self._call("itts_r_query", work.data_ptr(), self.WqT.data_ptr(), Q.data_ptr(), n, st)
-                self._call("itts_r_attention", work.data_ptr(), xbm.data_ptr(), d_plan.data_ptr(), n, max_L,
-                           Q.data_ptr(), self.Wloc.data_ptr(), self.WdT.data_ptr(), self.v.data_ptr(),
-                           step, st)
-                self._conv(x_dec, self.dec_gemm, 4096, rows, resid_out=G, bn=64)
-                self._call("itts_r_lstm_cell", G.data_ptr(), work.data_ptr(), xbm.data_ptr(), DECH_OFF,
-                           DECC_OFF, d_plan.data_ptr(), n, step, st)
-                self._call("itts_r_proj", work.data_ptr(), d_plan.data_ptr(), n, self.WpT.data_ptr(),
-                           self.bp.data_ptr(), step, st)
-            self._call("itts_scatter_rows", d_dst.data_ptr(), work.data_ptr(), n, 4 * ROW, st)
-            mark.__exit__(None, None, None)
+            if self.use_graphs and max(steps) == C and max_L <= GRAPH_MAX_L:
+                bk = self._dec_bucket(n)
+                B = bk.B
+                plan = np.zeros((B, 8), dtype=np.int64)
+                src_all = np.full(B, bk.zero_row.data_ptr(), dtype=np.int64)
+                dst_all = bk.sink.data_ptr() + 4 * ROW * np.arange(B, dtype=np.int64)
+                src_all[:n], dst_all[:n] = src, dstp
+                for i, (state, _) in enumerate(pairs):
+                    req = state.req
+                    plan[i] = (a.ptr(req.extra["mem_off"]), a.ptr(req.extra["pm_off"]), req.seq_len,
+                               src[i] + 4 * ROW, dstp[i] + 4 * ROW, steps[i],
+                               bk.mel.data_ptr() + 4 * W.N_MEL * C * i, bk.gate.data_ptr() + 4 * C * i)
+                host = np.concatenate([plan.reshape(-1), src_all, dst_all])
+                self.h2d_bytes += host.nbytes
+                bk.packed.copy_(torch.from_numpy(host).pin_memory(), non_blocking=True)
+                with self._mark("decoder", dec_bytes):
+                    if bk.graph is None:
+                        bk.capture(self)
+                    bk.graph.replay()
+                    self.launches += bk.launches
+                mel_all, gate_all = bk.mel[:n].clone(), bk.gate[:n].clone()
+                mel_views = [mel_all[i, :steps[i]] for i in range(n)]
+                gate_views = [gate_all[i, :steps[i]] for i in range(n)]
+            else:
+                mel_off = np.concatenate([[0], np.cumsum(steps)]).astype(np.int64)
+                mel = torch.empty(int(mel_off[-1]), W.N_MEL, dtype=torch.float32, device=self.device)
+                gate = torch.empty(int(mel_off[-1]), dtype=torch.float32, device=self.device)
+                plan = np.zeros((n, 8), dtype=np.int64)
+                for i, (state, _) in enumerate(pairs):
+                    req = state.req
+                    plan[i] = (a.ptr(req.extra["mem_off"]), a.ptr(req.extra["pm_off"]), req.seq_len,
+                               src[i] + 4 * ROW, dstp[i] + 4 * ROW, steps[i],
+                               mel.data_ptr() + 4 * W.N_MEL * int(mel_off[i]), gate.data_ptr() + 4 * int(mel_off[i]))
+                packed = self._up(np.concatenate([plan.reshape(-1), src, dstp]))
+                bufs = _DecBuffers(self, n, packed)
+                with self._mark("decoder", dec_bytes):
+                    self._enqueue_decoder(bufs, max_L, max(steps))
+                mel_views = [mel[int(mel_off[i]):int(mel_off[i + 1])] for i in range(n)]
+                gate_views = [gate[int(mel_off[i]):int(mel_off[i + 1])] for i in range(n)]
         out = []
         for i, ((state, enc), dst) in enumerate(zip(pairs, dsts)):
             emitted = state.frames_emitted + steps[i]
-            mh = DeviceMelChunk(mel[int(mel_off[i]):int(mel_off[i + 1])], state.req)
-            res = DecodeChunkResult(mh, emitted >= state.target_frames,
+            res = DecodeChunkResult(DeviceMelChunk(mel_views[i], state.req), emitted >= state.target_frames,
                                     DeviceDecoderState(state.req, dst, emitted, state.target_frames))
-            object.__setattr__(res, "gate_logits", gate[int(mel_off[i]):int(mel_off[i + 1])])
+            object.__setattr__(res, "gate_logits", gate_views[i])
             out.append(res)
         return out
+
+    def _enqueue_decoder(self, b: "_DecBuffers", max_L: int, nsteps: int) -> None:
+        """K1 gather -> nsteps x (prenet, att GEMM, cell, query, attention, dec GEMM, cell, proj) -> K1 scatter."""
+        st, n = self._st(), b.n
+        self._call("itts_gather_rows", b.work.data_ptr(), b.d_src.data_ptr(), n, 4 * ROW, st)
+        self._call("itts_r_dec_prepare", b.work.data_ptr(), b.xbm.data_ptr(), n, st)
+        rows = self._iota(n)
+        x_att, x_dec = b.xbm[:, :1792], b.xbm[:, 256:]
+        for step in range(nsteps):
+            self._call("itts_r_prenet", b.work.data_ptr(), b.xbm.data_ptr(), self.W0T.data_ptr(),
+                       self.W1T.data_ptr(), b.d_plan.data_ptr(), b.H1.data_ptr(), n, step, st)
+            self._conv(x_att, self.att_gemm, 4096, rows, f32_out=b.G, ksplit=DEC_KSPLIT, bn=64)
+            self._call("itts_r_lstm_cell", b.G.data_ptr(), DEC_KSPLIT, self.att_bias.data_ptr(), b.work.data_ptr(),
+                       b.xbm.data_ptr(), ATTH_OFF, ATTC_OFF, b.d_plan.data_ptr(), n, step, st)
+            self._call("itts_r_query", b.work.data_ptr(), self.WqT.data_ptr(), b.Q.data_ptr(), n, st)
+            self._call("itts_r_attention", b.work.data_ptr(), b.xbm.data_ptr(), b.d_plan.data_ptr(), n, max_L,
+                       b.Q.data_ptr(), self.Wloc.data_ptr(), self.WdT.data_ptr(), self.v.data_ptr(), step, st)
+            self._conv(x_dec, self.dec_gemm, 4096, rows, f32_out=b.G, ksplit=DEC_KSPLIT, bn=64)
+            self._call("itts_r_lstm_cell", b.G.data_ptr(), DEC_KSPLIT, self.dec_bias.data_ptr(), b.work.data_ptr(),
+                       b.xbm.data_ptr(), DECH_OFF, DECC_OFF, b.d_plan.data_ptr(), n, step, st)
+            self._call("itts_r_proj", b.work.data_ptr(), b.d_plan.data_ptr(), n, self.WpT.data_ptr(),
+                       self.bp.data_ptr(), step, st)
+        self._call("itts_scatter_rows", b.d_dst.data_ptr(), b.work.data_ptr(), n, 4 * ROW, st)
+
+    def _dec_bucket(self, n: int) -> "_DecBucket":
+        B = -(-n // 16) * 16
+        if B not in self._dec_buckets:
+            self._dec_buckets[B] = _DecBucket(self, B, GRAPH_MAX_L)
+        return self._dec_buckets[B]
+
+    def prepare_graphs(self, max_batch: int = 256) -> None:
+        """Capture the decoder-chunk graph of every 16-row bucket up to ``max_batch`` now,
+        so no capture happens on the serving path."""
+        with torch.cuda.stream(self.stream):
+            for B in range(16, max_batch + 1, 16):
+                bk = self._dec_bucket(B)
+                if bk.graph is None:
+                    bk.idle_plan()
+                    bk.capture(self)
+        self.stream.synchronize()
 
     # ------------------------------------------------------------ vocoder
     def vocoder_batch(self, triples) -> list:
@@ -434,30 +477,29 @@ class TierREngine:
             mult *= u
             layouts.append(_Layout([T * mult for T in Ts], MRF_HALO))
         biggest = max(l.total * c for l, c in zip(layouts, STAGE_C))
-        f32 = [torch.empty(biggest, dtype=torch.float32, device=dev) for _ in range(3)]     # x, y, acc
-        b16 = [torch.empty(biggest, dtype=torch.bfloat16, device=dev) for _ in range(5)]   # xa, ya, tb, oa x2
+        # bf16 only: the residual stream is kept as lrelu(y, 0.1) and inverted on load
+        b16 = [torch.empty(biggest, dtype=torch.bfloat16, device=dev) for _ in range(6)]  # xa ya tb acc oa oa'
         for s, (u, lay) in enumerate(zip(UPS, layouts)):
             C = STAGE_C[s]
             view = lambda t: t[:lay.total * C].view(lay.total, C)
-            X, Y, ACC = (view(t) for t in f32)
-            XA, YA, TB = (view(t) for t in b16[:3])
-            OA_next = view(b16[3 + s % 2])
+            XA, YA, TB, ACC = (view(t) for t in b16[:4])
+            OA_next = view(b16[4 + s % 2])
             # transposed conv: each input row of the previous stage -> u output rows
             rmT = self._rowmap(prev, lay.first, u)
-            self._conv(act_in, self.ups[s], C, rmT, resid_out=X, act_out=XA, slope=0.1, zero_halo=False)
+            self._conv(act_in, self.ups[s], C, rmT, act_out=XA, slope=0.1, zero_halo=False)
             zplan = np.stack([lay.base, np.array(lay.rows, np.int64), np.full(n, lay.halo, np.int64)], 1)
             self._call("itts_r_zero_halo", self._up(zplan).data_ptr(), n, lay.halo, XA.data_ptr(), C, st)
             rm = self._rowmap(lay, lay.first, 1)
             slope_out = 0.1 if s < 3 else 0.01
             for j, layers in enumerate(self.res[s]):
                 for m, (c1, c2) in enumerate(layers):
-                    self._conv(XA if m == 0 else YA, c1, C, rm, act_out=TB, slope=0.1)
+                    ya_in = XA if m == 0 else YA
+                    self._conv(ya_in, c1, C, rm, act_out=TB, slope=0.1)
                     if m < 2:
-                        self._conv(TB, c2, C, rm, resid_in=X if m == 0 else Y, resid_out=Y, act_out=YA,
-                                   slope=0.1)
+                        self._conv(TB, c2, C, rm, res_in=ya_in, res_slope=0.1, act_out=YA, slope=0.1)
                     else:
                         mode = (tc.ACC_STORE, tc.ACC_ADD, tc.ACC_FINAL)[j]
-                        self._conv(TB, c2, C, rm, resid_in=Y, acc=ACC, acc_mode=mode,
+                        self._conv(TB, c2, C, rm, res_in=YA, res_slope=0.1, acc=ACC, acc_mode=mode,
                                    act_out=OA_next if j == 2 else None, slope=slope_out)
             prev, act_in = lay, OA_next
         return act_in
@@ -500,3 +542,58 @@ class TierREngine:
         O = self.cfg.overlap_frames
         raw = self._read(buf.off, self.voc_size())
         return raw[:O * W.N_MEL].reshape(O, W.N_MEL), raw[O * W.N_MEL:]
+
+
+class _DecBuffers:
+    """Work buffers of one decoder call (n pooled rows); `packed` = plan | src ptrs | dst ptrs."""
+
+    def __init__(self, eng: TierREngine, n: int, packed: torch.Tensor):
+        dev = eng.device
+        self.n = n
+        self.packed = packed
+        self.d_plan, self.d_src, self.d_dst = packed[:8 * n], packed[8 * n:9 * n], packed[9 * n:10 * n]
+        self.work = torch.empty(n, ROW, dtype=torch.float32, device=dev)
+        self.xbm = torch.empty(n, XB_ROW, dtype=torch.bfloat16, device=dev)
+        self.G = torch.empty(DEC_KSPLIT, n, 4096, dtype=torch.float32, device=dev)
+        self.Q = torch.empty(n, 128, dtype=torch.float32, device=dev)
+        self.H1 = torch.empty(n, 256, dtype=torch.float32, device=dev)
+
+
+class _DecBucket(_DecBuffers):
+    """Fixed-address buffers + a CUDA graph of the full 32-step decoder chunk for <= B rows.
+
+    Rows beyond the call's batch decode nothing (steps 0), gather a zero row
+    and scatter into a private sink, so one graph serves every n <= B.
+    """
+
+    def __init__(self, eng: TierREngine, B: int, L: int):
+        dev = eng.device
+        super().__init__(eng, B, torch.empty(10 * B, dtype=torch.int64, device=dev))
+        self.B, self.L = B, L
+        C = eng.cfg.chunk_frames
+        self.mel = torch.empty(B, C, W.N_MEL, dtype=torch.float32, device=dev)
+        self.gate = torch.empty(B, C, dtype=torch.float32, device=dev)
+        self.zero_row = torch.zeros(ROW, dtype=torch.float32, device=dev)
+        self.sink = torch.empty(B, ROW, dtype=torch.float32, device=dev)
+        self.graph = None
+        self.launches = 0
+
+    def idle_plan(self) -> None:
+        """Every row decodes nothing, gathers the zero row and scatters into its own sink."""
+        B = self.B
+        host = np.concatenate([np.zeros(8 * B, np.int64), np.full(B, self.zero_row.data_ptr(), np.int64),
+                               self.sink.data_ptr() + 4 * ROW * np.arange(B, dtype=np.int64)])
+        self.packed.copy_(torch.from_numpy(host))
+
+    def capture(self, eng: TierREngine) -> None:
+        C = eng.cfg.chunk_frames
+        if not eng._graph_warm:  # one eager pass per engine sets kernel attributes before any capture
+            eng._enqueue_decoder(self, self.L, C)
+            eng._graph_warm = True
+        g = torch.cuda.CUDAGraph()
+        before = eng.launches
+        with torch.cuda.graph(g, stream=eng.stream):
+            eng._enqueue_decoder(self, self.L, C)
+        self.launches = eng.launches - before
+        eng.launches = before
+        self.graph = g

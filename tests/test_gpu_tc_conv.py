@@ -50,7 +50,7 @@ def test_conv_matches_torch(c_in, c_out, k, dil):
     wt, offs = tc.conv_weights(w.to(DEV), dil)
     out = torch.full((rows, c_out), 7.0, device=DEV)
     act = torch.full((rows, c_out), 7.0, device=DEV, dtype=torch.bfloat16)
-    tc.conv1d_tc(x, wt, offs, bias.to(DEV), c_out, row_out.to(DEV), resid_out=out, act_out=act, slope=0.1)
+    tc.conv1d_tc(x, wt, offs, bias.to(DEV), c_out, row_out.to(DEV), f32_out=out, act_out=act, slope=0.1)
     torch.cuda.synchronize()
     for it, b, T in zip(items, bases, lengths):
         ref = F.conv1d(it.T[None], w, bias, dilation=dil, padding=dil * (k - 1) // 2)[0].T
@@ -64,6 +64,7 @@ def test_conv_matches_torch(c_in, c_out, k, dil):
 
 
 def test_residual_and_mrf_accumulate():
+    """bf16 residual stream stored as lrelu(y, 0.1) and inverted on load; bf16 MRF accumulator."""
     torch.manual_seed(1)
     C, k, dil = 64, 5, 3
     lengths, halo = [100, 61], 25
@@ -76,24 +77,48 @@ def test_residual_and_mrf_accumulate():
     bias = torch.randn(C).to(DEV)
     wt, offs = tc.conv_weights(w.to(DEV), dil)
     xb = x.to(torch.bfloat16)
-    y0 = torch.randn(rows, C, device=DEV)
-    acc = torch.randn(rows, C, device=DEV)
-    acc0 = acc.clone()
-    y1 = torch.empty_like(y0)
     ro = row_out.to(DEV)
-    tc.conv1d_tc(xb, wt, offs, bias, C, ro, resid_in=y0, resid_out=y1, acc=acc, acc_mode=tc.ACC_ADD)
-    act = torch.zeros(rows, C, device=DEV, dtype=torch.bfloat16)
-    acc2 = acc0.clone()
-    tc.conv1d_tc(xb, wt, offs, bias, C, ro, resid_in=y0, acc=acc2, acc_mode=tc.ACC_FINAL, act_out=act,
-                 slope=0.01)
-    torch.cuda.synchronize()
+    y0 = torch.randn(rows, C, device=DEV)
+    res = F.leaky_relu(y0, 0.1).to(torch.bfloat16)
+    acc0 = torch.randn(rows, C, device=DEV).to(torch.bfloat16)
     conv = F.conv1d(x.T[None].cpu(), w, bias.cpu(), dilation=dil, padding=dil * (k - 1) // 2)[0].T
-    ref_y = y0.cpu() + conv
+    y_in = torch.where(res.float() >= 0, res.float(), res.float() / 0.1).cpu()
+    ref_y = y_in + conv
     valid = row_out >= 0
-    assert (y1.cpu()[valid] - ref_y[valid]).abs().max() < 2e-3 * ref_y.abs().max()
-    assert (acc.cpu()[valid] - (acc0.cpu() + ref_y)[valid]).abs().max() < 2e-3 * ref_y.abs().max()
-    fin = F.leaky_relu((acc0.cpu() + ref_y) / 3.0, 0.01)
-    assert (act.float().cpu()[valid] - fin[valid]).abs().max() < 1e-2 * fin.abs().max()
+    scale = ref_y.abs().max()
+    # residual add -> act_out (stored as lrelu(y))
+    act = torch.zeros(rows, C, device=DEV, dtype=torch.bfloat16)
+    tc.conv1d_tc(xb, wt, offs, bias, C, ro, res_in=res, res_slope=0.1, act_out=act, slope=0.1)
+    # residual add -> accumulate
+    acc = acc0.clone()
+    tc.conv1d_tc(xb, wt, offs, bias, C, ro, res_in=res, res_slope=0.1, acc=acc, acc_mode=tc.ACC_ADD)
+    # finalize (acc + y) / 3 -> lrelu 0.01
+    fin_act = torch.zeros(rows, C, device=DEV, dtype=torch.bfloat16)
+    tc.conv1d_tc(xb, wt, offs, bias, C, ro, res_in=res, res_slope=0.1, acc=acc0.clone(), acc_mode=tc.ACC_FINAL,
+                 act_out=fin_act, slope=0.01)
+    torch.cuda.synchronize()
+    assert (act.float().cpu()[valid] - F.leaky_relu(ref_y, 0.1)[valid]).abs().max() < 1e-2 * scale
+    assert (acc.float().cpu()[valid] - (acc0.float().cpu() + ref_y)[valid]).abs().max() < 1e-2 * scale
+    fin = F.leaky_relu((acc0.float().cpu() + ref_y) / 3.0, 0.01)
+    assert (fin_act.float().cpu()[valid] - fin[valid]).abs().max() < 1e-2 * fin.abs().max()
+
+
+@pytest.mark.parametrize("B,K,ksplit", [(1, 1792, 4), (37, 2560, 4), (200, 1792, 1), (130, 2560, 2)])
+def test_gemm_ksplit_on_column_slice(B, K, ksplit):
+    """Decoder gate GEMM: x is a column slice of a wider bf16 row (ld 2816); K-split partials."""
+    torch.manual_seed(3)
+    full = bf(torch.randn(B, 2816)).to(DEV).to(torch.bfloat16)
+    x = full[:, 2816 - K:]
+    w = bf(torch.randn(4096, K) / K ** 0.5)
+    out = torch.zeros(ksplit, B, 4096, device=DEV)
+    rows = torch.arange(B, dtype=torch.int32, device=DEV)
+    bias = torch.randn(4096, device=DEV)
+    tc.conv1d_tc(x, w.to(DEV).to(torch.bfloat16)[None].contiguous(), [0], bias, 4096, rows, f32_out=out,
+                 ksplit=ksplit, bn=64)
+    torch.cuda.synchronize()
+    ref = x.float().cpu() @ w.T + bias.cpu()
+    got = out.sum(0).cpu()
+    assert (got - ref).abs().max() <= 2e-3 * ref.abs().max()
 
 
 @pytest.mark.parametrize("c_in,c_out,u", [(512, 256, 8), (256, 128, 8), (128, 64, 2), (64, 32, 2)])
@@ -111,7 +136,7 @@ def test_transposed_conv_matches_torch(c_in, c_out, u):
     x = pack(items, bases, rows, halo_in, c_in).to(DEV).to(torch.bfloat16)
     wp, offs = tc.convt_weights(w.to(DEV), u)
     out = torch.zeros(out_rows, c_out, device=DEV)
-    tc.conv1d_tc(x, wp, offs, bias.to(DEV), c_out, row_out.to(DEV), resid_out=out, zero_halo=False)
+    tc.conv1d_tc(x, wp, offs, bias.to(DEV), c_out, row_out.to(DEV), f32_out=out, zero_halo=False)
     torch.cuda.synchronize()
     for it, ob, T in zip(items, out_bases, lengths):
         ref = F.conv_transpose1d(it.T[None], w, bias, stride=u, padding=u // 2)[0].T
