@@ -227,7 +227,6 @@ def run_ours(args) -> None:
            if r.lcl is not None and r.error is None and r.samples]
     missing = sum(1 for r in inside if r.fcl is None)
     window_s = t1 - t0
-    steps_in = [rep for rep in run.reports[-(len(run.reports)):]]
     batch_sizes = [len(rep.decoder_ids) for rep in run.reports]
 
     timers = marks.get("timers") or []
@@ -238,8 +237,112 @@ def run_ours(args) -> None:
         a[0] += ms
         a[1] += units
         a[2] += 1
-    l0, h0, d0 = marks["start"]
-    l1, h1, d1 = marks["end"]
+
+    from paper_2211_13939_b200.harness import merge_rank_stats
+    merged = merge_rank_stats({"fcl": fcl, "fcl_c": fcl_c, "lcl": lcl, "rtf": rtf, "window": window_s,
+                               "missing": missing, "launch": marks["end"][0] - marks["start"][0],
+                               "h2d": marks["end"][1] - marks["start"][1], "d2h": marks["end"][2] - marks["start"][2]},
+                              dist)
+    if merged is None:  # non-zero rank
+        dist.barrier()
+        dist.destroy_process_group()
+        return
+    fcl, fcl_c, lcl, rtf = merged["fcl"], merged["fcl_c"], merged["lcl"], merged["rtf"]
+    window_s, missing = merged["window"], merged["missing"]
+    p50, p99 = _percentiles(fcl)
+    return {"value": p99, "p50": p50, "unit": "ms", "cores": cores, "kind": "port",
+            "iterations": it, "requests": len(sent), "served_first_chunk": len(first),
+            "sample": f"{seconds:.0f} s of Poisson {qps:g} QPS U{{20..200}}-char arrivals through the "
+                      "oracle CPU modules (torch fp32, all host threads) behind the same scheduler; "
+                      "requests without a first chunk at the end are censored at the budget end"}
+
+
+def run_reference(args) -> None:
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    t0 = time.perf_counter()
+    res = cpu_serving_baseline(args.qps, args.cpu_seconds, args.seed, max_iters=args.steps + args.warmup)
+    wall = time.perf_counter() - t0
+    line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "ms", "n_gpus": args.gpus,
+            "steps": res["iterations"], "warmup": 0,
+            "ms_per_step": round(1e3 * wall / max(res["iterations"], 1), 3), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"C3: Poisson {args.qps:g} QPS, U{{20..200}} chars, Tacotron2+HiFi-GAN V1 "
+                                   "(random init), chunk 32, overlap 4", "qps_per_gpu": args.qps},
+            "p50_ms": res["p50"], "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": res["value"], "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "requests": res["requests"], "served_first_chunk": res["served_first_chunk"]}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args) -> None:
+    import torch
+
+    from paper_2211_13939_b200.domain import PipelineConfig
+    from paper_2211_13939_b200.frontend import default_lexicon
+    from paper_2211_13939_b200.harness import poisson_trace, serve
+    from paper_2211_13939_b200.modules import build_engine, modules_for
+
+    world, rank, local = _dist()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    device = f"cuda:{local}"
+    torch.cuda.set_device(local)
+    cfg, lex = PipelineConfig(), default_lexicon()
+    engine = build_engine(cfg, args.tier, device)
+    if hasattr(engine, "prepare_graphs"):
+        engine.prepare_graphs(max_batch=512)
+    mods = modules_for(engine, lex)
+
+    # untimed warm-up of every code path (tensor maps, smem attributes, allocator pools)
+    warm = serve(mods, cfg, poisson_trace(50, 1.0, seed=args.seed + 7, lexicon=lex), warmup_iters=0,
+                 timed_iters=2, drain_seconds=0.0)
+    del warm
+    torch.cuda.synchronize()
+
+    peaks = _peaks()
+    sampler = ClockSampler(local)
+    marks = {}
+
+    def on_window(kind, idx):
+        if kind == "start":
+            torch.cuda.synchronize()
+            engine.timers = []
+            marks["start"] = (engine.launches, engine.h2d_bytes, engine.d2h_bytes)
+            sampler.start()
+        else:
+            marks["clocks"] = sampler.stop()
+            marks["end"] = (engine.launches, engine.h2d_bytes, engine.d2h_bytes)
+            marks["timers"], engine.timers = engine.timers, None
+
+    if dist is not None:
+        dist.barrier()
+    trace = poisson_trace(args.qps, 3600.0, seed=args.seed + 1000 * rank, lexicon=lex)
+    run = serve(mods, cfg, trace, warmup_iters=args.warmup, warmup_seconds=args.warmup_seconds,
+                timed_iters=args.steps, on_window=on_window, drain_seconds=args.drain_seconds)
+    torch.cuda.synchronize()
+    t0, t1 = run.window
+    inside = [r for r in run.timings if t0 <= r.send_time < t1]
+    fcl = [1e3 * r.fcl for r in inside if r.fcl is not None]
+    fcl_c = [1e3 * r.fcl_client for r in inside if r.fcl_client is not None]
+    lcl = [1e3 * r.lcl for r in inside if r.lcl is not None and r.error is None]
+    rtf = [r.lcl / (r.samples / cfg.sample_rate) for r in inside
+           if r.lcl is not None and r.error is None and r.samples]
+    missing = sum(1 for r in inside if r.fcl is None)
+    window_s = t1 - t0
+    batch_sizes = [len(rep.decoder_ids) for rep in run.reports]
+
+    timers = marks.get("timers") or []
+    agg = {}
+    for kind, e0, e1, units in timers:
+        ms = e0.elapsed_time(e1)
+        a = agg.setdefault(kind, [0.0, 0.0, 0])
+        a[0] += ms
+        a[1] += units
+        a[2] += 1
 
     if dist is not None:
         gathered = [None] * world
@@ -298,18 +401,41 @@ def run_ours(args) -> None:
                              "unit": "GB/s", "frac": round(dec_gbs / peaks["hbm_gbs"], 4) if dec_gbs else None,
                              "algorithmic": "37.04 MB weights per step + per-item state/memory reads"},
         "e2e": {"value": round(c99, 3) if c99 is not None else None, "p50": c50, "unit": "ms",
-                "h2d_bytes_per_step": int((h1 - h0) / args.steps), "d2h_bytes_per_step": int((d1 - d0) / args.steps)},
-        "gpu_launches": int(l1 - l0),
+                "h2d_bytes_per_step": int(merged["h2d"] / args.steps / world),
+                "d2h_bytes_per_step": int(merged["d2h"] / args.steps / world)},
+        "gpu_launches": int(merged["launch"]),
         "clocks": marks.get("clocks"),
     }
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+    if args.sweep and world == 1:
+        line["qps_sweep"] = qps_sweep(mods, cfg, lex, args)
+        ok = [r["qps"] for r in line["qps_sweep"] if r["p99_ms"] is not None and r["p99_ms"] < 80.0]
+        ok += [args.qps] if p99 is not None and p99 < 80.0 else []
+        line["max_qps_p99_under_80ms"] = max(ok) if ok else None
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = {k: v for k, v in cpu_serving_baseline(args.qps, args.cpu_seconds, args.seed).items()
                                 if k in ("value", "unit", "cores", "kind", "sample", "p50", "served_first_chunk",
                                          "requests")}
     print(json.dumps(line), flush=True)
+
+
+def qps_sweep(mods, cfg, lex, args) -> list[dict]:
+    """Shorter runs at each sweep QPS (same engine) -> p50/p99 FCL; stops after the first overload."""
+    from paper_2211_13939_b200.harness import poisson_trace, serve
+    rows = []
+    for q in [float(x) for x in args.sweep.split(",") if x]:
+        run = serve(mods, cfg, poisson_trace(q, 3600.0, seed=args.seed + int(q), lexicon=lex), warmup_iters=3,
+                    warmup_seconds=4.0, timed_iters=args.sweep_steps, drain_seconds=2.0)
+        t0, t1 = run.window
+        fcl = [1e3 * r.fcl for r in run.timings if t0 <= r.send_time < t1 and r.fcl is not None]
+        p50, p99 = _percentiles(fcl)
+        rows.append({"qps": q, "p50_ms": p50, "p99_ms": p99, "requests": len(fcl),
+                     "ms_per_step": round(1e3 * (t1 - t0) / args.sweep_steps, 3)})
+        if p99 is None or p99 > 200.0:
+            break
+    return rows
 
 
 def main() -> None:
@@ -325,6 +451,8 @@ def main() -> None:
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", default="110,120,130,140,150", help="extra QPS levels for max-QPS (empty: off)")
+    ap.add_argument("--sweep-steps", type=int, default=150)
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -74,6 +74,7 @@ class RequestTiming:
     samples: int = 0
     chunks: int = 0
     error: str | None = None
+    done: bool = False
 
     @property
     def fcl(self) -> float | None:
@@ -153,6 +154,7 @@ def serve(modules: PipelineModules, cfg, trace: list[TimedRequest], *, warmup_it
                 rec.chunks += 1
         except Exception as exc:  # noqa: BLE001 -- recorded, reported by the caller
             rec.error = str(exc)
+        rec.done = True
 
     with loop, ThreadPoolExecutor(max_workers=max_clients, thread_name_prefix="client") as clients:
         origin = time.perf_counter()
@@ -161,7 +163,7 @@ def serve(modules: PipelineModules, cfg, trace: list[TimedRequest], *, warmup_it
             now = time.perf_counter()
             if run.window is not None and run.window[1] is not None:
                 inside = [r for r in run.timings if run.window[0] <= r.send_time < run.window[1]]
-                if all(r.last_recv is not None or r.error for r in inside) or now - run.window[1] > drain_seconds:
+                if all(r.done for r in inside) or now - run.window[1] > drain_seconds:
                     break
             rid, stream = loop.submit(req.text)
             rec = RequestTiming(rid, req.text, time.perf_counter())
@@ -177,3 +179,26 @@ def serve(modules: PipelineModules, cfg, trace: list[TimedRequest], *, warmup_it
                 run.timings.append(rec)
             clients.submit(consume, rec, stream)
     return run
+
+
+def merge_rank_stats(local: dict, dist=None) -> dict | None:
+    """Multi-rank bench aggregation (one pool per GPU, no data-path collective).
+
+    ``local`` holds this rank's per-request latency lists (``fcl``, ``fcl_c``,
+    ``lcl``, ``rtf``), its timed-window length ``window`` and counters.  Rank 0
+    receives the concatenated lists, the MAX window over ranks (device time of
+    the slowest rank) and summed counters; other ranks get None.
+    """
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return dict(local)
+    world = dist.get_world_size()
+    gathered = [None] * world
+    dist.all_gather_object(gathered, local)
+    if dist.get_rank() != 0:
+        return None
+    merged = {k: [x for g in gathered for x in g[k]] for k in ("fcl", "fcl_c", "lcl", "rtf")}
+    merged["window"] = max(g["window"] for g in gathered)
+    for k in ("missing", "launch", "h2d", "d2h"):
+        merged[k] = sum(g.get(k, 0) for g in gathered)
+    merged["per_rank_window"] = [g["window"] for g in gathered]
+    return merged
