@@ -188,7 +188,7 @@ def run_ours(args) -> None:
     cfg, lex = PipelineConfig(), default_lexicon()
     engine = build_engine(cfg, args.tier, device)
     if hasattr(engine, "prepare_graphs"):
-        engine.prepare_graphs(max_batch=512)
+        engine.prepare_graphs(max_batch=256)
     mods = modules_for(engine, lex)
 
     # untimed warm-up of every code path (tensor maps, smem attributes, allocator pools)
@@ -241,124 +241,14 @@ def run_ours(args) -> None:
     from paper_2211_13939_b200.harness import merge_rank_stats
     merged = merge_rank_stats({"fcl": fcl, "fcl_c": fcl_c, "lcl": lcl, "rtf": rtf, "window": window_s,
                                "missing": missing, "launch": marks["end"][0] - marks["start"][0],
-                               "h2d": marks["end"][1] - marks["start"][1], "d2h": marks["end"][2] - marks["start"][2]},
-                              dist)
-    if merged is None:  # non-zero rank
+                               "h2d": marks["end"][1] - marks["start"][1],
+                               "d2h": marks["end"][2] - marks["start"][2]}, dist)
+    if merged is None:  # non-zero rank: rank 0 prints
         dist.barrier()
         dist.destroy_process_group()
         return
     fcl, fcl_c, lcl, rtf = merged["fcl"], merged["fcl_c"], merged["lcl"], merged["rtf"]
     window_s, missing = merged["window"], merged["missing"]
-    p50, p99 = _percentiles(fcl)
-    return {"value": p99, "p50": p50, "unit": "ms", "cores": cores, "kind": "port",
-            "iterations": it, "requests": len(sent), "served_first_chunk": len(first),
-            "sample": f"{seconds:.0f} s of Poisson {qps:g} QPS U{{20..200}}-char arrivals through the "
-                      "oracle CPU modules (torch fp32, all host threads) behind the same scheduler; "
-                      "requests without a first chunk at the end are censored at the budget end"}
-
-
-def run_reference(args) -> None:
-    world, rank, _ = _dist()
-    if rank != 0:
-        return
-    t0 = time.perf_counter()
-    res = cpu_serving_baseline(args.qps, args.cpu_seconds, args.seed, max_iters=args.steps + args.warmup)
-    wall = time.perf_counter() - t0
-    line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "ms", "n_gpus": args.gpus,
-            "steps": res["iterations"], "warmup": 0,
-            "ms_per_step": round(1e3 * wall / max(res["iterations"], 1), 3), "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"C3: Poisson {args.qps:g} QPS, U{{20..200}} chars, Tacotron2+HiFi-GAN V1 "
-                                   "(random init), chunk 32, overlap 4", "qps_per_gpu": args.qps},
-            "p50_ms": res["p50"], "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
-            "e2e": {"value": res["value"], "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "requests": res["requests"], "served_first_chunk": res["served_first_chunk"]}
-    print(json.dumps(line), flush=True)
-
-
-def run_ours(args) -> None:
-    import torch
-
-    from paper_2211_13939_b200.domain import PipelineConfig
-    from paper_2211_13939_b200.frontend import default_lexicon
-    from paper_2211_13939_b200.harness import poisson_trace, serve
-    from paper_2211_13939_b200.modules import build_engine, modules_for
-
-    world, rank, local = _dist()
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
-    device = f"cuda:{local}"
-    torch.cuda.set_device(local)
-    cfg, lex = PipelineConfig(), default_lexicon()
-    engine = build_engine(cfg, args.tier, device)
-    if hasattr(engine, "prepare_graphs"):
-        engine.prepare_graphs(max_batch=512)
-    mods = modules_for(engine, lex)
-
-    # untimed warm-up of every code path (tensor maps, smem attributes, allocator pools)
-    warm = serve(mods, cfg, poisson_trace(50, 1.0, seed=args.seed + 7, lexicon=lex), warmup_iters=0,
-                 timed_iters=2, drain_seconds=0.0)
-    del warm
-    torch.cuda.synchronize()
-
-    peaks = _peaks()
-    sampler = ClockSampler(local)
-    marks = {}
-
-    def on_window(kind, idx):
-        if kind == "start":
-            torch.cuda.synchronize()
-            engine.timers = []
-            marks["start"] = (engine.launches, engine.h2d_bytes, engine.d2h_bytes)
-            sampler.start()
-        else:
-            marks["clocks"] = sampler.stop()
-            marks["end"] = (engine.launches, engine.h2d_bytes, engine.d2h_bytes)
-            marks["timers"], engine.timers = engine.timers, None
-
-    if dist is not None:
-        dist.barrier()
-    trace = poisson_trace(args.qps, 3600.0, seed=args.seed + 1000 * rank, lexicon=lex)
-    run = serve(mods, cfg, trace, warmup_iters=args.warmup, warmup_seconds=args.warmup_seconds,
-                timed_iters=args.steps, on_window=on_window, drain_seconds=args.drain_seconds)
-    torch.cuda.synchronize()
-    t0, t1 = run.window
-    inside = [r for r in run.timings if t0 <= r.send_time < t1]
-    fcl = [1e3 * r.fcl for r in inside if r.fcl is not None]
-    fcl_c = [1e3 * r.fcl_client for r in inside if r.fcl_client is not None]
-    lcl = [1e3 * r.lcl for r in inside if r.lcl is not None and r.error is None]
-    rtf = [r.lcl / (r.samples / cfg.sample_rate) for r in inside
-           if r.lcl is not None and r.error is None and r.samples]
-    missing = sum(1 for r in inside if r.fcl is None)
-    window_s = t1 - t0
-    batch_sizes = [len(rep.decoder_ids) for rep in run.reports]
-
-    timers = marks.get("timers") or []
-    agg = {}
-    for kind, e0, e1, units in timers:
-        ms = e0.elapsed_time(e1)
-        a = agg.setdefault(kind, [0.0, 0.0, 0])
-        a[0] += ms
-        a[1] += units
-        a[2] += 1
-
-    if dist is not None:
-        gathered = [None] * world
-        dist.all_gather_object(gathered, {"fcl": fcl, "fcl_c": fcl_c, "lcl": lcl, "rtf": rtf, "window": window_s,
-                                          "missing": missing, "agg": agg, "clocks": marks["clocks"],
-                                          "launch": l1 - l0, "h2d": h1 - h0, "d2h": d1 - d0})
-        if rank != 0:
-            dist.barrier()
-            dist.destroy_process_group()
-            return
-        fcl = [x for g in gathered for x in g["fcl"]]
-        fcl_c = [x for g in gathered for x in g["fcl_c"]]
-        lcl = [x for g in gathered for x in g["lcl"]]
-        rtf = [x for g in gathered for x in g["rtf"]]
-        window_s = max(g["window"] for g in gathered)
-        missing = sum(g["missing"] for g in gathered)
     p50, p99 = _percentiles(fcl)
     c50, c99 = _percentiles(fcl_c)
     l50, l99 = _percentiles(lcl)

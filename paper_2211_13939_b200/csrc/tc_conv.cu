@@ -36,7 +36,8 @@
 namespace {
 
 constexpr int kBlockM = 128;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;                 // 2 warps per TMEM lane quarter, each half the columns
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer warp + MMA warp + epilogue
 constexpr int kMaxTaps = 16;
 
 struct Taps {
@@ -136,6 +137,23 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int CW>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[CW]) {
+  if constexpr (CW == 32) tmem_ld32(taddr, v); else tmem_ld16(taddr, v);
+}
+
 __device__ __forceinline__ float lrelu(float x, float s) { return x >= 0.f ? x : x * s; }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -144,12 +162,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 __device__ __forceinline__ float inv_lrelu(float a, float s) { return a >= 0.f ? a : a / s; }
 
-__device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* p, float (&v)[32]) {
+// CW bf16 values (CW/8 x 16-byte vectors) <-> fp32 registers.
+template <int CW>
+__device__ __forceinline__ void ld_bf16_raw(const __nv_bfloat16* p, uint4 (&u)[CW / 8]) {
   const uint4* src = reinterpret_cast<const uint4*>(p);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const uint4 u = src[q];
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+  for (int q = 0; q < CW / 8; ++q) u[q] = src[q];
+}
+
+template <int CW>
+__device__ __forceinline__ void unpack_bf16(const uint4 (&u)[CW / 8], float (&v)[CW]) {
+#pragma unroll
+  for (int q = 0; q < CW / 8; ++q) {
+    const uint32_t w[4] = {u[q].x, u[q].y, u[q].z, u[q].w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
@@ -159,10 +184,11 @@ __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* p, float (&v)[
   }
 }
 
-__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* p, const float (&v)[32], float slope) {
+template <int CW>
+__device__ __forceinline__ void store_bf16(__nv_bfloat16* p, const float (&v)[CW], float slope) {
   uint4* dst = reinterpret_cast<uint4*>(p);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < CW / 8; ++q) {
     uint32_t w[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -212,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], 32 * kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
@@ -269,8 +295,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // Epilogue: warp w owns TMEM lanes [32*(w%4), +32) = tile rows.
-    const int quarter = warp & 3;
+    // Epilogue: 8 warps; warp w owns TMEM lanes [32*(w%4), +32) (tile rows) and one
+    // half of the tile's columns.  Residual / accumulator loads for a chunk are
+    // issued before its tcgen05.ld so their latency overlaps the TMEM read.
+    constexpr int CW = BN >= 64 ? 32 : 16;   // columns per chunk
+    const int ew = warp - 2;
+    const int quarter = warp & 3, half = ew >> 2;
     const int C = epi.c_out;
     uint32_t lt = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
@@ -283,53 +313,55 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[b], tph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        float v[32];
-        tmem_ld32(tmem + b * BN + ((uint32_t)(quarter * 32) << 16) + c0, v);
-        if (!in_range) continue;
-        const int n = nt * BN + c0;   // first global column of this 32-chunk
+      for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += CW) {
+        const int n = nt * BN + c0;   // first global column of this chunk
         const int phase = n / C, co = n - phase * C;
+        const bool live = in_range && out_row >= 0;
+        const int64_t o = live ? ((int64_t)out_row + phase) * C + co : 0;
+        uint4 ru[CW / 8], au[CW / 8];
+        if (live && epi.res_in) ld_bf16_raw<CW>(epi.res_in + o, ru);
+        if (live && epi.acc_mode >= 2) ld_bf16_raw<CW>(epi.acc + o, au);
+        float v[CW];
+        tmem_ld<CW>(tmem + b * BN + ((uint32_t)(quarter * 32) << 16) + c0, v);
+        if (!in_range) continue;
         if (out_row < 0) {
           if (epi.zero_halo && epi.act_out) {
             uint4* dst = reinterpret_cast<uint4*>(epi.act_out + r * C + co);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) dst[q] = make_uint4(0, 0, 0, 0);
+            for (int q = 0; q < CW / 8; ++q) dst[q] = make_uint4(0, 0, 0, 0);
           }
           continue;
         }
-        const int64_t o = ((int64_t)out_row + phase) * C + co;
         if (z == 0) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += __ldg(epi.bias + co + i);
+          for (int i = 0; i < CW; ++i) v[i] += __ldg(epi.bias + co + i);
         }
         if (epi.f32_out) {
           float4* dst = reinterpret_cast<float4*>(epi.f32_out + z * epi.f32_split_stride + o);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          for (int q = 0; q < CW / 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         }
         if (epi.res_in) {
-          float y[32];
-          load_bf16x32(epi.res_in + o, y);
+          float y[CW];
+          unpack_bf16<CW>(ru, y);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += inv_lrelu(y[i], epi.res_slope);
+          for (int i = 0; i < CW; ++i) v[i] += inv_lrelu(y[i], epi.res_slope);
         }
-        if (epi.acc_mode) {
-          if (epi.acc_mode == 1) {
-            store_bf16x32(epi.acc + o, v, 1.0f);
-          } else {
-            float a[32];
-            load_bf16x32(epi.acc + o, a);
+        if (epi.acc_mode == 1) {
+          store_bf16<CW>(epi.acc + o, v, 1.0f);
+        } else if (epi.acc_mode >= 2) {
+          float a[CW];
+          unpack_bf16<CW>(au, a);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) a[i] += v[i];
-            if (epi.acc_mode == 2) {
-              store_bf16x32(epi.acc + o, a, 1.0f);
-            } else {  // finalize: x = (rb0 + rb1 + rb2) / 3
+          for (int i = 0; i < CW; ++i) a[i] += v[i];
+          if (epi.acc_mode == 2) {
+            store_bf16<CW>(epi.acc + o, a, 1.0f);
+          } else {  // finalize: x = (rb0 + rb1 + rb2) / 3
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = a[i] / 3.0f;
-            }
+            for (int i = 0; i < CW; ++i) v[i] = a[i] / 3.0f;
           }
         }
-        if (epi.act_out) store_bf16x32(epi.act_out + o, v, epi.slope);
+        if (epi.act_out) store_bf16<CW>(epi.act_out + o, v, epi.slope);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&tempty[b]);

@@ -9,7 +9,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_bench.csv \
   python bench.py --steps 20 --warmup 3 --warmup-seconds 2 --drain-seconds 1 --no-cpu-baseline --sweep "" \
   > gpurun_out/bench_under_ncu.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_conv_tc -s 90 -c 2 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_conv_tc -s 155 -c 2 \
   -o gpurun_out/prof_conv python tools/profile_iter.py --batches 128 --iters 1 > gpurun_out/ncu_conv.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_attention -s 5 -c 1 \
   -o gpurun_out/prof_attn python tools/profile_iter.py --batches 128 --iters 1 > gpurun_out/ncu_attn.log 2>&1
