@@ -115,12 +115,14 @@ int itts_r_prenet(float* state, void* xb, const float* W0T, const float* W1T, co
 int itts_r_lstm_cell(const float* gates, int32_t nsplit, const float* bias, float* state, void* xb,
                      int32_t h_off, int32_t c_off, const int64_t* plan, int32_t B, int32_t step,
                      void* stream);
+/* query partials: Q = fp32 [8][B][128] K-slices of Wq . att_h, summed (fixed order) by
+ * itts_r_attention; proj partials = fp32 [8][B][81] scratch. */
 int itts_r_query(const float* state, const float* WqT, float* Q, int32_t B, void* stream);
 int itts_r_attention(float* state, void* xb, const int64_t* plan, int32_t B, int32_t max_len,
                      const float* Q, const float* Wloc, const float* WdT, const float* v, int32_t step,
                      void* stream);
 int itts_r_proj(float* state, const int64_t* plan, int32_t B, const float* WpT, const float* bp,
-                int32_t step, void* stream);
+                float* partials, int32_t step, void* stream);
 
 /* K5 encoder (replaces encode_batch + init_decoder_state, acoustic.py:222-231,
  * :118-133, with the Tacotron2 encoder, paper Eq. 1).  plan = int64 [n][6]

@@ -35,7 +35,7 @@ SIGNATURES: dict[str, list] = {
     "itts_r_lstm_cell": [_p, _i32, _p, _p, _p, _i32, _i32, _p, _i32, _i32, _p],
     "itts_r_query": [_p, _p, _p, _i32, _p],
     "itts_r_attention": [_p, _p, _p, _i32, _i32, _p, _p, _p, _p, _i32, _p],
-    "itts_r_proj": [_p, _p, _i32, _p, _p, _i32, _p],
+    "itts_r_proj": [_p, _p, _i32, _p, _p, _p, _i32, _p],
     "itts_r_enc_embed": [_p, _i64, _p, _i32, _i64, _p, _p, _p, _p, _p, _p],
     "itts_r_bilstm": [_p, _p, _i32, _p, _p],
     "itts_r_pmem": [_p, _i32, _i64, _p, _p],

@@ -63,6 +63,7 @@ __global__ void k_dec_prepare(const float* __restrict__ state, __nv_bfloat16* __
 // fixed order, so results do not depend on the batch composition.
 constexpr int IT = 8;
 constexpr int GW = 8;  // warps per CTA
+constexpr int QKS = 8;  // K slices of the attention query GEMV (partials summed by k_attention)
 
 struct GemvIO {
   const float* x;   // rows of the input, x_ld floats apart
@@ -77,16 +78,45 @@ struct GemvIO {
   const int64_t* plan; int step;      // proj mode: plan rows + step (mel / gate outputs)
 };
 
-template <int NPL, int MODE>  // MODE 0 generic, 1 mel/gate projection
-__global__ void __launch_bounds__(GW * 32) k_gemv(GemvIO io, int B) {
+// Epilogue of one output element (generic: bias, ReLU, fp32 + optional bf16 mirror;
+// projection mode: state.last_frame + the chunk's mel / gate outputs).
+template <int MODE>
+__device__ __forceinline__ void gemv_store(const GemvIO& io, int b, int n, float v) {
+  if (io.bias) v += io.bias[n];
+  if (MODE == 0) {
+    if (io.plan && io.step >= io.plan[b * DPLAN + 5]) return;
+    if (io.relu) v = fmaxf(v, 0.f);
+    io.y[(int64_t)b * io.y_ld + io.y_off + n] = v;
+    if (io.yb) io.yb[(int64_t)b * io.yb_ld + io.y_off + n] = __float2bfloat16_rn(v);
+  } else {
+    const int64_t* p = io.plan + b * DPLAN;
+    if (io.step >= p[5]) return;
+    if (n < NMEL) {
+      io.y[(int64_t)b * io.y_ld + LAST_OFF + n] = v;
+      reinterpret_cast<float*>(p[6])[io.step * NMEL + n] = v;
+    } else {
+      reinterpret_cast<float*>(p[7])[io.step] = v;
+    }
+  }
+}
+
+// Grid (item tiles of IT, column tiles of 32*NPL, K slices).  The CTA's 8 warps split its
+// K slice; warp partials are reduced in a fixed order.  With one K slice the epilogue is
+// applied here; otherwise partials go to `part_out` [KS][B][N] and k_gemv_finish (or the
+// consumer) sums them in slice order.
+template <int NPL, int MODE>
+__global__ void __launch_bounds__(GW * 32) k_gemv(GemvIO io, int B, float* __restrict__ part_out) {
   const int b0 = blockIdx.x * IT, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nb = min(IT, B - b0);
-  const int K = io.len0 + io.len1;
+  const int n0 = blockIdx.y * 32 * NPL;
+  const int K = io.len0 + io.len1, KS = gridDim.z;
+  const int ks0 = (int)((int64_t)K * blockIdx.z / KS), ks1 = (int)((int64_t)K * (blockIdx.z + 1) / KS);
+  const int KL = ks1 - ks0;
   extern __shared__ float sm[];
-  float* xs = sm;                       // [IT][K]
-  float* part = sm + IT * K;            // [GW][IT][NPL*32]
-  for (int i = tid; i < IT * K; i += GW * 32) {
-    const int it = i / K, k = i % K;
+  float* xs = sm;                       // [IT][KL]
+  float* part = sm + IT * KL;           // [GW][IT][32*NPL]
+  for (int i = tid; i < IT * KL; i += GW * 32) {
+    const int it = i / KL, k = ks0 + i % KL;
     float v = 0.f;
     if (it < nb) {
       const float* row = io.x + (int64_t)(b0 + it) * io.x_ld;
@@ -95,25 +125,38 @@ __global__ void __launch_bounds__(GW * 32) k_gemv(GemvIO io, int B) {
     xs[i] = v;
   }
   __syncthreads();
-  const int kw = (K + GW - 1) / GW, k0 = warp * kw, k1 = min(K, k0 + kw);
+  const int kw = (KL + GW - 1) / GW, k0 = warp * kw, k1 = min(KL, k0 + kw);
   float acc[IT][NPL];
 #pragma unroll
   for (int i = 0; i < IT; ++i)
 #pragma unroll
     for (int j = 0; j < NPL; ++j) acc[i][j] = 0.f;
-#pragma unroll 2
-  for (int k = k0; k < k1; ++k) {
-    float w[NPL];
+  int k = k0;
+  for (; k + 4 <= k1; k += 4) {  // 4*NPL independent weight loads in flight per iteration
+    float w[4][NPL];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int j = 0; j < NPL; ++j) {
+        const int n = n0 + lane + 32 * j;
+        w[u][j] = n < io.N ? __ldg(io.wT + (int64_t)(ks0 + k + u) * io.N + n) : 0.f;
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int i = 0; i < IT; ++i) {
+        const float xv = xs[i * KL + k + u];
+#pragma unroll
+        for (int j = 0; j < NPL; ++j) acc[i][j] = fmaf(w[u][j], xv, acc[i][j]);
+      }
+  }
+  for (; k < k1; ++k) {
 #pragma unroll
     for (int j = 0; j < NPL; ++j) {
-      const int n = lane + 32 * j;
-      w[j] = n < io.N ? __ldg(io.wT + (int64_t)k * io.N + n) : 0.f;
-    }
+      const int n = n0 + lane + 32 * j;
+      const float w = n < io.N ? __ldg(io.wT + (int64_t)(ks0 + k) * io.N + n) : 0.f;
 #pragma unroll
-    for (int i = 0; i < IT; ++i) {
-      const float xv = xs[i * K + k];
-#pragma unroll
-      for (int j = 0; j < NPL; ++j) acc[i][j] = fmaf(w[j], xv, acc[i][j]);
+      for (int i = 0; i < IT; ++i) acc[i][j] = fmaf(w, xs[i * KL + k], acc[i][j]);
     }
   }
 #pragma unroll
@@ -121,40 +164,42 @@ __global__ void __launch_bounds__(GW * 32) k_gemv(GemvIO io, int B) {
 #pragma unroll
     for (int j = 0; j < NPL; ++j) part[(warp * IT + i) * (NPL * 32) + lane + 32 * j] = acc[i][j];
   __syncthreads();
-  for (int e = tid; e < nb * io.N; e += GW * 32) {
-    const int it = e / io.N, n = e % io.N, b = b0 + it;
-    float v = part[it * (NPL * 32) + n];
+  for (int e = tid; e < nb * NPL * 32; e += GW * 32) {
+    const int it = e / (NPL * 32), c = e % (NPL * 32), n = n0 + c, b = b0 + it;
+    if (n >= io.N) continue;
+    float v = part[it * (NPL * 32) + c];
 #pragma unroll
-    for (int w = 1; w < GW; ++w) v += part[(w * IT + it) * (NPL * 32) + n];
-    if (io.bias) v += io.bias[n];
-    if (MODE == 0) {
-      if (io.plan && io.step >= io.plan[b * DPLAN + 5]) continue;
-      if (io.relu) v = fmaxf(v, 0.f);
-      io.y[(int64_t)b * io.y_ld + io.y_off + n] = v;
-      if (io.yb) io.yb[(int64_t)b * io.yb_ld + io.y_off + n] = __float2bfloat16_rn(v);
-    } else {
-      const int64_t* p = io.plan + b * DPLAN;
-      if (io.step >= p[5]) continue;
-      if (n < NMEL) {
-        io.y[(int64_t)b * io.y_ld + LAST_OFF + n] = v;
-        reinterpret_cast<float*>(p[6])[io.step * NMEL + n] = v;
-      } else {
-        reinterpret_cast<float*>(p[7])[io.step] = v;
-      }
-    }
+    for (int w = 1; w < GW; ++w) v += part[(w * IT + it) * (NPL * 32) + c];
+    if (KS == 1) gemv_store<MODE>(io, b, n, v);
+    else part_out[((int64_t)blockIdx.z * B + b) * io.N + n] = v;
   }
 }
 
+template <int MODE>
+__global__ void k_gemv_finish(GemvIO io, int B, int KS, const float* __restrict__ part) {
+  const int e = blockIdx.x * 256 + threadIdx.x;
+  if (e >= B * io.N) return;
+  const int b = e / io.N, n = e % io.N;
+  float v = part[e];
+  for (int z = 1; z < KS; ++z) v += part[(int64_t)z * B * io.N + e];
+  gemv_store<MODE>(io, b, n, v);
+}
+
+// part: scratch of KS*B*N floats (only when KS > 1).  finish=false leaves the partials
+// for the consumer (the attention kernel sums query slices itself).
 template <int NPL, int MODE>
-int launch_gemv(const GemvIO& io, int B, cudaStream_t st) {
+int launch_gemv(const GemvIO& io, int B, int KS, float* part, bool finish, cudaStream_t st) {
   const int K = io.len0 + io.len1;
-  const size_t smem = (size_t)(IT * K + GW * IT * NPL * 32) * 4;
-  static size_t configured = 0;
-  if (smem > configured) {
+  const int KL = (K + KS - 1) / KS + 1;
+  const size_t smem = (size_t)(IT * KL + GW * IT * NPL * 32) * 4;
+  static bool configured = false;
+  if (!configured) {
     cudaFuncSetAttribute(k_gemv<NPL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = 200 * 1024;
+    configured = true;
   }
-  k_gemv<NPL, MODE><<<(B + IT - 1) / IT, GW * 32, smem, st>>>(io, B);
+  dim3 grid((B + IT - 1) / IT, (io.N + 32 * NPL - 1) / (32 * NPL), KS);
+  k_gemv<NPL, MODE><<<grid, GW * 32, smem, st>>>(io, B, part);
+  if (KS > 1 && finish) k_gemv_finish<MODE><<<(B * io.N + 255) / 256, 256, 0, st>>>(io, B, KS, part);
   ITTS_RETURN_LAUNCH();
 }
 
@@ -181,62 +226,66 @@ __global__ void __launch_bounds__(256) k_lstm_cell(const float* __restrict__ G, 
   xb[(int64_t)b * XB_ROW + h_off + j] = __float2bfloat16_rn(h);
 }
 
-// One CTA (16 warps) per item.  Q [B][128] (query, from k_gemv), Wloc [32][2][31],
-// WdT [32][128], v [128].  Dynamic smem: W_prev, W_acc, energies (3L) + location
-// features [L][33].
-constexpr int AT_WARPS = 16;
-constexpr int LT = 256;  // positions per location-feature tile
+// One 4-CTA cluster per item (8 warps each): CTA r owns text positions [r*L/4, (r+1)*L/4)
+// for the location features, energies, softmax numerators and the partial context; the
+// softmax max / sum and the context are reduced across the cluster through distributed
+// shared memory in rank order (deterministic, independent of the batch).
+// Q = query K-slice partials [QKS][B][128], Wloc [32][2][31], WdT [32][128], v [128].
+constexpr int AT_CL = 4;
+constexpr int AT_WARPS = 8;
+constexpr int LT = 128;  // positions per location-feature tile
 
-__global__ void __launch_bounds__(AT_WARPS * 32) k_attention(float* __restrict__ state, __nv_bfloat16* __restrict__ xb,
-                                                             const int64_t* __restrict__ plan,
-                                                             const float* __restrict__ Q,
-                                                             const float* __restrict__ Wloc,
-                                                             const float* __restrict__ WdT,
-                                                             const float* __restrict__ v, int step) {
-  constexpr int NT = AT_WARPS * 32;
-  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+__global__ void __cluster_dims__(AT_CL, 1, 1) __launch_bounds__(AT_WARPS * 32)
+    k_attention(float* __restrict__ state, __nv_bfloat16* __restrict__ xb, const int64_t* __restrict__ plan,
+                const float* __restrict__ Q, const float* __restrict__ Wloc, const float* __restrict__ WdT,
+                const float* __restrict__ v, int step) {
+  constexpr int NT = AT_WARPS * 32, HALO = (KLOC - 1) / 2;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int b = blockIdx.x / AT_CL, B = gridDim.x / AT_CL;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t* p = plan + b * DPLAN;
-  if (step >= p[5]) return;
+  if (step >= p[5]) return;  // the whole cluster returns together
   const float* mem = reinterpret_cast<const float*>(p[0]);
   const float* pm = reinterpret_cast<const float*>(p[1]);
   const int L = (int)p[2];
   const float* wsrc = reinterpret_cast<const float*>(step == 0 ? p[3] : p[4]);
   float* wdst = reinterpret_cast<float*>(p[4]);
-  float* s = state + (int64_t)b * ROW;
+  const int t_lo = (int)((int64_t)L * rank / AT_CL), t_hi = (int)((int64_t)L * (rank + 1) / AT_CL);
+  const int Ls = t_hi - t_lo, Lh = Ls + 2 * HALO;
 
   extern __shared__ float dyn[];
-  float* w_prev = dyn;
-  float* w_acc = dyn + L;
-  float* e = dyn + 2 * L;
-  float* locf = dyn + ((3 * L + 3) & ~3);  // [LT][33]; later reused for the context partials
+  float* w_prev = dyn;             // [Lh] positions t_lo-HALO .. t_hi+HALO (zero outside [0, L))
+  float* w_acc = dyn + Lh;         // [Lh]
+  float* e = dyn + 2 * Lh;         // [Ls]
+  float* locf = dyn + ((2 * Lh + Ls + 3) & ~3);  // [LT][33]; later the context partials
   __shared__ float q[ATT], sWloc[NF * 2 * KLOC], sWd[NF * ATT], sv[ATT], red[32];
-  float4 (*cpart)[EMB / 4] = reinterpret_cast<float4 (*)[EMB / 4]>(locf);  // [AT_WARPS][128]
+  __shared__ float cl_max[AT_CL], cl_sum[AT_CL];
+  __shared__ __align__(16) float ctx_local[EMB];
 
-  for (int i = tid; i < L; i += NT) {
-    w_prev[i] = wsrc[i];
-    w_acc[i] = wsrc[L + i];
+  for (int i = tid; i < Lh; i += NT) {
+    const int t = t_lo - HALO + i;
+    const bool in = t >= 0 && t < L;
+    w_prev[i] = in ? wsrc[t] : 0.f;
+    w_acc[i] = in ? wsrc[L + t] : 0.f;
   }
   if (tid < ATT) {
-    q[tid] = Q[(int64_t)b * ATT + tid];
+    float qa = Q[(int64_t)b * ATT + tid];
+    for (int z = 1; z < QKS; ++z) qa += Q[((int64_t)z * B + b) * ATT + tid];  // query K-slices, fixed order
+    q[tid] = qa;
     sv[tid] = v[tid];
   }
   for (int i = tid; i < NF * 2 * KLOC; i += NT) sWloc[i] = Wloc[i];
   for (int i = tid; i < NF * ATT; i += NT) sWd[i] = WdT[i];
   __syncthreads();
-  // Tiles of LT positions: location features (conv1d over [W_prev, W_acc], 2 -> 32
-  // filters, k 31, pad 15; one (t, f) per thread) then energies
-  // e_t = v . tanh(q + W_d loc_t + pm_t) (one warp per position, 4 dims per lane).
-  for (int t0 = 0; t0 < L; t0 += LT) {
-    const int nt = min(LT, L - t0);
+  for (int t0 = 0; t0 < Ls; t0 += LT) {
+    const int nt = min(LT, Ls - t0);
     for (int i = tid; i < nt * NF; i += NT) {
-      const int t = t0 + i / NF, f = i % NF;
+      const int tl = t0 + i / NF, f = i % NF;  // local position; halo index = tl + k
       const float* wf = sWloc + f * 2 * KLOC;
       float c = 0.f;
-      const int k_lo = max(0, (KLOC - 1) / 2 - t), k_hi = min(KLOC, L + (KLOC - 1) / 2 - t);
-      for (int k = k_lo; k < k_hi; ++k) {
-        const int u = t + k - (KLOC - 1) / 2;
-        c = fmaf(wf[k], w_prev[u], fmaf(wf[KLOC + k], w_acc[u], c));
-      }
+#pragma unroll
+      for (int k = 0; k < KLOC; ++k) c = fmaf(wf[k], w_prev[tl + k], fmaf(wf[KLOC + k], w_acc[tl + k], c));
       locf[(i / NF) * (NF + 1) + f] = c;
     }
     __syncthreads();
@@ -253,47 +302,59 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attention(float* __restrict__
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int a = lane + 32 * i;
-        en = fmaf(sv[a], tanhf((q[a] + loc[i]) + pm[(int64_t)(t0 + tt) * ATT + a]), en);
+        en = fmaf(sv[a], tanhf((q[a] + loc[i]) + pm[(int64_t)(t_lo + t0 + tt) * ATT + a]), en);
       }
       en = itts::warp_sum(en);
       if (lane == 0) e[t0 + tt] = en;
     }
     __syncthreads();
   }
+  // softmax over the whole text: cluster max, then cluster sum (rank order)
   float lmax = -INFINITY;
-  for (int t = tid; t < L; t += NT) lmax = fmaxf(lmax, e[t]);
-  const float M = itts::block_reduce<float, true>(lmax, red);
+  for (int t = tid; t < Ls; t += NT) lmax = fmaxf(lmax, e[t]);
+  lmax = itts::block_reduce<float, true>(lmax, red);
+  if (tid < AT_CL) *cluster.map_shared_rank(&cl_max[rank], tid) = lmax;
+  cluster.sync();
+  float M = cl_max[0];
+#pragma unroll
+  for (int r = 1; r < AT_CL; ++r) M = fmaxf(M, cl_max[r]);
   float lsum = 0.f;
-  for (int t = tid; t < L; t += NT) {
+  for (int t = tid; t < Ls; t += NT) {
     const float x = expf(e[t] - M);
     e[t] = x;
     lsum += x;
   }
-  const float Z = itts::block_reduce<float, false>(lsum, red);
-  for (int t = tid; t < L; t += NT) {
+  lsum = itts::block_reduce<float, false>(lsum, red);
+  if (tid < AT_CL) *cluster.map_shared_rank(&cl_sum[rank], tid) = lsum;
+  cluster.sync();
+  float Z = cl_sum[0];
+#pragma unroll
+  for (int r = 1; r < AT_CL; ++r) Z += cl_sum[r];
+  for (int t = tid; t < Ls; t += NT) {
     const float a = e[t] / Z;
     e[t] = a;
-    wdst[t] = a;
-    wdst[L + t] = w_acc[t] + a;
+    wdst[t_lo + t] = a;
+    wdst[L + t_lo + t] = w_acc[HALO + t] + a;
   }
   __syncthreads();
-  // context = sum_t a_t memory[t]: warp w takes rows t = w (mod 16), lane holds 16 dims (4 float4)
+  // partial context over this CTA's positions: warp w takes rows t = w (mod 8), lane 16 dims
   float4 acc[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
   const float4* mem4 = reinterpret_cast<const float4*>(mem);
-#pragma unroll 2
-  for (int t = warp; t < L; t += AT_WARPS) {
+#pragma unroll 4
+  for (int t = warp; t < Ls; t += AT_WARPS) {
     const float a = e[t];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const float4 m4 = mem4[(int64_t)t * (EMB / 4) + lane + 32 * j];
+      const float4 m4 = mem4[(int64_t)(t_lo + t) * (EMB / 4) + lane + 32 * j];
       acc[j].x = fmaf(a, m4.x, acc[j].x);
       acc[j].y = fmaf(a, m4.y, acc[j].y);
       acc[j].z = fmaf(a, m4.z, acc[j].z);
       acc[j].w = fmaf(a, m4.w, acc[j].w);
     }
   }
+  float4 (*cpart)[EMB / 4] = reinterpret_cast<float4 (*)[EMB / 4]>(locf);  // [AT_WARPS][128]
 #pragma unroll
   for (int j = 0; j < 4; ++j) cpart[warp][lane + 32 * j] = acc[j];
   __syncthreads();
@@ -302,9 +363,20 @@ __global__ void __launch_bounds__(AT_WARPS * 32) k_attention(float* __restrict__
     float c = cp[d];
 #pragma unroll
     for (int w = 1; w < AT_WARPS; ++w) c += cp[w * EMB + d];
-    s[CTX_OFF + d] = c;
-    xb[(int64_t)b * XB_ROW + CTX_OFF + d] = __float2bfloat16_rn(c);
+    ctx_local[d] = c;
   }
+  cluster.sync();
+  if (rank == 0) {
+    float* s = state + (int64_t)b * ROW;
+    for (int d = tid; d < EMB; d += NT) {
+      float c = ctx_local[d];
+#pragma unroll
+      for (int r = 1; r < AT_CL; ++r) c += cluster.map_shared_rank(ctx_local, r)[d];
+      s[CTX_OFF + d] = c;
+      xb[(int64_t)b * XB_ROW + CTX_OFF + d] = __float2bfloat16_rn(c);
+    }
+  }
+  cluster.sync();  // keep every CTA's shared memory alive until rank 0 has read it
 }
 
 // ----------------------------------------------------------------- encoder
@@ -515,16 +587,17 @@ ITTS_API int itts_r_prenet(float* state, void* xb, const float* W0T, const float
   if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   GemvIO a{state, ROW, LAST_OFF, NMEL, 0, 0, W0T, PRE, H1, PRE, 0, nullptr, 0, nullptr, 1, nullptr, step};
-  int r = launch_gemv<8, 0>(a, B, st);
+  int r = launch_gemv<1, 0>(a, B, 1, nullptr, false, st);
   if (r) return r;
   GemvIO c{H1, PRE, 0, PRE, 0, 0, W1T, PRE, state, ROW, P_OFF, (__nv_bfloat16*)xb, XB_ROW, nullptr, 1, plan, step};
-  return launch_gemv<8, 0>(c, B, st);
+  return launch_gemv<1, 0>(c, B, 1, nullptr, false, st);
 }
 
-ITTS_API int itts_r_query(const float* state, const float* WqT, float* Q, int32_t B, void* stream) {
+// Query q = Wq . att_h as QKS K-slice partials Qp [QKS][B][128] (summed by k_attention).
+ITTS_API int itts_r_query(const float* state, const float* WqT, float* Qp, int32_t B, void* stream) {
   if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
-  GemvIO io{state, ROW, ATTH_OFF, HID, 0, 0, WqT, ATT, Q, ATT, 0, nullptr, 0, nullptr, 0, nullptr, 0};
-  return launch_gemv<4, 0>(io, B, (cudaStream_t)stream);
+  GemvIO io{state, ROW, ATTH_OFF, HID, 0, 0, WqT, ATT, nullptr, ATT, 0, nullptr, 0, nullptr, 0, nullptr, 0};
+  return launch_gemv<1, 0>(io, B, QKS, Qp, false, (cudaStream_t)stream);
 }
 
 ITTS_API int itts_r_lstm_cell(const float* G, int32_t nsplit, const float* bias, float* state, void* xb,
@@ -541,24 +614,27 @@ ITTS_API int itts_r_attention(float* state, void* xb, const int64_t* plan, int32
                               const float* Q, const float* Wloc, const float* WdT, const float* v,
                               int32_t step, void* stream) {
   if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
+  const int ls = (max_len + AT_CL - 1) / AT_CL + 1, lh = ls + KLOC;
+  const size_t smem = ((size_t)(2 * lh + ls + 4) + (size_t)LT * (NF + 1)) * sizeof(float);
   static_assert(LT * (NF + 1) >= AT_WARPS * EMB, "context partials alias the location tile");
-  const size_t smem = ((size_t)3 * max_len + 4 + (size_t)LT * (NF + 1)) * sizeof(float);
-  if (smem > 160 * 1024) return ITTS_EUNSUPPORTED;  // L <= ~10,900 phonemes per request
+  if (smem > 150 * 1024) return ITTS_EUNSUPPORTED;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024);
     configured = true;
   }
-  k_attention<<<B, AT_WARPS * 32, smem, (cudaStream_t)stream>>>(state, (__nv_bfloat16*)xb, plan, Q, Wloc, WdT, v,
-                                                                step);
+  k_attention<<<B * AT_CL, AT_WARPS * 32, smem, (cudaStream_t)stream>>>(state, (__nv_bfloat16*)xb, plan, Q, Wloc,
+                                                                        WdT, v, step);
   ITTS_RETURN_LAUNCH();
 }
 
+// Mel/gate projection; Pp = scratch [PKS][B][81].
+constexpr int PKS = 8;
 ITTS_API int itts_r_proj(float* state, const int64_t* plan, int32_t B, const float* WpT, const float* bp,
-                         int32_t step, void* stream) {
+                         float* Pp, int32_t step, void* stream) {
   if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
   GemvIO io{state, ROW, DECH_OFF, HID, CTX_OFF, EMB, WpT, NMEL + 1, state, ROW, 0, nullptr, 0, bp, 0, plan, step};
-  return launch_gemv<3, 1>(io, B, (cudaStream_t)stream);
+  return launch_gemv<1, 1>(io, B, PKS, Pp, true, (cudaStream_t)stream);
 }
 
 ITTS_API int itts_r_enc_embed(const int32_t* tok4, int64_t total, const int64_t* plan, int32_t n,

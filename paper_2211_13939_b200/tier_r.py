@@ -45,7 +45,7 @@ MRF_HALO = 25       # k11 dilation 5
 UPS = (8, 8, 2, 2)
 STAGE_C = (256, 128, 64, 32)
 DEC_KSPLIT = 4      # K-split of the decoder gate GEMMs (partials summed in fixed order by the cell kernel)
-GRAPH_MAX_L = 4096  # attention smem is sized for this in captured graphs; longer texts run eagerly
+GRAPH_MAX_L = 8192  # attention smem is sized for this in captured graphs; longer texts run eagerly
 
 
 def _hifigan_macs_per_frame() -> int:
@@ -364,7 +364,7 @@ class TierREngine:
             self._call("itts_r_lstm_cell", b.G.data_ptr(), DEC_KSPLIT, self.dec_bias.data_ptr(), b.work.data_ptr(),
                        b.xbm.data_ptr(), DECH_OFF, DECC_OFF, b.d_plan.data_ptr(), n, step, st)
             self._call("itts_r_proj", b.work.data_ptr(), b.d_plan.data_ptr(), n, self.WpT.data_ptr(),
-                       self.bp.data_ptr(), step, st)
+                       self.bp.data_ptr(), b.P.data_ptr(), step, st)
         self._call("itts_scatter_rows", b.d_dst.data_ptr(), b.work.data_ptr(), n, 4 * ROW, st)
 
     def _dec_bucket(self, n: int) -> "_DecBucket":
@@ -555,7 +555,8 @@ class _DecBuffers:
         self.work = torch.empty(n, ROW, dtype=torch.float32, device=dev)
         self.xbm = torch.empty(n, XB_ROW, dtype=torch.bfloat16, device=dev)
         self.G = torch.empty(DEC_KSPLIT, n, 4096, dtype=torch.float32, device=dev)
-        self.Q = torch.empty(n, 128, dtype=torch.float32, device=dev)
+        self.Q = torch.empty(8, n, 128, dtype=torch.float32, device=dev)    # query K-slice partials
+        self.P = torch.empty(8, n, 81, dtype=torch.float32, device=dev)     # projection K-slice partials
         self.H1 = torch.empty(n, 256, dtype=torch.float32, device=dev)
 
 
