@@ -306,6 +306,8 @@ def run_ours(args) -> None:
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+    if args.side_configs and world == 1:
+        line["side_configs"] = side_configs(mods, cfg, lex, args)
     if args.sweep and world == 1:
         line["qps_sweep"] = qps_sweep(mods, cfg, lex, args)
         ok = [r["qps"] for r in line["qps_sweep"] if r["p99_ms"] is not None and r["p99_ms"] < 80.0]
@@ -316,6 +318,41 @@ def run_ours(args) -> None:
                                 if k in ("value", "unit", "cores", "kind", "sample", "p50", "served_first_chunk",
                                          "requests")}
     print(json.dumps(line), flush=True)
+
+
+def side_configs(mods, cfg, lex, args) -> dict:
+    """BASELINE configs C1 (one ~50-char request, batch 1), C2 (16 concurrent U{20..200}-char
+    requests) and C5 (1000-char paragraphs every 2 s mixed with U{20..50} background)."""
+    import random as _r
+
+    from paper_2211_13939_b200.harness import TimedRequest, poisson_trace, random_text, serve
+    out = {}
+    rng = _r.Random(args.seed + 11)
+    fcl = []
+    for _ in range(10):
+        run = serve(mods, cfg, [TimedRequest(0.0, random_text(rng, 50, 50, lex))], warmup_iters=0,
+                    timed_iters=None, drain_seconds=0.0)
+        r = run.timings[0]
+        fcl.append(1e3 * r.fcl)
+    out["c1_single_50char_fcl_ms_median"] = sorted(fcl)[len(fcl) // 2]
+    texts = [random_text(rng, 20, 200, lex) for _ in range(16)]
+    run = serve(mods, cfg, [TimedRequest(0.0, t) for t in texts], warmup_iters=0, timed_iters=None,
+                drain_seconds=0.0)
+    out["c2_16_concurrent"] = {"fcl_max_ms": max(1e3 * r.fcl for r in run.timings),
+                               "lcl_max_ms": max(1e3 * r.lcl for r in run.timings),
+                               "iterations": len(run.reports)}
+    bg = poisson_trace(args.c5_qps, 20.0, lo=20, hi=50, seed=args.seed + 5, lexicon=lex)
+    longs = [TimedRequest(2.0 * i + 0.5, random_text(rng, 1000, 1000, lex), "long") for i in range(10)]
+    trace = sorted(bg + longs, key=lambda r: r.send_at)
+    run = serve(mods, cfg, trace, warmup_iters=3, warmup_seconds=2.0, timed_iters=400, drain_seconds=1.0)
+    t0, t1 = run.window or (0.0, float("inf"))
+    ins = [r for r in run.timings if t0 <= r.send_time < (t1 or float("inf")) and r.fcl is not None]
+    lf = [1e3 * r.fcl for r in ins if len(r.text) >= 1000]
+    sf = [1e3 * r.fcl for r in ins if len(r.text) < 1000]
+    out["c5_long_paragraph_mix"] = {"background_qps": args.c5_qps, "long_requests": len(lf),
+                                    "long_fcl_max_ms": max(lf) if lf else None,
+                                    "short_fcl_p99_ms": _percentiles(sf)[1], "short_requests": len(sf)}
+    return out
 
 
 def qps_sweep(mods, cfg, lex, args) -> list[dict]:
@@ -351,6 +388,8 @@ def main() -> None:
     ap.add_argument("--sweep", default="125,150,175,200,225,250,275,300",
                     help="extra QPS levels for max-QPS (empty: off); stops at the first p99 > 200 ms")
     ap.add_argument("--sweep-steps", type=int, default=150)
+    ap.add_argument("--side-configs", type=int, default=1, help="also run C1, C2, C5 (1 = on)")
+    ap.add_argument("--c5-qps", type=float, default=50.0)
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

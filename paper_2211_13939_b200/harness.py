@@ -108,7 +108,8 @@ class ServeRun:
 
 def serve(modules: PipelineModules, cfg, trace: list[TimedRequest], *, warmup_iters: int = 3,
           warmup_seconds: float = 0.0, timed_iters: int | None = None, drain_seconds: float = 30.0,
-          on_window=None, max_clients: int = 4096, sample_rate: int = 22050) -> ServeRun:
+          on_window=None, max_clients: int = 4096, sample_rate: int = 22050,
+          tail_seconds: float = 120.0) -> ServeRun:
     """Plays ``trace`` against a fresh SchedulerLoop and records every request.
 
     The timed window is iterations ``[w, w + timed_iters)`` where ``w`` is the
@@ -178,6 +179,10 @@ def serve(modules: PipelineModules, cfg, trace: list[TimedRequest], *, warmup_it
             with lock:
                 run.timings.append(rec)
             clients.submit(consume, rec, stream)
+        else:  # trace exhausted before the window closed: let in-flight requests finish
+            end = time.perf_counter() + tail_seconds
+            while time.perf_counter() < end and not all(r.done for r in run.timings):
+                time.sleep(0.001)
     return run
 
 

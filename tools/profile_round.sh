@@ -1,18 +1,14 @@
 #!/bin/bash
-# GPU-side profiling pass for one round (run under gpurun).  Produces in gpurun_out/:
-#   launches_bench.csv   ncu launch list (gpu__time_duration.sum) of a short bench run
-#   prof_conv.ncu-rep    ncu --set full of 2 HiFi-GAN conv launches (stage-2 MRF)
-#   prof_attn.ncu-rep    ncu --set full of the attention kernel
-#   prof_gemm.ncu-rep    ncu --set full of a decoder gate GEMM
-set -x
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/launches_bench.csv \
-  python bench.py --steps 20 --warmup 3 --warmup-seconds 2 --drain-seconds 1 --no-cpu-baseline --sweep "" \
-  > gpurun_out/bench_under_ncu.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_conv_tc -s 155 -c 2 \
-  -o gpurun_out/prof_conv python tools/profile_iter.py --batches 128 --iters 1 > gpurun_out/ncu_conv.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_attention -s 5 -c 1 \
-  -o gpurun_out/prof_attn python tools/profile_iter.py --batches 128 --iters 1 > gpurun_out/ncu_attn.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_conv_tc -s 6 -c 1 \
-  -o gpurun_out/prof_gemm python tools/profile_iter.py --batches 128 --iters 1 > gpurun_out/ncu_gemm.log 2>&1
+# GPU-side profiling pass for one round (run under gpurun).  Outputs in gpurun_out/:
+#   launches_b128.csv   ncu launch list (gpu__time_duration.sum) of one decoder + vocoder call at B=128
+#   prof_conv.ncu-rep   ncu --set full: 2 stage-2 HiFi-GAN MRF convs (k=3 c1, k=3 c2 +residual)
+#   prof_attn.ncu-rep   ncu --set full: the attention kernel (4-CTA clusters)
+#   prof_gemm.ncu-rep   ncu --set full: a decoder gate GEMM (K-split)
+# (ncu on bench.py itself distorts the serving dynamics -- the pool grows while kernels are
+#  serialised -- so the launch list is taken on the fixed-batch profile_iter workload.)
+P="python tools/profile_iter.py --batches 128 --iters 1 --no-graphs"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_b128.csv $P > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_conv_tc -s 89 -c 2 -o gpurun_out/prof_conv $P > gpurun_out/ncu_conv.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_attention -s 5 -c 1 -o gpurun_out/prof_attn $P > gpurun_out/ncu_attn.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_conv_tc -s 6 -c 1 -o gpurun_out/prof_gemm $P > gpurun_out/ncu_gemm.log 2>&1
 ls -la gpurun_out
