@@ -97,6 +97,14 @@ def _dist():
     return world, rank, local
 
 
+_T0 = time.perf_counter()
+
+
+def log(msg: str) -> None:
+    """Progress on stderr (the JSON line is the only stdout output)."""
+    print(f"[bench {time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def _percentiles(values):
     from paper_2211_13939_b200.harness import nearest_rank
     return (nearest_rank(values, 50), nearest_rank(values, 99)) if values else (None, None)
@@ -187,8 +195,10 @@ def run_ours(args) -> None:
     torch.cuda.set_device(local)
     cfg, lex = PipelineConfig(), default_lexicon()
     engine = build_engine(cfg, args.tier, device)
+    log("engine built")
     if hasattr(engine, "prepare_graphs"):
         engine.prepare_graphs(max_batch=256)
+    log("decoder graphs captured")
     mods = modules_for(engine, lex)
 
     # The serving loop allocates many short-lived objects (handles, chunks); a gen-2 collection
@@ -222,6 +232,7 @@ def run_ours(args) -> None:
     if dist is not None:
         dist.barrier()
     trace = poisson_trace(args.qps, 3600.0, seed=args.seed + 1000 * rank, lexicon=lex)
+    log(f"C3 main window: {args.qps:g} QPS, {args.steps} timed iterations")
     run = serve(mods, cfg, trace, warmup_iters=args.warmup, warmup_seconds=args.warmup_seconds,
                 timed_iters=args.steps, on_window=on_window, drain_seconds=args.drain_seconds)
     torch.cuda.synchronize()
@@ -306,6 +317,7 @@ def run_ours(args) -> None:
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+    log(f"C3 done: p50 {p50} p99 {p99} ms")
     if args.side_configs and world == 1:
         line["side_configs"] = side_configs(mods, cfg, lex, args)
     if args.sweep and world == 1:
@@ -314,6 +326,7 @@ def run_ours(args) -> None:
         ok += [args.qps] if p99 is not None and p99 < 80.0 else []
         line["max_qps_p99_under_80ms"] = max(ok) if ok else None
     if rank == 0 and not args.no_cpu_baseline:
+        log("cpu baseline")
         line["cpu_baseline"] = {k: v for k, v in cpu_serving_baseline(args.qps, args.cpu_seconds, args.seed).items()
                                 if k in ("value", "unit", "cores", "kind", "sample", "p50", "served_first_chunk",
                                          "requests")}
@@ -335,6 +348,7 @@ def side_configs(mods, cfg, lex, args) -> dict:
         r = run.timings[0]
         fcl.append(1e3 * r.fcl)
     out["c1_single_50char_fcl_ms_median"] = sorted(fcl)[len(fcl) // 2]
+    log("C1 done")
     texts = [random_text(rng, 20, 200, lex) for _ in range(16)]
     run = serve(mods, cfg, [TimedRequest(0.0, t) for t in texts], warmup_iters=0, timed_iters=None,
                 drain_seconds=0.0)
@@ -352,22 +366,32 @@ def side_configs(mods, cfg, lex, args) -> dict:
     out["c5_long_paragraph_mix"] = {"background_qps": args.c5_qps, "long_requests": len(lf),
                                     "long_fcl_max_ms": max(lf) if lf else None,
                                     "short_fcl_p99_ms": _percentiles(sf)[1], "short_requests": len(sf)}
+    log("C5 done")
     return out
 
 
 def qps_sweep(mods, cfg, lex, args) -> list[dict]:
-    """Shorter runs at each sweep QPS (same engine) -> p50/p99 FCL; stops after the first overload."""
+    """Bounded runs at each sweep QPS (same engine): 3 s warm-up, a window of --sweep-seconds,
+    requests sent in the window that have no first chunk 2 s after it closes count as censored
+    at that time.  Stops after the first level whose p99 exceeds 80 ms."""
     from paper_2211_13939_b200.harness import poisson_trace, serve
     rows = []
     for q in [float(x) for x in args.sweep.split(",") if x]:
         run = serve(mods, cfg, poisson_trace(q, 3600.0, seed=args.seed + int(q), lexicon=lex), warmup_iters=3,
-                    warmup_seconds=4.0, timed_iters=args.sweep_steps, drain_seconds=2.0)
+                    warmup_seconds=3.0, timed_iters=None, timed_seconds=args.sweep_seconds, drain_seconds=2.0)
         t0, t1 = run.window
-        fcl = [1e3 * r.fcl for r in run.timings if t0 <= r.send_time < t1 and r.fcl is not None]
+        end = t1 + 2.0
+        inside = [r for r in run.timings if t0 <= r.send_time < t1]
+        fcl = [1e3 * (r.fcl if r.fcl is not None else end - r.send_time) for r in inside]
         p50, p99 = _percentiles(fcl)
+        win = [r for r, e in zip(run.reports, run.iteration_end) if t0 < e <= t1]
+        iters = len(win)
         rows.append({"qps": q, "p50_ms": p50, "p99_ms": p99, "requests": len(fcl),
-                     "ms_per_step": round(1e3 * (t1 - t0) / args.sweep_steps, 3)})
-        if p99 is None or p99 > 200.0:
+                     "censored": sum(1 for r in inside if r.fcl is None),
+                     "ms_per_step": round(1e3 * (t1 - t0) / max(iters, 1), 3),
+                     "pooled_batch_mean": round(sum(len(r.decoder_ids) for r in win) / max(iters, 1), 1)})
+        log(f"sweep {q:g} QPS: p50 {p50} p99 {p99}")
+        if p99 is None or p99 > 80.0:
             break
     return rows
 
@@ -378,16 +402,16 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--warmup-seconds", type=float, default=5.0)
-    ap.add_argument("--drain-seconds", type=float, default=20.0)
+    ap.add_argument("--drain-seconds", type=float, default=10.0)
     ap.add_argument("--qps", type=float, default=100.0)
     ap.add_argument("--tier", default="r", choices=("r", "s"))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sweep", default="125,150,175,200,225,250,275,300",
-                    help="extra QPS levels for max-QPS (empty: off); stops at the first p99 > 200 ms")
-    ap.add_argument("--sweep-steps", type=int, default=150)
+    ap.add_argument("--sweep", default="125,150,175,200,225,250,275,300,350,400",
+                    help="extra QPS levels for max-QPS (empty: off); stops at the first p99 > 80 ms")
+    ap.add_argument("--sweep-seconds", type=float, default=5.0)
     ap.add_argument("--side-configs", type=int, default=1, help="also run C1, C2, C5 (1 = on)")
     ap.add_argument("--c5-qps", type=float, default=50.0)
     args = ap.parse_args()

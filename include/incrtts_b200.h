@@ -101,6 +101,23 @@ int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, cons
                    float* f32_out, int32_t ksplit, void* acc, int32_t acc_mode, void* act_out,
                    float slope, int32_t zero_halo, int32_t bn, void* stream);
 
+/* K7 fused HiFi-GAN ResBlock1 layer (one MRF branch step; replaces, with the
+ * vocoder_batch stand-in src/vocoder.py:52-60, the pair of itts_conv1d_tc calls
+ * c1 -> c2 of HiFi-GAN V1).  x = bf16 [rows][c] holding lrelu(x, 0.1), items
+ * packed with zero halos >= 25 rows; w1/w2 = bf16 [taps][c][c] (K-major);
+ * b1/b2 = fp32 [c]; row_out[r] < 0 marks halo rows.  y = x + c2(lrelu(c1(x)));
+ * acc_mode 0: act_out = lrelu(y, slope); 1: acc = y; 2: acc += y;
+ * 3: act_out = lrelu((acc + y) / 3, slope).  Exactly one output: act_out is given
+ * for modes 0 / 3 and NULL for modes 1 / 2.  Halo rows of the output are written as
+ * zeros.  c in {32, 64, 128, 256}, taps odd <= 11, dil <= 5.  act_out / acc must not
+ * alias x. */
+int itts_resblock_tc(const void* x, int64_t rows, int32_t c, const void* w1, const void* w2, const float* b1,
+                     const float* b2, int32_t taps, int32_t dil, const int32_t* row_out, void* acc,
+                     int32_t acc_mode, void* act_out, float slope, void* stream);
+/* Profiling aid: per-CTA barrier-wait cycle counters of later itts_resblock_tc launches
+ * ([grid][16] uint64 device buffer; NULL turns it off). */
+int itts_resblock_debug_trace(void* buf);
+
 /* K6 decoder-step chain (replaces decode_chunk_batch, acoustic.py:234-238,
  * with the Tacotron2 decoder, paper Eq. 2).  `state` = fp32 [B][4944] rows
  * gathered by itts_gather_rows: [p 256 | ctx 512 | att_h 1024 | dec_h 1024 |

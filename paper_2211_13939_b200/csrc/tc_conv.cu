@@ -32,8 +32,11 @@
 #include <cuda_bf16.h>
 
 #include "common.cuh"
+#include "tcgen05.cuh"
 
 namespace {
+
+using namespace tcg;
 
 constexpr int kBlockM = 128;
 constexpr int kEpiWarps = 8;                 // 2 warps per TMEM lane quarter, each half the columns
@@ -60,144 +63,6 @@ struct Epi {
   float slope;                // leaky-ReLU slope for act_out (1.0 = identity, 0.0 = ReLU)
   int zero_halo;              // write zeros into act_out for halo rows (CONV mode only)
 };
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(phase));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes));
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// UMMA shared-memory descriptor, K-major, swizzle SWZ bytes (128 or 64):
-// 8-row atoms of SWZ-byte rows, SBO = 8*SWZ, LBO unused (1), version 1.
-template <int SWZ>
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
-  constexpr uint64_t layout = SWZ == 128 ? 2ull : 4ull;
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;                               // LBO (ignored for swizzled K-major)
-  d |= (uint64_t)(((8 * SWZ) >> 4) & 0x3FFF) << 32;     // SBO
-  d |= (uint64_t)1 << 46;                               // version (sm100)
-  d |= layout << 61;
-  return d;
-}
-
-// Instruction descriptor: kind::f16, A/B bf16, D fp32, K-major both, M=128, N=BN.
-template <int BN>
-__device__ __forceinline__ uint32_t make_idesc() {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kBlockM >> 4) << 24);
-}
-
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(acc));
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-template <int CW>
-__device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[CW]) {
-  if constexpr (CW == 32) tmem_ld32(taddr, v); else tmem_ld16(taddr, v);
-}
-
-__device__ __forceinline__ float lrelu(float x, float s) { return x >= 0.f ? x : x * s; }
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ float inv_lrelu(float a, float s) { return a >= 0.f ? a : a / s; }
-
-// CW bf16 values (CW/8 x 16-byte vectors) <-> fp32 registers.
-template <int CW>
-__device__ __forceinline__ void ld_bf16_raw(const __nv_bfloat16* p, uint4 (&u)[CW / 8]) {
-  const uint4* src = reinterpret_cast<const uint4*>(p);
-#pragma unroll
-  for (int q = 0; q < CW / 8; ++q) u[q] = src[q];
-}
-
-template <int CW>
-__device__ __forceinline__ void unpack_bf16(const uint4 (&u)[CW / 8], float (&v)[CW]) {
-#pragma unroll
-  for (int q = 0; q < CW / 8; ++q) {
-    const uint32_t w[4] = {u[q].x, u[q].y, u[q].z, u[q].w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
-      v[8 * q + 2 * e] = f.x;
-      v[8 * q + 2 * e + 1] = f.y;
-    }
-  }
-}
-
-template <int CW>
-__device__ __forceinline__ void store_bf16(__nv_bfloat16* p, const float (&v)[CW], float slope) {
-  uint4* dst = reinterpret_cast<uint4*>(p);
-#pragma unroll
-  for (int q = 0; q < CW / 8; ++q) {
-    uint32_t w[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      __nv_bfloat162 b2 = __floats2bfloat162_rn(lrelu(v[8 * q + 2 * e], slope), lrelu(v[8 * q + 2 * e + 1], slope));
-      w[e] = *reinterpret_cast<uint32_t*>(&b2);
-    }
-    dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
-  }
-}
 
 struct TileSched {
   int n_tiles, ksplit, iters_per_split;
@@ -302,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - 2;
     const int quarter = warp & 3, half = ew >> 2;
     const int C = epi.c_out;
+    const float inv_res = 1.0f / epi.res_slope;
     uint32_t lt = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
       int mt, nt, z;
@@ -345,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float y[CW];
           unpack_bf16<CW>(ru, y);
 #pragma unroll
-          for (int i = 0; i < CW; ++i) v[i] += inv_lrelu(y[i], epi.res_slope);
+          for (int i = 0; i < CW; ++i) v[i] += inv_lrelu(y[i], inv_res);
         }
         if (epi.acc_mode == 1) {
           store_bf16<CW>(epi.acc + o, v, 1.0f);
@@ -358,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             store_bf16<CW>(epi.acc + o, a, 1.0f);
           } else {  // finalize: x = (rb0 + rb1 + rb2) / 3
 #pragma unroll
-            for (int i = 0; i < CW; ++i) v[i] = a[i] / 3.0f;
+            for (int i = 0; i < CW; ++i) v[i] = a[i] * (1.0f / 3.0f);
           }
         }
         if (epi.act_out) store_bf16<CW>(epi.act_out + o, v, epi.slope);
@@ -373,49 +239,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
-}
-
-// ------------------------------------------------------------------ host side
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeFn get_encode() {
-  static EncodeFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeFn>(p);
-  }
-  return fn;
-}
-
-bool encode_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
-               uint32_t box_inner, uint32_t box_outer, int swz) {
-  EncodeFn enc = get_encode();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * 2};
-  cuuint32_t box[2] = {box_inner, box_outer};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
-int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
 }
 
 template <int BN, int SWZ, int STAGES>

@@ -330,8 +330,9 @@ __global__ void __cluster_dims__(AT_CL, 1, 1) __launch_bounds__(AT_WARPS * 32)
   float Z = cl_sum[0];
 #pragma unroll
   for (int r = 1; r < AT_CL; ++r) Z += cl_sum[r];
+  const float iz = 1.0f / Z;
   for (int t = tid; t < Ls; t += NT) {
-    const float a = e[t] / Z;
+    const float a = e[t] * iz;
     e[t] = a;
     wdst[t_lo + t] = a;
     wdst[L + t_lo + t] = w_acc[HALO + t] + a;

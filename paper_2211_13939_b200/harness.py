@@ -109,7 +109,7 @@ class ServeRun:
 def serve(modules: PipelineModules, cfg, trace: list[TimedRequest], *, warmup_iters: int = 3,
           warmup_seconds: float = 0.0, timed_iters: int | None = None, drain_seconds: float = 30.0,
           on_window=None, max_clients: int = 4096, sample_rate: int = 22050,
-          tail_seconds: float = 120.0) -> ServeRun:
+          tail_seconds: float = 120.0, timed_seconds: float | None = None) -> ServeRun:
     """Plays ``trace`` against a fresh SchedulerLoop and records every request.
 
     The timed window is iterations ``[w, w + timed_iters)`` where ``w`` is the
@@ -135,8 +135,9 @@ def serve(modules: PipelineModules, cfg, trace: list[TimedRequest], *, warmup_it
             run.window = (now, None)
             if on_window:
                 on_window("start", i)
-        elif (state["start_idx"] is not None and state["end_idx"] is None and timed_iters is not None
-              and i >= state["start_idx"] + timed_iters):
+        elif (state["start_idx"] is not None and state["end_idx"] is None
+              and ((timed_iters is not None and i >= state["start_idx"] + timed_iters)
+                   or (timed_seconds is not None and now - run.window[0] >= timed_seconds))):
             state["end_idx"] = i
             run.window = (run.window[0], now)
             if on_window:

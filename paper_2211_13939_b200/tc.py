@@ -67,3 +67,21 @@ def conv1d_tc(x: torch.Tensor, wt: torch.Tensor, offs, bias: torch.Tensor, c_out
                  offs_arr, bias.data_ptr(), c_out, row_out.data_ptr(), ptr(res_in), float(res_slope),
                  ptr(f32_out), int(ksplit), ptr(acc), acc_mode, ptr(act_out), float(slope), int(zero_halo),
                  int(bn), st)
+
+
+def resblock_tc(x: torch.Tensor, c1, c2, dilation: int, row_out: torch.Tensor, *, acc=None, acc_mode=ACC_NONE,
+                act_out=None, slope: float = 0.1, stream=None) -> None:
+    """One fused ResBlock1 layer (resblock_tc.cu): y = x + c2(lrelu(c1(lrelu x))), then the
+    accumulator / leaky-ReLU epilogue.  x holds lrelu(x, 0.1) in bf16 [R][C]; c1 / c2 are
+    (Wt [k][C][C] bf16, tap offsets, bias) as made by :func:`conv_weights`.  Output buffers
+    must not alias x (neighbouring tiles still read it)."""
+    rows, c = x.shape
+    assert x.is_contiguous() and x.dtype == torch.bfloat16
+    (w1, offs1, b1), (w2, offs2, b2) = c1, c2
+    taps = w1.shape[0]
+    assert w1.shape == (taps, c, c) and w2.shape == (taps, c, c)
+    ptr = lambda t: 0 if t is None else t.data_ptr()
+    st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    _native.call("itts_resblock_tc", x.data_ptr(), rows, c, w1.data_ptr(), w2.data_ptr(), b1.data_ptr(),
+                 b2.data_ptr(), taps, int(dilation), row_out.data_ptr(), ptr(acc), acc_mode, ptr(act_out),
+                 float(slope), st)

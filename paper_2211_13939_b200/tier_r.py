@@ -104,6 +104,7 @@ class TierREngine:
         self.d2h_bytes = 0
         self.timers: list | None = None  # set to [] to record (kind, ev0, ev1, units) per module call
         self.use_graphs = True           # CUDA-graph the 32-step decoder chunk per (batch, L) bucket
+        self.fused_mrf = True            # one fused c1->c2 kernel per ResBlock1 layer (resblock_tc.cu)
         self._dec_buckets: dict = {}
         self._graph_warm = False
 
@@ -193,6 +194,10 @@ class TierREngine:
     def _conv(self, x, layer, c_out, row_out, **kw) -> None:
         wt, offs, bias = layer
         tc.conv1d_tc(x, wt, offs, bias, c_out, row_out, stream=self._st(), **kw)
+        self.launches += 1
+
+    def _resblock(self, x, c1, c2, dil, row_out, **kw) -> None:
+        tc.resblock_tc(x, c1, c2, dil, row_out, stream=self._st(), **kw)
         self.launches += 1
 
     def _iota(self, n: int) -> torch.Tensor:
@@ -491,6 +496,22 @@ class TierREngine:
             self._call("itts_r_zero_halo", self._up(zplan).data_ptr(), n, lay.halo, XA.data_ptr(), C, st)
             rm = self._rowmap(lay, lay.first, 1)
             slope_out = 0.1 if s < 3 else 0.01
+            if self.fused_mrf:
+                # one fused kernel per ResBlock1 layer; ping-pong YA/TB (a layer must not write its input)
+                for j, layers in enumerate(self.res[s]):
+                    src = XA
+                    for m, (c1, c2) in enumerate(layers):
+                        dil = W.HG_RES_DILATIONS[m]
+                        if m < 2:
+                            dst = YA if m == 0 else TB
+                            self._resblock(src, c1, c2, dil, rm, act_out=dst, slope=0.1)
+                            src = dst
+                        else:
+                            mode = (tc.ACC_STORE, tc.ACC_ADD, tc.ACC_FINAL)[j]
+                            self._resblock(src, c1, c2, dil, rm, acc=ACC, acc_mode=mode,
+                                           act_out=OA_next if j == 2 else None, slope=slope_out)
+                prev, act_in = lay, OA_next
+                continue
             for j, layers in enumerate(self.res[s]):
                 for m, (c1, c2) in enumerate(layers):
                     ya_in = XA if m == 0 else YA

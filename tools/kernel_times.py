@@ -55,6 +55,12 @@ def main():
         timed(tag, orig_conv, x, layer, c_out, row_out, **kw)
 
     eng._conv = conv
+    orig_rb = eng._resblock
+
+    def rb(x, c1, c2, dil, row_out, **kw):
+        timed(f"resblock C={x.shape[1]} k={c1[0].shape[0]}", orig_rb, x, c1, c2, dil, row_out, **kw)
+
+    eng._resblock = rb
     live = [(enc, st, VocoderState.initial()) for enc, st in encs]
     for rep in range(args.reps + 1):
         if rep == 1:

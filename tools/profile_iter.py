@@ -53,11 +53,14 @@ def main():
     ap.add_argument("--batches", default="1,16,64,128,256")
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--no-graphs", action="store_true", help="eager decoder (stable kernel order for ncu -s/-c)")
+    ap.add_argument("--unfused", action="store_true", help="MRF as two tc_conv launches per layer (A/B)")
     args = ap.parse_args()
     cfg = PipelineConfig()
     eng = build_engine(cfg, args.tier, "cuda:0")
     if args.no_graphs:
         eng.use_graphs = False
+    if args.unfused:
+        eng.fused_mrf = False
     lex = default_lexicon()
     rows = []
     for B in [int(b) for b in args.batches.split(",")]:
