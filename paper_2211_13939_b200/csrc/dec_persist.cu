@@ -1,0 +1,811 @@
+// K6P: the whole Tacotron2 decoder chunk (up to 32 autoregressive steps) as ONE persistent kernel.
+//
+// Replaces the per-step chain of ~10 launches (tier_r.cu k_gemv / k_lstm_cell / k_attention +
+// two tc_conv gate GEMMs) for decode_chunk_batch (reference acoustic.py:191-219, :234-238;
+// Tacotron2 decoder step = paper Eq. 2).  One CTA per SM; the phases of a
+// step are separated by a grid-wide barrier, so a step costs 8 barriers instead of 10 kernel
+// boundaries, and everything that is constant across steps stays on chip:
+//
+//   PRE1   mel(s-1) = bp + sum of the projection K-slices (fixed order) -> mel / gate outputs,
+//          last_frame; H1 = relu(W0 . last_frame)                      (8-item x 32-col tasks)
+//   PRE2   p = relu(W1 . H1) -> state + bf16 operand mirror
+//   ATT    gates = [p|ctx|att_h] . Wa^T on the tensor cores (mma.sync bf16 -> fp32), CTA c owns
+//          hidden units [8c, 8c+8) = 32 gate rows (interleaved on the host), its weight slice is
+//          bulk-copied (cp.async.bulk) into shared memory while the previous phases run; the
+//          LSTM cell is the GEMM epilogue (no gate round trip through HBM)
+//   QUERY  q = Wq . att_h as 8 K-slice partials
+//   ATT-A  per (item, position chunk): location conv, energies, chunk max, exp, chunk sum,
+//          unnormalised context partial
+//   ATT-B  per item: combine chunks (max / rescale / sum, chunk order) -> context, W, W_acc
+//   DEC    gates = [ctx|att_h|dec_h] . Wd^T + cell (as ATT)
+//   PROJ   mel/gate projection as 8 K-slice partials (summed by the next PRE1)
+//
+// The bf16 operand mirror keeps two banks of att_h / dec_h (step parity) so a GEMM phase never
+// reads the h it is overwriting.  All reductions run in a fixed order: results do not depend
+// on the batch composition or on the number of SMs.
+
+#include <cuda_bf16.h>
+
+#include "tcgen05.cuh"
+
+namespace {
+
+constexpr int NMEL = 80, EMB = 512, HID = 1024, PRE = 256, ATT = 128, NF = 32, KLOC = 31;
+constexpr int P_OFF = 0, CTX_OFF = 256, ATTH_OFF = 768, DECH_OFF = 1792, ATTC_OFF = 2816, DECC_OFF = 3840,
+              LAST_OFF = 4864, ROW = 4944;
+constexpr int XB2 = 4864;        // bf16 mirror row: [p | ctx | att_h b0 | dec_h b0 | att_h b1 | dec_h b1]
+constexpr int DPLAN = 8;
+constexpr int NT = 256, NW = 8;  // threads / warps per CTA
+constexpr int QKS = 8, PKS = 8;  // query / projection K-slices
+constexpr int GEMM_CTAS = HID / 8;  // 128 CTAs x 8 hidden units
+constexpr int KA = 1792, KD = 2560;
+constexpr int MAXCH = 256;       // max position chunks per item
+constexpr int ACH = 32;          // max positions per attention chunk (pm + memory rows staged in smem)
+constexpr uint32_t ASTAGE = ACH * (ATT + EMB) * 4;  // one staging buffer (two: the next chunk streams in)
+constexpr int LT = 128;          // positions per location-feature tile
+constexpr int HALO = (KLOC - 1) / 2;
+
+__device__ __forceinline__ int att_off(int bank) { return 768 + bank * 2048; }
+__device__ __forceinline__ int dec_off(int bank) { return 1792 + bank * 2048; }
+__device__ __forceinline__ float sigm(float x) { return 1.0f / (1.0f + expf(-x)); }
+// tanh via one exp2 and one reciprocal: absolute error ~1e-7 (the energies only sum it)
+__device__ __forceinline__ float tanh_fast(float x) { return 1.0f - __fdividef(2.0f, 1.0f + __expf(2.0f * x)); }
+
+struct DecArgs {
+  int B, nsteps, step0;            // rows, steps in this launch, global index of the first step
+  const int64_t* plan;             // [B][8]
+  float* work;                     // [B][ROW]
+  __nv_bfloat16* xb;               // [B16][XB2] (rows padded to 16)
+  const float* W0T;                // [80][256]
+  const float* W1T;                // [256][256]
+  const __nv_bfloat16* Wa;         // [128][32][1792] unit-interleaved att gate rows
+  const float* ba;                 // [128][32]
+  const __nv_bfloat16* Wd;         // [128][32][2560]
+  const float* bd;                 // [128][32]
+  const float* WqT;                // [1024][128]
+  const float* WlocD;              // [2][31][128] = location conv composed with the location dense layer
+  const float* v;                  // [128]
+  const float* WpT;                // [1536][81]
+  const float* bp;                 // [81]
+  float* H1;                       // [B][256]
+  float* Qp;                       // [QKS][B][128]
+  float* Pp;                       // [PKS][B][81]
+  float* U;                        // [B][u_ld] unnormalised attention numerators
+  int64_t u_ld;
+  float* AP;                       // [B][MAXCH][2 + 512] chunk max, sum, context partial
+  unsigned* bar;                   // [2] grid barrier (zeroed before launch)
+  unsigned long long* trace;       // debug: [16] ns per phase summed over steps (CTA 0), or null
+};
+
+unsigned long long* g_dec_trace = nullptr;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ------------------------------------------------------------------ grid barrier
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {  // arrive (release) on one counter, spin (acquire) until all CTAs arrived
+    ++gen;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned seen;
+    do {  // relaxed polling (an acquire load per poll would invalidate L1 every iteration)
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(bar) : "memory");
+    } while (seen < gen * gridDim.x);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+// L2-coherent loads for data produced inside this kernel by other CTAs (never cached in L1).
+__device__ __forceinline__ float ldf(const float* p) { return __ldcg(p); }
+__device__ __forceinline__ uint32_t ldu(const void* p) { return __ldcg(reinterpret_cast<const unsigned int*>(p)); }
+
+// per-item L and step counts, cached in shared memory at kernel start (B <= 256)
+struct PlanCache {
+  int L[256], steps[256];
+};
+__device__ __forceinline__ bool active(const PlanCache& pc, int b, int s) { return s < pc.steps[b]; }
+
+// ------------------------------------------------------------------ small batched GEMV task
+// Y[b][n] (n in [n0, n0+32)) for items [b0, b0+8): sum over k in [k0, k1) of X[b][k] W^T[k][n].
+// x(b, k) is supplied by the caller; the 8 warps split the K range, partials reduced in warp order.
+template <int KWM, typename XF, typename OUT>
+__device__ __forceinline__ void gemv_task(int b0, int nb, int n0, int N, int k0, int k1, const float* __restrict__ wT,
+                                          float* sx, float* spart, XF xf, OUT out) {
+  // KWM >= rows per warp: every weight load of the warp's K-slice is issued before the first FMA
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int KL = k1 - k0;
+  const int kw = (KL + NW - 1) / NW, ka = warp * kw, kb = min(KL, ka + kw);
+  const int n = n0 + lane;
+  float w[KWM];
+#pragma unroll
+  for (int u = 0; u < KWM; ++u) w[u] = (ka + u < kb && n < N) ? __ldg(wT + (int64_t)(k0 + ka + u) * N + n) : 0.f;
+  for (int i = tid; i < 8 * KL; i += NT) {
+    const int it = i / KL, k = k0 + i % KL;
+    sx[i] = it < nb ? xf(b0 + it, k) : 0.f;
+  }
+  __syncthreads();
+  float acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+#pragma unroll
+  for (int u = 0; u < KWM; ++u)
+    if (ka + u < kb)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = fmaf(w[u], sx[i * KL + ka + u], acc[i]);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) spart[(warp * 8 + i) * 32 + lane] = acc[i];
+  __syncthreads();
+  {
+    const int it = tid >> 5, c = tid & 31;
+    if (it < nb && n0 + c < N) {
+      float vsum = spart[it * 32 + c];
+#pragma unroll
+      for (int w2 = 1; w2 < NW; ++w2) vsum += spart[(w2 * 8 + it) * 32 + c];
+      out(b0 + it, n0 + c, vsum);
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ tensor-core gate GEMM + LSTM cell
+// tcgen05: D[128 rows = items][32 gate columns] in TMEM; A (the bf16 operand mirror, 64-column
+// boxes of up to 128 item rows) and this CTA's 32 weight rows stream through a TMA ring; the
+// epilogue warps apply the LSTM cell straight from TMEM.
+constexpr int GS = 8;                          // ring stages (the ring doubles as the attention staging area)
+constexpr uint32_t GA_BYTES = 128 * 128;       // A stage: 128 rows x 64 bf16 (128B swizzle)
+constexpr uint32_t GW_BYTES = 32 * 128;        // W stage: 32 rows x 64 bf16
+
+struct GateSync {
+  uint64_t full[GS], empty[GS], accf, acce, abar[2];
+  uint32_t tmem;
+};
+static_assert(2 * ASTAGE <= GS * (GA_BYTES + GW_BYTES), "attention staging exceeds the ring");
+
+// MODE 0: attention LSTM (A = [p | ctx | att_h(old bank)], K = 1792)
+// MODE 1: decoder LSTM   (A = [ctx | att_h(new bank) | dec_h(old bank)], K = 2560)
+template <int MODE>
+__device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy, const CUtensorMap* mapA,
+                           const CUtensorMap* mapW, uint32_t a_box_bytes, uint32_t& g_ring, uint32_t& lt_tile,
+                           const PlanCache& pc) {
+  // g_ring / lt_tile: ring-stage and tile counters, kept per thread and advanced identically by all
+  constexpr int K = MODE == 0 ? KA : KD;
+  constexpr int NKC = K / 64;
+  const int c = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int oldb = s & 1, newb = oldb ^ 1;
+  const int ntile = (a.B + 127) / 128;
+  uint8_t* sA = ring;
+  uint8_t* sWt = ring + GS * GA_BYTES;
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // xb rows written by generic stores
+      uint32_t g = g_ring;
+      for (int mt = 0; mt < ntile; ++mt)
+        for (int kc = 0; kc < NKC; ++kc, ++g) {
+          const uint32_t st = g % GS, ph = (g / GS) & 1;
+          tcg::mbar_wait(&gsy.empty[st], ph ^ 1);
+          const int k0 = kc * 64;
+          int col;
+          if (MODE == 0) col = k0 < 768 ? k0 : att_off(oldb) + (k0 - 768);
+          else col = k0 < 512 ? CTX_OFF + k0 : (k0 < 1536 ? att_off(newb) + (k0 - 512) : dec_off(oldb) + (k0 - 1536));
+          tcg::mbar_expect_tx(&gsy.full[st], a_box_bytes + GW_BYTES);
+          tcg::tma_load_2d(sA + st * GA_BYTES, mapA, &gsy.full[st], col, mt * 128);
+          tcg::tma_load_2d(sWt + st * GW_BYTES, mapW, &gsy.full[st], k0, c * 32);
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = tcg::make_idesc<32>();
+      uint32_t g = g_ring, lt = lt_tile;
+      for (int mt = 0; mt < ntile; ++mt, ++lt) {
+        tcg::mbar_wait(&gsy.acce, (lt & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int kc = 0; kc < NKC; ++kc, ++g) {
+          const uint32_t st = g % GS, ph = (g / GS) & 1;
+          tcg::mbar_wait(&gsy.full[st], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = tcg::make_desc<128>(tcg::smem_u32(sA + st * GA_BYTES));
+          const uint64_t db = tcg::make_desc<128>(tcg::smem_u32(sWt + st * GW_BYTES));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, da + 2 * kk, db + 2 * kk, idesc, (kc | kk) != 0);
+          tcg::umma_commit(&gsy.empty[st]);
+        }
+        tcg::umma_commit(&gsy.accf);
+      }
+    }
+  } else if (warp >= 4) {
+    // epilogue: TMEM lane quarter q = warp & 3 -> item row; 32 columns = 4 gates x 8 units
+    const int q = warp & 3;
+    const float* bias = (MODE == 0 ? a.ba : a.bd) + c * 32;
+    const int h_off = MODE == 0 ? ATTH_OFF : DECH_OFF, c_off = MODE == 0 ? ATTC_OFF : DECC_OFF;
+    const int hb_off = MODE == 0 ? att_off(newb) : dec_off(newb);
+    uint32_t lt = lt_tile;
+    for (int mt = 0; mt < ntile; ++mt, ++lt) {
+      const int b = mt * 128 + q * 32 + lane;
+      const bool live = b < a.B && active(pc, b, s);
+      float* st = a.work + (int64_t)b * ROW;
+      float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0;
+      if (live) {
+        c0 = __ldcg(reinterpret_cast<const float4*>(st + c_off + c * 8));
+        c1 = __ldcg(reinterpret_cast<const float4*>(st + c_off + c * 8 + 4));
+      }
+      tcg::mbar_wait(&gsy.accf, lt & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float v[32];
+      tcg::tmem_ld32(gsy.tmem + ((uint32_t)(q * 32) << 16), v);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) tcg::mbar_arrive(&gsy.acce);
+      if (live) {
+        const float cold[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        float hn[8], cn[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const float gi = v[u] + __ldg(bias + u), gf = v[8 + u] + __ldg(bias + 8 + u);
+          const float gg = v[16 + u] + __ldg(bias + 16 + u), go = v[24 + u] + __ldg(bias + 24 + u);
+          cn[u] = sigm(gf) * cold[u] + sigm(gi) * tanhf(gg);
+          hn[u] = sigm(go) * tanhf(cn[u]);
+        }
+        *reinterpret_cast<float4*>(st + c_off + c * 8) = make_float4(cn[0], cn[1], cn[2], cn[3]);
+        *reinterpret_cast<float4*>(st + c_off + c * 8 + 4) = make_float4(cn[4], cn[5], cn[6], cn[7]);
+        *reinterpret_cast<float4*>(st + h_off + c * 8) = make_float4(hn[0], hn[1], hn[2], hn[3]);
+        *reinterpret_cast<float4*>(st + h_off + c * 8 + 4) = make_float4(hn[4], hn[5], hn[6], hn[7]);
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(hn[2 * e], hn[2 * e + 1]);
+          w[e] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        *reinterpret_cast<uint4*>(a.xb + (int64_t)b * XB2 + hb_off + c * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+  }
+  g_ring += ntile * NKC;
+  lt_tile += ntile;
+}
+
+// ------------------------------------------------------------------ attention
+struct AttSmem {
+  float q[ATT], sv[ATT];
+  __align__(16) float sWl[2 * 32 * ATT];  // [c][k][a], k < 31 (tap 31 = 0): loc[a] = sum sWl[c][k][a] w_c[t+k-15]
+  float red[32];
+  float scale[MAXCH];
+  int tstart[257];             // prefix sum of chunks per item (ATT-A task list), B <= 256
+  float wp[ACH + 2 * HALO + 2], wa[ACH + 2 * HALO + 2], e[ACH];
+  __align__(16) float locf[LT * (NF + 1)];   // scratch: gemv / context partials [8][512]
+};
+static_assert(LT * (NF + 1) >= NW * EMB, "context partials alias the location tile");
+
+__device__ __forceinline__ float block_max(float v, float* red) {
+  v = itts::warp_max(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float r = red[0];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) r = fmaxf(r, red[w]);
+  return r;
+}
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = itts::warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float r = red[0];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) r += red[w];
+  return r;
+}
+
+// ATT-A for one (item b, chunk [ta, tb)).
+// Thread 0: the chunk's processed-memory and memory rows (contiguous) -> a staging buffer.
+__device__ __forceinline__ void att_prefetch(const DecArgs& a, int b, int ta, int tb, uint8_t* stage, uint64_t* bar) {
+  const int64_t* p = a.plan + b * DPLAN;
+  const int n = tb - ta;
+  float* sPm = reinterpret_cast<float*>(stage);
+  float* sMem = sPm + ACH * ATT;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tcg::mbar_expect_tx(bar, (uint32_t)n * (ATT + EMB) * 4);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tcg::smem_u32(sPm)),
+               "l"(reinterpret_cast<const float*>(p[1]) + (int64_t)ta * ATT), "r"(n * ATT * 4), "r"(tcg::smem_u32(bar))
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tcg::smem_u32(sMem)),
+               "l"(reinterpret_cast<const float*>(p[0]) + (int64_t)ta * EMB), "r"(n * EMB * 4), "r"(tcg::smem_u32(bar))
+               : "memory");
+}
+
+// ATT-A for one (item b, chunk [ta, tb)) whose rows are (being) staged in `stage`.
+__device__ void att_chunk(const DecArgs& a, AttSmem& sm, int s, int b, int ch, int ta, int tb, const uint8_t* stage,
+                          uint64_t* abar, uint32_t& aphase) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool tr = a.trace && blockIdx.x == 0 && tid == 0;
+  unsigned long long t0 = tr ? gtimer() : 0;
+  auto mark = [&](int slot) {
+    if (tr) {
+      const unsigned long long t1 = gtimer();
+      a.trace[slot] += t1 - t0;
+      t0 = t1;
+    }
+  };
+  const int64_t* p = a.plan + b * DPLAN;
+  const int L = (int)p[2];
+  const float* wsrc = reinterpret_cast<const float*>(a.step0 + s == 0 ? p[3] : p[4]);
+  const int n = tb - ta, nh = n + 2 * HALO;
+  const float* sPm = reinterpret_cast<const float*>(stage);
+  const float* sMem = sPm + ACH * ATT;
+  if (tid < ATT) {
+    float qa = ldf(a.Qp + (int64_t)b * ATT + tid);
+#pragma unroll
+    for (int z = 1; z < QKS; ++z) qa += ldf(a.Qp + ((int64_t)z * a.B + b) * ATT + tid);
+    sm.q[tid] = qa;
+  }
+  for (int i = tid; i < nh; i += NT) {
+    const int t = ta - HALO + i;
+    const bool in = t >= 0 && t < L;
+    sm.wp[i] = in ? ldf(wsrc + t) : 0.f;
+    sm.wa[i] = in ? ldf(wsrc + L + t) : 0.f;
+  }
+  __syncthreads();
+  mark(8);
+  tcg::mbar_wait(abar, aphase);
+  aphase ^= 1;
+  mark(9);
+  // energies: warp w takes positions [4w, 4w+4) of the (<= 32-position) chunk, lane l dims 4l..4l+3.
+  // The location conv and dense layer are one 62-tap x 128 filter (composed on the host); each
+  // filter tap is loaded once per lane and applied to 4 positions held in a sliding register window.
+  {
+    const float4 q4 = reinterpret_cast<const float4*>(sm.q)[lane];
+    const float4 v4 = reinterpret_cast<const float4*>(sm.sv)[lane];
+    const float4* wl4 = reinterpret_cast<const float4*>(sm.sWl);
+    const int pb = warp * 4;
+    if (pb < n) {  // warp-uniform
+      float acc[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[q][u] = 0.f;
+#pragma unroll
+      for (int cch = 0; cch < 2; ++cch) {
+        const float* wv = (cch ? sm.wa : sm.wp) + pb;
+        // slot (q + k) & 3 holds w[pb + q + k]; unrolled by 4 taps so the rotation is static
+        float win[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) win[q] = wv[q];
+        const float4* wl = wl4 + cch * 32 * (ATT / 4) + lane;
+#pragma unroll 2
+        for (int k0 = 0; k0 < 32; k0 += 4) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const float4 w4 = wl[(k0 + kk) * (ATT / 4)];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float x = win[(q + kk) & 3];
+              acc[q][0] = fmaf(w4.x, x, acc[q][0]);
+              acc[q][1] = fmaf(w4.y, x, acc[q][1]);
+              acc[q][2] = fmaf(w4.z, x, acc[q][2]);
+              acc[q][3] = fmaf(w4.w, x, acc[q][3]);
+            }
+            win[kk] = wv[k0 + kk + 4];
+          }
+        }
+      }
+      float en[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 pv = reinterpret_cast<const float4*>(sPm + (pb + q) * ATT)[lane];
+        en[q] = v4.x * tanh_fast((q4.x + acc[q][0]) + pv.x);
+        en[q] = fmaf(v4.y, tanh_fast((q4.y + acc[q][1]) + pv.y), en[q]);
+        en[q] = fmaf(v4.z, tanh_fast((q4.z + acc[q][2]) + pv.z), en[q]);
+        en[q] = fmaf(v4.w, tanh_fast((q4.w + acc[q][3]) + pv.w), en[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) en[q] = itts::warp_sum(en[q]);
+      if (lane < 4 && pb + lane < n) {
+        float mine = en[0];
+#pragma unroll
+        for (int q = 1; q < 4; ++q) mine = lane == q ? en[q] : mine;
+        sm.e[pb + lane] = mine;
+      }
+    }
+  }
+  __syncthreads();
+  mark(10);
+  float lmax = -INFINITY;
+  for (int t = tid; t < n; t += NT) lmax = fmaxf(lmax, sm.e[t]);
+  const float M = block_max(lmax, sm.red);
+  float lsum = 0.f;
+  for (int t = tid; t < n; t += NT) {
+    const float x = expf(sm.e[t] - M);
+    sm.e[t] = x;
+    lsum += x;
+    a.U[(int64_t)b * a.u_ld + ta + t] = x;
+  }
+  const float Ssum = block_sum(lsum, sm.red);
+  mark(11);
+  // unnormalised context partial: warp w takes positions t = w (mod 8), lane 16 dims
+  float4 acc[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4* mem4 = reinterpret_cast<const float4*>(sMem);
+#pragma unroll 4
+  for (int t = warp; t < n; t += NW) {
+    const float w = sm.e[t];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 m4 = mem4[t * (EMB / 4) + lane + 32 * j];
+      acc[j].x = fmaf(w, m4.x, acc[j].x);
+      acc[j].y = fmaf(w, m4.y, acc[j].y);
+      acc[j].z = fmaf(w, m4.z, acc[j].z);
+      acc[j].w = fmaf(w, m4.w, acc[j].w);
+    }
+  }
+  float4(*cpart)[EMB / 4] = reinterpret_cast<float4(*)[EMB / 4]>(sm.locf);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) cpart[warp][lane + 32 * j] = acc[j];
+  __syncthreads();
+  float* ap = a.AP + ((int64_t)b * MAXCH + ch) * (2 + EMB);
+  const float* cp = reinterpret_cast<const float*>(cpart);
+  for (int d = tid; d < EMB; d += NT) {
+    float c = cp[d];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) c += cp[w * EMB + d];
+    ap[2 + d] = c;
+  }
+  if (tid == 0) {
+    ap[0] = M;
+    ap[1] = Ssum;
+  }
+  __syncthreads();
+  mark(12);
+  if (tr) a.trace[13] += 1;
+}
+
+// ATT-B for item b: combine the chunks (chunk order) -> context, W, W_acc.
+__device__ void att_combine(const DecArgs& a, AttSmem& sm, int s, int b, int chunk) {
+  const int tid = threadIdx.x;
+  const int64_t* p = a.plan + b * DPLAN;
+  const int L = (int)p[2];
+  const int nch = (L + chunk - 1) / chunk;
+  const float* wsrc = reinterpret_cast<const float*>(a.step0 + s == 0 ? p[3] : p[4]);
+  float* wdst = reinterpret_cast<float*>(p[4]);
+  const float* ap = a.AP + (int64_t)b * MAXCH * (2 + EMB);
+  float* scale = sm.scale;  // [MAXCH]
+  const float mc = tid < nch ? ldf(ap + tid * (2 + EMB)) : -INFINITY;
+  const float sc = tid < nch ? ldf(ap + tid * (2 + EMB) + 1) : 0.f;
+  const float M = block_max(mc, sm.red);
+  const float ec = tid < nch ? expf(mc - M) : 0.f;
+  const float Z = block_sum(sc * ec, sm.red);  // chunk order within a warp, then warp order
+  if (tid < nch) scale[tid] = ec / Z;
+  __syncthreads();
+  float* st = a.work + (int64_t)b * ROW;
+  for (int d = tid; d < EMB; d += NT) {
+    float c = 0.f;
+    for (int k = 0; k < nch; ++k) c = fmaf(scale[k], ldf(ap + k * (2 + EMB) + 2 + d), c);
+    st[CTX_OFF + d] = c;
+    a.xb[(int64_t)b * XB2 + CTX_OFF + d] = __float2bfloat16_rn(c);
+  }
+  for (int t = tid; t < L; t += NT) {
+    const float w = ldf(a.U + (int64_t)b * a.u_ld + t) * scale[t / chunk];
+    const float acc = ldf(wsrc + L + t);
+    wdst[t] = w;
+    wdst[L + t] = acc + w;
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ the kernel
+__global__ void __launch_bounds__(NT, 1)
+    k_dec_persist(DecArgs a, const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapWa,
+                  const __grid_constant__ CUtensorMap mapWd, uint32_t a_box_bytes) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* ring = tcg::align_smem_1024(smem_raw);
+  AttSmem& sm = *reinterpret_cast<AttSmem*>(ring + GS * (GA_BYTES + GW_BYTES));  // ring = gate pipeline / attention staging
+  float* scratch = reinterpret_cast<float*>(&sm.locf[0]);                       // gemv reductions
+  __shared__ GateSync gsy;
+  __shared__ PlanCache pc;
+  const int tid = threadIdx.x, G = gridDim.x, c = blockIdx.x;
+  const bool gemm_cta = c < GEMM_CTAS;
+  unsigned gen = 0;
+  uint32_t g_ring = 0, lt_tile = 0, aphase[2] = {0, 0};
+
+  if (tid == 0) {
+    for (int i = 0; i < GS; ++i) {
+      tcg::mbar_init(&gsy.full[i], 1);
+      tcg::mbar_init(&gsy.empty[i], 1);
+    }
+    tcg::mbar_init(&gsy.accf, 1);
+    tcg::mbar_init(&gsy.acce, 4);
+    tcg::mbar_init(&gsy.abar[0], 1);
+    tcg::mbar_init(&gsy.abar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapWa)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapWd)) : "memory");
+  }
+  if (gemm_cta && (tid >> 5) == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(tcg::smem_u32(&gsy.tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  for (int b = tid; b < a.B; b += NT) {
+    pc.L[b] = (int)a.plan[b * DPLAN + 2];
+    pc.steps[b] = (int)a.plan[b * DPLAN + 5];
+  }
+  // attention constants (resident for the whole chunk)
+  for (int i = tid; i < 2 * 32 * ATT / 4; i += NT) {
+    const int cch = i / (32 * ATT / 4), r = i - cch * (32 * ATT / 4), k = r / (ATT / 4);
+    reinterpret_cast<float4*>(sm.sWl)[i] =
+        k < KLOC ? __ldg(reinterpret_cast<const float4*>(a.WlocD) + (cch * KLOC + k) * (ATT / 4) + r % (ATT / 4))
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (tid < ATT) sm.sv[tid] = __ldg(a.v + tid);
+  __syncthreads();
+  // bf16 operand mirror, bank 0, from the gathered fp32 state rows
+  for (int b = c; b < a.B; b += G) {
+    const float* st = a.work + (int64_t)b * ROW;
+    __nv_bfloat16* x = a.xb + (int64_t)b * XB2;
+    for (int i = tid; i < ATTC_OFF; i += NT) x[i] = __float2bfloat16_rn(ldf(st + i));
+  }
+  grid_sync(a.bar, gen);
+
+  // position chunking of the attention: about two tasks per CTA
+  int maxL = 1;
+  for (int b = 0; b < a.B; ++b) maxL = max(maxL, pc.L[b]);
+  int64_t sumL = 0;
+  for (int b = 0; b < a.B; ++b) sumL += pc.L[b];
+  int chunk = (int)((sumL + G - 1) / G);   // about one task per CTA
+  chunk = max(chunk, (maxL + MAXCH - 1) / MAXCH);
+  chunk = min(ACH, max(16, (chunk + 15) / 16 * 16));
+  if ((maxL + chunk - 1) / chunk > MAXCH) chunk = (maxL + MAXCH - 1) / MAXCH;  // cannot exceed ACH for L <= 8192
+  const int nb8 = (a.B + 7) / 8;
+
+  unsigned long long tph = gtimer(), tacc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int ph_i = 0;
+  auto phase_end = [&]() {
+    grid_sync(a.bar, gen);
+    if (a.trace && c == 0 && tid == 0) {
+      const unsigned long long now = gtimer();
+      tacc[ph_i] += now - tph;
+      tph = now;
+    }
+    ph_i = ph_i == 7 ? 0 : ph_i + 1;
+  };
+  for (int s = 0; s < a.nsteps; ++s) {
+    const int gs = a.step0 + s;
+    // ---- PRE1: finish mel(s-1), H1 = relu(W0 . last)
+    for (int task = c; task < nb8 * 8; task += G) {
+      const int b0 = (task >> 3) * 8, n0 = (task & 7) * 32, nb = min(8, a.B - b0);
+      float* sx = scratch;               // [8][80]
+      if (s > 0) {
+        for (int i = tid; i < 8 * 81; i += NT) {
+          const int it = i / 81, k = i % 81, b = b0 + it;
+          if (it >= nb) continue;
+          float m = __ldg(a.bp + k);
+#pragma unroll
+          for (int z = 0; z < PKS; ++z) m += ldf(a.Pp + ((int64_t)z * a.B + b) * 81 + k);
+          const bool was = active(pc, b, gs - 1);
+          if (k < NMEL) sx[it * NMEL + k] = was ? m : ldf(a.work + (int64_t)b * ROW + LAST_OFF + k);
+          if (n0 == 0 && was) {
+            const int64_t* p = a.plan + b * DPLAN;
+            if (k < NMEL) {
+              reinterpret_cast<float*>(p[6])[(gs - 1) * NMEL + k] = m;
+              a.work[(int64_t)b * ROW + LAST_OFF + k] = m;
+            } else {
+              reinterpret_cast<float*>(p[7])[gs - 1] = m;
+            }
+          }
+        }
+      } else {
+        for (int i = tid; i < 8 * NMEL; i += NT) {
+          const int it = i / NMEL, k = i % NMEL;
+          sx[i] = it < nb ? ldf(a.work + (int64_t)(b0 + it) * ROW + LAST_OFF + k) : 0.f;
+        }
+      }
+      __syncthreads();
+      gemv_task<10>(b0, nb, n0, PRE, 0, NMEL, a.W0T, scratch + 8 * 81, scratch + 8 * 81 + 8 * NMEL,
+                    [&](int b, int k) { return sx[(b - b0) * NMEL + k]; },
+                    [&](int b, int n, float y) { a.H1[(int64_t)b * PRE + n] = fmaxf(y, 0.f); });
+    }
+    phase_end();
+    // ---- PRE2: p = relu(W1 . H1)
+    for (int task = c; task < nb8 * 8; task += G) {
+      const int b0 = (task >> 3) * 8, n0 = (task & 7) * 32, nb = min(8, a.B - b0);
+      gemv_task<32>(b0, nb, n0, PRE, 0, PRE, a.W1T, scratch, scratch + 8 * PRE,
+                [&](int b, int k) { return ldf(a.H1 + (int64_t)b * PRE + k); },
+                [&](int b, int n, float y) {
+                  if (!active(pc, b, gs)) return;
+                  y = fmaxf(y, 0.f);
+                  a.work[(int64_t)b * ROW + P_OFF + n] = y;
+                  a.xb[(int64_t)b * XB2 + P_OFF + n] = __float2bfloat16_rn(y);
+                });
+    }
+    phase_end();
+    // ---- ATT gates + cell
+    if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, &mapA, &mapWa, a_box_bytes, g_ring, lt_tile, pc);
+    phase_end();
+    // ---- QUERY partials
+    for (int task = c; task < nb8 * 4 * QKS; task += G) {
+      const int z = task % QKS, nt = (task / QKS) % 4, b0 = (task / (QKS * 4)) * 8, nb = min(8, a.B - b0);
+      gemv_task<16>(b0, nb, nt * 32, ATT, z * (HID / QKS), (z + 1) * (HID / QKS), a.WqT, scratch,
+                scratch + 8 * (HID / QKS),
+                [&](int b, int k) { return ldf(a.work + (int64_t)b * ROW + ATTH_OFF + k); },
+                [&](int b, int n, float y) { a.Qp[((int64_t)z * a.B + b) * ATT + n] = y; });
+    }
+    phase_end();
+    // ---- ATT-A: the non-empty (item, chunk) tasks of the live items, dealt round-robin
+    if (tid < 32) {  // task prefix over items: 8 items per lane, then a warp scan
+      int cnt[8], loc = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int b = tid * 8 + i;
+        cnt[i] = (b < a.B && active(pc, b, gs)) ? (pc.L[b] + chunk - 1) / chunk : 0;
+        loc += cnt[i];
+      }
+      int incl = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (tid >= o) incl += y;
+      }
+      int run = incl - loc;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int b = tid * 8 + i;
+        if (b <= a.B) sm.tstart[b] = run;
+        run += cnt[i];
+      }
+      if (tid == 31 && a.B == 256) sm.tstart[256] = run;
+    }
+    __syncthreads();
+    {
+      const int ntask = sm.tstart[a.B];
+      int bcur = 0, bnext = 0;
+      auto locate = [&](int task, int& b) {
+        while (sm.tstart[b + 1] <= task) ++b;
+      };
+      if (c < ntask) {
+        locate(c, bnext);
+        if (tid == 0) {
+          const int ta = (c - sm.tstart[bnext]) * chunk;
+          att_prefetch(a, bnext, ta, min(pc.L[bnext], ta + chunk), ring, &gsy.abar[0]);
+        }
+      }
+      int i = 0;
+      for (int task = c; task < ntask; task += G, ++i) {
+        const int buf = i & 1;
+        bcur = bnext;
+        const int ch = task - sm.tstart[bcur];
+        const int L = pc.L[bcur];
+        const int ta = ch * chunk, tb = min(L, ta + chunk);
+        if (task + G < ntask) {  // the next chunk streams into the other buffer during this one
+          locate(task + G, bnext);
+          if (tid == 0) {
+            const int ta2 = (task + G - sm.tstart[bnext]) * chunk;
+            att_prefetch(a, bnext, ta2, min(pc.L[bnext], ta2 + chunk), ring + (buf ^ 1) * ASTAGE,
+                         &gsy.abar[buf ^ 1]);
+          }
+        }
+        att_chunk(a, sm, gs, bcur, ch, ta, tb, ring + buf * ASTAGE, &gsy.abar[buf], aphase[buf]);
+      }
+    }
+    phase_end();
+    // ---- ATT-B
+    for (int b = c; b < a.B; b += G)
+      if (active(pc, b, gs)) att_combine(a, sm, gs, b, chunk);
+    phase_end();
+    // ---- DEC gates + cell
+    if (gemm_cta) gate_phase<1>(a, gs, ring, gsy, &mapA, &mapWd, a_box_bytes, g_ring, lt_tile, pc);
+    phase_end();
+    // ---- PROJ partials
+    for (int task = c; task < nb8 * 3 * PKS; task += G) {
+      const int z = task % PKS, nt = (task / PKS) % 3, b0 = (task / (PKS * 3)) * 8, nb = min(8, a.B - b0);
+      constexpr int KP = (HID + EMB) / PKS;  // 192
+      gemv_task<24>(b0, nb, nt * 32, NMEL + 1, z * KP, (z + 1) * KP, a.WpT, scratch, scratch + 8 * KP,
+                [&](int b, int k) {
+                  return ldf(a.work + (int64_t)b * ROW + (k < HID ? DECH_OFF + k : CTX_OFF + k - HID));
+                },
+                [&](int b, int n, float y) { a.Pp[((int64_t)z * a.B + b) * 81 + n] = y; });
+    }
+    phase_end();
+  }
+  // ---- finish mel of the last step
+  {
+    const int gs = a.step0 + a.nsteps;
+    for (int i = c * NT + tid; i < a.B * 81; i += G * NT) {
+      const int b = i / 81, k = i % 81;
+      if (!active(pc, b, gs - 1)) continue;
+      float m = __ldg(a.bp + k);
+#pragma unroll
+      for (int z = 0; z < PKS; ++z) m += ldf(a.Pp + ((int64_t)z * a.B + b) * 81 + k);
+      const int64_t* p = a.plan + b * DPLAN;
+      if (k < NMEL) {
+        reinterpret_cast<float*>(p[6])[(gs - 1) * NMEL + k] = m;
+        a.work[(int64_t)b * ROW + LAST_OFF + k] = m;
+      } else {
+        reinterpret_cast<float*>(p[7])[gs - 1] = m;
+      }
+    }
+  }
+  if (a.trace && c == 0 && tid == 0)
+    for (int i = 0; i < 8; ++i) a.trace[i] = tacc[i];
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (gemm_cta && (tid >> 5) == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(gsy.tmem));
+  }
+}
+
+}  // namespace
+
+// Debug: later itts_r_decode_persistent launches add per-phase wall time (ns, CTA 0, summed over
+// the steps) to buf[0..7]: PRE1, PRE2, ATT gates, QUERY, ATT-A, ATT-B, DEC gates, PROJ.  null = off.
+ITTS_API int itts_r_decode_debug_trace(void* buf) {
+  g_dec_trace = static_cast<unsigned long long*>(buf);
+  return ITTS_OK;
+}
+
+// Runs `nsteps` decoder steps for B gathered rows (see DecArgs).  Scratch buffers are owned by
+// the caller; `bar` (2 x u32) is zeroed here on the stream.  grid = min(#SMs, 148) CTAs.
+ITTS_API int itts_r_decode_persistent(int32_t B, int32_t nsteps, const int64_t* plan, float* work, void* xb,
+                                      const float* W0T, const float* W1T, const void* Wa, const float* ba,
+                                      const void* Wd, const float* bd, const float* WqT, const float* WlocD,
+                                      const float* v, const float* WpT, const float* bp,
+                                      float* H1, float* Qp, float* Pp, float* U, int64_t u_ld, float* AP,
+                                      unsigned* bar, void* stream) {
+  if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
+  if (B > 256) return ITTS_EUNSUPPORTED;  // attention task table in shared memory
+  if (nsteps <= 0 || !plan || !work || !xb || !Wa || !Wd || !bar) return ITTS_EINVAL;
+  if (tcg::num_sms() < GEMM_CTAS) return ITTS_EUNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  DecArgs a{B, nsteps, 0, plan, work, (__nv_bfloat16*)xb, W0T, W1T, (const __nv_bfloat16*)Wa, ba,
+            (const __nv_bfloat16*)Wd, bd, WqT, WlocD, v, WpT, bp, H1, Qp, Pp, U, u_ld, AP, bar,
+            g_dec_trace};
+  const size_t smem = 1024 + GS * (GA_BYTES + GW_BYTES) + sizeof(AttSmem);
+  const int b16 = (B + 15) / 16 * 16, arows = b16 < 128 ? b16 : 128;
+  CUtensorMap mA, mWa, mWd;
+  if (!tcg::encode_2d(&mA, xb, XB2, (uint64_t)b16, XB2, 64, arows, 128)) return ITTS_EINVAL;
+  if (!tcg::encode_2d(&mWa, Wa, KA, 4096, KA, 64, 32, 128)) return ITTS_EINVAL;
+  if (!tcg::encode_2d(&mWd, Wd, KD, 4096, KD, 64, 32, 128)) return ITTS_EINVAL;
+  uint32_t a_box_bytes = (uint32_t)arows * 128;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_dec_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    configured = true;
+  }
+  cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st);
+  if (e != cudaSuccess) return (int)e;
+  const int G = tcg::num_sms();
+  void* args[] = {&a, &mA, &mWa, &mWd, &a_box_bytes};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelExC(&cfg, (const void*)k_dec_persist, args);
+  return e == cudaSuccess ? ITTS_OK : (int)e;
+}

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int SWZ = K::SWZ, KT = K::KT, NKC = K::NKC, NB = K::NB, STAGES = K::STAGES;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sX = smem;
   uint8_t* sT = sX + K::X_BYTES;
   uint8_t* sW = sT + K::T_BYTES + K::TAIL;

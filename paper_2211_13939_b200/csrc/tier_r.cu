@@ -226,23 +226,28 @@ __global__ void __launch_bounds__(256) k_lstm_cell(const float* __restrict__ G, 
   xb[(int64_t)b * XB_ROW + h_off + j] = __float2bfloat16_rn(h);
 }
 
-// One 4-CTA cluster per item (8 warps each): CTA r owns text positions [r*L/4, (r+1)*L/4)
-// for the location features, energies, softmax numerators and the partial context; the
-// softmax max / sum and the context are reduced across the cluster through distributed
-// shared memory in rank order (deterministic, independent of the batch).
+// One CL-CTA cluster per item (8 warps each; CL = 8 for small pooled batches, 4 otherwise):
+// CTA r owns text positions [r*L/CL, (r+1)*L/CL) for the location features, energies,
+// softmax numerators and the partial context; the softmax max / sum and the context are
+// reduced across the cluster through distributed shared memory in rank order
+// (deterministic, independent of the batch).
 // Q = query K-slice partials [QKS][B][128], Wloc [32][2][31], WdT [32][128], v [128].
-constexpr int AT_CL = 4;
+//
+// Latency structure: every global load of a phase is issued before the first use (weights
+// staged with float4 loads, pm rows for 4 positions per warp in flight while the location
+// features are contracted), so a step costs a handful of memory round trips.
 constexpr int AT_WARPS = 8;
 constexpr int LT = 128;  // positions per location-feature tile
 
-__global__ void __cluster_dims__(AT_CL, 1, 1) __launch_bounds__(AT_WARPS * 32)
+template <int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(AT_WARPS * 32, 3)
     k_attention(float* __restrict__ state, __nv_bfloat16* __restrict__ xb, const int64_t* __restrict__ plan,
                 const float* __restrict__ Q, const float* __restrict__ Wloc, const float* __restrict__ WdT,
                 const float* __restrict__ v, int step) {
   constexpr int NT = AT_WARPS * 32, HALO = (KLOC - 1) / 2;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
-  const int b = blockIdx.x / AT_CL, B = gridDim.x / AT_CL;
+  const int b = blockIdx.x / CL, B = gridDim.x / CL;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t* p = plan + b * DPLAN;
   if (step >= p[5]) return;  // the whole cluster returns together
@@ -251,7 +256,7 @@ __global__ void __cluster_dims__(AT_CL, 1, 1) __launch_bounds__(AT_WARPS * 32)
   const int L = (int)p[2];
   const float* wsrc = reinterpret_cast<const float*>(step == 0 ? p[3] : p[4]);
   float* wdst = reinterpret_cast<float*>(p[4]);
-  const int t_lo = (int)((int64_t)L * rank / AT_CL), t_hi = (int)((int64_t)L * (rank + 1) / AT_CL);
+  const int t_lo = (int)((int64_t)L * rank / CL), t_hi = (int)((int64_t)L * (rank + 1) / CL);
   const int Ls = t_hi - t_lo, Lh = Ls + 2 * HALO;
 
   extern __shared__ float dyn[];
@@ -259,53 +264,119 @@ __global__ void __cluster_dims__(AT_CL, 1, 1) __launch_bounds__(AT_WARPS * 32)
   float* w_acc = dyn + Lh;         // [Lh]
   float* e = dyn + 2 * Lh;         // [Ls]
   float* locf = dyn + ((2 * Lh + Ls + 3) & ~3);  // [LT][33]; later the context partials
-  __shared__ float q[ATT], sWloc[NF * 2 * KLOC], sWd[NF * ATT], sv[ATT], red[32];
-  __shared__ float cl_max[AT_CL], cl_sum[AT_CL];
+  __shared__ __align__(16) float q[ATT], sv[ATT], sWd[NF * ATT], sWlT[2 * KLOC * NF];  // sWlT[c][k][f]
+  __shared__ float red[32];
+  __shared__ float cl_max[CL], cl_sum[CL];
   __shared__ __align__(16) float ctx_local[EMB];
 
-  for (int i = tid; i < Lh; i += NT) {
-    const int t = t_lo - HALO + i;
-    const bool in = t >= 0 && t < L;
-    w_prev[i] = in ? wsrc[t] : 0.f;
-    w_acc[i] = in ? wsrc[L + t] : 0.f;
+  // ---- prologue: all loads in flight, then the shared-memory stores
+  {
+    constexpr int NWL = NF * 2 * KLOC / 4, NWD = NF * ATT / 4;  // float4 counts (496, 1024)
+    float4 wl[(NWL + NT - 1) / NT], wd[NWD / NT];
+    const float4* wl4 = reinterpret_cast<const float4*>(Wloc);
+    const float4* wd4 = reinterpret_cast<const float4*>(WdT);
+#pragma unroll
+    for (int r = 0; r < (NWL + NT - 1) / NT; ++r)
+      if (tid + r * NT < NWL) wl[r] = __ldg(wl4 + tid + r * NT);
+#pragma unroll
+    for (int r = 0; r < NWD / NT; ++r) wd[r] = __ldg(wd4 + tid + r * NT);
+    float qz[QKS];
+    if (tid < ATT) {
+#pragma unroll
+      for (int z = 0; z < QKS; ++z) qz[z] = Q[((int64_t)z * B + b) * ATT + tid];
+    }
+    float wp[2], wa[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int i = tid + r * NT, t = t_lo - HALO + i;
+      const bool in = i < Lh && t >= 0 && t < L;
+      wp[r] = in ? wsrc[t] : 0.f;
+      wa[r] = in ? wsrc[L + t] : 0.f;
+    }
+    for (int i = tid + 2 * NT; i < Lh; i += NT) {  // long texts only
+      const int t = t_lo - HALO + i;
+      const bool in = t >= 0 && t < L;
+      w_prev[i] = in ? wsrc[t] : 0.f;
+      w_acc[i] = in ? wsrc[L + t] : 0.f;
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+      if (tid + r * NT < Lh) {
+        w_prev[tid + r * NT] = wp[r];
+        w_acc[tid + r * NT] = wa[r];
+      }
+#pragma unroll
+    for (int r = 0; r < (NWL + NT - 1) / NT; ++r) {
+      const int i4 = tid + r * NT;
+      if (i4 < NWL) {
+        const float w4[4] = {wl[r].x, wl[r].y, wl[r].z, wl[r].w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // source [f][c][k] -> [c][k][f]
+          const int src = 4 * i4 + u, f = src / (2 * KLOC), ck = src - f * 2 * KLOC;
+          sWlT[ck * NF + f] = w4[u];
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NWD / NT; ++r) reinterpret_cast<float4*>(sWd)[tid + r * NT] = wd[r];
+    if (tid < ATT) {
+      float qa = qz[0];
+#pragma unroll
+      for (int z = 1; z < QKS; ++z) qa += qz[z];  // query K-slices, fixed order
+      q[tid] = qa;
+      sv[tid] = v[tid];
+    }
   }
-  if (tid < ATT) {
-    float qa = Q[(int64_t)b * ATT + tid];
-    for (int z = 1; z < QKS; ++z) qa += Q[((int64_t)z * B + b) * ATT + tid];  // query K-slices, fixed order
-    q[tid] = qa;
-    sv[tid] = v[tid];
-  }
-  for (int i = tid; i < NF * 2 * KLOC; i += NT) sWloc[i] = Wloc[i];
-  for (int i = tid; i < NF * ATT; i += NT) sWd[i] = WdT[i];
   __syncthreads();
+
+  // ---- location features + energies, LT positions at a time.  Energies: 8 lanes per position
+  // (lane sl holds dims 4sl..4sl+3 of each 32-dim quarter), 4 positions per warp in flight.
+  const int sub = lane >> 3, sl = lane & 7;
   for (int t0 = 0; t0 < Ls; t0 += LT) {
     const int nt = min(LT, Ls - t0);
     for (int i = tid; i < nt * NF; i += NT) {
       const int tl = t0 + i / NF, f = i % NF;  // local position; halo index = tl + k
-      const float* wf = sWloc + f * 2 * KLOC;
       float c = 0.f;
 #pragma unroll
-      for (int k = 0; k < KLOC; ++k) c = fmaf(wf[k], w_prev[tl + k], fmaf(wf[KLOC + k], w_acc[tl + k], c));
+      for (int k = 0; k < KLOC; ++k)
+        c = fmaf(sWlT[k * NF + f], w_prev[tl + k], fmaf(sWlT[(KLOC + k) * NF + f], w_acc[tl + k], c));
       locf[(i / NF) * (NF + 1) + f] = c;
     }
     __syncthreads();
-    for (int tt = warp; tt < nt; tt += AT_WARPS) {
-      float loc[4] = {0.f, 0.f, 0.f, 0.f};
-      const float* lf = locf + tt * (NF + 1);
+    for (int tt = warp * 4 + sub; tt - sub < nt; tt += AT_WARPS * 4) {
+      const bool live = tt < nt;
+      float4 pv[4];
+      const float4* prow = reinterpret_cast<const float4*>(pm + (int64_t)(t_lo + t0 + (live ? tt : 0)) * ATT);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) pv[j] = prow[8 * j + sl];
+      float loc[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) loc[i] = 0.f;
+      const float* lf = locf + (live ? tt : 0) * (NF + 1);
 #pragma unroll 8
       for (int f = 0; f < NF; ++f) {
         const float cf = lf[f];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) loc[i] = fmaf(sWd[f * ATT + lane + 32 * i], cf, loc[i]);
+        for (int j = 0; j < 4; ++j) {
+          const float4 w4 = reinterpret_cast<const float4*>(sWd + f * ATT)[8 * j + sl];
+          loc[4 * j] = fmaf(w4.x, cf, loc[4 * j]);
+          loc[4 * j + 1] = fmaf(w4.y, cf, loc[4 * j + 1]);
+          loc[4 * j + 2] = fmaf(w4.z, cf, loc[4 * j + 2]);
+          loc[4 * j + 3] = fmaf(w4.w, cf, loc[4 * j + 3]);
+        }
       }
       float en = 0.f;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int a = lane + 32 * i;
-        en = fmaf(sv[a], tanhf((q[a] + loc[i]) + pm[(int64_t)(t_lo + t0 + tt) * ATT + a]), en);
+      for (int j = 0; j < 4; ++j) {
+        const int a0 = 32 * j + 4 * sl;
+        const float pa[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) en = fmaf(sv[a0 + u], tanhf((q[a0 + u] + loc[4 * j + u]) + pa[u]), en);
       }
-      en = itts::warp_sum(en);
-      if (lane == 0) e[t0 + tt] = en;
+      en += __shfl_xor_sync(0xffffffffu, en, 4);
+      en += __shfl_xor_sync(0xffffffffu, en, 2);
+      en += __shfl_xor_sync(0xffffffffu, en, 1);
+      if (live && sl == 0) e[t0 + tt] = en;
     }
     __syncthreads();
   }
@@ -313,11 +384,11 @@ __global__ void __cluster_dims__(AT_CL, 1, 1) __launch_bounds__(AT_WARPS * 32)
   float lmax = -INFINITY;
   for (int t = tid; t < Ls; t += NT) lmax = fmaxf(lmax, e[t]);
   lmax = itts::block_reduce<float, true>(lmax, red);
-  if (tid < AT_CL) *cluster.map_shared_rank(&cl_max[rank], tid) = lmax;
+  if (tid < CL) *cluster.map_shared_rank(&cl_max[rank], tid) = lmax;
   cluster.sync();
   float M = cl_max[0];
 #pragma unroll
-  for (int r = 1; r < AT_CL; ++r) M = fmaxf(M, cl_max[r]);
+  for (int r = 1; r < CL; ++r) M = fmaxf(M, cl_max[r]);
   float lsum = 0.f;
   for (int t = tid; t < Ls; t += NT) {
     const float x = expf(e[t] - M);
@@ -325,11 +396,11 @@ __global__ void __cluster_dims__(AT_CL, 1, 1) __launch_bounds__(AT_WARPS * 32)
     lsum += x;
   }
   lsum = itts::block_reduce<float, false>(lsum, red);
-  if (tid < AT_CL) *cluster.map_shared_rank(&cl_sum[rank], tid) = lsum;
+  if (tid < CL) *cluster.map_shared_rank(&cl_sum[rank], tid) = lsum;
   cluster.sync();
   float Z = cl_sum[0];
 #pragma unroll
-  for (int r = 1; r < AT_CL; ++r) Z += cl_sum[r];
+  for (int r = 1; r < CL; ++r) Z += cl_sum[r];
   const float iz = 1.0f / Z;
   for (int t = tid; t < Ls; t += NT) {
     const float a = e[t] * iz;
@@ -372,7 +443,7 @@ __global__ void __cluster_dims__(AT_CL, 1, 1) __launch_bounds__(AT_WARPS * 32)
     for (int d = tid; d < EMB; d += NT) {
       float c = ctx_local[d];
 #pragma unroll
-      for (int r = 1; r < AT_CL; ++r) c += cluster.map_shared_rank(ctx_local, r)[d];
+      for (int r = 1; r < CL; ++r) c += cluster.map_shared_rank(ctx_local, r)[d];
       s[CTX_OFF + d] = c;
       xb[(int64_t)b * XB_ROW + CTX_OFF + d] = __float2bfloat16_rn(c);
     }
@@ -611,22 +682,29 @@ ITTS_API int itts_r_lstm_cell(const float* G, int32_t nsplit, const float* bias,
   ITTS_RETURN_LAUNCH();
 }
 
-ITTS_API int itts_r_attention(float* state, void* xb, const int64_t* plan, int32_t B, int32_t max_len,
-                              const float* Q, const float* Wloc, const float* WdT, const float* v,
-                              int32_t step, void* stream) {
-  if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
-  const int ls = (max_len + AT_CL - 1) / AT_CL + 1, lh = ls + KLOC;
+template <int CL>
+int launch_attention(float* state, void* xb, const int64_t* plan, int32_t B, int32_t max_len, const float* Q,
+                     const float* Wloc, const float* WdT, const float* v, int32_t step, cudaStream_t st) {
+  const int ls = (max_len + CL - 1) / CL + 1, lh = ls + KLOC;
   const size_t smem = ((size_t)(2 * lh + ls + 4) + (size_t)LT * (NF + 1)) * sizeof(float);
   static_assert(LT * (NF + 1) >= AT_WARPS * EMB, "context partials alias the location tile");
   if (smem > 150 * 1024) return ITTS_EUNSUPPORTED;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024);
+    cudaFuncSetAttribute(k_attention<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024);
     configured = true;
   }
-  k_attention<<<B * AT_CL, AT_WARPS * 32, smem, (cudaStream_t)stream>>>(state, (__nv_bfloat16*)xb, plan, Q, Wloc,
-                                                                        WdT, v, step);
+  k_attention<CL><<<B * CL, AT_WARPS * 32, smem, st>>>(state, (__nv_bfloat16*)xb, plan, Q, Wloc, WdT, v, step);
   ITTS_RETURN_LAUNCH();
+}
+
+ITTS_API int itts_r_attention(float* state, void* xb, const int64_t* plan, int32_t B, int32_t max_len,
+                              const float* Q, const float* Wloc, const float* WdT, const float* v,
+                              int32_t step, void* stream) {
+  if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
+  // small pooled batches spread each item over 8 SMs, large ones over 4 (one wave either way)
+  if (B <= 48) return launch_attention<8>(state, xb, plan, B, max_len, Q, Wloc, WdT, v, step, (cudaStream_t)stream);
+  return launch_attention<4>(state, xb, plan, B, max_len, Q, Wloc, WdT, v, step, (cudaStream_t)stream);
 }
 
 // Mel/gate projection; Pp = scratch [PKS][B][81].

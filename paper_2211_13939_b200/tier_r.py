@@ -46,6 +46,10 @@ UPS = (8, 8, 2, 2)
 STAGE_C = (256, 128, 64, 32)
 DEC_KSPLIT = 4      # K-split of the decoder gate GEMMs (partials summed in fixed order by the cell kernel)
 GRAPH_MAX_L = 8192  # attention smem is sized for this in captured graphs; longer texts run eagerly
+HID = 1024
+XB2 = 4864          # persistent decoder's bf16 mirror row (two banks of att_h / dec_h)
+PERSIST_MAX_L = 8192  # 256 attention chunks of <= 32 positions
+PERSIST_MAX_B = 192   # above this the per-kernel chain (tc_conv gate GEMMs + cluster attention) is faster
 
 
 def _hifigan_macs_per_frame() -> int:
@@ -105,6 +109,7 @@ class TierREngine:
         self.timers: list | None = None  # set to [] to record (kind, ev0, ev1, units) per module call
         self.use_graphs = True           # CUDA-graph the 32-step decoder chunk per (batch, L) bucket
         self.fused_mrf = True            # one fused c1->c2 kernel per ResBlock1 layer (resblock_tc.cu)
+        self.persistent_decoder = True   # whole decoder chunk in one grid-synchronised kernel (dec_persist.cu)
         self._dec_buckets: dict = {}
         self._graph_warm = False
 
@@ -157,10 +162,18 @@ class TierREngine:
         wd = torch.cat([wih[:, 1024:], wih[:, :1024], w["dec_rnn.w_hh"]], 1)             # [ctx|att_h|dec_h]
         self.dec_bias = f32(w["dec_rnn.b_ih"] + w["dec_rnn.b_hh"])
         self.dec_gemm = (wd.to(d).to(torch.bfloat16)[None].contiguous(), [0], zeros)
+        # persistent decoder: gate rows interleaved per CTA c = [q gate][8 units 8c..8c+7]
+        perm = lambda t: t.reshape(4, HID // 8, 8, -1).permute(1, 0, 2, 3).reshape(4 * HID, -1)
+        self.Wa_p = perm(wa.to(d)).to(torch.bfloat16).contiguous()
+        self.ba_p = perm(self.att_bias[:, None]).reshape(-1).contiguous()
+        self.Wd_p = perm(wd.to(d)).to(torch.bfloat16).contiguous()
+        self.bd_p = perm(self.dec_bias[:, None]).reshape(-1).contiguous()
         self.WqT = f32(w["att.query_layer"].T)                                           # [1024][128]
         self.Wloc = f32(w["att.location_conv"])                                          # [32][2][31]
         self.WdT = f32(w["att.location_dense"].T)                                        # [32][128]
         self.v = f32(w["att.v"][0])
+        # location conv (32 x 2 x 31) composed with the location dense layer (32 -> 128): [2][31][128]
+        self.WlocD = torch.einsum("fck,fa->cka", self.Wloc.double(), self.WdT.double()).float().contiguous()
         self.WpT = f32(torch.cat([w["proj.w"], w["gate.w"]], 0).T)                      # [1536][81]
         self.bp = f32(torch.cat([w["proj.b"], w["gate.b"]]))
         # HiFi-GAN
@@ -353,6 +366,16 @@ class TierREngine:
         """K1 gather -> nsteps x (prenet, att GEMM, cell, query, attention, dec GEMM, cell, proj) -> K1 scatter."""
         st, n = self._st(), b.n
         self._call("itts_gather_rows", b.work.data_ptr(), b.d_src.data_ptr(), n, 4 * ROW, st)
+        if self.persistent_decoder and max_L <= PERSIST_MAX_L and n <= PERSIST_MAX_B:
+            b.ensure_persistent(max_L)
+            self._call("itts_r_decode_persistent", n, nsteps, b.d_plan.data_ptr(), b.work.data_ptr(),
+                       b.xb2.data_ptr(), self.W0T.data_ptr(), self.W1T.data_ptr(), self.Wa_p.data_ptr(),
+                       self.ba_p.data_ptr(), self.Wd_p.data_ptr(), self.bd_p.data_ptr(), self.WqT.data_ptr(),
+                       self.WlocD.data_ptr(), self.v.data_ptr(), self.WpT.data_ptr(),
+                       self.bp.data_ptr(), b.H1.data_ptr(), b.Q.data_ptr(), b.P.data_ptr(), b.U.data_ptr(),
+                       b.U.shape[1], b.AP.data_ptr(), b.bar.data_ptr(), st)
+            self._call("itts_scatter_rows", b.d_dst.data_ptr(), b.work.data_ptr(), n, 4 * ROW, st)
+            return
         self._call("itts_r_dec_prepare", b.work.data_ptr(), b.xbm.data_ptr(), n, st)
         rows = self._iota(n)
         x_att, x_dec = b.xbm[:, :1792], b.xbm[:, 256:]
@@ -579,6 +602,17 @@ class _DecBuffers:
         self.Q = torch.empty(8, n, 128, dtype=torch.float32, device=dev)    # query K-slice partials
         self.P = torch.empty(8, n, 81, dtype=torch.float32, device=dev)     # projection K-slice partials
         self.H1 = torch.empty(n, 256, dtype=torch.float32, device=dev)
+        self.dev, self.xb2, self.U, self.AP, self.bar = dev, None, None, None, None
+
+    def ensure_persistent(self, max_L: int) -> None:
+        """Scratch of the persistent decoder kernel (allocated once per buffer set)."""
+        if self.U is not None and self.U.shape[1] >= max_L:
+            return
+        n16 = -(-self.n // 16) * 16
+        self.xb2 = torch.zeros(n16, XB2, dtype=torch.bfloat16, device=self.dev)
+        self.U = torch.empty(self.n, max(max_L, 256), dtype=torch.float32, device=self.dev)
+        self.AP = torch.empty(self.n, 256, 2 + 512, dtype=torch.float32, device=self.dev)
+        self.bar = torch.zeros(2, dtype=torch.int32, device=self.dev)
 
 
 class _DecBucket(_DecBuffers):

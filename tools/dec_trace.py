@@ -1,0 +1,46 @@
+"""Per-phase time breakdown of the persistent decoder kernel (itts_r_decode_debug_trace).
+
+    python tools/dec_trace.py [--batches 16,64,128]
+"""
+import argparse
+import random
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
+from paper_2211_13939_b200 import _native  # noqa: E402
+from paper_2211_13939_b200.domain import PipelineConfig  # noqa: E402
+from paper_2211_13939_b200.frontend import default_lexicon, run_frontend  # noqa: E402
+from paper_2211_13939_b200.harness import random_text  # noqa: E402
+from paper_2211_13939_b200.tier_r import TierREngine  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--batches", default="16,64,128")
+args = ap.parse_args()
+eng = TierREngine(PipelineConfig(), "cuda:0")
+eng.use_graphs = False
+lex = default_lexicon()
+names = ["PRE1", "PRE2", "ATT gates", "QUERY", "ATT-A", "ATT-B", "DEC gates", "PROJ"]
+for B in [int(x) for x in args.batches.split(",")]:
+    rng = random.Random(B)
+    fos = [run_frontend(random_text(rng, 20, 200, lex), lex) for _ in range(B)]
+    encs = eng.encoder_batch(fos)
+    eng.decoder_batch([(st, enc) for enc, st in encs])
+    torch.cuda.synchronize()
+    buf = torch.zeros(16, dtype=torch.int64, device="cuda")
+    _native.call("itts_r_decode_debug_trace", buf.data_ptr())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(eng.stream)
+    eng.decoder_batch([(st, enc) for enc, st in encs])
+    e1.record(eng.stream)
+    torch.cuda.synchronize()
+    _native.call("itts_r_decode_debug_trace", None)
+    t = buf.cpu().tolist()
+    print(f"B={B}: chunk {e0.elapsed_time(e1):.3f} ms; per step (us): " +
+          ", ".join(f"{n} {t[i] / 32e3:.1f}" for i, n in enumerate(names)))
+    if t[13]:
+        sub = ["q/w loads", "bulk wait", "energies", "softmax", "context+store"]
+        print(f"   ATT-A CTA0: {t[13] / 32:.1f} tasks/step; per task (us): " +
+              ", ".join(f"{n} {t[8 + i] / t[13] / 1e3:.2f}" for i, n in enumerate(sub)))
