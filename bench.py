@@ -208,10 +208,17 @@ def run_ours(args) -> None:
     gc.collect()
     gc.freeze()
     gc.set_threshold(200000, 100, 100)
-    # untimed warm-up of every code path (tensor maps, smem attributes, allocator pools)
+    # untimed warm-up of every code path (tensor maps, smem attributes, lazy module loading,
+    # allocator pools): a Poisson second, then bursts of simultaneous arrivals (large encoder batches)
+    from paper_2211_13939_b200.harness import TimedRequest, random_text
     warm = serve(mods, cfg, poisson_trace(50, 1.0, seed=args.seed + 7, lexicon=lex), warmup_iters=0,
                  timed_iters=2, drain_seconds=0.0)
+    wr = random.Random(args.seed + 8)
+    for burst in (8, 32, 64):
+        warm = serve(mods, cfg, [TimedRequest(0.0, random_text(wr, 20, 200, lex)) for _ in range(burst)],
+                     warmup_iters=0, timed_iters=None, drain_seconds=0.0)
     del warm
+    log("warm-up done")
     torch.cuda.synchronize()
 
     peaks = _peaks()

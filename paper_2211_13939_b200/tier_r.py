@@ -98,7 +98,8 @@ class TierREngine:
         w = weights if weights is not None else W.tier_r_weights(seed)
         with torch.cuda.stream(self.stream):
             self._prepare_weights(w)
-            self.arena = RaggedArena(self.dtype, self.device, 1 << 24, self.stream)
+            # 2 GB up front: growing (re-allocate + copy) inside a serving window stalls an iteration
+            self.arena = RaggedArena(self.dtype, self.device, 1 << 29, self.stream)
             curve = cached_curve(cfg.overlap_samples)
             self.fade = torch.from_numpy(np.concatenate([curve.fade_in, curve.fade_out])).float().to(self.device)
             self.iota = torch.arange(1 << 16, dtype=torch.int32, device=self.device)
@@ -111,6 +112,7 @@ class TierREngine:
         self.fused_mrf = True            # one fused c1->c2 kernel per ResBlock1 layer (resblock_tc.cu)
         self.persistent_decoder = True   # whole decoder chunk in one grid-synchronised kernel (dec_persist.cu)
         self._dec_buckets: dict = {}
+        self._pool: dict = {}
         self._graph_warm = False
 
     def _mark(self, kind: str, units: float):
@@ -213,16 +215,57 @@ class TierREngine:
         tc.resblock_tc(x, c1, c2, dil, row_out, stream=self._st(), **kw)
         self.launches += 1
 
+    def _buf(self, name: str, numel: int, dtype=torch.bfloat16, zero: bool = False) -> torch.Tensor:
+        """Persistent grow-only work buffer (the first `numel` elements), so steady-state serving
+        never reaches cudaMalloc.  All users run on the engine stream, so reuse is ordered."""
+        t = self._pool.get(name)
+        if t is None or t.numel() < numel or t.dtype != dtype:
+            t = torch.empty(max(int(numel * 1.25), 1024), dtype=dtype, device=self.device)
+            self._pool[name] = t
+        v = t[:numel]
+        if zero:
+            v.zero_()
+        return v
+
+    def reserve_vocoder(self, max_batch: int, frames: int | None = None) -> None:
+        """Grow the vocoder work buffers for `max_batch` chunks of `frames` (default O + C) frames."""
+        T = frames or (self.cfg.overlap_frames + self.cfg.chunk_frames)
+        rows0 = max_batch * (T + 2 * MEL_HALO)
+        self._buf("x0", rows0 * 128)
+        self._buf("act_in", rows0 * 512)
+        biggest, mult = 0, 1
+        for u, C in zip(UPS, STAGE_C):
+            mult *= u
+            biggest = max(biggest, max_batch * (T * mult + 2 * MRF_HALO) * C)
+        for i in range(6):
+            self._buf(f"b16_{i}", biggest)
+        self._buf("audio", max_batch * T * self.cfg.hop_samples, torch.float32)
+        for name, m in (("rm0", 1), ("rmT0", 1), ("rm_s0", 8), ("rmT1", 8), ("rm_s1", 64), ("rmT2", 64),
+                        ("rm_s2", 128), ("rmT3", 128), ("rm_s3", 256)):
+            self._buf(name, max_batch * (T * m + 2 * MRF_HALO), torch.int32)
+
+    def prewarm_pinned(self, max_batch: int = 256) -> None:
+        """Fill the caching host allocator with pinned blocks of every power-of-two size the
+        serving path requests (plans up to the audio of `max_batch` chunks), so cudaHostAlloc --
+        slow, and synchronising -- never runs inside a serving iteration."""
+        top = max(4 * max_batch * (self.cfg.overlap_frames + self.cfg.chunk_frames) * self.cfg.hop_samples, 1 << 16)
+        blocks = []
+        for k in range(12, top.bit_length() + 1):
+            for _ in range(4 if k < 20 else 3):
+                blocks.append(torch.empty(1 << k, dtype=torch.uint8, pin_memory=True))
+        del blocks
+
     def _iota(self, n: int) -> torch.Tensor:
         if n > self.iota.numel():
             self.iota = torch.arange(2 * n, dtype=torch.int32, device=self.device)
         return self.iota[:n]
 
-    def _rowmap(self, layout: _Layout, out_first: np.ndarray, up: int) -> torch.Tensor:
+    def _rowmap(self, layout: _Layout, out_first: np.ndarray, up: int, name: str | None = None) -> torch.Tensor:
         n = len(layout.rows)
         plan = np.stack([layout.base, np.array(layout.rows, np.int64), np.full(n, layout.halo, np.int64),
                          out_first.astype(np.int64), np.full(n, up, np.int64)], 1)
-        rm = torch.empty(layout.total, dtype=torch.int32, device=self.device)
+        rm = (self._buf(name, layout.total, torch.int32) if name is not None
+              else torch.empty(layout.total, dtype=torch.int32, device=self.device))
         self._call("itts_r_rowmap", self._up(plan).data_ptr(), n,
                    int(max(layout.rows)) + 2 * layout.halo, rm.data_ptr(), self._st())
         return rm
@@ -402,9 +445,12 @@ class TierREngine:
         return self._dec_buckets[B]
 
     def prepare_graphs(self, max_batch: int = 256) -> None:
-        """Capture the decoder-chunk graph of every 16-row bucket up to ``max_batch`` now,
-        so no capture happens on the serving path."""
+        """Capture the decoder-chunk graph of every 16-row bucket up to ``max_batch`` now, and
+        grow the vocoder work buffers for that batch, so no capture or cudaMalloc happens on
+        the serving path."""
+        self.prewarm_pinned(max_batch)
         with torch.cuda.stream(self.stream):
+            self.reserve_vocoder(max_batch)
             for B in range(16, max_batch + 1, 16):
                 bk = self._dec_bucket(B)
                 if bk.graph is None:
@@ -474,12 +520,15 @@ class TierREngine:
                 results.append((req, dst, int(vstate.emitted_samples)))
             d_mplan = self._up(mplan)
             d_pplan = self._up(pplan)
-            audio = torch.empty(max(int(out_off[-1]), 1), dtype=torch.float32, device=dev)
+            audio = self._buf("audio", max(int(out_off[-1]), 1), torch.float32)
             with self._mark("vocoder", 2.0 * HIFIGAN_MACS_PER_FRAME * sum(Ts)):
                 x4 = self._hifigan(Ts, lay0, d_mplan)
             self._call("itts_r_post_splice", x4.data_ptr(), d_pplan.data_ptr(), n, max(mt[4] for mt in metas),
                        self.wpost.data_ptr(), self.bpost, self.fade.data_ptr(), O, S, audio.data_ptr(), st)
-            host = torch.empty(audio.numel(), dtype=torch.float32, pin_memory=True)
+            # fresh pinned block per call (the chunks alias it); power-of-two sizes keep the
+            # caching host allocator from calling cudaHostAlloc in steady state
+            host = torch.empty(1 << max(12, (audio.numel() - 1).bit_length()), dtype=torch.float32,
+                               pin_memory=True)[:audio.numel()]
             host.copy_(audio, non_blocking=True)
         self.stream.synchronize()
         self.d2h_bytes += 4 * int(out_off[-1])
@@ -495,10 +544,11 @@ class TierREngine:
     def _hifigan(self, Ts: list[int], lay0: _Layout, d_mplan: torch.Tensor) -> torch.Tensor:
         """HiFi-GAN V1 over a packed batch of spliced chunks -> stage-4 bf16 act (lrelu 0.01 applied)."""
         dev, st, n = self.device, self._st(), len(Ts)
-        x0 = torch.zeros(lay0.total, 128, dtype=torch.bfloat16, device=dev)
+        with torch.cuda.stream(self.stream):
+            x0 = self._buf("x0", lay0.total * 128, zero=True).view(lay0.total, 128)
         self._call("itts_r_mel_assemble", d_mplan.data_ptr(), n, max(Ts), x0.data_ptr(), 128, st)
-        rm0 = self._rowmap(lay0, lay0.first, 1)
-        act_in = torch.empty(lay0.total, 512, dtype=torch.bfloat16, device=dev)
+        rm0 = self._rowmap(lay0, lay0.first, 1, "rm0")
+        act_in = self._buf("act_in", lay0.total * 512).view(lay0.total, 512)
         self._conv(x0, self.conv_pre, 512, rm0, act_out=act_in, slope=0.1)
         prev, mult, layouts = lay0, 1, []
         for u in UPS:
@@ -506,18 +556,18 @@ class TierREngine:
             layouts.append(_Layout([T * mult for T in Ts], MRF_HALO))
         biggest = max(l.total * c for l, c in zip(layouts, STAGE_C))
         # bf16 only: the residual stream is kept as lrelu(y, 0.1) and inverted on load
-        b16 = [torch.empty(biggest, dtype=torch.bfloat16, device=dev) for _ in range(6)]  # xa ya tb acc oa oa'
+        b16 = [self._buf(f"b16_{i}", biggest) for i in range(6)]  # xa ya tb acc oa oa'
         for s, (u, lay) in enumerate(zip(UPS, layouts)):
             C = STAGE_C[s]
             view = lambda t: t[:lay.total * C].view(lay.total, C)
             XA, YA, TB, ACC = (view(t) for t in b16[:4])
             OA_next = view(b16[4 + s % 2])
             # transposed conv: each input row of the previous stage -> u output rows
-            rmT = self._rowmap(prev, lay.first, u)
+            rmT = self._rowmap(prev, lay.first, u, f"rmT{s}")
             self._conv(act_in, self.ups[s], C, rmT, act_out=XA, slope=0.1, zero_halo=False)
             zplan = np.stack([lay.base, np.array(lay.rows, np.int64), np.full(n, lay.halo, np.int64)], 1)
             self._call("itts_r_zero_halo", self._up(zplan).data_ptr(), n, lay.halo, XA.data_ptr(), C, st)
-            rm = self._rowmap(lay, lay.first, 1)
+            rm = self._rowmap(lay, lay.first, 1, f"rm_s{s}")
             slope_out = 0.1 if s < 3 else 0.01
             if self.fused_mrf:
                 # one fused kernel per ResBlock1 layer; ping-pong YA/TB (a layer must not write its input)
