@@ -128,17 +128,19 @@ int itts_resblock_debug_trace(void* buf);
  * The gate GEMMs between these calls are itts_conv1d_tc with one tap. */
 /* K6P: the whole decoder chunk (nsteps steps) as one persistent, grid-synchronised kernel
  * (dec_persist.cu).  work = fp32 [B][4944] gathered state rows, plan as above; xb = bf16
- * [ceil16(B)][4864] scratch mirror; Wa / Wd = bf16 gate weights with rows interleaved per
- * 8 hidden units ([128][4 gates x 8 units][K], K = 1792 / 2560), ba / bd the same order;
+ * scratch operand mirror, ceil(B/128) x 76 x 128 x 64 (UMMA-swizzled tiles); Wa / Wd = bf16
+ * gate weights as [32 groups][K/64 chunks][128 rows = 32 units x 4 gates][64] swizzled tiles
+ * (K = 1792 / 2560), ba / bd fp32 [32][128] in the same row order; Gp = fp32
+ * [4][32][ceil16(B)][128] K-split partials;
  * W0T [80][256], W1T [256][256], WqT [1024][128], v [128], WpT [1536][81], bp [81] fp32;
  * WlocD [2][31][128] = the location conv composed with the location dense layer
  * (sum_f Wloc[f][c][k] WdT[f][a]).  Scratch: H1 [B][256], Q [8][B][128], P [8][B][81],
- * U [B][u_ld >= max L], AP [B][256][514], bar = 2 x u32.  Texts up to 8192 phonemes. */
+ * U [B][u_ld >= max L], AP [B][256][514], bar = 34 x u32.  B <= 256, texts <= 8192 phonemes. */
 int itts_r_decode_persistent(int32_t B, int32_t nsteps, const int64_t* plan, float* work, void* xb,
                              const float* W0T, const float* W1T, const void* Wa, const float* ba,
                              const void* Wd, const float* bd, const float* WqT, const float* WlocD,
                              const float* v, const float* WpT, const float* bp,
-                             float* H1, float* Q, float* P, float* U, int64_t u_ld, float* AP,
+                             float* Gp, float* H1, float* Q, float* P, float* U, int64_t u_ld, float* AP,
                              unsigned* bar, void* stream);
 /* Profiling aid: per-phase wall time of later persistent-decoder launches ([8] u64 ns). */
 int itts_r_decode_debug_trace(void* buf);

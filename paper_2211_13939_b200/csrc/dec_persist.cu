@@ -34,6 +34,22 @@ constexpr int NMEL = 80, EMB = 512, HID = 1024, PRE = 256, ATT = 128, NF = 32, K
 constexpr int P_OFF = 0, CTX_OFF = 256, ATTH_OFF = 768, DECH_OFF = 1792, ATTC_OFF = 2816, DECC_OFF = 3840,
               LAST_OFF = 4864, ROW = 4944;
 constexpr int XB2 = 4864;        // bf16 mirror row: [p | ctx | att_h b0 | dec_h b0 | att_h b1 | dec_h b1]
+constexpr int NCC = XB2 / 64;    // 64-column chunks of the mirror
+
+// The bf16 operand mirror is kept in the UMMA-ready layout: per (128-item block, 64-column chunk)
+// one [128 rows][128 B] tile with the 128B swizzle applied, so the A operand of a gate-GEMM
+// stage is ONE contiguous bulk copy (no per-row TMA requests).
+__device__ __forceinline__ int64_t xb_off(int r, int col) {
+  const int cc = col >> 6, j = (col >> 3) & 7, e = col & 7;
+  return ((int64_t)((r >> 7) * NCC + cc) * 128 + (r & 127)) * 64 + ((j ^ (r & 7)) << 3) + e;
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tcg::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(tcg::smem_u32(bar))
+               : "memory");
+}
 constexpr int DPLAN = 8;
 constexpr int NT = 256, NW = 8;  // threads / warps per CTA
 constexpr int QKS = 8, PKS = 8;  // query / projection K-slices
@@ -55,25 +71,26 @@ struct DecArgs {
   int B, nsteps, step0;            // rows, steps in this launch, global index of the first step
   const int64_t* plan;             // [B][8]
   float* work;                     // [B][ROW]
-  __nv_bfloat16* xb;               // [B16][XB2] (rows padded to 16)
+  __nv_bfloat16* xb;               // [ceil(B/128)][NCC][128][64] swizzled tiles (see xb_off)
   const float* W0T;                // [80][256]
   const float* W1T;                // [256][256]
-  const __nv_bfloat16* Wa;         // [128][32][1792] unit-interleaved att gate rows
+  const __nv_bfloat16* Wa;         // [128 CTAs][28 chunks][32 rows][64] swizzled tiles, unit-interleaved rows
   const float* ba;                 // [128][32]
-  const __nv_bfloat16* Wd;         // [128][32][2560]
+  const __nv_bfloat16* Wd;         // [128][40][32][64]
   const float* bd;                 // [128][32]
   const float* WqT;                // [1024][128]
   const float* WlocD;              // [2][31][128] = location conv composed with the location dense layer
   const float* v;                  // [128]
   const float* WpT;                // [1536][81]
   const float* bp;                 // [81]
+  float* Gp;                       // [4 splits][32 groups][B16][128] gate GEMM K-split partials
   float* H1;                       // [B][256]
   float* Qp;                       // [QKS][B][128]
   float* Pp;                       // [PKS][B][81]
   float* U;                        // [B][u_ld] unnormalised attention numerators
   int64_t u_ld;
   float* AP;                       // [B][MAXCH][2 + 512] chunk max, sum, context partial
-  unsigned* bar;                   // [2] grid barrier (zeroed before launch)
+  unsigned* bar;                   // [2 + 32] grid barrier + gate-group counters (zeroed before launch)
   unsigned long long* trace;       // debug: [16] ns per phase summed over steps (CTA 0), or null
 };
 
@@ -165,117 +182,165 @@ __device__ __forceinline__ void gemv_task(int b0, int nb, int n0, int N, int k0,
 // tcgen05: D[128 rows = items][32 gate columns] in TMEM; A (the bf16 operand mirror, 64-column
 // boxes of up to 128 item rows) and this CTA's 32 weight rows stream through a TMA ring; the
 // epilogue warps apply the LSTM cell straight from TMEM.
-constexpr int GS = 8;                          // ring stages (the ring doubles as the attention staging area)
-constexpr uint32_t GA_BYTES = 128 * 128;       // A stage: 128 rows x 64 bf16 (128B swizzle)
-constexpr uint32_t GW_BYTES = 32 * 128;        // W stage: 32 rows x 64 bf16
+constexpr uint32_t RING_BYTES = 160 * 1024;   // gate bulk-copy ring / attention staging area
+constexpr int MAXGS = 10;                      // ring stages (W tile 16 KB + X tile items x 128 B)
 
 struct GateSync {
-  uint64_t full[GS], empty[GS], accf, acce, abar[2];
+  uint64_t full[MAXGS], empty[MAXGS], accf, acce, abar[2];
   uint32_t tmem;
 };
-static_assert(2 * ASTAGE <= GS * (GA_BYTES + GW_BYTES), "attention staging exceeds the ring");
+static_assert(2 * ASTAGE <= RING_BYTES, "attention staging exceeds the ring");
 
-// MODE 0: attention LSTM (A = [p | ctx | att_h(old bank)], K = 1792)
-// MODE 1: decoder LSTM   (A = [ctx | att_h(new bank) | dec_h(old bank)], K = 2560)
+// Gate GEMM with the WEIGHTS as the MMA's M operand: CTA c owns unit group ug = c / 4 (32 hidden
+// units = 128 gate rows, ordered [unit][gate]) and K split ks = c % 4.  D[128 gate rows][items] =
+// W[rows][K/4] . X[items][K/4]^T accumulates in TMEM (N = items padded to 16), so a tiny pooled
+// batch costs a tiny N instead of a 128-row M tile, and each CTA issues 7 / 10 K-chunks of 4 MMAs.
+// The 4 K-split partials of a group are written to global, the group syncs on a counter, and each
+// CTA then sums the partials in split order (deterministic) for 8 of the 32 units and applies the
+// LSTM cell.
+// MODE 0: attention LSTM (X = [p | ctx | att_h(old bank)], K = 1792)
+// MODE 1: decoder LSTM   (X = [ctx | att_h(new bank) | dec_h(old bank)], K = 2560)
+constexpr int KSPLIT = 4;
+constexpr uint32_t GW_TILE = 128 * 128;  // weight stage: 128 rows x 64 bf16
+
 template <int MODE>
-__device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy, const CUtensorMap* mapA,
-                           const CUtensorMap* mapW, uint32_t a_box_bytes, uint32_t& g_ring, uint32_t& lt_tile,
-                           const PlanCache& pc) {
-  // g_ring / lt_tile: ring-stage and tile counters, kept per thread and advanced identically by all
+__device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy, uint32_t x_stage_bytes, int nst,
+                           uint32_t& g_ring, uint32_t& lt_tile, const PlanCache& pc, unsigned& grp_gen) {
   constexpr int K = MODE == 0 ? KA : KD;
   constexpr int NKC = K / 64;
-  const int c = blockIdx.x;
+  constexpr int KCS = NKC / KSPLIT;
+  const int c = blockIdx.x, ug = c >> 2, ks = c & 3;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int oldb = s & 1, newb = oldb ^ 1;
-  const int ntile = (a.B + 127) / 128;
-  uint8_t* sA = ring;
-  uint8_t* sWt = ring + GS * GA_BYTES;
-  if (warp == 0) {
+  const int n16 = (a.B + 15) / 16 * 16;
+  const bool tr = a.trace && c == 0 && lane == 0;
+  const unsigned long long t_in = tr ? gtimer() : 0;
+  auto mark = [&](int slot) {
+    if (tr) a.trace[16 + MODE * 8 + slot] += gtimer() - t_in;
+  };
+  uint8_t* sW = ring;
+  uint8_t* sX = ring + nst * GW_TILE;
+  ++grp_gen;
+  if (warp == 0 || warp == 2 || warp == 3) {
     if (lane == 0) {
-      asm volatile("fence.proxy.async.global;" ::: "memory");  // xb rows written by generic stores
+      const uint32_t pi = warp == 0 ? 0 : warp - 1;
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // xb tiles written by generic stores
       uint32_t g = g_ring;
-      for (int mt = 0; mt < ntile; ++mt)
-        for (int kc = 0; kc < NKC; ++kc, ++g) {
-          const uint32_t st = g % GS, ph = (g / GS) & 1;
-          tcg::mbar_wait(&gsy.empty[st], ph ^ 1);
-          const int k0 = kc * 64;
-          int col;
-          if (MODE == 0) col = k0 < 768 ? k0 : att_off(oldb) + (k0 - 768);
-          else col = k0 < 512 ? CTX_OFF + k0 : (k0 < 1536 ? att_off(newb) + (k0 - 512) : dec_off(oldb) + (k0 - 1536));
-          tcg::mbar_expect_tx(&gsy.full[st], a_box_bytes + GW_BYTES);
-          tcg::tma_load_2d(sA + st * GA_BYTES, mapA, &gsy.full[st], col, mt * 128);
-          tcg::tma_load_2d(sWt + st * GW_BYTES, mapW, &gsy.full[st], k0, c * 32);
-        }
+      for (int i = 0; i < KCS; ++i, ++g) {
+        if (g % 3 != pi) continue;
+        const uint32_t st = g % nst, ph = (g / nst) & 1;
+        tcg::mbar_wait(&gsy.empty[st], ph ^ 1);
+        const int kc = ks * KCS + i, k0 = kc * 64;
+        int col;
+        if (MODE == 0) col = k0 < 768 ? k0 : att_off(oldb) + (k0 - 768);
+        else col = k0 < 512 ? CTX_OFF + k0 : (k0 < 1536 ? att_off(newb) + (k0 - 512) : dec_off(oldb) + (k0 - 1536));
+        tcg::mbar_expect_tx(&gsy.full[st], GW_TILE + n16 * 128);
+        bulk_g2s(sW + st * GW_TILE, (MODE == 0 ? a.Wa : a.Wd) + ((int64_t)ug * NKC + kc) * 128 * 64, GW_TILE,
+                 &gsy.full[st]);
+        const int r0 = min(n16, 128);
+        bulk_g2s(sX + st * x_stage_bytes, a.xb + (int64_t)(col >> 6) * 128 * 64, r0 * 128, &gsy.full[st]);
+        if (n16 > 128)  // items 128.. live in the next 128-row block of the mirror
+          bulk_g2s(sX + st * x_stage_bytes + 128 * 128, a.xb + (int64_t)(NCC + (col >> 6)) * 128 * 64,
+                   (n16 - 128) * 128, &gsy.full[st]);
+      }
+      if (pi == 0) mark(0);
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = tcg::make_idesc<32>();
-      uint32_t g = g_ring, lt = lt_tile;
-      for (int mt = 0; mt < ntile; ++mt, ++lt) {
-        tcg::mbar_wait(&gsy.acce, (lt & 1) ^ 1);
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n16 >> 3) << 17) | ((128u >> 4) << 24);
+      uint32_t g = g_ring;
+      tcg::mbar_wait(&gsy.acce, (lt_tile & 1) ^ 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int i = 0; i < KCS; ++i, ++g) {
+        const uint32_t st = g % nst, ph = (g / nst) & 1;
+        tcg::mbar_wait(&gsy.full[st], ph);
+        if (i == 0) mark(1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        for (int kc = 0; kc < NKC; ++kc, ++g) {
-          const uint32_t st = g % GS, ph = (g / GS) & 1;
-          tcg::mbar_wait(&gsy.full[st], ph);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint64_t da = tcg::make_desc<128>(tcg::smem_u32(sA + st * GA_BYTES));
-          const uint64_t db = tcg::make_desc<128>(tcg::smem_u32(sWt + st * GW_BYTES));
+        const uint64_t dw = tcg::make_desc<128>(tcg::smem_u32(sW + st * GW_TILE));
+        const uint64_t dx = tcg::make_desc<128>(tcg::smem_u32(sX + st * x_stage_bytes));
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, da + 2 * kk, db + 2 * kk, idesc, (kc | kk) != 0);
-          tcg::umma_commit(&gsy.empty[st]);
-        }
-        tcg::umma_commit(&gsy.accf);
+        for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, dw + 2 * kk, dx + 2 * kk, idesc, (i | kk) != 0);
+        tcg::umma_commit(&gsy.empty[st]);
       }
+      tcg::umma_commit(&gsy.accf);
+      mark(2);
     }
-  } else if (warp >= 4) {
-    // epilogue: TMEM lane quarter q = warp & 3 -> item row; 32 columns = 4 gates x 8 units
-    const int q = warp & 3;
-    const float* bias = (MODE == 0 ? a.ba : a.bd) + c * 32;
+  } else {
+    // epilogue warps 4..7: TMEM lanes 32q.. = gate rows; columns = items -> K-split partial
+    const int q = warp & 3, r = q * 32 + lane;
+    float* part = a.Gp + ((int64_t)ks * GEMM_CTAS / KSPLIT + ug) * n16 * 128;  // [ks][ug][item][row]
+    tcg::mbar_wait(&gsy.accf, lt_tile & 1);
+    if (q == 0) mark(3);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    for (int c0 = 0; c0 < n16; c0 += 16) {
+      float v[16];
+      tcg::tmem_ld16(gsy.tmem + ((uint32_t)(q * 32) << 16) + c0, v);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) __stcg(part + (int64_t)(c0 + i) * 128 + r, v[i]);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) tcg::mbar_arrive(&gsy.acce);
+    // group sync: the 4 K-split CTAs of this unit group have written their partials
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    if (warp == 4 && lane == 0) {
+      unsigned* cnt = a.bar + 2 + ug;
+      __threadfence();
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+      unsigned seen;
+      do {
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
+      } while (seen < KSPLIT * grp_gen);
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    if (q == 0) mark(4);
+  }
+  __syncthreads();
+  {
+    // fixup (all 256 threads): this CTA finishes units [8ks, 8ks+8) of the group for every live
+    // item; 4 cells per thread in flight (partials + c state loaded before any arithmetic)
+    const float* bias = (MODE == 0 ? a.ba : a.bd) + ug * 128;
     const int h_off = MODE == 0 ? ATTH_OFF : DECH_OFF, c_off = MODE == 0 ? ATTC_OFF : DECC_OFF;
     const int hb_off = MODE == 0 ? att_off(newb) : dec_off(newb);
-    uint32_t lt = lt_tile;
-    for (int mt = 0; mt < ntile; ++mt, ++lt) {
-      const int b = mt * 128 + q * 32 + lane;
-      const bool live = b < a.B && active(pc, b, s);
-      float* st = a.work + (int64_t)b * ROW;
-      float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0;
-      if (live) {
-        c0 = __ldcg(reinterpret_cast<const float4*>(st + c_off + c * 8));
-        c1 = __ldcg(reinterpret_cast<const float4*>(st + c_off + c * 8 + 4));
+    for (int e0 = threadIdx.x; e0 < 8 * a.B; e0 += 4 * NT) {
+      float4 gs4[4];
+      float cold[4];
+      bool live[4];
+#pragma unroll
+      for (int z = 0; z < 4; ++z) {
+        const int e = e0 + z * NT, b = e >> 3, ul = ks * 8 + (e & 7), j = ug * 32 + ul;
+        live[z] = e < 8 * a.B && active(pc, b, s);
+        gs4[z] = make_float4(0.f, 0.f, 0.f, 0.f);
+        cold[z] = 0.f;
+        if (!live[z]) continue;
+        gs4[z] = __ldg(reinterpret_cast<const float4*>(bias + ul * 4));
+#pragma unroll
+        for (int k2 = 0; k2 < KSPLIT; ++k2) {
+          const float4 pv = __ldcg(reinterpret_cast<const float4*>(
+              a.Gp + (((int64_t)k2 * GEMM_CTAS / KSPLIT + ug) * n16 + b) * 128 + ul * 4));
+          gs4[z].x += pv.x;
+          gs4[z].y += pv.y;
+          gs4[z].z += pv.z;
+          gs4[z].w += pv.w;
+        }
+        cold[z] = ldf(a.work + (int64_t)b * ROW + c_off + j);
       }
-      tcg::mbar_wait(&gsy.accf, lt & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float v[32];
-      tcg::tmem_ld32(gsy.tmem + ((uint32_t)(q * 32) << 16), v);
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) tcg::mbar_arrive(&gsy.acce);
-      if (live) {
-        const float cold[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-        float hn[8], cn[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const float gi = v[u] + __ldg(bias + u), gf = v[8 + u] + __ldg(bias + 8 + u);
-          const float gg = v[16 + u] + __ldg(bias + 16 + u), go = v[24 + u] + __ldg(bias + 24 + u);
-          cn[u] = sigm(gf) * cold[u] + sigm(gi) * tanhf(gg);
-          hn[u] = sigm(go) * tanhf(cn[u]);
-        }
-        *reinterpret_cast<float4*>(st + c_off + c * 8) = make_float4(cn[0], cn[1], cn[2], cn[3]);
-        *reinterpret_cast<float4*>(st + c_off + c * 8 + 4) = make_float4(cn[4], cn[5], cn[6], cn[7]);
-        *reinterpret_cast<float4*>(st + h_off + c * 8) = make_float4(hn[0], hn[1], hn[2], hn[3]);
-        *reinterpret_cast<float4*>(st + h_off + c * 8 + 4) = make_float4(hn[4], hn[5], hn[6], hn[7]);
-        uint32_t w[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(hn[2 * e], hn[2 * e + 1]);
-          w[e] = *reinterpret_cast<uint32_t*>(&b2);
-        }
-        *reinterpret_cast<uint4*>(a.xb + (int64_t)b * XB2 + hb_off + c * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+      for (int z = 0; z < 4; ++z) {
+        if (!live[z]) continue;
+        const int e = e0 + z * NT, b = e >> 3, ul = ks * 8 + (e & 7), j = ug * 32 + ul;
+        const float cn = sigm(gs4[z].y) * cold[z] + sigm(gs4[z].x) * tanhf(gs4[z].z);
+        const float hn = sigm(gs4[z].w) * tanhf(cn);
+        float* st = a.work + (int64_t)b * ROW;
+        st[c_off + j] = cn;
+        st[h_off + j] = hn;
+        a.xb[xb_off(b, hb_off + j)] = __float2bfloat16_rn(hn);
       }
     }
   }
-  g_ring += ntile * NKC;
-  lt_tile += ntile;
+  g_ring += KCS;
+  lt_tile += 1;
 }
 
 // ------------------------------------------------------------------ attention
@@ -498,7 +563,7 @@ __device__ void att_combine(const DecArgs& a, AttSmem& sm, int s, int b, int chu
     float c = 0.f;
     for (int k = 0; k < nch; ++k) c = fmaf(scale[k], ldf(ap + k * (2 + EMB) + 2 + d), c);
     st[CTX_OFF + d] = c;
-    a.xb[(int64_t)b * XB2 + CTX_OFF + d] = __float2bfloat16_rn(c);
+    a.xb[xb_off(b, CTX_OFF + d)] = __float2bfloat16_rn(c);
   }
   for (int t = tid; t < L; t += NT) {
     const float w = ldf(a.U + (int64_t)b * a.u_ld + t) * scale[t / chunk];
@@ -511,11 +576,11 @@ __device__ void att_combine(const DecArgs& a, AttSmem& sm, int s, int b, int chu
 
 // ------------------------------------------------------------------ the kernel
 __global__ void __launch_bounds__(NT, 1)
-    k_dec_persist(DecArgs a, const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapWa,
-                  const __grid_constant__ CUtensorMap mapWd, uint32_t a_box_bytes) {
+    k_dec_persist(DecArgs a, uint32_t a_box_bytes) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = tcg::align_smem_1024(smem_raw);
-  AttSmem& sm = *reinterpret_cast<AttSmem*>(ring + GS * (GA_BYTES + GW_BYTES));  // ring = gate pipeline / attention staging
+  AttSmem& sm = *reinterpret_cast<AttSmem*>(ring + RING_BYTES);  // ring = gate pipeline / attention staging
+  const int nst = min(MAXGS, (int)(RING_BYTES / (GW_TILE + a_box_bytes)));
   float* scratch = reinterpret_cast<float*>(&sm.locf[0]);                       // gemv reductions
   __shared__ GateSync gsy;
   __shared__ PlanCache pc;
@@ -523,9 +588,10 @@ __global__ void __launch_bounds__(NT, 1)
   const bool gemm_cta = c < GEMM_CTAS;
   unsigned gen = 0;
   uint32_t g_ring = 0, lt_tile = 0, aphase[2] = {0, 0};
+  unsigned grp_gen = 0;
 
   if (tid == 0) {
-    for (int i = 0; i < GS; ++i) {
+    for (int i = 0; i < MAXGS; ++i) {
       tcg::mbar_init(&gsy.full[i], 1);
       tcg::mbar_init(&gsy.empty[i], 1);
     }
@@ -534,12 +600,9 @@ __global__ void __launch_bounds__(NT, 1)
     tcg::mbar_init(&gsy.abar[0], 1);
     tcg::mbar_init(&gsy.abar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapWa)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapWd)) : "memory");
   }
   if (gemm_cta && (tid >> 5) == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(tcg::smem_u32(&gsy.tmem)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(tcg::smem_u32(&gsy.tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -561,8 +624,7 @@ __global__ void __launch_bounds__(NT, 1)
   // bf16 operand mirror, bank 0, from the gathered fp32 state rows
   for (int b = c; b < a.B; b += G) {
     const float* st = a.work + (int64_t)b * ROW;
-    __nv_bfloat16* x = a.xb + (int64_t)b * XB2;
-    for (int i = tid; i < ATTC_OFF; i += NT) x[i] = __float2bfloat16_rn(ldf(st + i));
+    for (int i = tid; i < ATTC_OFF; i += NT) a.xb[xb_off(b, i)] = __float2bfloat16_rn(ldf(st + i));
   }
   grid_sync(a.bar, gen);
 
@@ -634,12 +696,12 @@ __global__ void __launch_bounds__(NT, 1)
                   if (!active(pc, b, gs)) return;
                   y = fmaxf(y, 0.f);
                   a.work[(int64_t)b * ROW + P_OFF + n] = y;
-                  a.xb[(int64_t)b * XB2 + P_OFF + n] = __float2bfloat16_rn(y);
+                  a.xb[xb_off(b, P_OFF + n)] = __float2bfloat16_rn(y);
                 });
     }
     phase_end();
     // ---- ATT gates + cell
-    if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, &mapA, &mapWa, a_box_bytes, g_ring, lt_tile, pc);
+    if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen);
     phase_end();
     // ---- QUERY partials
     for (int task = c; task < nb8 * 4 * QKS; task += G) {
@@ -712,7 +774,7 @@ __global__ void __launch_bounds__(NT, 1)
       if (active(pc, b, gs)) att_combine(a, sm, gs, b, chunk);
     phase_end();
     // ---- DEC gates + cell
-    if (gemm_cta) gate_phase<1>(a, gs, ring, gsy, &mapA, &mapWd, a_box_bytes, g_ring, lt_tile, pc);
+    if (gemm_cta) gate_phase<1>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen);
     phase_end();
     // ---- PROJ partials
     for (int task = c; task < nb8 * 3 * PKS; task += G) {
@@ -750,7 +812,7 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   if (gemm_cta && (tid >> 5) == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(gsy.tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(gsy.tmem));
   }
 }
 
@@ -769,33 +831,29 @@ ITTS_API int itts_r_decode_persistent(int32_t B, int32_t nsteps, const int64_t* 
                                       const float* W0T, const float* W1T, const void* Wa, const float* ba,
                                       const void* Wd, const float* bd, const float* WqT, const float* WlocD,
                                       const float* v, const float* WpT, const float* bp,
-                                      float* H1, float* Qp, float* Pp, float* U, int64_t u_ld, float* AP,
-                                      unsigned* bar, void* stream) {
+                                      float* Gp, float* H1, float* Qp, float* Pp, float* U, int64_t u_ld,
+                                      float* AP, unsigned* bar, void* stream) {
   if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
-  if (B > 256) return ITTS_EUNSUPPORTED;  // attention task table in shared memory
+  if (B > 256) return ITTS_EUNSUPPORTED;  // attention task table in shared memory; MMA N <= 256
   if (nsteps <= 0 || !plan || !work || !xb || !Wa || !Wd || !bar) return ITTS_EINVAL;
   if (tcg::num_sms() < GEMM_CTAS) return ITTS_EUNSUPPORTED;
   cudaStream_t st = (cudaStream_t)stream;
   DecArgs a{B, nsteps, 0, plan, work, (__nv_bfloat16*)xb, W0T, W1T, (const __nv_bfloat16*)Wa, ba,
-            (const __nv_bfloat16*)Wd, bd, WqT, WlocD, v, WpT, bp, H1, Qp, Pp, U, u_ld, AP, bar,
+            (const __nv_bfloat16*)Wd, bd, WqT, WlocD, v, WpT, bp, Gp, H1, Qp, Pp, U, u_ld, AP, bar,
             g_dec_trace};
-  const size_t smem = 1024 + GS * (GA_BYTES + GW_BYTES) + sizeof(AttSmem);
-  const int b16 = (B + 15) / 16 * 16, arows = b16 < 128 ? b16 : 128;
-  CUtensorMap mA, mWa, mWd;
-  if (!tcg::encode_2d(&mA, xb, XB2, (uint64_t)b16, XB2, 64, arows, 128)) return ITTS_EINVAL;
-  if (!tcg::encode_2d(&mWa, Wa, KA, 4096, KA, 64, 32, 128)) return ITTS_EINVAL;
-  if (!tcg::encode_2d(&mWd, Wd, KD, 4096, KD, 64, 32, 128)) return ITTS_EINVAL;
-  uint32_t a_box_bytes = (uint32_t)arows * 128;
+  const size_t smem = 1024 + RING_BYTES + sizeof(AttSmem);
+  const int b16 = (B + 15) / 16 * 16;
+  uint32_t a_box_bytes = (uint32_t)b16 * 128;  // X stage: all items x 64 columns
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k_dec_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
-  cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st);
+  cudaError_t e = cudaMemsetAsync(bar, 0, (2 + 32) * sizeof(unsigned), st);
   if (e != cudaSuccess) return (int)e;
   const int G = tcg::num_sms();
-  void* args[] = {&a, &mA, &mWa, &mWd, &a_box_bytes};
+  void* args[] = {&a, &a_box_bytes};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(G);
   cfg.blockDim = dim3(NT);

@@ -72,6 +72,19 @@ def _h2d(arr: np.ndarray, device) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(arr)).pin_memory().to(device, non_blocking=True)
 
 
+def _swizzle_tiles(w: torch.Tensor, rows: int = 32) -> torch.Tensor:
+    """[N][K] bf16 (row groups of `rows`) -> [N/rows][K/64][rows][64] with the UMMA 128B swizzle
+    (16-byte group j of row r stored at j ^ (r % 8)): each (group, 64-column chunk) stage of the
+    persistent decoder's gate GEMM is one contiguous bulk copy."""
+    n, k = w.shape
+    t = w.reshape(n // rows, rows, k // 64, 8, 8).permute(0, 2, 1, 3, 4).contiguous()   # [grp][chunk][row][g][e]
+    r = torch.arange(rows, device=w.device)[:, None]
+    j = torch.arange(8, device=w.device)[None, :]
+    src_grp = (j ^ (r % 8))          # stored group j holds logical group j ^ (r % 8)
+    out = torch.gather(t, 3, src_grp[None, None, :, :, None].expand(t.shape))
+    return out.reshape(n // rows, k // 64, rows, 64).contiguous()
+
+
 class _Layout:
     """Packed rows of one activation stage: item i at [base_i, base_i + 2*halo + rows_i)."""
 
@@ -164,11 +177,12 @@ class TierREngine:
         wd = torch.cat([wih[:, 1024:], wih[:, :1024], w["dec_rnn.w_hh"]], 1)             # [ctx|att_h|dec_h]
         self.dec_bias = f32(w["dec_rnn.b_ih"] + w["dec_rnn.b_hh"])
         self.dec_gemm = (wd.to(d).to(torch.bfloat16)[None].contiguous(), [0], zeros)
-        # persistent decoder: gate rows interleaved per CTA c = [q gate][8 units 8c..8c+7]
-        perm = lambda t: t.reshape(4, HID // 8, 8, -1).permute(1, 0, 2, 3).reshape(4 * HID, -1)
-        self.Wa_p = perm(wa.to(d)).to(torch.bfloat16).contiguous()
+        # persistent decoder: gate rows regrouped per 32-unit group g as [unit u][gate q]
+        # (row 128g + 4u + q <- original row q*1024 + 32g + u), then UMMA-swizzled 64-column tiles
+        perm = lambda t: t.reshape(4, HID // 32, 32, -1).permute(1, 2, 0, 3).reshape(4 * HID, -1)
+        self.Wa_p = _swizzle_tiles(perm(wa.to(d)).to(torch.bfloat16), 128)
         self.ba_p = perm(self.att_bias[:, None]).reshape(-1).contiguous()
-        self.Wd_p = perm(wd.to(d)).to(torch.bfloat16).contiguous()
+        self.Wd_p = _swizzle_tiles(perm(wd.to(d)).to(torch.bfloat16), 128)
         self.bd_p = perm(self.dec_bias[:, None]).reshape(-1).contiguous()
         self.WqT = f32(w["att.query_layer"].T)                                           # [1024][128]
         self.Wloc = f32(w["att.location_conv"])                                          # [32][2][31]
@@ -415,7 +429,8 @@ class TierREngine:
                        b.xb2.data_ptr(), self.W0T.data_ptr(), self.W1T.data_ptr(), self.Wa_p.data_ptr(),
                        self.ba_p.data_ptr(), self.Wd_p.data_ptr(), self.bd_p.data_ptr(), self.WqT.data_ptr(),
                        self.WlocD.data_ptr(), self.v.data_ptr(), self.WpT.data_ptr(),
-                       self.bp.data_ptr(), b.H1.data_ptr(), b.Q.data_ptr(), b.P.data_ptr(), b.U.data_ptr(),
+                       self.bp.data_ptr(), b.Gp.data_ptr(), b.H1.data_ptr(), b.Q.data_ptr(), b.P.data_ptr(),
+                       b.U.data_ptr(),
                        b.U.shape[1], b.AP.data_ptr(), b.bar.data_ptr(), st)
             self._call("itts_scatter_rows", b.d_dst.data_ptr(), b.work.data_ptr(), n, 4 * ROW, st)
             return
@@ -652,17 +667,18 @@ class _DecBuffers:
         self.Q = torch.empty(8, n, 128, dtype=torch.float32, device=dev)    # query K-slice partials
         self.P = torch.empty(8, n, 81, dtype=torch.float32, device=dev)     # projection K-slice partials
         self.H1 = torch.empty(n, 256, dtype=torch.float32, device=dev)
-        self.dev, self.xb2, self.U, self.AP, self.bar = dev, None, None, None, None
+        self.dev, self.xb2, self.U, self.AP, self.bar, self.Gp = dev, None, None, None, None, None
 
     def ensure_persistent(self, max_L: int) -> None:
         """Scratch of the persistent decoder kernel (allocated once per buffer set)."""
         if self.U is not None and self.U.shape[1] >= max_L:
             return
-        n16 = -(-self.n // 16) * 16
-        self.xb2 = torch.zeros(n16, XB2, dtype=torch.bfloat16, device=self.dev)
+        nblk = -(-self.n // 128)
+        self.xb2 = torch.zeros(nblk * (XB2 // 64) * 128 * 64, dtype=torch.bfloat16, device=self.dev)
         self.U = torch.empty(self.n, max(max_L, 256), dtype=torch.float32, device=self.dev)
         self.AP = torch.empty(self.n, 256, 2 + 512, dtype=torch.float32, device=self.dev)
-        self.bar = torch.zeros(2, dtype=torch.int32, device=self.dev)
+        self.bar = torch.zeros(64, dtype=torch.int32, device=self.dev)
+        self.Gp = torch.empty(4 * 32 * (-(-self.n // 16) * 16) * 128, dtype=torch.float32, device=self.dev)
 
 
 class _DecBucket(_DecBuffers):

@@ -29,7 +29,7 @@ for B in [int(x) for x in args.batches.split(",")]:
     encs = eng.encoder_batch(fos)
     eng.decoder_batch([(st, enc) for enc, st in encs])
     torch.cuda.synchronize()
-    buf = torch.zeros(16, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(32, dtype=torch.int64, device="cuda")
     _native.call("itts_r_decode_debug_trace", buf.data_ptr())
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(eng.stream)
@@ -40,6 +40,10 @@ for B in [int(x) for x in args.batches.split(",")]:
     t = buf.cpu().tolist()
     print(f"B={B}: chunk {e0.elapsed_time(e1):.3f} ms; per step (us): " +
           ", ".join(f"{n} {t[i] / 32e3:.1f}" for i, n in enumerate(names)))
+    for m, nm in ((0, "ATT"), (1, "DEC")):
+        g = [t[16 + 8 * m + i] / 32e3 for i in range(6)]
+        print(f"   {nm} gates CTA0 (us from phase start): producer issued {g[0]:.1f}, first stage {g[1]:.1f}, "
+              f"MMA done {g[2]:.1f}, acc ready {g[3]:.1f}, epilogue done {g[4]:.1f}; MMA waited on data {g[5]:.1f}")
     if t[13]:
         sub = ["q/w loads", "bulk wait", "energies", "softmax", "context+store"]
         print(f"   ATT-A CTA0: {t[13] / 32:.1f} tasks/step; per task (us): " +
