@@ -251,6 +251,7 @@ def run_ours(args) -> None:
     rtf = [r.lcl / (r.samples / cfg.sample_rate) for r in inside
            if r.lcl is not None and r.error is None and r.samples]
     missing = sum(1 for r in inside if r.fcl is None)
+    failed = sum(1 for r in inside if r.error is not None)
     window_s = t1 - t0
     batch_sizes = [len(rep.decoder_ids) for rep in run.reports]
 
@@ -298,7 +299,7 @@ def run_ours(args) -> None:
                    "qps_per_gpu": args.qps, "qps_total": args.qps * world, "parallelism": f"pool-per-gpu x{world}",
                    "l2": "inputs larger than L2 (vocoder activations > 1 GB per iteration)",
                    "warmup_seconds": args.warmup_seconds, "requests_measured": len(fcl),
-                   "requests_missing_first_chunk": missing},
+                   "requests_missing_first_chunk": missing, "requests_failed": failed},
         "p50_ms": round(p50, 3) if p50 is not None else None,
         "lcl_p50_ms": l50, "lcl_p99_ms": l99,
         "rtf_mean": (sum(rtf) / len(rtf)) if rtf else None,
@@ -395,6 +396,7 @@ def qps_sweep(mods, cfg, lex, args) -> list[dict]:
         iters = len(win)
         rows.append({"qps": q, "p50_ms": p50, "p99_ms": p99, "requests": len(fcl),
                      "censored": sum(1 for r in inside if r.fcl is None),
+                     "failed": sum(1 for r in inside if r.error is not None),
                      "ms_per_step": round(1e3 * (t1 - t0) / max(iters, 1), 3),
                      "pooled_batch_mean": round(sum(len(r.decoder_ids) for r in win) / max(iters, 1), 1)})
         log(f"sweep {q:g} QPS: p50 {p50} p99 {p99}")

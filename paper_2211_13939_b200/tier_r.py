@@ -126,6 +126,7 @@ class TierREngine:
         self.persistent_decoder = True   # whole decoder chunk in one grid-synchronised kernel (dec_persist.cu)
         self._dec_buckets: dict = {}
         self._pool: dict = {}
+        self._pin_out = torch.empty(1 << 22, dtype=torch.float32, pin_memory=True)  # audio D2H
         self._graph_warm = False
 
     def _mark(self, kind: str, units: float):
@@ -540,14 +541,13 @@ class TierREngine:
                 x4 = self._hifigan(Ts, lay0, d_mplan)
             self._call("itts_r_post_splice", x4.data_ptr(), d_pplan.data_ptr(), n, max(mt[4] for mt in metas),
                        self.wpost.data_ptr(), self.bpost, self.fade.data_ptr(), O, S, audio.data_ptr(), st)
-            # fresh pinned block per call (the chunks alias it); power-of-two sizes keep the
-            # caching host allocator from calling cudaHostAlloc in steady state
-            host = torch.empty(1 << max(12, (audio.numel() - 1).bit_length()), dtype=torch.float32,
-                               pin_memory=True)[:audio.numel()]
+            if self._pin_out.numel() < audio.numel():   # grow-only persistent D2H buffer
+                self._pin_out = torch.empty(int(audio.numel() * 1.5), dtype=torch.float32, pin_memory=True)
+            host = self._pin_out[:audio.numel()]
             host.copy_(audio, non_blocking=True)
         self.stream.synchronize()
         self.d2h_bytes += 4 * int(out_off[-1])
-        flat = host.numpy()
+        flat = host.numpy()[:int(out_off[-1])].copy()   # the chunks own their samples
         if not np.isfinite(flat[:out_off[-1]]).all():
             raise ValueError("array contains non-finite values")
         out = []

@@ -15,6 +15,8 @@ from paper_2211_13939_b200.frontend import default_lexicon  # noqa: E402
 from paper_2211_13939_b200.harness import poisson_trace, serve  # noqa: E402
 from paper_2211_13939_b200.modules import build_engine, modules_for  # noqa: E402
 from paper_2211_13939_b200.scheduler import PipelineModules  # noqa: E402
+import random  # noqa: E402
+from paper_2211_13939_b200.harness import TimedRequest, random_text  # noqa: E402
 import gc  # noqa: E402
 import time  # noqa: E402
 
@@ -42,12 +44,23 @@ def wrap(name, fn):
 mods = PipelineModules(*(wrap(n, f) for n, f in zip("FEDV", (base.frontend_batch, base.encoder_batch,
                                                              base.decoder_batch, base.vocoder_batch))))
 serve(mods, cfg, poisson_trace(50, 1.0, seed=7, lexicon=lex), warmup_iters=0, timed_iters=2, drain_seconds=0.0)
+wr = random.Random(8)
+for burst in (8, 32, 64):
+    serve(mods, cfg, [TimedRequest(0.0, random_text(wr, 20, 200, lex)) for _ in range(burst)], warmup_iters=0,
+          timed_iters=None, drain_seconds=0.0)
 torch.cuda.synchronize()
+gc.collect()
+gc.freeze()
+gc.set_threshold(200000, 100, 100)
 gc_pauses = []
 gc.callbacks.append(lambda phase, info: gc_pauses.append((phase, time.perf_counter(), info.get("generation"))))
 per_iter = []
 from paper_2211_13939_b200 import scheduler  # noqa: E402
 orig = scheduler.run_iteration
+
+
+def _host_allocs():
+    return 0  # torch.cuda.host_memory_stats() per iteration perturbed the pinned allocator
 
 
 def timed_iter(*a, **k):
