@@ -200,6 +200,17 @@ def run_ours(args) -> None:
         engine.prepare_graphs(max_batch=256)
     log("decoder graphs captured")
     mods = modules_for(engine, lex)
+    if args.l2_flush:
+        from paper_2211_13939_b200.scheduler import PipelineModules
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)   # > 126 MB L2
+        dec_fn = mods.decoder_batch
+
+        def decoder_with_flush(pairs):
+            with torch.cuda.stream(engine.stream):
+                flush.fill_(1)
+            return dec_fn(pairs)
+
+        mods = PipelineModules(mods.frontend_batch, mods.encoder_batch, decoder_with_flush, mods.vocoder_batch)
 
     # The serving loop allocates many short-lived objects (handles, chunks); a gen-2 collection
     # mid-window would stall the loop thread.  Handles free device memory by refcount
@@ -297,7 +308,8 @@ def run_ours(args) -> None:
                                "lexicon), random-init Tacotron2 (512 enc, 1024 LSTM) + HiFi-GAN V1 22.05 kHz, "
                                "chunk 32, overlap 4, tier r",
                    "qps_per_gpu": args.qps, "qps_total": args.qps * world, "parallelism": f"pool-per-gpu x{world}",
-                   "l2": "inputs larger than L2 (vocoder activations > 1 GB per iteration)",
+                   "l2": ("flushed: a 256 MB write on the engine stream before every iteration's decoder call "
+                          "(inside the timed region)") if args.l2_flush else "not flushed (steady-state serving)",
                    "warmup_seconds": args.warmup_seconds, "requests_measured": len(fcl),
                    "requests_missing_first_chunk": missing, "requests_failed": failed},
         "p50_ms": round(p50, 3) if p50 is not None else None,
@@ -408,7 +420,7 @@ def qps_sweep(mods, cfg, lex, args) -> list[dict]:
 def main() -> None:
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=600)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--warmup-seconds", type=float, default=5.0)
     ap.add_argument("--drain-seconds", type=float, default=10.0)
@@ -423,6 +435,9 @@ def main() -> None:
     ap.add_argument("--sweep-seconds", type=float, default=5.0)
     ap.add_argument("--side-configs", type=int, default=1, help="also run C1, C2, C5 (1 = on)")
     ap.add_argument("--c5-qps", type=float, default=50.0)
+    ap.add_argument("--l2-flush", type=int, default=1,
+                    help="1: write a 256 MB buffer on the engine stream before every decoder call, so each "
+                         "serving iteration starts with a cold L2 (timing rule); 0: steady-state caches")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -502,22 +502,38 @@ __global__ void __cluster_dims__(BL_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   cluster.sync();
 
   const int r = tid % BL_ROWS, half = tid / BL_ROWS;  // 2 K-halves of 128
-  const int grow = (r / BL_UNITS) * EH + rank * BL_UNITS + (r % BL_UNITS);
+  // the input projection of step s+1 does not depend on h: load it while step s computes
+  float4 pre_n = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto load_pre = [&](int64_t s) {
+    if (tid < BL_UNITS && s < L) {
+      const int64_t t = dir ? L - 1 - s : s;
+      const float* pre = PRE + (row0 + t) * (8 * EH) + dir * 4 * EH;
+      const int j = rank * BL_UNITS + tid;
+      pre_n = make_float4(pre[j], pre[EH + j], pre[2 * EH + j], pre[3 * EH + j]);
+    }
+  };
+  load_pre(0);
   for (int64_t s = 0; s < L; ++s) {
     const int64_t t = dir ? L - 1 - s : s;
     const float* h = hbuf[s & 1];
-    float a = 0.f;
+    const float4 pre_c = pre_n;
+    load_pre(s + 1);
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;  // four independent FMA chains
 #pragma unroll 8
-    for (int k = half * 128; k < half * 128 + 128; ++k) a = fmaf(wsm[k * BL_ROWS + r], h[k], a);
-    gpart[half][r] = a;
+    for (int k = half * 128; k < half * 128 + 128; k += 4) {
+      a0 = fmaf(wsm[k * BL_ROWS + r], h[k], a0);
+      a1 = fmaf(wsm[(k + 1) * BL_ROWS + r], h[k + 1], a1);
+      a2 = fmaf(wsm[(k + 2) * BL_ROWS + r], h[k + 2], a2);
+      a3 = fmaf(wsm[(k + 3) * BL_ROWS + r], h[k + 3], a3);
+    }
+    gpart[half][r] = (a0 + a1) + (a2 + a3);
     __syncthreads();
     if (tid < BL_UNITS) {
-      const float* pre = PRE + (row0 + t) * (8 * EH) + dir * 4 * EH;
       const int u = tid, j = rank * BL_UNITS + u;
-      float gi = pre[j] + (gpart[0][u] + gpart[1][u]);
-      float gf = pre[EH + j] + (gpart[0][BL_UNITS + u] + gpart[1][BL_UNITS + u]);
-      float gg = pre[2 * EH + j] + (gpart[0][2 * BL_UNITS + u] + gpart[1][2 * BL_UNITS + u]);
-      float go = pre[3 * EH + j] + (gpart[0][3 * BL_UNITS + u] + gpart[1][3 * BL_UNITS + u]);
+      float gi = pre_c.x + (gpart[0][u] + gpart[1][u]);
+      float gf = pre_c.y + (gpart[0][BL_UNITS + u] + gpart[1][BL_UNITS + u]);
+      float gg = pre_c.z + (gpart[0][2 * BL_UNITS + u] + gpart[1][2 * BL_UNITS + u]);
+      float go = pre_c.w + (gpart[0][3 * BL_UNITS + u] + gpart[1][3 * BL_UNITS + u]);
       const float c = sigm(gf) * cst[u] + sigm(gi) * tanhf(gg);
       const float hn = sigm(go) * tanhf(c);
       cst[u] = c;
@@ -527,7 +543,6 @@ __global__ void __cluster_dims__(BL_CLUSTER, 1, 1) __launch_bounds__(256, 1)
       for (int q = 0; q < BL_CLUSTER; ++q) cluster.map_shared_rank(nxt, q)[j] = hn;
     }
     cluster.sync();
-    (void)grow;
   }
 }
 
