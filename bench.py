@@ -295,10 +295,10 @@ def run_ours(args) -> None:
     enc = agg.get("encoder", [0.0, 0.0, 0])
     voc_tflops = voc[1] / (voc[0] * 1e-3) / 1e12 if voc[0] else None
     dec_gbs = dec[1] / (dec[0] * 1e-3) / 1e9 if dec[0] else None
-    traffic = None
+    traffic = {}
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get("hifigan_conv_dram_bytes_per_launch")
+        traffic = json.loads(tf.read_text())
     line = {
         "metric": METRIC, "value": round(p99, 3) if p99 is not None else None, "unit": "ms",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -318,16 +318,24 @@ def run_ours(args) -> None:
         "pooled_batch_mean": round(sum(batch_sizes) / max(len(batch_sizes), 1), 1),
         "pooled_batch_max": max(batch_sizes) if batch_sizes else 0,
         "module_device_ms_per_step": {k: round(v[0] / args.steps, 3) for k, v in agg.items()},
-        "roofline": {"kernel": "k_conv_tc (HiFi-GAN conv stack, tcgen05 bf16)", "bound": "tensor",
-                     "achieved": round(voc_tflops, 2) if voc_tflops else None,
-                     "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
-                     "frac": round(voc_tflops / peaks["bf16_tflops_sustained"], 4) if voc_tflops else None,
-                     "traffic": traffic, "peak_source": peaks["source"] + " sustained bf16",
-                     "algorithmic": "2 x 307,052,544 MAC per spliced mel frame"},
-        "roofline_decoder": {"kernel": "decoder-step chain", "bound": "hbm",
-                             "achieved": round(dec_gbs, 1) if dec_gbs else None, "peak": peaks["hbm_gbs"],
-                             "unit": "GB/s", "frac": round(dec_gbs / peaks["hbm_gbs"], 4) if dec_gbs else None,
-                             "algorithmic": "37.04 MB weights per step + per-item state/memory reads"},
+        # dominant kernel of the C3 step: the persistent decoder-chunk kernel (one launch per iteration)
+        "roofline": {"kernel": "k_dec_persist (32-step Tacotron2 decoder chunk, one launch per iteration)",
+                     "bound": "hbm", "achieved": round(dec_gbs, 1) if dec_gbs else None, "peak": peaks["hbm_gbs"],
+                     "unit": "GB/s", "frac": round(dec_gbs / peaks["hbm_gbs"], 4) if dec_gbs else None,
+                     "traffic": traffic.get("k_dec_persist_dram_bytes_per_launch_b24"),
+                     "peak_source": peaks["source"] + " copy bandwidth",
+                     "algorithmic": "per step: 36.7 MB gate/GEMV weights + per item 20 KB state + L x 2.5 KB "
+                                    "memory/processed-memory; achieved = those bytes / CUDA-event time of the call",
+                     "traffic_note": "ncu DRAM bytes of one launch at B=24 (cold cache): the weights stay "
+                                     "L2-resident across the 32 steps, so DRAM traffic is far below the "
+                                     "algorithmic bytes; the kernel is barrier/latency bound"},
+        "roofline_vocoder": {"kernel": "HiFi-GAN V1 chunk vocoder (k_resblock_tc fused MRF layers + k_conv_tc)",
+                             "bound": "tensor", "achieved": round(voc_tflops, 2) if voc_tflops else None,
+                             "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                             "frac": round(voc_tflops / peaks["bf16_tflops_sustained"], 4) if voc_tflops else None,
+                             "traffic": traffic.get("k_resblock_tc_c128_k7_dram_bytes_per_launch_b24"),
+                             "peak_source": peaks["source"] + " sustained bf16",
+                             "algorithmic": "2 x 307,052,544 MAC per spliced mel frame"},
         "e2e": {"value": round(c99, 3) if c99 is not None else None, "p50": c50, "unit": "ms",
                 "h2d_bytes_per_step": int(merged["h2d"] / args.steps / world),
                 "d2h_bytes_per_step": int(merged["d2h"] / args.steps / world)},
