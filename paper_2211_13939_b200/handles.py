@@ -118,17 +118,49 @@ class DeviceDecoderState:
 
 
 class DeviceMelChunk:
-    """Duck-types ``MelChunk`` (``domain.py:181-199``): a view into a decode output."""
+    """Duck-types ``MelChunk`` (``domain.py:181-199``): a view into a decode output.
 
-    __slots__ = ("data", "req", "__weakref__")
+    Built either from a tensor view, or lazily as row `row` of a [n][C][mel_dim] call output
+    (the serving path: no per-item tensor slicing on the host); ``ptr`` / ``width`` /
+    ``frame_count`` are plain ints either way.
+    """
+
+    __slots__ = ("_data", "_base", "_row", "_m", "_gate", "req", "__weakref__")
 
     def __init__(self, data, req: DeviceRequest | None):
-        self.data = data  # torch tensor [m, mel_dim] on device (view of the call's output)
+        self._data, self._base, self._row, self._m, self._gate = data, None, 0, int(data.shape[0]), None
         self.req = req
+
+    @classmethod
+    def row_of(cls, base, row: int, frames: int, req: DeviceRequest | None, gate=None) -> "DeviceMelChunk":
+        obj = cls.__new__(cls)
+        obj._data, obj._base, obj._row, obj._m, obj._gate, obj.req = None, base, row, frames, gate, req
+        return obj
+
+    @property
+    def data(self):
+        if self._data is None:
+            self._data = self._base[self._row, :self._m]
+        return self._data
+
+    @property
+    def ptr(self) -> int:
+        if self._data is not None:
+            return self._data.data_ptr()
+        return self._base.data_ptr() + self._row * self._base.stride(0) * self._base.element_size()
+
+    @property
+    def width(self) -> int:
+        return int((self._data if self._data is not None else self._base).shape[-1])
+
+    @property
+    def gate_logits(self):
+        """The chunk's stop-gate logits (Tier R computes them; stop itself is the frame counter)."""
+        return None if self._gate is None else self._gate[self._row, :self._m]
 
     @property
     def frame_count(self) -> int:
-        return int(self.data.shape[0])
+        return self._m
 
     @property
     def frames(self) -> np.ndarray:

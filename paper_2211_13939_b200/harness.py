@@ -13,6 +13,7 @@ exactly K scheduler iterations after W warm-up iterations.
 from __future__ import annotations
 
 import math
+import queue
 import random
 import threading
 import time
@@ -109,7 +110,8 @@ class ServeRun:
 def serve(modules: PipelineModules, cfg, trace: list[TimedRequest], *, warmup_iters: int = 3,
           warmup_seconds: float = 0.0, timed_iters: int | None = None, drain_seconds: float = 30.0,
           on_window=None, max_clients: int = 4096, sample_rate: int = 22050,
-          tail_seconds: float = 120.0, timed_seconds: float | None = None) -> ServeRun:
+          tail_seconds: float = 120.0, timed_seconds: float | None = None,
+          consumers: bool = True, client: str = "poller") -> ServeRun:
     """Plays ``trace`` against a fresh SchedulerLoop and records every request.
 
     The timed window is iterations ``[w, w + timed_iters)`` where ``w`` is the
@@ -143,7 +145,53 @@ def serve(modules: PipelineModules, cfg, trace: list[TimedRequest], *, warmup_it
             if on_window:
                 on_window("end", i)
 
-    loop = SchedulerLoop(modules, CostModel.zero(), cfg, report_sink=sink)
+    wake = threading.Event()
+    live: list = []                      # (rec, stream) the poller still drains
+
+    def sink_and_wake(rep: IterationReport) -> None:
+        sink(rep)
+        wake.set()
+
+    loop = SchedulerLoop(modules, CostModel.zero(), cfg, report_sink=sink_and_wake if client == "poller" else sink)
+    stop_poll = threading.Event()
+
+    def poller() -> None:
+        pending: list = []
+        while not (stop_poll.is_set() and not pending and not live):
+            wake.wait(0.002)
+            wake.clear()
+            with lock:
+                pending.extend(live)
+                live.clear()
+            keep = []
+            for rec, stream in pending:
+                try:
+                    while True:
+                        chunk = stream.get(timeout=0)
+                        now = time.perf_counter()
+                        if chunk is None:
+                            rec.done = True
+                            break
+                        if rec.first_recv is None:
+                            rec.first_recv = now
+                        rec.last_recv = now
+                        rec.samples += chunk.sample_count
+                        rec.chunks += 1
+                except queue.Empty:
+                    keep.append((rec, stream))
+                except Exception as exc:  # noqa: BLE001 -- recorded, reported by the caller
+                    rec.error = str(exc)
+                    rec.done = True
+            pending = keep
+            if stop_poll.is_set() and time.perf_counter() > stop_deadline[0]:
+                for rec, _ in pending:
+                    rec.done = True
+                return
+
+    stop_deadline = [float("inf")]
+    poll_thread = threading.Thread(target=poller, name="client-poller", daemon=True)
+    if consumers and client == "poller":
+        poll_thread.start()
 
     def consume(rec: RequestTiming, stream) -> None:
         try:
@@ -179,11 +227,21 @@ def serve(modules: PipelineModules, cfg, trace: list[TimedRequest], *, warmup_it
             stream._push = timed_push
             with lock:
                 run.timings.append(rec)
-            clients.submit(consume, rec, stream)
+                if consumers and client == "poller":
+                    live.append((rec, stream))
+            if consumers and client == "threads":
+                clients.submit(consume, rec, stream)
+            elif not consumers:  # server-side timing only
+                rec.done = True
         else:  # trace exhausted before the window closed: let in-flight requests finish
             end = time.perf_counter() + tail_seconds
             while time.perf_counter() < end and not all(r.done for r in run.timings):
                 time.sleep(0.001)
+    if poll_thread.is_alive():
+        stop_deadline[0] = time.perf_counter() + 1.0
+        stop_poll.set()
+        wake.set()
+        poll_thread.join(timeout=5.0)
     return run
 
 

@@ -354,36 +354,53 @@ class TierREngine:
         if n == 0:
             return []
         C = self.cfg.chunk_frames
-        steps, taken, dsts = [], set(), []
-        for state, enc in pairs:
-            if not isinstance(state, DeviceDecoderState) or not isinstance(enc, DeviceEncodedFeatures):
-                raise TypeError("Tier-R GPU decoder needs handles produced by its own encoder")
-            if state.req is not enc.req or state.req.engine is not self:
-                raise ValueError("decoder state does not match encoded features")
-            if state.frames_emitted >= state.target_frames:
-                raise ValueError("decode past stop")
-            steps.append(min(C, state.target_frames - state.frames_emitted))
-        for state, _ in pairs:
-            dsts.append(state.req.claim(state.req.state_bufs, self.state_size(state.req.seq_len), taken))
         a = self.arena
-        max_L = max(s.req.seq_len for s, _ in pairs)
-        dec_bytes = max(steps) * DEC_WEIGHT_BYTES + sum(
-            k * (2 * 4 * ROW + s.req.seq_len * (4 * 512 + 4 * 128 + 16) + 4 * 81) for k, (s, _) in zip(steps, pairs))
-        src = np.array([a.ptr(st_.buf.off) for st_, _ in pairs], dtype=np.int64)
-        dstp = np.array([a.ptr(d.off) for d in dsts], dtype=np.int64)
+        # one pass over the items (host work here delays the decoder launch)
+        steps, dsts, Ls, mem_off, pm_off, src_off, dst_off, taken = [], [], [], [], [], [], [], set()
+        for state, enc in pairs:
+            if type(state) is not DeviceDecoderState or type(enc) is not DeviceEncodedFeatures:
+                if not isinstance(state, DeviceDecoderState) or not isinstance(enc, DeviceEncodedFeatures):
+                    raise TypeError("Tier-R GPU decoder needs handles produced by its own encoder")
+            req = state.req
+            if req is not enc.req or req.engine is not self:
+                raise ValueError("decoder state does not match encoded features")
+            left = state.target_frames - state.frames_emitted
+            if left <= 0:
+                raise ValueError("decode past stop")
+            steps.append(C if left > C else left)
+            L = req.seq_len
+            Ls.append(L)
+            d = req.claim(req.state_bufs, ROW + 2 * L, taken)
+            dsts.append(d)
+            ex = req.extra
+            mem_off.append(ex["mem_off"])
+            pm_off.append(ex["pm_off"])
+            src_off.append(state.buf.off)
+            dst_off.append(d.off)
+        base = a.ptr(0)
+        max_L, max_steps = max(Ls), max(steps)
+        steps_np = np.array(steps, dtype=np.int64)
+        Ls_np = np.array(Ls, dtype=np.int64)
+        src = base + 4 * np.array(src_off, dtype=np.int64)
+        dstp = base + 4 * np.array(dst_off, dtype=np.int64)
+        dec_bytes = max_steps * DEC_WEIGHT_BYTES + int(
+            (steps_np * (2 * 4 * ROW + Ls_np * (4 * 512 + 4 * 128 + 16) + 4 * 81)).sum())
         with torch.cuda.stream(self.stream):
-            if self.use_graphs and max(steps) == C and max_L <= GRAPH_MAX_L:
+            if self.use_graphs and max_steps == C and max_L <= GRAPH_MAX_L:
                 bk = self._dec_bucket(n)
                 B = bk.B
                 plan = np.zeros((B, 8), dtype=np.int64)
+                plan[:n, 0] = base + 4 * np.array(mem_off, dtype=np.int64)
+                plan[:n, 1] = base + 4 * np.array(pm_off, dtype=np.int64)
+                plan[:n, 2] = Ls_np
+                plan[:n, 3] = src + 4 * ROW
+                plan[:n, 4] = dstp + 4 * ROW
+                plan[:n, 5] = steps_np
+                plan[:n, 6] = bk.mel.data_ptr() + 4 * W.N_MEL * C * np.arange(n, dtype=np.int64)
+                plan[:n, 7] = bk.gate.data_ptr() + 4 * C * np.arange(n, dtype=np.int64)
                 src_all = np.full(B, bk.zero_row.data_ptr(), dtype=np.int64)
                 dst_all = bk.sink.data_ptr() + 4 * ROW * np.arange(B, dtype=np.int64)
                 src_all[:n], dst_all[:n] = src, dstp
-                for i, (state, _) in enumerate(pairs):
-                    req = state.req
-                    plan[i] = (a.ptr(req.extra["mem_off"]), a.ptr(req.extra["pm_off"]), req.seq_len,
-                               src[i] + 4 * ROW, dstp[i] + 4 * ROW, steps[i],
-                               bk.mel.data_ptr() + 4 * W.N_MEL * C * i, bk.gate.data_ptr() + 4 * C * i)
                 host = np.concatenate([plan.reshape(-1), src_all, dst_all])
                 self.h2d_bytes += host.nbytes
                 bk.packed.copy_(torch.from_numpy(host).pin_memory(), non_blocking=True)
@@ -393,31 +410,34 @@ class TierREngine:
                     bk.graph.replay()
                     self.launches += bk.launches
                 mel_all, gate_all = bk.mel[:n].clone(), bk.gate[:n].clone()
-                mel_views = [mel_all[i, :steps[i]] for i in range(n)]
-                gate_views = [gate_all[i, :steps[i]] for i in range(n)]
+                mels = [DeviceMelChunk.row_of(mel_all, i, steps[i], st.req, gate_all)
+                        for i, (st, _) in enumerate(pairs)]
             else:
-                mel_off = np.concatenate([[0], np.cumsum(steps)]).astype(np.int64)
+                mel_off = np.concatenate([[0], np.cumsum(steps_np)]).astype(np.int64)
                 mel = torch.empty(int(mel_off[-1]), W.N_MEL, dtype=torch.float32, device=self.device)
                 gate = torch.empty(int(mel_off[-1]), dtype=torch.float32, device=self.device)
                 plan = np.zeros((n, 8), dtype=np.int64)
-                for i, (state, _) in enumerate(pairs):
-                    req = state.req
-                    plan[i] = (a.ptr(req.extra["mem_off"]), a.ptr(req.extra["pm_off"]), req.seq_len,
-                               src[i] + 4 * ROW, dstp[i] + 4 * ROW, steps[i],
-                               mel.data_ptr() + 4 * W.N_MEL * int(mel_off[i]), gate.data_ptr() + 4 * int(mel_off[i]))
+                plan[:, 0] = base + 4 * np.array(mem_off, dtype=np.int64)
+                plan[:, 1] = base + 4 * np.array(pm_off, dtype=np.int64)
+                plan[:, 2] = Ls_np
+                plan[:, 3] = src + 4 * ROW
+                plan[:, 4] = dstp + 4 * ROW
+                plan[:, 5] = steps_np
+                plan[:, 6] = mel.data_ptr() + 4 * W.N_MEL * mel_off[:-1]
+                plan[:, 7] = gate.data_ptr() + 4 * mel_off[:-1]
                 packed = self._up(np.concatenate([plan.reshape(-1), src, dstp]))
                 bufs = _DecBuffers(self, n, packed)
                 with self._mark("decoder", dec_bytes):
-                    self._enqueue_decoder(bufs, max_L, max(steps))
-                mel_views = [mel[int(mel_off[i]):int(mel_off[i + 1])] for i in range(n)]
-                gate_views = [gate[int(mel_off[i]):int(mel_off[i + 1])] for i in range(n)]
+                    self._enqueue_decoder(bufs, max_L, max_steps)
+                mels = [DeviceMelChunk(mel[int(mel_off[i]):int(mel_off[i + 1])], st.req)
+                        for i, (st, _) in enumerate(pairs)]
+                for i, m in enumerate(mels):
+                    m._gate, m._row = gate[int(mel_off[i]):int(mel_off[i + 1])][None], 0
         out = []
-        for i, ((state, enc), dst) in enumerate(zip(pairs, dsts)):
-            emitted = state.frames_emitted + steps[i]
-            res = DecodeChunkResult(DeviceMelChunk(mel_views[i], state.req), emitted >= state.target_frames,
-                                    DeviceDecoderState(state.req, dst, emitted, state.target_frames))
-            object.__setattr__(res, "gate_logits", gate_views[i])
-            out.append(res)
+        for (state, _), dst, k, m in zip(pairs, dsts, steps, mels):
+            emitted = state.frames_emitted + k
+            out.append(DecodeChunkResult(m, emitted >= state.target_frames,
+                                         DeviceDecoderState(state.req, dst, emitted, state.target_frames)))
         return out
 
     def _enqueue_decoder(self, b: "_DecBuffers", max_L: int, nsteps: int) -> None:
@@ -490,7 +510,7 @@ class TierREngine:
             if not has_tail and not is_last and m * H <= S:
                 raise ValueError("non-final chunk shorter than the overlap window")
             if isinstance(mel, DeviceMelChunk):
-                if mel.data.shape[1] != W.N_MEL:
+                if mel.width != W.N_MEL:
                     raise ValueError("mel chunk width must be 80")
             else:
                 frames = np.asarray(mel.frames, dtype=np.float32)
@@ -516,7 +536,7 @@ class TierREngine:
             for i, ((vstate, mel, is_last), (m, has_tail, last, T, G, cnt)) in enumerate(zip(triples, metas)):
                 req, dst = owners[i]
                 if isinstance(mel, DeviceMelChunk):
-                    mel_ptr = mel.data.data_ptr()
+                    mel_ptr = mel.ptr
                 else:
                     mel_ptr = hm.data_ptr() + 4 * hpos
                     hpos += m * W.N_MEL

@@ -26,6 +26,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--qps", type=float, default=150)
 ap.add_argument("--seconds", type=float, default=8)
 ap.add_argument("--switch", type=float, default=None, help="sys.setswitchinterval")
+ap.add_argument("--no-consumers", action="store_true", help="no client threads (isolates GIL hand-offs)")
 args = ap.parse_args()
 if args.switch:
     sys.setswitchinterval(args.switch)
@@ -67,7 +68,8 @@ def timed_iter(*a, **k):
 scheduler.run_iteration = timed_iter
 eng.timers = []
 run = serve(mods, cfg, poisson_trace(args.qps, args.seconds, seed=3, lexicon=lex), warmup_iters=3,
-            warmup_seconds=1.0, timed_iters=None, timed_seconds=args.seconds - 2, drain_seconds=1.0, tail_seconds=5)
+            warmup_seconds=1.0, timed_iters=None, timed_seconds=args.seconds - 2, drain_seconds=1.0, tail_seconds=5,
+            consumers=not args.no_consumers)
 torch.cuda.synchronize()
 dev = collections.defaultdict(float)
 for kind, e0, e1, _ in eng.timers:
