@@ -197,7 +197,7 @@ def run_ours(args) -> None:
     engine = build_engine(cfg, args.tier, device)
     log("engine built")
     if hasattr(engine, "prepare_graphs"):
-        engine.prepare_graphs(max_batch=256)
+        engine.prepare_graphs(max_batch=512)
     log("decoder graphs captured")
     mods = modules_for(engine, lex)
     if args.l2_flush:
@@ -262,7 +262,7 @@ def run_ours(args) -> None:
     rtf = [r.lcl / (r.samples / cfg.sample_rate) for r in inside
            if r.lcl is not None and r.error is None and r.samples]
     missing = sum(1 for r in inside if r.fcl is None)
-    failed = sum(1 for r in inside if r.error is not None)
+    failed = sum(1 for r in inside if r.error is not None and "cancelled" not in r.error)
     window_s = t1 - t0
     batch_sizes = [len(rep.decoder_ids) for rep in run.reports]
 
@@ -416,7 +416,8 @@ def qps_sweep(mods, cfg, lex, args) -> list[dict]:
         iters = len(win)
         rows.append({"qps": q, "p50_ms": p50, "p99_ms": p99, "requests": len(fcl),
                      "censored": sum(1 for r in inside if r.fcl is None),
-                     "failed": sum(1 for r in inside if r.error is not None),
+                     "failed": sum(1 for r in inside if r.error is not None and "cancelled" not in r.error),
+                     "cancelled_at_end": sum(1 for r in inside if r.error is not None and "cancelled" in r.error),
                      "ms_per_step": round(1e3 * (t1 - t0) / max(iters, 1), 3),
                      "pooled_batch_mean": round(sum(len(r.decoder_ids) for r in win) / max(iters, 1), 1)})
         log(f"sweep {q:g} QPS: p50 {p50} p99 {p99}")
