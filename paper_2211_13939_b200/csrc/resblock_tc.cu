@@ -42,8 +42,6 @@ namespace {
 
 using namespace tcg;
 
-constexpr int kEpiWarps = 8;
-constexpr int kThreads = 32 * (3 + kEpiWarps);
 constexpr int kMaxK = 11;
 
 struct RbArgs {
@@ -82,19 +80,27 @@ __device__ __forceinline__ int swz_chunk(int row, int c) {
   return SWZ == 128 ? (c ^ (row & 7)) : (c ^ ((row >> 1) & 3));
 }
 
+// C >= 128: one CTA per SM, 8 epilogue warps, acc1 + acc2 fill the 512 TMEM columns.
+// C <= 64: half-size tiles and 4 epilogue warps so TWO CTAs share an SM: while one waits on its
+// epilogue (the c1 -> c2 dependency of a tile) the other one's MMAs run.
 template <int C>
 struct Cfg {
   static constexpr int SWZ = C >= 64 ? 128 : 64;
   static constexpr int KT = SWZ / 2;            // channels per panel
   static constexpr int NKC = C / KT;            // panels
-  static constexpr int NB = 256 / C;            // 128-row M blocks per tile
+  static constexpr int CPS = C >= 128 ? 1 : 2;  // CTAs per SM
+  static constexpr int EW = C >= 128 ? 8 : 4;   // epilogue warps
+  static constexpr int HP = EW / 4;             // epilogue warps per TMEM lane quarter
+  static constexpr int THREADS = 32 * (3 + EW);
+  static constexpr int NB = 256 / (C * CPS);    // 128-row M blocks per tile
+  static constexpr uint32_t TMEM_COLS = 2 * NB * C;
   static constexpr int XR_MAX = NB * 128 + 5 * (kMaxK - 1);
   static constexpr int NBOX_MAX = (XR_MAX + 255) / 256;
   static constexpr int BOXR_MAX = ((XR_MAX + NBOX_MAX - 1) / NBOX_MAX + 7) / 8 * 8;
   static constexpr int XR = NBOX_MAX * BOXR_MAX;  // allocated X rows per panel
   static constexpr int TR = NB * 128;             // T rows per panel (taps past the end read the next panel:
                                                   // only discarded output rows see them)
-  static constexpr int STAGES = C == 256 ? 2 : C == 128 ? 4 : C == 64 ? 8 : 16;
+  static constexpr int STAGES = C == 256 ? 2 : C == 128 ? 4 : C == 64 ? 4 : 16;
   static constexpr uint32_t X_BYTES = (uint32_t)NKC * XR * SWZ;
   static constexpr uint32_t T_BYTES = (uint32_t)NKC * TR * SWZ;
   static constexpr uint32_t W_BYTES = (uint32_t)C * SWZ;  // one (tap, panel) weight stage
@@ -103,12 +109,13 @@ struct Cfg {
 };
 
 template <int C>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Cfg<C>::THREADS, Cfg<C>::CPS)
     k_resblock_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW1,
                   const __grid_constant__ CUtensorMap mapW2, const __grid_constant__ CUtensorMap mapR,
                   const __grid_constant__ CUtensorMap mapO, const __grid_constant__ CUtensorMap mapO2, RbArgs a) {
   using K = Cfg<C>;
   constexpr int SWZ = K::SWZ, KT = K::KT, NKC = K::NKC, NB = K::NB, STAGES = K::STAGES;
+  constexpr int kEpiWarps = K::EW, HP = K::HP;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
@@ -157,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(512));
+                 "r"(K::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -216,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- MMA issuer
     if (lane == 0) {
       const uint32_t idesc = make_idesc<C>();
-      const uint32_t acc1 = tmem, acc2 = tmem + 256;
+      const uint32_t acc1 = tmem, acc2 = tmem + NB * C;
       uint32_t g = 0, lt = 0;
       Tw tw;
       const long long t_start = clock64();
@@ -274,9 +281,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Each warp owns 4 (block, 32-column) items per phase.  Row validity for the whole tile is
     // loaded into bit masks before the accumulators are ready; residual / accumulator rows of
     // item n+1 are in flight while item n is processed.
-    constexpr int NIT = NB * (C / 32) / 2;   // items per warp per phase (= 4)
+    constexpr int NIT = NB * (C / 32) / HP;  // items per warp per phase
     constexpr int CPP = KT / 32;             // 32-column chunks per panel
-    const int q = warp & 3, h = (warp - 3) >> 2;
+    const int q = warp & 3, h = (warp - 3) >> 2;  // h < HP
     const int et = threadIdx.x - 96;
     for (int i = et; i < C; i += 32 * kEpiWarps) {
       sB1[i] = a.b1[i];
@@ -309,8 +316,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int kc = 0; kc < NKC; ++kc) {
 #pragma unroll
-        for (int n = 0; n < (NB * CPP) / 2; ++n) {
-          const int item = 2 * n + h;
+        for (int n = 0; n < (NB * CPP) / HP; ++n) {
+          const int item = HP * n + h;
           const int b = item / CPP, cw = item - b * CPP;
           const int i = b * 128 + q * 32 + lane;
           const bool valid = (vT >> b) & 1;
@@ -350,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float oslope = to_acc ? 1.0f : a.slope;
       uint4 au[2][4];
       auto issue = [&](int n, int slot) {
-        const int item = 2 * n + h;
+        const int item = HP * n + h;
         const int b = item / (C / 32), c0 = (item - b * (C / 32)) * 32;
         const int64_t off = (r0 + b * 128 + q * 32 + lane) * C + c0;
         if (a.acc_mode >= 2 && ((vO >> b) & 1)) ld_bf16_raw<32>(a.acc + off, au[slot]);
@@ -363,12 +370,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int n = 0; n < NIT; ++n) {
         if (n + 1 < NIT) issue(n + 1, (n + 1) & 1);
-        const int item = 2 * n + h;
+        const int item = HP * n + h;
         const int b = item / (C / 32), c0 = (item - b * (C / 32)) * 32;
         const int o = b * 128 + q * 32 + lane;
         const bool valid = (vO >> b) & 1;
         float v[32];
-        tmem_ld32(tmem + 256 + b * C + ((uint32_t)(q * 32) << 16) + c0, v);
+        tmem_ld32(tmem + NB * C + b * C + ((uint32_t)(q * 32) << 16) + c0, v);
         const int kc = c0 / KT, cw = (c0 - kc * KT) / 32;
         uint8_t* rowp = sT + (size_t)kc * K::TR * SWZ + (size_t)o * SWZ;
         uint4 ru[4];
@@ -424,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(K::TMEM_COLS));
   }
 }
 
@@ -455,8 +462,9 @@ int launch(const void* x, int64_t rows, const void* w1, const void* w2, int taps
   if (!encode_2d(&mo2, out, C, (uint64_t)rows, C, K::KT, a.m_out - 128 * ((a.m_out - 1) / 128), K::SWZ))
     return ITTS_EINVAL;
   a.num_tiles = (int)((rows + a.m_out - 1) / a.m_out);
-  const int grid = a.num_tiles < num_sms() ? a.num_tiles : num_sms();
-  k_resblock_tc<C><<<grid, kThreads, K::SMEM, st>>>(mx, m1, m2, mr, mo, mo2, a);
+  const int slots = num_sms() * K::CPS;
+  const int grid = a.num_tiles < slots ? a.num_tiles : slots;
+  k_resblock_tc<C><<<grid, K::THREADS, K::SMEM, st>>>(mx, m1, m2, mr, mo, mo2, a);
   ITTS_RETURN_LAUNCH();
 }
 
@@ -493,5 +501,5 @@ ITTS_API int itts_resblock_tc(const void* x, int64_t rows, int32_t c, const void
 }
 
 static_assert(Cfg<256>::SMEM + 8 * 256 <= 232448 && Cfg<128>::SMEM + 8 * 128 <= 232448 &&
-                  Cfg<64>::SMEM + 8 * 64 <= 232448 && Cfg<32>::SMEM + 8 * 32 <= 232448,
+                  2 * (Cfg<64>::SMEM + 8 * 64 + 1024) <= 233472 && 2 * (Cfg<32>::SMEM + 8 * 32 + 1024) <= 233472,
               "resblock tile exceeds the 227 KB dynamic shared memory limit");

@@ -618,6 +618,10 @@ __global__ void k_zero_halo(const int64_t* __restrict__ plan, __nv_bfloat16* __r
 // Vocoder state region (fp32): mel tail [O][80] then held [S].
 constexpr int PPLAN = 8;
 
+// conv_post weights [32][7] in constant memory: every FMA below takes its weight as a
+// constant-bank operand (copied on the stream before each launch)
+__constant__ float c_wpost[32 * 7];
+
 __global__ void __launch_bounds__(256) k_post_splice(const __nv_bfloat16* __restrict__ X4,
                                                      const int64_t* __restrict__ plan,
                                                      const float* __restrict__ wpost,  // [32][7]
@@ -627,26 +631,40 @@ __global__ void __launch_bounds__(256) k_post_splice(const __nv_bfloat16* __rest
   const int64_t G = p[1];
   const bool has_tail = p[2] & 1, is_last = p[2] & 2;
   const int64_t g = (int64_t)blockIdx.x * 256 + threadIdx.x;
-  __shared__ float w[32 * 7];
-  if (threadIdx.x < 32 * 7) w[threadIdx.x] = wpost[threadIdx.x];
-  __syncthreads();
   float* dst = reinterpret_cast<float*>(p[4]);
   if (!is_last && g < (int64_t)O * NMEL) {  // new mel tail = last O frames of this chunk
     const float* mel = reinterpret_cast<const float*>(p[6]);
     dst[g] = mel[(p[7] - O) * NMEL + g];
   }
+  // stage the block's 256 + 6 halo rows of the 32-channel stage-4 activation (coalesced 16-byte
+  // loads; rows padded to 80 bytes so the per-sample 16-byte reads below are conflict-free)
+  __shared__ uint4 xs[(256 + 6) * 5];
+  const int64_t g0 = (int64_t)blockIdx.x * 256;
+  if (g0 >= G) return;  // the whole block is past this item's samples
+  const uint4* src = reinterpret_cast<const uint4*>(X4 + (p[0] + g0 - 3) * 32);
+  const int64_t rows_avail = G + 6 - g0;  // valid staged rows (the stage buffer has a zero halo of 25)
+  for (int i = threadIdx.x; i < (256 + 6) * 4; i += 256) {
+    const int r = i >> 2, c = i & 3;
+    xs[r * 5 + c] = r < rows_avail ? src[i] : make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
   if (g >= G) return;
-  const __nv_bfloat16* x = X4 + (p[0] + g - 3) * 32;
-  float acc = bpost;
+  float acc4[4] = {bpost, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int j = 0; j < 7; ++j) {
-    const __nv_bfloat162* row = reinterpret_cast<const __nv_bfloat162*>(x + j * 32);
 #pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      const float2 f = __bfloat1622float2(row[c]);
-      acc = fmaf(w[(2 * c) * 7 + j], f.x, fmaf(w[(2 * c + 1) * 7 + j], f.y, acc));
+    for (int c4 = 0; c4 < 4; ++c4) {
+      const uint4 u = xs[(threadIdx.x + j) * 5 + c4];
+      const uint32_t wds[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wds[e]));
+        const int c = c4 * 4 + e;
+        acc4[e] = fmaf(c_wpost[(2 * c) * 7 + j], f.x, fmaf(c_wpost[(2 * c + 1) * 7 + j], f.y, acc4[e]));
+      }
     }
   }
+  const float acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
   float v = tanhf(acc);
   const int64_t count = is_last ? G : G - S;
   if (g < count) {
@@ -784,6 +802,9 @@ ITTS_API int itts_r_post_splice(const void* X4, const int64_t* plan, int32_t n, 
                                 int32_t overlap_samples, float* audio, void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
   const int64_t work = max(max_g, (int64_t)overlap_frames * NMEL);
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_wpost, wpost, sizeof(float) * 32 * 7, 0, cudaMemcpyDeviceToDevice,
+                                          (cudaStream_t)stream);
+  if (e != cudaSuccess) return (int)e;
   k_post_splice<<<grid2(work, n), 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)X4, plan, wpost, bpost,
                                                                   fade, overlap_frames, overlap_samples, audio);
   ITTS_RETURN_LAUNCH();

@@ -32,7 +32,7 @@ if args.switch:
     sys.setswitchinterval(args.switch)
 cfg, lex = PipelineConfig(), default_lexicon()
 eng = build_engine(cfg, "r", "cuda:0")
-eng.prepare_graphs(max_batch=256)
+eng.prepare_graphs(max_batch=512)
 base = modules_for(eng, lex)
 serve(base, cfg, poisson_trace(50, 1.0, seed=7, lexicon=lex), warmup_iters=0, timed_iters=2, drain_seconds=0.0)
 torch.cuda.synchronize()
