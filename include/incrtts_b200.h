@@ -178,9 +178,11 @@ int itts_r_mel_assemble(const int64_t* plan, int32_t n, int64_t max_rows, void* 
                         void* stream);
 int itts_r_rowmap(const int64_t* plan, int32_t n, int64_t max_span, int32_t* row_out, void* stream);
 int itts_r_zero_halo(const int64_t* plan, int32_t n, int64_t max_halo, void* X, int32_t C, void* stream);
+/* pcm16 (optional, may be NULL): int16 [total] 16-bit PCM of `audio` as the reference
+ * pcm16_encode (src/vocoder.py:146-149), produced in the same pass. */
 int itts_r_post_splice(const void* X4, const int64_t* plan, int32_t n, int64_t max_g, const float* wpost,
                        float bpost, const float* fade, int32_t overlap_frames, int32_t overlap_samples,
-                       float* audio, void* stream);
+                       float* audio, void* pcm16, void* stream);
 
 #ifdef __cplusplus
 }

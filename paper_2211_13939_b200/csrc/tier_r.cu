@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(256) k_post_splice(const __nv_bfloat16* __rest
                                                      const int64_t* __restrict__ plan,
                                                      const float* __restrict__ wpost,  // [32][7]
                                                      float bpost, const float* __restrict__ fade, int O, int S,
-                                                     float* __restrict__ audio) {
+                                                     float* __restrict__ audio, int16_t* __restrict__ pcm) {
   const int64_t* p = plan + blockIdx.y * PPLAN;
   const int64_t G = p[1];
   const bool has_tail = p[2] & 1, is_last = p[2] & 2;
@@ -670,6 +670,8 @@ __global__ void __launch_bounds__(256) k_post_splice(const __nv_bfloat16* __rest
   if (g < count) {
     if (has_tail && g < S) v = fade[g] * v + fade[S + g] * reinterpret_cast<const float*>(p[3])[g];
     audio[p[5] + g] = v;
+    if (pcm)  // f1: 16-bit PCM as pcm16_encode (src/vocoder.py:146-149): clamp, x 32767, round half to even
+      pcm[p[5] + g] = (int16_t)__double2int_rn(fmin(fmax((double)v, -1.0), 1.0) * 32767.0);
   } else {
     dst[(int64_t)O * NMEL + (g - count)] = v;  // held tail for the next seam
   }
@@ -799,13 +801,14 @@ ITTS_API int itts_r_zero_halo(const int64_t* plan, int32_t n, int64_t max_halo, 
 
 ITTS_API int itts_r_post_splice(const void* X4, const int64_t* plan, int32_t n, int64_t max_g,
                                 const float* wpost, float bpost, const float* fade, int32_t overlap_frames,
-                                int32_t overlap_samples, float* audio, void* stream) {
+                                int32_t overlap_samples, float* audio, void* pcm16, void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
   const int64_t work = max(max_g, (int64_t)overlap_frames * NMEL);
   cudaError_t e = cudaMemcpyToSymbolAsync(c_wpost, wpost, sizeof(float) * 32 * 7, 0, cudaMemcpyDeviceToDevice,
                                           (cudaStream_t)stream);
   if (e != cudaSuccess) return (int)e;
   k_post_splice<<<grid2(work, n), 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)X4, plan, wpost, bpost,
-                                                                  fade, overlap_frames, overlap_samples, audio);
+                                                                  fade, overlap_frames, overlap_samples, audio,
+                                                                  (int16_t*)pcm16);
   ITTS_RETURN_LAUNCH();
 }

@@ -184,3 +184,14 @@ class AudioChunk:
     @property
     def sample_count(self) -> int:
         return int(self.samples.shape[0])
+
+    def pcm16(self) -> bytes:
+        """16-bit little-endian PCM of the samples (the reference's ``pcm16_encode``,
+        ``src/vocoder.py:146-149``, applied on the wire by ``src/server.py:176-200``).  GPU modules
+        built with ``pcm16=True`` produce it on device in the splice pass, so the
+        serving path skips the host conversion; otherwise it is computed here."""
+        pre = self.__dict__.get("_pcm16")
+        if pre is not None:
+            return pre
+        from .audio import pcm16_encode
+        return pcm16_encode(self.samples)

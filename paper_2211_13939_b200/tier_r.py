@@ -124,6 +124,7 @@ class TierREngine:
         self.use_graphs = True           # CUDA-graph the 32-step decoder chunk per (batch, L) bucket
         self.fused_mrf = True            # one fused c1->c2 kernel per ResBlock1 layer (resblock_tc.cu)
         self.persistent_decoder = True   # whole decoder chunk in one grid-synchronised kernel (dec_persist.cu)
+        self.pcm16 = False               # also produce 16-bit PCM on device in the splice pass (f1)
         self._dec_buckets: dict = {}
         self._pool: dict = {}
         self._pin_out = torch.empty(1 << 22, dtype=torch.float32, pin_memory=True)  # audio D2H
@@ -559,8 +560,13 @@ class TierREngine:
             audio = self._buf("audio", max(int(out_off[-1]), 1), torch.float32)
             with self._mark("vocoder", 2.0 * HIFIGAN_MACS_PER_FRAME * sum(Ts)):
                 x4 = self._hifigan(Ts, lay0, d_mplan)
+            pcm = self._buf("pcm16", max(int(out_off[-1]), 1), torch.int16) if self.pcm16 else None
             self._call("itts_r_post_splice", x4.data_ptr(), d_pplan.data_ptr(), n, max(mt[4] for mt in metas),
-                       self.wpost.data_ptr(), self.bpost, self.fade.data_ptr(), O, S, audio.data_ptr(), st)
+                       self.wpost.data_ptr(), self.bpost, self.fade.data_ptr(), O, S, audio.data_ptr(),
+                       0 if pcm is None else pcm.data_ptr(), st)
+            if pcm is not None:
+                host_pcm = torch.empty(pcm.numel(), dtype=torch.int16, pin_memory=True)
+                host_pcm.copy_(pcm, non_blocking=True)
             if self._pin_out.numel() < audio.numel():   # grow-only persistent D2H buffer
                 self._pin_out = torch.empty(int(audio.numel() * 1.5), dtype=torch.float32, pin_memory=True)
             host = self._pin_out[:audio.numel()]
@@ -571,9 +577,13 @@ class TierREngine:
         if not np.isfinite(flat[:out_off[-1]]).all():
             raise ValueError("array contains non-finite values")
         out = []
+        pcm_np = host_pcm.numpy() if self.pcm16 else None
         for i, (req, dst, emitted) in enumerate(results):
-            out.append((AudioChunk.trusted(flat[out_off[i]:out_off[i + 1]], emitted),
-                        DeviceVocoderState(req, dst, emitted + counts[i])))
+            chunk = AudioChunk.trusted(flat[out_off[i]:out_off[i + 1]], emitted)
+            if pcm_np is not None:
+                object.__setattr__(chunk, "_pcm16", pcm_np[out_off[i]:out_off[i + 1]].astype("<i2").tobytes())
+                self.d2h_bytes += 2 * counts[i]
+            out.append((chunk, DeviceVocoderState(req, dst, emitted + counts[i])))
         return out
 
     def _hifigan(self, Ts: list[int], lay0: _Layout, d_mplan: torch.Tensor) -> torch.Tensor:

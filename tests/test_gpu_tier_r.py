@@ -175,3 +175,24 @@ def test_graph_replay_equals_eager(engine, lexicon):
         assert np.array_equal(g.mel.frames, g2.mel.frames)
         assert np.array_equal(e.state.attn_weights_sum, g.state.attn_weights_sum)
         assert np.array_equal(e.state.dec_hidden, g2.state.dec_hidden)
+
+
+def test_device_pcm16_matches_reference_encoding(engine, lexicon):
+    """f1: PCM16 produced in the splice pass == pcm16_encode of the float chunk, bit-exact."""
+    from paper_2211_13939_b200.audio import pcm16_encode
+    engine.pcm16 = True
+    try:
+        fos = [run_frontend(t, lexicon) for t in random_texts(lexicon, 3, 11, 20, 60)]
+        encs = engine.encoder_batch(fos)
+        live = [(enc, st, VocoderState.initial()) for enc, st in encs]
+        checked = 0
+        while live and checked < 6:
+            res = engine.decoder_batch([(st, enc) for enc, st, _ in live])
+            outs = engine.vocoder_batch([(vs, r.mel, r.stop) for (_, _, vs), r in zip(live, res)])
+            for chunk, _ in outs:
+                assert chunk.pcm16() == pcm16_encode(chunk.samples)
+                assert "_pcm16" in chunk.__dict__
+            checked += 1
+            live = [(enc, r.state, vs) for (enc, _, _), r, (_, vs) in zip(live, res, outs) if not r.stop]
+    finally:
+        engine.pcm16 = False
