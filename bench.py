@@ -395,7 +395,43 @@ def side_configs(mods, cfg, lex, args) -> dict:
                                     "long_fcl_max_ms": max(lf) if lf else None,
                                     "short_fcl_p99_ms": _percentiles(sf)[1], "short_requests": len(sf)}
     log("C5 done")
+    out["incr_vs_non_incr"] = incr_vs_non_incr(mods, cfg, lex, args)
+    log("INCR vs Non-INCR done")
     return out
+
+
+def incr_vs_non_incr(mods, cfg, lex, args) -> dict:
+    """Paper Table 1 comparison on the GPU: the same Poisson trace (U{20..200} chars) through the
+    incremental pool (first-chunk latency) and through the round-based non-incremental twin
+    (``baseline.py``; its only chunk is the whole waveform, so first-chunk = last-chunk latency)."""
+    import threading as _th
+
+    from paper_2211_13939_b200.baseline import BaselineServer
+    from paper_2211_13939_b200.harness import poisson_trace, serve
+    from paper_2211_13939_b200.scheduler import CostModel
+    qps, secs = args.twin_qps, 8.0
+    trace = poisson_trace(qps, secs, seed=args.seed + 21, lexicon=lex)
+    run = serve(mods, cfg, trace, warmup_iters=0, timed_iters=None, drain_seconds=0.0, tail_seconds=30.0)
+    incr = [1e3 * r.fcl for r in run.timings if r.fcl is not None]
+    pushed, sent = {}, {}
+    with BaselineServer(mods, CostModel.zero(), cfg) as srv:
+        origin = time.perf_counter()
+        for req in trace:
+            while time.perf_counter() < origin + req.send_at:
+                time.sleep(0.0005)
+            rid, stream = srv.submit(req.text)
+            sent[rid] = time.perf_counter()
+            push = stream._push
+            stream._push = (lambda c, _p=push, _r=rid: (pushed.setdefault(_r, time.perf_counter()), _p(c)))
+        deadline = time.perf_counter() + 60.0
+        while len(pushed) < len(sent) and time.perf_counter() < deadline:
+            time.sleep(0.01)
+    lat = [1e3 * (pushed[r] - t) for r, t in sent.items() if r in pushed]
+    p50i, p99i = _percentiles(incr)
+    p50b, p99b = _percentiles(lat)
+    return {"qps": qps, "requests": len(trace), "incr_fcl_p50_ms": p50i, "incr_fcl_p99_ms": p99i,
+            "non_incr_latency_p50_ms": p50b, "non_incr_latency_p99_ms": p99b,
+            "note": "server-side: submit -> the (single, whole-waveform) chunk visible on the stream"}
 
 
 def qps_sweep(mods, cfg, lex, args) -> list[dict]:
@@ -444,6 +480,7 @@ def main() -> None:
     ap.add_argument("--sweep-seconds", type=float, default=5.0)
     ap.add_argument("--side-configs", type=int, default=1, help="also run C1, C2, C5 (1 = on)")
     ap.add_argument("--c5-qps", type=float, default=50.0)
+    ap.add_argument("--twin-qps", type=float, default=30.0, help="QPS of the INCR vs Non-INCR comparison")
     ap.add_argument("--l2-flush", type=int, default=1,
                     help="1: write a 256 MB buffer on the engine stream before every decoder call, so each "
                          "serving iteration starts with a cold L2 (timing rule); 0: steady-state caches")
