@@ -475,7 +475,7 @@ def main() -> None:
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sweep", default="125,150,175,200,225,250,275,300,350,400",
+    ap.add_argument("--sweep", default="150,175,200,225,250,275,300,350",
                     help="extra QPS levels for max-QPS (empty: off); stops at the first p99 > 80 ms")
     ap.add_argument("--sweep-seconds", type=float, default=5.0)
     ap.add_argument("--side-configs", type=int, default=1, help="also run C1, C2, C5 (1 = on)")
