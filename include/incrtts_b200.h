@@ -184,6 +184,24 @@ int itts_r_post_splice(const void* X4, const int64_t* plan, int32_t n, int64_t m
                        float bpost, const float* fade, int32_t overlap_frames, int32_t overlap_samples,
                        float* audio, void* pcm16, void* stream);
 
+/* K7 native launch sequence: the whole HiFi-GAN V1 stack of one pooled vocoder
+ * call (replaces the per-layer host loop over vocode_batch's conv stack,
+ * src/vocoder.py:92-143) issued from C++ after a single H2D copy of a packed
+ * plan.  weights = 154 device pointers, (w, bias) pairs in the order conv_pre,
+ * ups[0..3], then res[stage][branch][layer][c1, c2] in the layouts
+ * itts_conv1d_tc / itts_resblock_tc take.  run: frames = host int32 [n] spliced
+ * frame counts T_i; mel_plan = the device plan of itts_r_mel_assemble;
+ * multi_stream = 1 runs the three MRF branches of a stage on three streams
+ * (same arithmetic); *x4_out receives the stage-4 activations (bf16
+ * [rows][32], lrelu 0.01 applied) for itts_r_post_splice, valid until the next
+ * run on the handle.  Work buffers are owned by the handle (grow-only;
+ * itts_r_voc_reserve pre-sizes them so serving never allocates). */
+int itts_r_voc_create(void** handle, const int64_t* weights, int32_t count);
+int itts_r_voc_reserve(void* handle, int32_t n, int32_t frames, void* stream);
+int itts_r_voc_run(void* handle, int32_t n, const int32_t* frames, const int64_t* mel_plan,
+                   int32_t multi_stream, void** x4_out, void* stream);
+int itts_r_voc_destroy(void* handle);
+
 #ifdef __cplusplus
 }
 #endif

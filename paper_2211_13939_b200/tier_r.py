@@ -24,6 +24,9 @@ in Tier S; the gate logit is computed and returned but not used.
 
 from __future__ import annotations
 
+import ctypes
+import weakref
+
 import numpy as np
 import torch
 
@@ -125,6 +128,11 @@ class TierREngine:
         self.fused_mrf = True            # one fused c1->c2 kernel per ResBlock1 layer (resblock_tc.cu)
         self.persistent_decoder = True   # whole decoder chunk in one grid-synchronised kernel (dec_persist.cu)
         self.pcm16 = False               # also produce 16-bit PCM on device in the splice pass (f1)
+        self.mrf_streams = True          # run the 3 MRF branches of a stage on 3 streams (fused path)
+        self.native_vocoder = True       # issue the fused HiFi-GAN stack from C++ (voc_run.cu)
+        self._voc = self._create_native_vocoder()
+        self._side = [torch.cuda.Stream(self.device) for _ in range(2)]
+        self._ev = [torch.cuda.Event() for _ in range(3)]
         self._dec_buckets: dict = {}
         self._pool: dict = {}
         self._pin_out = torch.empty(1 << 22, dtype=torch.float32, pin_memory=True)  # audio D2H
@@ -214,6 +222,21 @@ class TierREngine:
         self.wpost = f32(w["hg.conv_post.w"][0])                                        # [32][7]
         self.bpost = float(w["hg.conv_post.b"][0])
 
+    def _create_native_vocoder(self) -> int:
+        """Handle of the C++ launch sequence (voc_run.cu) over this engine's HiFi-GAN weights."""
+        ptrs = [self.conv_pre[0], self.conv_pre[2]]
+        for wp, _, bias in self.ups:
+            ptrs += [wp, bias]
+        for blocks in self.res:
+            for layers in blocks:
+                for c1, c2 in layers:
+                    ptrs += [c1[0], c1[2], c2[0], c2[2]]
+        arr = (ctypes.c_int64 * len(ptrs))(*[t.data_ptr() for t in ptrs])
+        h = ctypes.c_void_p()
+        _native.call("itts_r_voc_create", ctypes.byref(h), arr, len(ptrs))
+        weakref.finalize(self, _native.lib().itts_r_voc_destroy, h.value)
+        return h.value
+
     # ------------------------------------------------------------ helpers
     def _st(self) -> int:
         return self.stream.cuda_stream
@@ -227,8 +250,9 @@ class TierREngine:
         tc.conv1d_tc(x, wt, offs, bias, c_out, row_out, stream=self._st(), **kw)
         self.launches += 1
 
-    def _resblock(self, x, c1, c2, dil, row_out, **kw) -> None:
-        tc.resblock_tc(x, c1, c2, dil, row_out, stream=self._st(), **kw)
+    def _resblock(self, x, c1, c2, dil, row_out, stream=None, **kw) -> None:
+        st = self._st() if stream is None else stream.cuda_stream
+        tc.resblock_tc(x, c1, c2, dil, row_out, stream=st, **kw)
         self.launches += 1
 
     def _buf(self, name: str, numel: int, dtype=torch.bfloat16, zero: bool = False) -> torch.Tensor:
@@ -253,8 +277,11 @@ class TierREngine:
         for u, C in zip(UPS, STAGE_C):
             mult *= u
             biggest = max(biggest, max_batch * (T * mult + 2 * MRF_HALO) * C)
-        for i in range(6):
-            self._buf(f"b16_{i}", biggest)
+        if self.native_vocoder:
+            self._call("itts_r_voc_reserve", self._voc, max_batch, T, self._st())
+        else:
+            for i in range(10):
+                self._buf(f"b16_{i}", biggest)
         self._buf("audio", max_batch * T * self.cfg.hop_samples, torch.float32)
         for name, m in (("rm0", 1), ("rmT0", 1), ("rm_s0", 8), ("rmT1", 8), ("rm_s1", 64), ("rmT2", 64),
                         ("rm_s2", 128), ("rmT3", 128), ("rm_s3", 256)):
@@ -561,7 +588,7 @@ class TierREngine:
             with self._mark("vocoder", 2.0 * HIFIGAN_MACS_PER_FRAME * sum(Ts)):
                 x4 = self._hifigan(Ts, lay0, d_mplan)
             pcm = self._buf("pcm16", max(int(out_off[-1]), 1), torch.int16) if self.pcm16 else None
-            self._call("itts_r_post_splice", x4.data_ptr(), d_pplan.data_ptr(), n, max(mt[4] for mt in metas),
+            self._call("itts_r_post_splice", x4 if isinstance(x4, int) else x4.data_ptr(), d_pplan.data_ptr(), n, max(mt[4] for mt in metas),
                        self.wpost.data_ptr(), self.bpost, self.fade.data_ptr(), O, S, audio.data_ptr(),
                        0 if pcm is None else pcm.data_ptr(), st)
             if pcm is not None:
@@ -586,9 +613,47 @@ class TierREngine:
             out.append((chunk, DeviceVocoderState(req, dst, emitted + counts[i])))
         return out
 
+    def _mrf_branches(self, s: int, XA, ACC, OA_next, scratch, rm, slope_out: float) -> None:
+        """One MRF stage with its three ResBlock1 branches on three streams.
+
+        Branch j's first two layers only read XA and write the branch's own ping-pong pair, so
+        branches 1 and 2 run on side streams concurrently with branch 0 on the engine stream;
+        the three last layers sum into ACC in branch order (STORE, ADD, FINAL) on the engine
+        stream, after waiting for the side branch that produced their input.  At small pooled
+        batches a layer fills only part of the GPU, so the stage's critical path drops from 9
+        layers to 5; the arithmetic (and the order of the ACC sum) is unchanged."""
+        main = self.stream
+        ev_x, ev_1, ev_2 = self._ev
+        ev_x.record(main)
+        tails = []
+        for j, layers in enumerate(self.res[s]):
+            ya, tb = scratch[j]
+            st = main if j == 0 else self._side[j - 1]
+            if j:
+                st.wait_event(ev_x)
+            (c1a, c2a), (c1b, c2b) = layers[0], layers[1]
+            self._resblock(XA, c1a, c2a, W.HG_RES_DILATIONS[0], rm, stream=st, act_out=ya, slope=0.1)
+            self._resblock(ya, c1b, c2b, W.HG_RES_DILATIONS[1], rm, stream=st, act_out=tb, slope=0.1)
+            if j:
+                (ev_1, ev_2)[j - 1].record(st)
+            tails.append(tb)
+        for j, layers in enumerate(self.res[s]):
+            if j:
+                main.wait_event((ev_1, ev_2)[j - 1])
+            c1, c2 = layers[2]
+            mode = (tc.ACC_STORE, tc.ACC_ADD, tc.ACC_FINAL)[j]
+            self._resblock(tails[j], c1, c2, W.HG_RES_DILATIONS[2], rm, acc=ACC, acc_mode=mode,
+                           act_out=OA_next if j == 2 else None, slope=slope_out)
+
     def _hifigan(self, Ts: list[int], lay0: _Layout, d_mplan: torch.Tensor) -> torch.Tensor:
         """HiFi-GAN V1 over a packed batch of spliced chunks -> stage-4 bf16 act (lrelu 0.01 applied)."""
         dev, st, n = self.device, self._st(), len(Ts)
+        if self.native_vocoder and self.fused_mrf:
+            x4 = ctypes.c_void_p()
+            self._call("itts_r_voc_run", self._voc, n, np.ascontiguousarray(Ts, np.int32).ctypes.data,
+                       d_mplan.data_ptr(), int(self.mrf_streams), ctypes.byref(x4), st)
+            self.launches += 54   # 9 row maps, mel assembly, conv_pre, 4 x (convT, halo, 9 ResBlock layers)
+            return x4.value
         with torch.cuda.stream(self.stream):
             x0 = self._buf("x0", lay0.total * 128, zero=True).view(lay0.total, 128)
         self._call("itts_r_mel_assemble", d_mplan.data_ptr(), n, max(Ts), x0.data_ptr(), 128, st)
@@ -601,7 +666,8 @@ class TierREngine:
             layouts.append(_Layout([T * mult for T in Ts], MRF_HALO))
         biggest = max(l.total * c for l, c in zip(layouts, STAGE_C))
         # bf16 only: the residual stream is kept as lrelu(y, 0.1) and inverted on load
-        b16 = [self._buf(f"b16_{i}", biggest) for i in range(6)]  # xa ya tb acc oa oa'
+        # xa ya tb acc oa oa' (+ ya/tb of MRF branches 1 and 2 when they run on side streams)
+        b16 = [self._buf(f"b16_{i}", biggest) for i in range(10 if self.fused_mrf and self.mrf_streams else 6)]
         for s, (u, lay) in enumerate(zip(UPS, layouts)):
             C = STAGE_C[s]
             view = lambda t: t[:lay.total * C].view(lay.total, C)
@@ -614,6 +680,11 @@ class TierREngine:
             self._call("itts_r_zero_halo", self._up(zplan).data_ptr(), n, lay.halo, XA.data_ptr(), C, st)
             rm = self._rowmap(lay, lay.first, 1, f"rm_s{s}")
             slope_out = 0.1 if s < 3 else 0.01
+            if self.fused_mrf and self.mrf_streams:
+                self._mrf_branches(s, XA, ACC, OA_next, [(YA, TB)] + [(view(b16[6 + 2 * j]), view(b16[7 + 2 * j]))
+                                                                      for j in range(2)], rm, slope_out)
+                prev, act_in = lay, OA_next
+                continue
             if self.fused_mrf:
                 # one fused kernel per ResBlock1 layer; ping-pong YA/TB (a layer must not write its input)
                 for j, layers in enumerate(self.res[s]):

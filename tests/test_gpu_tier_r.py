@@ -196,3 +196,26 @@ def test_device_pcm16_matches_reference_encoding(engine, lexicon):
             live = [(enc, r.state, vs) for (enc, _, _), r, (_, vs) in zip(live, res, outs) if not r.stop]
     finally:
         engine.pcm16 = False
+
+
+@pytest.mark.parametrize("sizes", [(1,), (5, 3, 40), (24,)])
+def test_native_vocoder_sequence_equals_python_launches(engine, sizes):
+    """voc_run.cu (C++ launch sequence, 1 or 3 streams) == the per-layer Python launch loop, bit-exact."""
+    rng = np.random.default_rng(sum(sizes))
+    triples = []
+    for k, B in enumerate(sizes):
+        for i in range(B):
+            m = int(rng.integers(1, 33)) if i % 7 == 3 else 32
+            triples.append((VocoderState.initial(), MelChunk(rng.uniform(-0.2, 0.2, (m, 80))), m < 32))
+    got = {}
+    for native in (False, True):
+        for streams in (False, True):
+            engine.native_vocoder, engine.mrf_streams = native, streams
+            try:
+                got[native, streams] = [a.samples for a, _ in engine.vocoder_batch(triples)]
+            finally:
+                engine.native_vocoder, engine.mrf_streams = True, True
+    want = got[False, False]
+    for key, outs in got.items():
+        for a, b in zip(outs, want):
+            assert np.array_equal(a, b), key

@@ -33,6 +33,7 @@ def main():
     args = ap.parse_args()
     eng = TierREngine(PipelineConfig(), "cuda:0")
     eng.use_graphs = False
+    eng.mrf_streams = False  # events on the engine stream only
     lex = default_lexicon()
     rng = random.Random(1)
     fos = [run_frontend(random_text(rng, 20, 200, lex), lex) for _ in range(args.batch)]

@@ -54,6 +54,7 @@ def main():
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--no-graphs", action="store_true", help="eager decoder (stable kernel order for ncu -s/-c)")
     ap.add_argument("--unfused", action="store_true", help="MRF as two tc_conv launches per layer (A/B)")
+    ap.add_argument("--serial-mrf", action="store_true", help="MRF branches one after another on one stream")
     args = ap.parse_args()
     cfg = PipelineConfig()
     eng = build_engine(cfg, args.tier, "cuda:0")
@@ -61,6 +62,8 @@ def main():
         eng.use_graphs = False
     if args.unfused:
         eng.fused_mrf = False
+    if args.serial_mrf:
+        eng.mrf_streams = False
     lex = default_lexicon()
     rows = []
     for B in [int(b) for b in args.batches.split(",")]:
