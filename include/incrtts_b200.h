@@ -178,6 +178,10 @@ int itts_r_mel_assemble(const int64_t* plan, int32_t n, int64_t max_rows, void* 
                         void* stream);
 int itts_r_rowmap(const int64_t* plan, int32_t n, int64_t max_span, int32_t* row_out, void* stream);
 int itts_r_zero_halo(const int64_t* plan, int32_t n, int64_t max_halo, void* X, int32_t C, void* stream);
+/* MRF merge of HiFi-GAN V1 (the xs / num_kernels average of the three ResBlock1 branches):
+ * out = bf16(lrelu((y0 + y1 + y2) / 3, slope)) over n bf16 elements (n % 8 == 0). */
+int itts_r_mrf_combine(const void* y0, const void* y1, const void* y2, int64_t n, float slope, void* out,
+                       void* stream);
 /* pcm16 (optional, may be NULL): int16 [total] 16-bit PCM of `audio` as the reference
  * pcm16_encode (src/vocoder.py:146-149), produced in the same pass. */
 int itts_r_post_splice(const void* X4, const int64_t* plan, int32_t n, int64_t max_g, const float* wpost,

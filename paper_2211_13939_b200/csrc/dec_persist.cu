@@ -2,23 +2,22 @@
 //
 // Replaces the per-step chain of ~10 launches (tier_r.cu k_gemv / k_lstm_cell / k_attention +
 // two tc_conv gate GEMMs) for decode_chunk_batch (reference acoustic.py:191-219, :234-238;
-// Tacotron2 decoder step = paper Eq. 2).  One CTA per SM; the phases of a
-// step are separated by a grid-wide barrier, so a step costs 8 barriers instead of 10 kernel
-// boundaries, and everything that is constant across steps stays on chip:
+// Tacotron2 decoder step = paper Eq. 2).  One CTA per SM; the five phases of
+// a step are separated by a grid-wide barrier, and everything that is constant across steps
+// stays on chip:
 //
-//   PRE1   mel(s-1) = bp + sum of the projection K-slices (fixed order) -> mel / gate outputs,
-//          last_frame; H1 = relu(W0 . last_frame)                      (8-item x 32-col tasks)
-//   PRE2   p = relu(W1 . H1) -> state + bf16 operand mirror
-//   ATT    gates = [p|ctx|att_h] . Wa^T on the tensor cores (mma.sync bf16 -> fp32), CTA c owns
-//          hidden units [8c, 8c+8) = 32 gate rows (interleaved on the host), its weight slice is
-//          bulk-copied (cp.async.bulk) into shared memory while the previous phases run; the
-//          LSTM cell is the GEMM epilogue (no gate round trip through HBM)
-//   QUERY  q = Wq . att_h as 8 K-slice partials
-//   ATT-A  per (item, position chunk): location conv, energies, chunk max, exp, chunk sum,
-//          unnormalised context partial
+//   PRE    mel(s-1) = bp + the 33 projection partials (fixed order) -> mel / gate outputs,
+//          last_frame; H1 = relu(W0 . last_frame) (in shared memory); p = relu(W1 . H1)
+//          (8-item x 32-column tasks)
+//   ATT    gates = [p|ctx|att_h] . Wa^T on the tensor cores (tcgen05, weights as M), 4-way
+//          K-split per 32-unit group; the LSTM cell is the fixup epilogue, which also emits the
+//          group's query partial q_g = Wq[:, group] . att_h[group]  (no separate query phase)
+//   ATT-A  per (item, position chunk): q = sum of the 32 group partials, location features,
+//          energies, chunk max, exp, chunk sum, unnormalised context partial
 //   ATT-B  per item: combine chunks (max / rescale / sum, chunk order) -> context, W, W_acc
-//   DEC    gates = [ctx|att_h|dec_h] . Wd^T + cell (as ATT)
-//   PROJ   mel/gate projection as 8 K-slice partials (summed by the next PRE1)
+//   DEC    gates = [ctx|att_h|dec_h] . Wd^T + cell (as ATT); the fixup emits the group's
+//          mel/gate projection partial of dec_h while the CTAs without a gate group project the
+//          context (the 33rd partial), so the projection is summed by the next PRE
 //
 // The bf16 operand mirror keeps two banks of att_h / dec_h (step parity) so a GEMM phase never
 // reads the h it is overwriting.  All reductions run in a fixed order: results do not depend
@@ -52,7 +51,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 constexpr int DPLAN = 8;
 constexpr int NT = 256, NW = 8;  // threads / warps per CTA
-constexpr int QKS = 8, PKS = 8;  // query / projection K-slices
+constexpr int NGRP = HID / 32;   // 32-unit gate groups: query partials, projection partials (+1 ctx)
 constexpr int GEMM_CTAS = HID / 8;  // 128 CTAs x 8 hidden units
 constexpr int KA = 1792, KD = 2560;
 constexpr int MAXCH = 256;       // max position chunks per item
@@ -85,8 +84,8 @@ struct DecArgs {
   const float* bp;                 // [81]
   float* Gp;                       // [4 splits][32 groups][B16][128] gate GEMM K-split partials
   float* H1;                       // [B][256]
-  float* Qp;                       // [QKS][B][128]
-  float* Pp;                       // [PKS][B][81]
+  float* Qp;                       // [NGRP][B][128] query partials per unit group
+  float* Pp;                       // [NGRP + 1][B][81] projection partials (groups of dec_h, then ctx)
   float* U;                        // [B][u_ld] unnormalised attention numerators
   int64_t u_ld;
   float* AP;                       // [B][MAXCH][2 + 512] chunk max, sum, context partial
@@ -205,7 +204,7 @@ constexpr uint32_t GW_TILE = 128 * 128;  // weight stage: 128 rows x 64 bf16
 
 template <int MODE>
 __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy, uint32_t x_stage_bytes, int nst,
-                           uint32_t& g_ring, uint32_t& lt_tile, const PlanCache& pc, unsigned& grp_gen) {
+                           uint32_t& g_ring, uint32_t& lt_tile, const PlanCache& pc, unsigned& grp_gen, float* hs) {
   constexpr int K = MODE == 0 ? KA : KD;
   constexpr int NKC = K / 64;
   constexpr int KCS = NKC / KSPLIT;
@@ -225,6 +224,7 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
     if (lane == 0) {
       const uint32_t pi = warp == 0 ? 0 : warp - 1;
       asm volatile("fence.proxy.async.global;" ::: "memory");  // xb tiles written by generic stores
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the ring doubles as PRE scratch
       uint32_t g = g_ring;
       for (int i = 0; i < KCS; ++i, ++g) {
         if (g % 3 != pi) continue;
@@ -283,9 +283,8 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
     if (lane == 0) tcg::mbar_arrive(&gsy.acce);
     // group sync: the 4 K-split CTAs of this unit group have written their partials
     asm volatile("bar.sync 2, 128;" ::: "memory");
-    if (warp == 4 && lane == 0) {
+    if (warp == 4 && lane == 0) {  // release: the partials of the 4 epilogue warps (ordered by bar.sync)
       unsigned* cnt = a.bar + 2 + ug;
-      __threadfence();
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
       unsigned seen;
       do {
@@ -298,19 +297,20 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
   }
   __syncthreads();
   {
-    // fixup (all 256 threads): this CTA finishes units [8ks, 8ks+8) of the group for every live
-    // item; 4 cells per thread in flight (partials + c state loaded before any arithmetic)
+    // fixup (all 256 threads): this CTA finishes all 32 units of the group for items b = ks + 4i;
+    // 4 cells per thread in flight (partials + c state loaded before any arithmetic)
     const float* bias = (MODE == 0 ? a.ba : a.bd) + ug * 128;
     const int h_off = MODE == 0 ? ATTH_OFF : DECH_OFF, c_off = MODE == 0 ? ATTC_OFF : DECC_OFF;
     const int hb_off = MODE == 0 ? att_off(newb) : dec_off(newb);
-    for (int e0 = threadIdx.x; e0 < 8 * a.B; e0 += 4 * NT) {
+    const int nmine = (a.B - ks + KSPLIT - 1) / KSPLIT;
+    for (int e0 = threadIdx.x; e0 < 32 * nmine; e0 += 4 * NT) {
       float4 gs4[4];
       float cold[4];
       bool live[4];
 #pragma unroll
       for (int z = 0; z < 4; ++z) {
-        const int e = e0 + z * NT, b = e >> 3, ul = ks * 8 + (e & 7), j = ug * 32 + ul;
-        live[z] = e < 8 * a.B && active(pc, b, s);
+        const int e = e0 + z * NT, b = ks + KSPLIT * (e >> 5), ul = e & 31, j = ug * 32 + ul;
+        live[z] = e < 32 * nmine && active(pc, b, s);
         gs4[z] = make_float4(0.f, 0.f, 0.f, 0.f);
         cold[z] = 0.f;
         if (!live[z]) continue;
@@ -328,16 +328,51 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       }
 #pragma unroll
       for (int z = 0; z < 4; ++z) {
-        if (!live[z]) continue;
-        const int e = e0 + z * NT, b = e >> 3, ul = ks * 8 + (e & 7), j = ug * 32 + ul;
-        const float cn = sigm(gs4[z].y) * cold[z] + sigm(gs4[z].x) * tanhf(gs4[z].z);
-        const float hn = sigm(gs4[z].w) * tanhf(cn);
-        float* st = a.work + (int64_t)b * ROW;
-        st[c_off + j] = cn;
-        st[h_off + j] = hn;
-        a.xb[xb_off(b, hb_off + j)] = __float2bfloat16_rn(hn);
+        const int e = e0 + z * NT;
+        if (e >= 32 * nmine) continue;
+        const int b = ks + KSPLIT * (e >> 5), ul = e & 31, j = ug * 32 + ul;
+        float hn = 0.f;
+        if (live[z]) {
+          const float cn = sigm(gs4[z].y) * cold[z] + sigm(gs4[z].x) * tanhf(gs4[z].z);
+          hn = sigm(gs4[z].w) * tanhf(cn);
+          float* st = a.work + (int64_t)b * ROW;
+          st[c_off + j] = cn;
+          st[h_off + j] = hn;
+          a.xb[xb_off(b, hb_off + j)] = __float2bfloat16_rn(hn);
+        }
+        hs[e] = hn;
       }
     }
+    __syncthreads();
+    if (threadIdx.x == 0) mark(6);
+    // this group's share of the next linear layer: query (MODE 0, 128 outputs) or the mel/gate
+    // projection of dec_h (MODE 1, 81 outputs); 32-term dot products in unit order
+    constexpr int N = MODE == 0 ? ATT : NMEL + 1;
+    const int n = threadIdx.x & 127, half = threadIdx.x >> 7;
+    if (n < N) {
+      const float* W = (MODE == 0 ? a.WqT : a.WpT) + (int64_t)ug * 32 * N + n;
+      float* out = (MODE == 0 ? a.Qp : a.Pp) + (int64_t)ug * a.B * N + n;
+      float w[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) w[u] = __ldg(W + u * N);
+      for (int i = half; i < nmine; i += 2) {
+        const int b = ks + KSPLIT * i;
+        if (!active(pc, b, s)) continue;
+        const float4* h4 = reinterpret_cast<const float4*>(hs + i * 32);
+        float acc = 0.f;
+#pragma unroll
+        for (int u4 = 0; u4 < 8; ++u4) {
+          const float4 h = h4[u4];
+          acc = fmaf(w[4 * u4], h.x, acc);
+          acc = fmaf(w[4 * u4 + 1], h.y, acc);
+          acc = fmaf(w[4 * u4 + 2], h.z, acc);
+          acc = fmaf(w[4 * u4 + 3], h.w, acc);
+        }
+        out[(int64_t)b * N] = acc;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) mark(5);
   }
   g_ring += KCS;
   lt_tile += 1;
@@ -414,10 +449,13 @@ __device__ void att_chunk(const DecArgs& a, AttSmem& sm, int s, int b, int ch, i
   const int n = tb - ta, nh = n + 2 * HALO;
   const float* sPm = reinterpret_cast<const float*>(stage);
   const float* sMem = sPm + ACH * ATT;
-  if (tid < ATT) {
-    float qa = ldf(a.Qp + (int64_t)b * ATT + tid);
+  if (tid < ATT) {  // q = sum of the 32 unit-group partials, group order (8 loads in flight)
+    float qv[NGRP];
 #pragma unroll
-    for (int z = 1; z < QKS; ++z) qa += ldf(a.Qp + ((int64_t)z * a.B + b) * ATT + tid);
+    for (int z = 0; z < NGRP; ++z) qv[z] = ldf(a.Qp + ((int64_t)z * a.B + b) * ATT + tid);
+    float qa = qv[0];
+#pragma unroll
+    for (int z = 1; z < NGRP; ++z) qa += qv[z];
     sm.q[tid] = qa;
   }
   for (int i = tid; i < nh; i += NT) {
@@ -541,7 +579,7 @@ __device__ void att_chunk(const DecArgs& a, AttSmem& sm, int s, int b, int ch, i
   if (tr) a.trace[13] += 1;
 }
 
-// ATT-B for item b: combine the chunks (chunk order) -> context, W, W_acc.
+// ATT-B for item b: combine the chunks (max, sum, context partial; chunk order) -> context, W, W_acc.
 __device__ void att_combine(const DecArgs& a, AttSmem& sm, int s, int b, int chunk) {
   const int tid = threadIdx.x;
   const int64_t* p = a.plan + b * DPLAN;
@@ -561,7 +599,15 @@ __device__ void att_combine(const DecArgs& a, AttSmem& sm, int s, int b, int chu
   float* st = a.work + (int64_t)b * ROW;
   for (int d = tid; d < EMB; d += NT) {
     float c = 0.f;
-    for (int k = 0; k < nch; ++k) c = fmaf(scale[k], ldf(ap + k * (2 + EMB) + 2 + d), c);
+    int k = 0;
+    for (; k + 4 <= nch; k += 4) {  // 4 partial loads in flight, summed in chunk order
+      float v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = ldf(ap + (k + j) * (2 + EMB) + 2 + d);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c = fmaf(scale[k + j], v[j], c);
+    }
+    for (; k < nch; ++k) c = fmaf(scale[k], ldf(ap + k * (2 + EMB) + 2 + d), c);
     st[CTX_OFF + d] = c;
     a.xb[xb_off(b, CTX_OFF + d)] = __float2bfloat16_rn(c);
   }
@@ -629,6 +675,7 @@ __global__ void __launch_bounds__(NT, 1)
   grid_sync(a.bar, gen);
 
   // position chunking of the attention: about two tasks per CTA
+  // position chunking of the attention: about two tasks per CTA
   int maxL = 1;
   for (int b = 0; b < a.B; ++b) maxL = max(maxL, pc.L[b]);
   int64_t sumL = 0;
@@ -648,69 +695,115 @@ __global__ void __launch_bounds__(NT, 1)
       tacc[ph_i] += now - tph;
       tph = now;
     }
-    ph_i = ph_i == 7 ? 0 : ph_i + 1;
+    ph_i = ph_i == 4 ? 0 : ph_i + 1;
   };
+  // mel / gate value k of item b for the step whose projection partials are in Pp (group order, ctx last)
+  auto mel_value = [&](int b, int k) {
+    float pv[NGRP + 1];
+#pragma unroll
+    for (int z = 0; z <= NGRP; ++z) pv[z] = ldf(a.Pp + ((int64_t)z * a.B + b) * 81 + k);
+    float m = __ldg(a.bp + k);
+#pragma unroll
+    for (int z = 0; z <= NGRP; ++z) m += pv[z];
+    return m;
+  };
+  float* ringf = reinterpret_cast<float*>(ring);  // generic scratch outside the gate / staging uses
   for (int s = 0; s < a.nsteps; ++s) {
     const int gs = a.step0 + s;
-    // ---- PRE1: finish mel(s-1), H1 = relu(W0 . last)
+    // ---- PRE: finish mel(s-1); H1 = relu(W0 . last) for the task's 8 items; p = relu(W1 . H1)
     for (int task = c; task < nb8 * 8; task += G) {
       const int b0 = (task >> 3) * 8, n0 = (task & 7) * 32, nb = min(8, a.B - b0);
-      float* sx = scratch;               // [8][80]
-      if (s > 0) {
-        for (int i = tid; i < 8 * 81; i += NT) {
-          const int it = i / 81, k = i % 81, b = b0 + it;
-          if (it >= nb) continue;
-          float m = __ldg(a.bp + k);
+      const bool trp = a.trace && c == 0 && tid == 0;
+      unsigned long long tp0 = trp ? gtimer() : 0;
+      auto pmark = [&](int slot) {
+        if (trp) {
+          const unsigned long long t1 = gtimer();
+          a.trace[slot] += t1 - tp0;
+          tp0 = t1;
+        }
+      };
+      float* sx = ringf;                 // [8][80]
+      float* sh = sx + 8 * NMEL;         // [8][256]
+      float* gsc = sh + 8 * PRE;         // gemv scratch
+
+      {  // warp w: item b0 + w; lane l: mel / gate values k = l, l + 32, l + 64 (< 81), all 3 x 34
+         // partial loads in flight before the sums
+        const int it = tid >> 5, lane = tid & 31, b = b0 + it;
+        const bool was = it < nb && s > 0 && active(pc, b, gs - 1);
+        float m[3] = {0.f, 0.f, 0.f};
+        if (was) {
+          float pv[3][NGRP + 1];
 #pragma unroll
-          for (int z = 0; z < PKS; ++z) m += ldf(a.Pp + ((int64_t)z * a.B + b) * 81 + k);
-          const bool was = active(pc, b, gs - 1);
-          if (k < NMEL) sx[it * NMEL + k] = was ? m : ldf(a.work + (int64_t)b * ROW + LAST_OFF + k);
+          for (int j = 0; j < 3; ++j) {
+            const int k = lane + 32 * j;
+#pragma unroll
+            for (int z = 0; z <= NGRP; ++z) pv[j][z] = k < 81 ? ldf(a.Pp + ((int64_t)z * a.B + b) * 81 + k) : 0.f;
+          }
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            const int k = lane + 32 * j;
+            m[j] = k < 81 ? __ldg(a.bp + k) : 0.f;
+#pragma unroll
+            for (int z = 0; z <= NGRP; ++z) m[j] += pv[j][z];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const int k = lane + 32 * j;
+          if (k >= 81) continue;
+          if (k < NMEL)
+            sx[it * NMEL + k] = it >= nb ? 0.f : was ? m[j] : ldf(a.work + (int64_t)b * ROW + LAST_OFF + k);
           if (n0 == 0 && was) {
             const int64_t* p = a.plan + b * DPLAN;
             if (k < NMEL) {
-              reinterpret_cast<float*>(p[6])[(gs - 1) * NMEL + k] = m;
-              a.work[(int64_t)b * ROW + LAST_OFF + k] = m;
+              reinterpret_cast<float*>(p[6])[(gs - 1) * NMEL + k] = m[j];
+              a.work[(int64_t)b * ROW + LAST_OFF + k] = m[j];
             } else {
-              reinterpret_cast<float*>(p[7])[gs - 1] = m;
+              reinterpret_cast<float*>(p[7])[gs - 1] = m[j];
             }
           }
         }
-      } else {
-        for (int i = tid; i < 8 * NMEL; i += NT) {
-          const int it = i / NMEL, k = i % NMEL;
-          sx[i] = it < nb ? ldf(a.work + (int64_t)(b0 + it) * ROW + LAST_OFF + k) : 0.f;
-        }
       }
       __syncthreads();
-      gemv_task<10>(b0, nb, n0, PRE, 0, NMEL, a.W0T, scratch + 8 * 81, scratch + 8 * 81 + 8 * NMEL,
-                    [&](int b, int k) { return sx[(b - b0) * NMEL + k]; },
-                    [&](int b, int n, float y) { a.H1[(int64_t)b * PRE + n] = fmaxf(y, 0.f); });
+      pmark(5);
+      {  // thread n: unit n of H1 for the 8 items (k order)
+        static_assert(NT == PRE, "one thread per prenet unit");
+        float acc[8];
+#pragma unroll
+        for (int it = 0; it < 8; ++it) acc[it] = 0.f;
+        const float4* sx4 = reinterpret_cast<const float4*>(sx);
+#pragma unroll 2
+        for (int k4 = 0; k4 < NMEL / 4; ++k4) {
+          float w[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) w[j] = __ldg(a.W0T + (4 * k4 + j) * PRE + tid);
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const float4 x = sx4[it * (NMEL / 4) + k4];
+            acc[it] = fmaf(w[0], x.x, acc[it]);
+            acc[it] = fmaf(w[1], x.y, acc[it]);
+            acc[it] = fmaf(w[2], x.z, acc[it]);
+            acc[it] = fmaf(w[3], x.w, acc[it]);
+          }
+        }
+#pragma unroll
+        for (int it = 0; it < 8; ++it) sh[it * PRE + tid] = fmaxf(acc[it], 0.f);
+      }
+      __syncthreads();
+      pmark(6);
+      gemv_task<32>(b0, nb, n0, PRE, 0, PRE, a.W1T, gsc, gsc + 8 * PRE,
+                    [&](int b, int k) { return sh[(b - b0) * PRE + k]; },
+                    [&](int b, int n, float y) {
+                      if (!active(pc, b, gs)) return;
+                      y = fmaxf(y, 0.f);
+                      a.work[(int64_t)b * ROW + P_OFF + n] = y;
+                      a.xb[xb_off(b, P_OFF + n)] = __float2bfloat16_rn(y);
+                    });
+      pmark(7);
     }
     phase_end();
-    // ---- PRE2: p = relu(W1 . H1)
-    for (int task = c; task < nb8 * 8; task += G) {
-      const int b0 = (task >> 3) * 8, n0 = (task & 7) * 32, nb = min(8, a.B - b0);
-      gemv_task<32>(b0, nb, n0, PRE, 0, PRE, a.W1T, scratch, scratch + 8 * PRE,
-                [&](int b, int k) { return ldf(a.H1 + (int64_t)b * PRE + k); },
-                [&](int b, int n, float y) {
-                  if (!active(pc, b, gs)) return;
-                  y = fmaxf(y, 0.f);
-                  a.work[(int64_t)b * ROW + P_OFF + n] = y;
-                  a.xb[xb_off(b, P_OFF + n)] = __float2bfloat16_rn(y);
-                });
-    }
-    phase_end();
-    // ---- ATT gates + cell
-    if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen);
-    phase_end();
-    // ---- QUERY partials
-    for (int task = c; task < nb8 * 4 * QKS; task += G) {
-      const int z = task % QKS, nt = (task / QKS) % 4, b0 = (task / (QKS * 4)) * 8, nb = min(8, a.B - b0);
-      gemv_task<16>(b0, nb, nt * 32, ATT, z * (HID / QKS), (z + 1) * (HID / QKS), a.WqT, scratch,
-                scratch + 8 * (HID / QKS),
-                [&](int b, int k) { return ldf(a.work + (int64_t)b * ROW + ATTH_OFF + k); },
-                [&](int b, int n, float y) { a.Qp[((int64_t)z * a.B + b) * ATT + n] = y; });
-    }
+    // ---- ATT gates + cell + query partials
+    if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen, sm.locf);
     phase_end();
     // ---- ATT-A: the non-empty (item, chunk) tasks of the live items, dealt round-robin
     if (tid < 32) {  // task prefix over items: 8 items per lane, then a warp scan
@@ -773,18 +866,19 @@ __global__ void __launch_bounds__(NT, 1)
     for (int b = c; b < a.B; b += G)
       if (active(pc, b, gs)) att_combine(a, sm, gs, b, chunk);
     phase_end();
-    // ---- DEC gates + cell
-    if (gemm_cta) gate_phase<1>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen);
-    phase_end();
-    // ---- PROJ partials
-    for (int task = c; task < nb8 * 3 * PKS; task += G) {
-      const int z = task % PKS, nt = (task / PKS) % 3, b0 = (task / (PKS * 3)) * 8, nb = min(8, a.B - b0);
-      constexpr int KP = (HID + EMB) / PKS;  // 192
-      gemv_task<24>(b0, nb, nt * 32, NMEL + 1, z * KP, (z + 1) * KP, a.WpT, scratch, scratch + 8 * KP,
-                [&](int b, int k) {
-                  return ldf(a.work + (int64_t)b * ROW + (k < HID ? DECH_OFF + k : CTX_OFF + k - HID));
-                },
-                [&](int b, int n, float y) { a.Pp[((int64_t)z * a.B + b) * 81 + n] = y; });
+    // ---- DEC gates + cell + projection partials of dec_h; the other CTAs project the context
+    if (gemm_cta) gate_phase<1>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen, sm.locf);
+    {
+      const int c0 = G > GEMM_CTAS ? GEMM_CTAS : 0, nsp = G - c0;
+      if (c >= c0)
+        for (int task = c - c0; task < nb8 * 3; task += nsp) {
+          const int b0 = (task / 3) * 8, n0 = (task % 3) * 32, nb = min(8, a.B - b0);
+          gemv_task<EMB / NW>(b0, nb, n0, NMEL + 1, HID, HID + EMB, a.WpT, ringf, ringf + 8 * EMB,
+                              [&](int b, int k) { return ldf(a.work + (int64_t)b * ROW + CTX_OFF + k - HID); },
+                              [&](int b, int n, float y) {
+                                if (active(pc, b, gs)) a.Pp[((int64_t)NGRP * a.B + b) * 81 + n] = y;
+                              });
+        }
     }
     phase_end();
   }
@@ -794,9 +888,7 @@ __global__ void __launch_bounds__(NT, 1)
     for (int i = c * NT + tid; i < a.B * 81; i += G * NT) {
       const int b = i / 81, k = i % 81;
       if (!active(pc, b, gs - 1)) continue;
-      float m = __ldg(a.bp + k);
-#pragma unroll
-      for (int z = 0; z < PKS; ++z) m += ldf(a.Pp + ((int64_t)z * a.B + b) * 81 + k);
+      const float m = mel_value(b, k);
       const int64_t* p = a.plan + b * DPLAN;
       if (k < NMEL) {
         reinterpret_cast<float*>(p[6])[(gs - 1) * NMEL + k] = m;
@@ -807,7 +899,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
   }
   if (a.trace && c == 0 && tid == 0)
-    for (int i = 0; i < 8; ++i) a.trace[i] = tacc[i];
+    for (int i = 0; i < 5; ++i) a.trace[i] = tacc[i];
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (gemm_cta && (tid >> 5) == 1) {
@@ -819,14 +911,14 @@ __global__ void __launch_bounds__(NT, 1)
 }  // namespace
 
 // Debug: later itts_r_decode_persistent launches add per-phase wall time (ns, CTA 0, summed over
-// the steps) to buf[0..7]: PRE1, PRE2, ATT gates, QUERY, ATT-A, ATT-B, DEC gates, PROJ.  null = off.
+// the steps) to buf[0..4]: PRE, ATT gates (+query), ATT-A, ATT-B, DEC gates (+projection).  null = off.
 ITTS_API int itts_r_decode_debug_trace(void* buf) {
   g_dec_trace = static_cast<unsigned long long*>(buf);
   return ITTS_OK;
 }
 
 // Runs `nsteps` decoder steps for B gathered rows (see DecArgs).  Scratch buffers are owned by
-// the caller; `bar` (2 x u32) is zeroed here on the stream.  grid = min(#SMs, 148) CTAs.
+// the caller; `bar` (2 + 32 u32) is zeroed here on the stream.  grid = min(#SMs, 148) CTAs.
 ITTS_API int itts_r_decode_persistent(int32_t B, int32_t nsteps, const int64_t* plan, float* work, void* xb,
                                       const float* W0T, const float* W1T, const void* Wa, const float* ba,
                                       const void* Wd, const float* bd, const float* WqT, const float* WlocD,
@@ -850,7 +942,7 @@ ITTS_API int itts_r_decode_persistent(int32_t B, int32_t nsteps, const int64_t* 
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
-  cudaError_t e = cudaMemsetAsync(bar, 0, (2 + 32) * sizeof(unsigned), st);
+  cudaError_t e = cudaMemsetAsync(bar, 0, (2 + NGRP) * sizeof(unsigned), st);
   if (e != cudaSuccess) return (int)e;
   const int G = tcg::num_sms();
   void* args[] = {&a, &a_box_bytes};

@@ -30,6 +30,7 @@
 // so the two gate GEMM operands are contiguous column slices of one bf16
 // mirror: X_att = [p|ctx|att_h] (K=1792), X_dec = [ctx|att_h|dec_h] (K=2560).
 
+#include <algorithm>
 #include <cooperative_groups.h>
 #include <cuda_bf16.h>
 
@@ -789,6 +790,43 @@ ITTS_API int itts_r_mel_assemble(const int64_t* plan, int32_t n, int64_t max_row
 ITTS_API int itts_r_rowmap(const int64_t* plan, int32_t n, int64_t max_span, int32_t* row_out, void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
   k_rowmap<<<grid2(max_span, n), 256, 0, (cudaStream_t)stream>>>(plan, row_out);
+  ITTS_RETURN_LAUNCH();
+}
+
+// MRF branch merge: out = bf16(lrelu((y0 + y1 + y2) / 3, slope)), 8 bf16 per thread (16-byte
+// accesses).  The three branches' last ResBlock1 layers write their y independently, so they can
+// run concurrently; halo rows are zero in every input and stay zero.
+__global__ void __launch_bounds__(256) k_mrf_combine(const uint4* __restrict__ y0, const uint4* __restrict__ y1,
+                                                     const uint4* __restrict__ y2, int64_t n8, float slope,
+                                                     uint4* __restrict__ out) {
+  const float third = 1.0f / 3.0f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 a = __ldcs(y0 + i), b = __ldcs(y1 + i), c = __ldcs(y2 + i);
+    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
+    const __nv_bfloat162* pc = reinterpret_cast<const __nv_bfloat162*>(&c);
+    uint4 o;
+    __nv_bfloat162* po = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 fa = __bfloat1622float2(pa[j]), fb = __bfloat1622float2(pb[j]), fc = __bfloat1622float2(pc[j]);
+      float vx = ((fa.x + fb.x) + fc.x) * third, vy = ((fa.y + fb.y) + fc.y) * third;
+      vx = vx > 0.f ? vx : vx * slope;
+      vy = vy > 0.f ? vy : vy * slope;
+      po[j] = __floats2bfloat162_rn(vx, vy);
+    }
+    out[i] = o;
+  }
+}
+
+ITTS_API int itts_r_mrf_combine(const void* y0, const void* y1, const void* y2, int64_t n, float slope, void* out,
+                                void* stream) {
+  if (n < 0 || n % 8) return ITTS_EINVAL;
+  if (n == 0) return ITTS_OK;
+  const int64_t n8 = n / 8;
+  const int blocks = (int)std::min<int64_t>((n8 + 255) / 256, 148 * 8);
+  k_mrf_combine<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4*)y0, (const uint4*)y1, (const uint4*)y2, n8,
+                                                          slope, (uint4*)out);
   ITTS_RETURN_LAUNCH();
 }
 

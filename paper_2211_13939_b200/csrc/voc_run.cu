@@ -6,10 +6,12 @@
 // small pooled batches that host issue time (~20 us per launch) exceeded the
 // GPU time of the stack.  Here the whole sequence -- spliced-mel assembly,
 // conv_pre, the four transposed convs, 36 fused ResBlock1 layers with the three
-// MRF branches of a stage on three streams, halo re-zeroing -- is issued from
+// MRF branches of a stage on three streams and one merge pass per stage, halo
+// re-zeroing -- is issued from
 // C++ after one H2D copy of a packed plan that holds every row map and halo plan
 // of the call.  Work buffers are owned here (grow-only).  The arithmetic and
-// the order of every accumulation are those of the per-call path in tier_r.py.
+// the order of every accumulation are those of the per-call path in tier_r.py
+// (fused_mrf, native_vocoder=False).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -29,7 +31,7 @@ constexpr int kMelHalo = 3;   // conv_pre k7
 constexpr int kMrfHalo = 25;  // k11 dilation 5
 constexpr int kNumWeights = 2 * (1 + kStages + kStages * 3 * 3 * 2);  // (w, bias) pairs
 constexpr int kPlanPerItem = 9 * 5 + 4 * 3;                             // 9 row maps + 4 halo plans
-constexpr int ACC_NONE = 0, ACC_STORE = 1, ACC_ADD = 2, ACC_FINAL = 3;
+constexpr int ACC_NONE = 0, ACC_STORE = 1;
 
 struct Layout {
   std::vector<int64_t> rows, base;
@@ -76,7 +78,7 @@ struct Vocoder {
   const float* b[kNumWeights / 2];
   cudaStream_t side[2] = {nullptr, nullptr};
   cudaEvent_t ev_x = nullptr, ev_side[2] = {nullptr, nullptr}, ev_plan = nullptr;
-  DevBuf<uint16_t> x0, act_in, b16[10];
+  DevBuf<uint16_t> x0, act_in, b16[12];
   DevBuf<int32_t> rowmaps;
   DevBuf<int64_t> dplan;
   int64_t* hplan = nullptr;
@@ -251,33 +253,24 @@ struct Vocoder {
       if ((st = itts_r_zero_halo(z_plan[s], n, kMrfHalo, XA, C, stream))) return st;
       const int32_t* rms = rm[2 + 2 * s];
       const float slope_out = s < 3 ? 0.1f : 0.01f;
-      // MRF: three ResBlock1 branches; branch j's last layer sums into ACC in order STORE, ADD, FINAL
+      // MRF: three ResBlock1 branches, each writing its own y; one merge pass averages them.
+      // With multi_stream, branches 1 and 2 run on side streams concurrently with branch 0.
       uint16_t* ya[3] = {YA, b16[6].p, b16[8].p};
       uint16_t* tb[3] = {TB, b16[7].p, b16[9].p};
-      if (!multi_stream) {
-        for (int j = 0; j < 3; ++j) {
-          if ((st = resblock(s, j, 0, XA, L.total, rms, nullptr, ACC_NONE, YA, 0.1f, stream))) return st;
-          if ((st = resblock(s, j, 1, YA, L.total, rms, nullptr, ACC_NONE, TB, 0.1f, stream))) return st;
-          const int mode = j == 0 ? ACC_STORE : j == 1 ? ACC_ADD : ACC_FINAL;
-          if ((st = resblock(s, j, 2, TB, L.total, rms, ACC, mode, j == 2 ? OA : nullptr, slope_out, stream)))
-            return st;
-        }
-      } else {
-        if ((e = cudaEventRecord(ev_x, stream)) != cudaSuccess) return (int)e;
-        for (int j = 0; j < 3; ++j) {
-          cudaStream_t sj = j == 0 ? stream : side[j - 1];
-          if (j && (e = cudaStreamWaitEvent(sj, ev_x, 0)) != cudaSuccess) return (int)e;
-          if ((st = resblock(s, j, 0, XA, L.total, rms, nullptr, ACC_NONE, ya[j], 0.1f, sj))) return st;
-          if ((st = resblock(s, j, 1, ya[j], L.total, rms, nullptr, ACC_NONE, tb[j], 0.1f, sj))) return st;
-          if (j && (e = cudaEventRecord(ev_side[j - 1], sj)) != cudaSuccess) return (int)e;
-        }
-        for (int j = 0; j < 3; ++j) {
-          if (j && (e = cudaStreamWaitEvent(stream, ev_side[j - 1], 0)) != cudaSuccess) return (int)e;
-          const int mode = j == 0 ? ACC_STORE : j == 1 ? ACC_ADD : ACC_FINAL;
-          if ((st = resblock(s, j, 2, tb[j], L.total, rms, ACC, mode, j == 2 ? OA : nullptr, slope_out, stream)))
-            return st;
-        }
+      uint16_t* yo[3] = {ACC, b16[10].p, b16[11].p};
+      if (multi_stream && (e = cudaEventRecord(ev_x, stream)) != cudaSuccess) return (int)e;
+      for (int j = 0; j < 3; ++j) {
+        cudaStream_t sj = (j == 0 || !multi_stream) ? stream : side[j - 1];
+        if (sj != stream && (e = cudaStreamWaitEvent(sj, ev_x, 0)) != cudaSuccess) return (int)e;
+        if ((st = resblock(s, j, 0, XA, L.total, rms, nullptr, ACC_NONE, ya[j], 0.1f, sj))) return st;
+        if ((st = resblock(s, j, 1, ya[j], L.total, rms, nullptr, ACC_NONE, tb[j], 0.1f, sj))) return st;
+        if ((st = resblock(s, j, 2, tb[j], L.total, rms, yo[j], ACC_STORE, nullptr, 0.f, sj))) return st;
+        if (sj != stream && (e = cudaEventRecord(ev_side[j - 1], sj)) != cudaSuccess) return (int)e;
       }
+      if (multi_stream)
+        for (int j = 0; j < 2; ++j)
+          if ((e = cudaStreamWaitEvent(stream, ev_side[j], 0)) != cudaSuccess) return (int)e;
+      if ((st = itts_r_mrf_combine(yo[0], yo[1], yo[2], L.total * C, slope_out, OA, stream))) return st;
       act = OA;
       c_prev = C;
     }

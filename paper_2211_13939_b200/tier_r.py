@@ -280,7 +280,7 @@ class TierREngine:
         if self.native_vocoder:
             self._call("itts_r_voc_reserve", self._voc, max_batch, T, self._st())
         else:
-            for i in range(10):
+            for i in range(12):
                 self._buf(f"b16_{i}", biggest)
         self._buf("audio", max_batch * T * self.cfg.hop_samples, torch.float32)
         for name, m in (("rm0", 1), ("rmT0", 1), ("rm_s0", 8), ("rmT1", 8), ("rm_s1", 64), ("rmT2", 64),
@@ -613,37 +613,33 @@ class TierREngine:
             out.append((chunk, DeviceVocoderState(req, dst, emitted + counts[i])))
         return out
 
-    def _mrf_branches(self, s: int, XA, ACC, OA_next, scratch, rm, slope_out: float) -> None:
-        """One MRF stage with its three ResBlock1 branches on three streams.
-
-        Branch j's first two layers only read XA and write the branch's own ping-pong pair, so
-        branches 1 and 2 run on side streams concurrently with branch 0 on the engine stream;
-        the three last layers sum into ACC in branch order (STORE, ADD, FINAL) on the engine
-        stream, after waiting for the side branch that produced their input.  At small pooled
-        batches a layer fills only part of the GPU, so the stage's critical path drops from 9
-        layers to 5; the arithmetic (and the order of the ACC sum) is unchanged."""
+    def _mrf_branches(self, s: int, XA, OA_next, scratch, outs, rm, slope_out: float) -> None:
+        """One MRF stage: the three ResBlock1 branches each write their own y (last layer in
+        ACC_STORE mode), then one merge pass writes lrelu((y0 + y1 + y2) / 3).  With mrf_streams,
+        branches 1 and 2 run on side streams concurrently with branch 0 (same arithmetic): at small
+        pooled batches a layer fills only part of the GPU, so the stage's critical path drops from
+        9 layers to 3 plus the merge."""
         main = self.stream
         ev_x, ev_1, ev_2 = self._ev
-        ev_x.record(main)
-        tails = []
+        if self.mrf_streams:
+            ev_x.record(main)
         for j, layers in enumerate(self.res[s]):
             ya, tb = scratch[j]
-            st = main if j == 0 else self._side[j - 1]
-            if j:
+            st = main if j == 0 or not self.mrf_streams else self._side[j - 1]
+            if st is not main:
                 st.wait_event(ev_x)
-            (c1a, c2a), (c1b, c2b) = layers[0], layers[1]
+            (c1a, c2a), (c1b, c2b), (c1c, c2c) = layers
             self._resblock(XA, c1a, c2a, W.HG_RES_DILATIONS[0], rm, stream=st, act_out=ya, slope=0.1)
             self._resblock(ya, c1b, c2b, W.HG_RES_DILATIONS[1], rm, stream=st, act_out=tb, slope=0.1)
-            if j:
+            self._resblock(tb, c1c, c2c, W.HG_RES_DILATIONS[2], rm, stream=st, acc=outs[j],
+                           acc_mode=tc.ACC_STORE, slope=0.0)
+            if st is not main:
                 (ev_1, ev_2)[j - 1].record(st)
-            tails.append(tb)
-        for j, layers in enumerate(self.res[s]):
-            if j:
-                main.wait_event((ev_1, ev_2)[j - 1])
-            c1, c2 = layers[2]
-            mode = (tc.ACC_STORE, tc.ACC_ADD, tc.ACC_FINAL)[j]
-            self._resblock(tails[j], c1, c2, W.HG_RES_DILATIONS[2], rm, acc=ACC, acc_mode=mode,
-                           act_out=OA_next if j == 2 else None, slope=slope_out)
+        if self.mrf_streams:
+            main.wait_event(ev_1)
+            main.wait_event(ev_2)
+        self._call("itts_r_mrf_combine", outs[0].data_ptr(), outs[1].data_ptr(), outs[2].data_ptr(),
+                   outs[0].numel(), slope_out, OA_next.data_ptr(), self._st())
 
     def _hifigan(self, Ts: list[int], lay0: _Layout, d_mplan: torch.Tensor) -> torch.Tensor:
         """HiFi-GAN V1 over a packed batch of spliced chunks -> stage-4 bf16 act (lrelu 0.01 applied)."""
@@ -652,7 +648,7 @@ class TierREngine:
             x4 = ctypes.c_void_p()
             self._call("itts_r_voc_run", self._voc, n, np.ascontiguousarray(Ts, np.int32).ctypes.data,
                        d_mplan.data_ptr(), int(self.mrf_streams), ctypes.byref(x4), st)
-            self.launches += 54   # 9 row maps, mel assembly, conv_pre, 4 x (convT, halo, 9 ResBlock layers)
+            self.launches += 58   # 9 row maps, mel assembly, conv_pre, 4 x (convT, halo, 9 ResBlock layers, merge)
             return x4.value
         with torch.cuda.stream(self.stream):
             x0 = self._buf("x0", lay0.total * 128, zero=True).view(lay0.total, 128)
@@ -666,8 +662,8 @@ class TierREngine:
             layouts.append(_Layout([T * mult for T in Ts], MRF_HALO))
         biggest = max(l.total * c for l, c in zip(layouts, STAGE_C))
         # bf16 only: the residual stream is kept as lrelu(y, 0.1) and inverted on load
-        # xa ya tb acc oa oa' (+ ya/tb of MRF branches 1 and 2 when they run on side streams)
-        b16 = [self._buf(f"b16_{i}", biggest) for i in range(10 if self.fused_mrf and self.mrf_streams else 6)]
+        # xa ya tb acc oa oa' (+ ya/tb/y of MRF branches 1 and 2 in the fused path)
+        b16 = [self._buf(f"b16_{i}", biggest) for i in range(12 if self.fused_mrf else 6)]
         for s, (u, lay) in enumerate(zip(UPS, layouts)):
             C = STAGE_C[s]
             view = lambda t: t[:lay.total * C].view(lay.total, C)
@@ -680,25 +676,10 @@ class TierREngine:
             self._call("itts_r_zero_halo", self._up(zplan).data_ptr(), n, lay.halo, XA.data_ptr(), C, st)
             rm = self._rowmap(lay, lay.first, 1, f"rm_s{s}")
             slope_out = 0.1 if s < 3 else 0.01
-            if self.fused_mrf and self.mrf_streams:
-                self._mrf_branches(s, XA, ACC, OA_next, [(YA, TB)] + [(view(b16[6 + 2 * j]), view(b16[7 + 2 * j]))
-                                                                      for j in range(2)], rm, slope_out)
-                prev, act_in = lay, OA_next
-                continue
             if self.fused_mrf:
-                # one fused kernel per ResBlock1 layer; ping-pong YA/TB (a layer must not write its input)
-                for j, layers in enumerate(self.res[s]):
-                    src = XA
-                    for m, (c1, c2) in enumerate(layers):
-                        dil = W.HG_RES_DILATIONS[m]
-                        if m < 2:
-                            dst = YA if m == 0 else TB
-                            self._resblock(src, c1, c2, dil, rm, act_out=dst, slope=0.1)
-                            src = dst
-                        else:
-                            mode = (tc.ACC_STORE, tc.ACC_ADD, tc.ACC_FINAL)[j]
-                            self._resblock(src, c1, c2, dil, rm, acc=ACC, acc_mode=mode,
-                                           act_out=OA_next if j == 2 else None, slope=slope_out)
+                self._mrf_branches(s, XA, OA_next, [(YA, TB)] + [(view(b16[6 + 2 * j]), view(b16[7 + 2 * j]))
+                                                                 for j in range(2)],
+                                   [ACC, view(b16[10]), view(b16[11])], rm, slope_out)
                 prev, act_in = lay, OA_next
                 continue
             for j, layers in enumerate(self.res[s]):
@@ -765,8 +746,10 @@ class _DecBuffers:
         self.work = torch.empty(n, ROW, dtype=torch.float32, device=dev)
         self.xbm = torch.empty(n, XB_ROW, dtype=torch.bfloat16, device=dev)
         self.G = torch.empty(DEC_KSPLIT, n, 4096, dtype=torch.float32, device=dev)
-        self.Q = torch.empty(8, n, 128, dtype=torch.float32, device=dev)    # query K-slice partials
-        self.P = torch.empty(8, n, 81, dtype=torch.float32, device=dev)     # projection K-slice partials
+        # query / projection partials: 8 K-slices (per-kernel chain) or 32 unit groups (+1 context
+        # projection) in the persistent decoder
+        self.Q = torch.empty(32, n, 128, dtype=torch.float32, device=dev)
+        self.P = torch.empty(33, n, 81, dtype=torch.float32, device=dev)
         self.H1 = torch.empty(n, 256, dtype=torch.float32, device=dev)
         self.dev, self.xb2, self.U, self.AP, self.bar, self.Gp = dev, None, None, None, None, None
 

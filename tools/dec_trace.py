@@ -22,7 +22,7 @@ args = ap.parse_args()
 eng = TierREngine(PipelineConfig(), "cuda:0")
 eng.use_graphs = False
 lex = default_lexicon()
-names = ["PRE1", "PRE2", "ATT gates", "QUERY", "ATT-A", "ATT-B", "DEC gates", "PROJ"]
+names = ["PRE", "ATT gates+q", "ATT-A", "ATT-B", "DEC gates+proj"]
 for B in [int(x) for x in args.batches.split(",")]:
     rng = random.Random(B)
     fos = [run_frontend(random_text(rng, 20, 200, lex), lex) for _ in range(B)]
@@ -40,10 +40,11 @@ for B in [int(x) for x in args.batches.split(",")]:
     t = buf.cpu().tolist()
     print(f"B={B}: chunk {e0.elapsed_time(e1):.3f} ms; per step (us): " +
           ", ".join(f"{n} {t[i] / 32e3:.1f}" for i, n in enumerate(names)))
+    print(f"   PRE CTA0 (us): mel partials {t[5] / 32e3:.2f}, H1 {t[6] / 32e3:.2f}, p gemv {t[7] / 32e3:.2f}")
     for m, nm in ((0, "ATT"), (1, "DEC")):
-        g = [t[16 + 8 * m + i] / 32e3 for i in range(6)]
+        g = [t[16 + 8 * m + i] / 32e3 for i in range(7)]
         print(f"   {nm} gates CTA0 (us from phase start): producer issued {g[0]:.1f}, first stage {g[1]:.1f}, "
-              f"MMA done {g[2]:.1f}, acc ready {g[3]:.1f}, epilogue done {g[4]:.1f}; MMA waited on data {g[5]:.1f}")
+              f"MMA done {g[2]:.1f}, acc ready {g[3]:.1f}, group synced {g[4]:.1f}, cells {g[6]:.1f}, partials {g[5]:.1f}")
     if t[13]:
         sub = ["q/w loads", "bulk wait", "energies", "softmax", "context+store"]
         print(f"   ATT-A CTA0: {t[13] / 32:.1f} tasks/step; per task (us): " +
