@@ -15,12 +15,17 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "common.cuh"
 
 namespace {
+
+int g_fail_line = 0;
+#define FAIL_AT(x) (g_fail_line = __LINE__, (x))
 
 constexpr int kStages = 4;
 constexpr int kUps[kStages] = {8, 8, 2, 2};
@@ -170,15 +175,15 @@ struct Vocoder {
     std::vector<int64_t> Ts(Ts_in, Ts_in + n);
     int64_t maxT = 0;
     for (int64_t T : Ts) {
-      if (T < 1) return ITTS_EINVAL;
+      if (T < 1) return FAIL_AT(ITTS_EINVAL);
       maxT = std::max(maxT, T);
     }
     size_t rows0, big, rm_total;
     stage_rows(Ts, &rows0, &big, &rm_total);
     const size_t plan_n = (size_t)n * kPlanPerItem;
     int st = grow_all(stream, rows0, big, rm_total, plan_n);
-    if (st) return st;
-    if ((st = host_plan(plan_n))) return st;
+    if (st) return FAIL_AT(st);
+    if ((st = host_plan(plan_n))) return FAIL_AT(st);
 
     Layout lay[kStages + 1];
     lay[0].build(Ts, kMelHalo);
@@ -226,20 +231,20 @@ struct Vocoder {
     }
     cudaError_t e = cudaMemcpyAsync(dplan.p, hplan, (size_t)(hp - hplan) * sizeof(int64_t), cudaMemcpyHostToDevice,
                                     stream);
-    if (e != cudaSuccess) return (int)e;
-    if ((e = cudaEventRecord(ev_plan, stream)) != cudaSuccess) return (int)e;
+    if (e != cudaSuccess) return FAIL_AT((int)e);
+    if ((e = cudaEventRecord(ev_plan, stream)) != cudaSuccess) return FAIL_AT((int)e);
     plan_pending = true;
 
     int32_t* rm[9];
     for (int k = 0; k < 9; ++k) {
       rm[k] = rowmaps.p + rm_off[k];
-      if ((st = itts_r_rowmap(rm_plan[k], n, rm_span[k], rm[k], stream))) return st;
+      if ((st = itts_r_rowmap(rm_plan[k], n, rm_span[k], rm[k], stream))) return FAIL_AT(st);
     }
     // spliced mel -> conv_pre -> lrelu(0.1)
     if ((e = cudaMemsetAsync(x0.p, 0, (size_t)lay[0].total * 128 * sizeof(uint16_t), stream)) != cudaSuccess)
-      return (int)e;
-    if ((st = itts_r_mel_assemble(d_mplan, n, maxT, x0.p, 128, stream))) return st;
-    if ((st = conv(x0.p, lay[0].total, 128, 0, 512, 7, 1, 512, rm[0], act_in.p, 0.1f, 1, stream))) return st;
+      return FAIL_AT((int)e);
+    if ((st = itts_r_mel_assemble(d_mplan, n, maxT, x0.p, 128, stream))) return FAIL_AT(st);
+    if ((st = conv(x0.p, lay[0].total, 128, 0, 512, 7, 1, 512, rm[0], act_in.p, 0.1f, 1, stream))) return FAIL_AT(st);
 
     const void* act = act_in.p;
     int c_prev = 512;
@@ -249,8 +254,8 @@ struct Vocoder {
       uint16_t *XA = b16[0].p, *YA = b16[1].p, *TB = b16[2].p, *ACC = b16[3].p, *OA = b16[4 + s % 2].p;
       // transposed conv: each input row -> u output rows, then re-zero the output halos
       if ((st = conv(act, lay[s].total, c_prev, 1 + s, u * C, 3, 1, C, rm[1 + 2 * s], XA, 0.1f, 0, stream)))
-        return st;
-      if ((st = itts_r_zero_halo(z_plan[s], n, kMrfHalo, XA, C, stream))) return st;
+        return FAIL_AT(st);
+      if ((st = itts_r_zero_halo(z_plan[s], n, kMrfHalo, XA, C, stream))) return FAIL_AT(st);
       const int32_t* rms = rm[2 + 2 * s];
       const float slope_out = s < 3 ? 0.1f : 0.01f;
       // MRF: three ResBlock1 branches, each writing its own y; one merge pass averages them.
@@ -258,19 +263,19 @@ struct Vocoder {
       uint16_t* ya[3] = {YA, b16[6].p, b16[8].p};
       uint16_t* tb[3] = {TB, b16[7].p, b16[9].p};
       uint16_t* yo[3] = {ACC, b16[10].p, b16[11].p};
-      if (multi_stream && (e = cudaEventRecord(ev_x, stream)) != cudaSuccess) return (int)e;
+      if (multi_stream && (e = cudaEventRecord(ev_x, stream)) != cudaSuccess) return FAIL_AT((int)e);
       for (int j = 0; j < 3; ++j) {
         cudaStream_t sj = (j == 0 || !multi_stream) ? stream : side[j - 1];
-        if (sj != stream && (e = cudaStreamWaitEvent(sj, ev_x, 0)) != cudaSuccess) return (int)e;
-        if ((st = resblock(s, j, 0, XA, L.total, rms, nullptr, ACC_NONE, ya[j], 0.1f, sj))) return st;
-        if ((st = resblock(s, j, 1, ya[j], L.total, rms, nullptr, ACC_NONE, tb[j], 0.1f, sj))) return st;
-        if ((st = resblock(s, j, 2, tb[j], L.total, rms, yo[j], ACC_STORE, nullptr, 0.f, sj))) return st;
-        if (sj != stream && (e = cudaEventRecord(ev_side[j - 1], sj)) != cudaSuccess) return (int)e;
+        if (sj != stream && (e = cudaStreamWaitEvent(sj, ev_x, 0)) != cudaSuccess) return FAIL_AT((int)e);
+        if ((st = resblock(s, j, 0, XA, L.total, rms, nullptr, ACC_NONE, ya[j], 0.1f, sj))) return FAIL_AT(st);
+        if ((st = resblock(s, j, 1, ya[j], L.total, rms, nullptr, ACC_NONE, tb[j], 0.1f, sj))) return FAIL_AT(st);
+        if ((st = resblock(s, j, 2, tb[j], L.total, rms, yo[j], ACC_STORE, nullptr, 0.f, sj))) return FAIL_AT(st);
+        if (sj != stream && (e = cudaEventRecord(ev_side[j - 1], sj)) != cudaSuccess) return FAIL_AT((int)e);
       }
       if (multi_stream)
         for (int j = 0; j < 2; ++j)
-          if ((e = cudaStreamWaitEvent(stream, ev_side[j], 0)) != cudaSuccess) return (int)e;
-      if ((st = itts_r_mrf_combine(yo[0], yo[1], yo[2], L.total * C, slope_out, OA, stream))) return st;
+          if ((e = cudaStreamWaitEvent(stream, ev_side[j], 0)) != cudaSuccess) return FAIL_AT((int)e);
+      if ((st = itts_r_mrf_combine(yo[0], yo[1], yo[2], L.total * C, slope_out, OA, stream))) return FAIL_AT(st);
       act = OA;
       c_prev = C;
     }
@@ -329,7 +334,9 @@ ITTS_API int itts_r_voc_reserve(void* handle, int32_t n, int32_t frames, void* s
 ITTS_API int itts_r_voc_run(void* handle, int32_t n, const int32_t* frames, const int64_t* mel_plan,
                             int32_t multi_stream, void** x4_out, void* stream) {
   if (!handle || n < 1 || !frames || !mel_plan || !x4_out) return ITTS_EINVAL;
-  return static_cast<Vocoder*>(handle)->run(n, frames, mel_plan, multi_stream, x4_out, (cudaStream_t)stream);
+  const int st = static_cast<Vocoder*>(handle)->run(n, frames, mel_plan, multi_stream, x4_out, (cudaStream_t)stream);
+  if (st && getenv("ITTS_DEBUG")) fprintf(stderr, "itts_r_voc_run: status %d at line %d\n", st, g_fail_line);
+  return st;
 }
 
 ITTS_API int itts_r_voc_destroy(void* handle) {

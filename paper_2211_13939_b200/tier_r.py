@@ -646,8 +646,9 @@ class TierREngine:
         dev, st, n = self.device, self._st(), len(Ts)
         if self.native_vocoder and self.fused_mrf:
             x4 = ctypes.c_void_p()
-            self._call("itts_r_voc_run", self._voc, n, np.ascontiguousarray(Ts, np.int32).ctypes.data,
-                       d_mplan.data_ptr(), int(self.mrf_streams), ctypes.byref(x4), st)
+            frames = np.ascontiguousarray(Ts, np.int32)   # must outlive the call (raw pointer below)
+            self._call("itts_r_voc_run", self._voc, n, frames.ctypes.data, d_mplan.data_ptr(),
+                       int(self.mrf_streams), ctypes.byref(x4), st)
             self.launches += 58   # 9 row maps, mel assembly, conv_pre, 4 x (convT, halo, 9 ResBlock layers, merge)
             return x4.value
         with torch.cuda.stream(self.stream):

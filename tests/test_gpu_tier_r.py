@@ -219,3 +219,13 @@ def test_native_vocoder_sequence_equals_python_launches(engine, sizes):
     for key, outs in got.items():
         for a, b in zip(outs, want):
             assert np.array_equal(a, b), key
+
+
+def test_native_vocoder_large_pool(engine):
+    """A 256-chunk pooled call through voc_run (host frame table, grown work buffers) matches solo calls."""
+    rng = np.random.default_rng(9)
+    triples = [(VocoderState.initial(), MelChunk(rng.uniform(-0.2, 0.2, (32, 80))), False) for _ in range(256)]
+    batched = engine.vocoder_batch(triples)
+    for i in (0, 131, 255):
+        (solo, _), = engine.vocoder_batch([triples[i]])
+        assert np.array_equal(batched[i][0].samples, solo.samples)

@@ -26,7 +26,7 @@ ap.add_argument("--seconds", type=float, default=10)
 args = ap.parse_args()
 cfg, lex = PipelineConfig(), default_lexicon()
 eng = build_engine(cfg, "r", "cuda:0")
-eng.prepare_graphs(max_batch=256)
+eng.prepare_graphs(max_batch=512)
 base = modules_for(eng, lex)
 cur = {}
 
