@@ -52,7 +52,7 @@ GRAPH_MAX_L = 8192  # attention smem is sized for this in captured graphs; longe
 HID = 1024
 XB2 = 4864          # persistent decoder's bf16 mirror row (two banks of att_h / dec_h)
 PERSIST_MAX_L = 8192  # 256 attention chunks of <= 32 positions
-PERSIST_MAX_B = 192   # above this the per-kernel chain (tc_conv gate GEMMs + cluster attention) is faster
+PERSIST_MAX_B = 256   # kernel limit (MMA N, attention task table); larger pools use the per-kernel chain
 
 
 def _hifigan_macs_per_frame() -> int:

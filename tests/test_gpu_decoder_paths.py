@@ -33,7 +33,7 @@ def texts(n, seed, lo=20, hi=200):
     return ["".join(rng.choice(singles) for _ in range(rng.randint(lo, hi))) for _ in range(n)]
 
 
-@pytest.mark.parametrize("B", [1, 16, 100, 150, 192])
+@pytest.mark.parametrize("B", [1, 16, 100, 192, 256])
 def test_persistent_matches_chain(engine, B):
     lex = default_lexicon()
     encs = engine.encoder_batch([run_frontend(t, lex) for t in texts(B, B)])
