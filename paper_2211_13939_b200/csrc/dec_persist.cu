@@ -220,6 +220,29 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
   uint8_t* sW = ring;
   uint8_t* sX = ring + nst * GW_TILE;
   ++grp_gen;
+  // Loads that do not depend on this phase's GEMM, issued now so their latency hides behind the
+  // GEMM and the group sync: the group's slice of the next linear layer (query / projection)
+  // and, for the first fixup round, the gate biases and cell states.
+  constexpr int NP = MODE == 0 ? ATT : NMEL + 1;
+  const int pn = threadIdx.x & 127;
+  float wq[32];
+  const int nmine = (a.B - ks + KSPLIT - 1) / KSPLIT;
+  const int c_off = MODE == 0 ? ATTC_OFF : DECC_OFF;
+  const float* bias = (MODE == 0 ? a.ba : a.bd) + ug * 128;
+  float4 pre_b[4];
+  float pre_c[4];
+  auto prefetch = [&]() {  // issued by each warp after its GEMM-critical work
+#pragma unroll
+    for (int u = 0; u < 32; ++u)
+      wq[u] = pn < NP ? __ldg((MODE == 0 ? a.WqT : a.WpT) + ((int64_t)ug * 32 + u) * NP + pn) : 0.f;
+#pragma unroll
+    for (int z = 0; z < 4; ++z) {
+      const int e = threadIdx.x + z * NT, b = ks + KSPLIT * (e >> 5), ul = e & 31;
+      const bool live = e < 32 * nmine && active(pc, b, s);
+      pre_b[z] = live ? __ldg(reinterpret_cast<const float4*>(bias + ul * 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      pre_c[z] = live ? ldf(a.work + (int64_t)b * ROW + c_off + ug * 32 + ul) : 0.f;
+    }
+  };
   if (warp == 0 || warp == 2 || warp == 3) {
     if (lane == 0) {
       const uint32_t pi = warp == 0 ? 0 : warp - 1;
@@ -245,6 +268,7 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       }
       if (pi == 0) mark(0);
     }
+    prefetch();
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n16 >> 3) << 17) | ((128u >> 4) << 24);
@@ -265,7 +289,9 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       tcg::umma_commit(&gsy.accf);
       mark(2);
     }
+    prefetch();
   } else {
+    prefetch();
     // epilogue warps 4..7: TMEM lanes 32q.. = gate rows; columns = items -> K-split partial
     const int q = warp & 3, r = q * 32 + lane;
     float* part = a.Gp + ((int64_t)ks * GEMM_CTAS / KSPLIT + ug) * n16 * 128;  // [ks][ug][item][row]
@@ -299,10 +325,8 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
   {
     // fixup (all 256 threads): this CTA finishes all 32 units of the group for items b = ks + 4i;
     // 4 cells per thread in flight (partials + c state loaded before any arithmetic)
-    const float* bias = (MODE == 0 ? a.ba : a.bd) + ug * 128;
-    const int h_off = MODE == 0 ? ATTH_OFF : DECH_OFF, c_off = MODE == 0 ? ATTC_OFF : DECC_OFF;
+    const int h_off = MODE == 0 ? ATTH_OFF : DECH_OFF;
     const int hb_off = MODE == 0 ? att_off(newb) : dec_off(newb);
-    const int nmine = (a.B - ks + KSPLIT - 1) / KSPLIT;
     for (int e0 = threadIdx.x; e0 < 32 * nmine; e0 += 4 * NT) {
       float4 gs4[4];
       float cold[4];
@@ -314,7 +338,8 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
         gs4[z] = make_float4(0.f, 0.f, 0.f, 0.f);
         cold[z] = 0.f;
         if (!live[z]) continue;
-        gs4[z] = __ldg(reinterpret_cast<const float4*>(bias + ul * 4));
+        const bool first = e0 == (int)threadIdx.x;  // prefetched before the GEMM
+        gs4[z] = first ? pre_b[z] : __ldg(reinterpret_cast<const float4*>(bias + ul * 4));
 #pragma unroll
         for (int k2 = 0; k2 < KSPLIT; ++k2) {
           const float4 pv = __ldcg(reinterpret_cast<const float4*>(
@@ -324,7 +349,7 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
           gs4[z].z += pv.z;
           gs4[z].w += pv.w;
         }
-        cold[z] = ldf(a.work + (int64_t)b * ROW + c_off + j);
+        cold[z] = first ? pre_c[z] : ldf(a.work + (int64_t)b * ROW + c_off + j);
       }
 #pragma unroll
       for (int z = 0; z < 4; ++z) {
@@ -347,14 +372,11 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
     if (threadIdx.x == 0) mark(6);
     // this group's share of the next linear layer: query (MODE 0, 128 outputs) or the mel/gate
     // projection of dec_h (MODE 1, 81 outputs); 32-term dot products in unit order
-    constexpr int N = MODE == 0 ? ATT : NMEL + 1;
-    const int n = threadIdx.x & 127, half = threadIdx.x >> 7;
+    constexpr int N = NP;
+    const int n = pn, half = threadIdx.x >> 7;
     if (n < N) {
-      const float* W = (MODE == 0 ? a.WqT : a.WpT) + (int64_t)ug * 32 * N + n;
       float* out = (MODE == 0 ? a.Qp : a.Pp) + (int64_t)ug * a.B * N + n;
-      float w[32];
-#pragma unroll
-      for (int u = 0; u < 32; ++u) w[u] = __ldg(W + u * N);
+      const float* w = wq;
       for (int i = half; i < nmine; i += 2) {
         const int b = ks + KSPLIT * i;
         if (!active(pc, b, s)) continue;

@@ -475,7 +475,24 @@ __global__ void k_enc_embed(const int32_t* __restrict__ tok4, int64_t total, con
 // One 8-CTA cluster per (item, direction).  CTA r owns hidden units
 // [32r, 32r+32): gate rows {g*256 + 32r + u}.  WhhT [2][256 k][1024 rows].
 // PRE [rows][2048] = x . W_ih^T + b_ih + b_hh for both directions.
+// Thread (row r, K half) keeps its 128 recurrent weights in registers.  The 32 new h values of a
+// CTA go to every CTA of the cluster with st.async, which completes bytes on the receiver's
+// mbarrier: a step waits only for the 1 KB of h it needs (double-buffered), no cluster barrier.
 constexpr int BL_CLUSTER = 8, BL_UNITS = EH / BL_CLUSTER, BL_ROWS = 4 * BL_UNITS;
+
+__device__ __forceinline__ uint32_t cl_smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t cl_map(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cl_mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}" ::"r"(bar), "r"(parity) : "memory");
+}
 
 __global__ void __cluster_dims__(BL_CLUSTER, 1, 1) __launch_bounds__(256, 1)
     k_bilstm(const float* __restrict__ PRE, const int64_t* __restrict__ plan, const float* __restrict__ WhhT) {
@@ -488,21 +505,31 @@ __global__ void __cluster_dims__(BL_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   float* mem = reinterpret_cast<float*>(p[3]);
   const int tid = threadIdx.x;
 
-  extern __shared__ float wsm[];               // [256 k][128 rows] for this CTA's gate rows
-  __shared__ float hbuf[2][EH];
+  __shared__ __align__(16) float hbuf[2][EH];
   __shared__ float gpart[2][BL_ROWS];
   __shared__ float cst[BL_UNITS];
+  __shared__ __align__(8) uint64_t hbar[2];
   const float* Wd = WhhT + (int64_t)dir * EH * 4 * EH;  // this direction's [256 k][1024 rows]
-  for (int i = tid; i < EH * BL_ROWS; i += 256) {
-    const int k = i / BL_ROWS, r = i % BL_ROWS;
-    const int grow = (r / BL_UNITS) * EH + rank * BL_UNITS + (r % BL_UNITS);
-    wsm[i] = Wd[(int64_t)k * (4 * EH) + grow];
-  }
+  const int r = tid % BL_ROWS, half = tid / BL_ROWS;    // 2 K-halves of 128
+  const int grow = (r / BL_UNITS) * EH + rank * BL_UNITS + (r % BL_UNITS);
+  float w[128];
+#pragma unroll
+  for (int k = 0; k < 128; ++k) w[k] = __ldg(Wd + (int64_t)(half * 128 + k) * (4 * EH) + grow);
   for (int i = tid; i < EH; i += 256) hbuf[0][i] = 0.f;
   if (tid < BL_UNITS) cst[tid] = 0.f;
+  const uint32_t bar0 = cl_smem_u32(&hbar[0]);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   cluster.sync();
+  auto expect = [&](int b) {  // this CTA's next phase of hbar[b] receives 8 x 32 h values
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar0 + 8 * b), "r"(EH * 4)
+                 : "memory");
+  };
+  if (tid == 0 && L > 1) expect(1);  // h_1
 
-  const int r = tid % BL_ROWS, half = tid / BL_ROWS;  // 2 K-halves of 128
   // the input projection of step s+1 does not depend on h: load it while step s computes
   float4 pre_n = make_float4(0.f, 0.f, 0.f, 0.f);
   auto load_pre = [&](int64_t s) {
@@ -516,16 +543,24 @@ __global__ void __cluster_dims__(BL_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   load_pre(0);
   for (int64_t s = 0; s < L; ++s) {
     const int64_t t = dir ? L - 1 - s : s;
-    const float* h = hbuf[s & 1];
+    const int cur = (int)(s & 1);
+    if (s > 0) {
+      cl_mbar_wait(bar0 + 8 * cur, (uint32_t)((s - 1) >> 1) & 1u);
+      if (tid == 0 && s + 2 < L) expect(cur);  // h_{s+2} lands in this buffer next
+    } else if (tid == 0 && L > 2) {
+      expect(0);  // h_2
+    }
+    const float4* h4 = reinterpret_cast<const float4*>(hbuf[cur] + half * 128);
     const float4 pre_c = pre_n;
     load_pre(s + 1);
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;  // four independent FMA chains
-#pragma unroll 8
-    for (int k = half * 128; k < half * 128 + 128; k += 4) {
-      a0 = fmaf(wsm[k * BL_ROWS + r], h[k], a0);
-      a1 = fmaf(wsm[(k + 1) * BL_ROWS + r], h[k + 1], a1);
-      a2 = fmaf(wsm[(k + 2) * BL_ROWS + r], h[k + 2], a2);
-      a3 = fmaf(wsm[(k + 3) * BL_ROWS + r], h[k + 3], a3);
+#pragma unroll
+    for (int k4 = 0; k4 < 32; ++k4) {
+      const float4 h = h4[k4];
+      a0 = fmaf(w[4 * k4], h.x, a0);
+      a1 = fmaf(w[4 * k4 + 1], h.y, a1);
+      a2 = fmaf(w[4 * k4 + 2], h.z, a2);
+      a3 = fmaf(w[4 * k4 + 3], h.w, a3);
     }
     gpart[half][r] = (a0 + a1) + (a2 + a3);
     __syncthreads();
@@ -539,12 +574,19 @@ __global__ void __cluster_dims__(BL_CLUSTER, 1, 1) __launch_bounds__(256, 1)
       const float hn = sigm(go) * tanhf(c);
       cst[u] = c;
       mem[t * EMB + dir * EH + j] = hn;
-      float* nxt = hbuf[(s + 1) & 1];
+      if (s + 1 < L) {
+        const uint32_t dst = cl_smem_u32(&hbuf[cur ^ 1][j]), bar = bar0 + 8 * (cur ^ 1);
 #pragma unroll
-      for (int q = 0; q < BL_CLUSTER; ++q) cluster.map_shared_rank(nxt, q)[j] = hn;
+        for (int q = 0; q < BL_CLUSTER; ++q)
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                           cl_map(dst, q)),
+                       "r"(__float_as_uint(hn)), "r"(cl_map(bar, q))
+                       : "memory");
+      }
     }
-    cluster.sync();
+    __syncthreads();  // gpart / cst reuse
   }
+  cluster.sync();  // no CTA leaves while a peer may still address its shared memory
 }
 
 // pm[t][a] = sum_k mem[t][k] WmT[k][a]; 16 rows per block.
@@ -763,13 +805,7 @@ ITTS_API int itts_r_enc_embed(const int32_t* tok4, int64_t total, const int64_t*
 
 ITTS_API int itts_r_bilstm(const float* PRE, const int64_t* plan, int32_t n, const float* WhhT, void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
-  const size_t smem = (size_t)EH * BL_ROWS * sizeof(float);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_bilstm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
-  k_bilstm<<<n * 2 * BL_CLUSTER, 256, smem, (cudaStream_t)stream>>>(PRE, plan, WhhT);
+  k_bilstm<<<n * 2 * BL_CLUSTER, 256, 0, (cudaStream_t)stream>>>(PRE, plan, WhhT);
   ITTS_RETURN_LAUNCH();
 }
 

@@ -31,14 +31,17 @@ for B in [int(x) for x in args.batches.split(",")]:
     torch.cuda.synchronize()
     buf = torch.zeros(32, dtype=torch.int64, device="cuda")
     _native.call("itts_r_decode_debug_trace", buf.data_ptr())
+    REPS = 4
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(eng.stream)
-    eng.decoder_batch([(st, enc) for enc, st in encs])
+    for _ in range(REPS):
+        eng.decoder_batch([(st, enc) for enc, st in encs])
     e1.record(eng.stream)
     torch.cuda.synchronize()
     _native.call("itts_r_decode_debug_trace", None)
-    t = buf.cpu().tolist()
-    print(f"B={B}: chunk {e0.elapsed_time(e1):.3f} ms; per step (us): " +
+    raw = buf.cpu().tolist()
+    t = raw[:5] + [v / REPS for v in raw[5:]]   # phase totals are per launch (last one); the rest accumulate
+    print(f"B={B}: chunk {e0.elapsed_time(e1) / REPS:.3f} ms; per step (us): " +
           ", ".join(f"{n} {t[i] / 32e3:.1f}" for i, n in enumerate(names)))
     print(f"   PRE CTA0 (us): mel partials {t[5] / 32e3:.2f}, H1 {t[6] / 32e3:.2f}, p gemv {t[7] / 32e3:.2f}")
     for m, nm in ((0, "ATT"), (1, "DEC")):
