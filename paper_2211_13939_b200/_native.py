@@ -9,6 +9,7 @@ CPU or eager-PyTorch implementation.
 from __future__ import annotations
 
 import ctypes
+import os
 import re
 from functools import lru_cache
 from pathlib import Path
@@ -67,10 +68,12 @@ def header_symbols() -> list[str]:
 
 @lru_cache(maxsize=1)
 def lib() -> ctypes.CDLL:
-    if not LIB_PATH.exists():
-        raise NativeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+    # ITTS_LIB: an alternative build of the same library (A/B timing tools only)
+    path = Path(os.environ.get("ITTS_LIB", LIB_PATH))
+    if not path.exists():
+        raise NativeError(f"{path} is missing: run __graft_entry__.build() "
                           "(no CPU fallback exists for the GPU modules)")
-    handle = ctypes.CDLL(str(LIB_PATH))
+    handle = ctypes.CDLL(str(path))
     for name, argtypes in SIGNATURES.items():
         fn = getattr(handle, name)
         fn.argtypes = argtypes

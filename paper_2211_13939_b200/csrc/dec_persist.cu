@@ -27,6 +27,14 @@
 
 #include "tcgen05.cuh"
 
+// Gate-weight prefetch into the ring during the preceding phase (bit 0: attention-gate weights
+// during PRE; bit 1: decoder-gate weights during ATT-B).  Measured slower on B200 (the issuing
+// thread and the extra L2 traffic delay the latency-bound phases more than the gate GEMMs gain:
+// B=1 +8%, B=24 +8%), so off by default; tools/build_variant.py -DDEC_PREFETCH=n for A/B runs.
+#ifndef DEC_PREFETCH
+#define DEC_PREFETCH 0
+#endif
+
 namespace {
 
 constexpr int NMEL = 80, EMB = 512, HID = 1024, PRE = 256, ATT = 128, NF = 32, KLOC = 31;
@@ -55,8 +63,11 @@ constexpr int NGRP = HID / 32;   // 32-unit gate groups: query partials, project
 constexpr int GEMM_CTAS = HID / 8;  // 128 CTAs x 8 hidden units
 constexpr int KA = 1792, KD = 2560;
 constexpr int MAXCH = 256;       // max position chunks per item
-constexpr int ACH = 32;          // max positions per attention chunk (pm + memory rows staged in smem)
-constexpr uint32_t ASTAGE = ACH * (ATT + EMB) * 4;  // one staging buffer (two: the next chunk streams in)
+constexpr int ACH = 64;          // max positions per attention chunk (pm + memory rows staged in smem)
+// Staging: a chunk of n positions is [n pm rows][n memory rows].  One round of tasks (every CTA
+// at most one chunk): chunks up to 64 positions in one 160 KB buffer.  Several rounds: 32-position
+// chunks double-buffered (the next chunk streams in while this one computes).
+constexpr uint32_t ASTAGE = 32 * (ATT + EMB) * 4;
 constexpr int LT = 128;          // positions per location-feature tile
 constexpr int HALO = (KLOC - 1) / 2;
 
@@ -138,9 +149,10 @@ __device__ __forceinline__ bool active(const PlanCache& pc, int b, int s) { retu
 // ------------------------------------------------------------------ small batched GEMV task
 // Y[b][n] (n in [n0, n0+32)) for items [b0, b0+8): sum over k in [k0, k1) of X[b][k] W^T[k][n].
 // x(b, k) is supplied by the caller; the 8 warps split the K range, partials reduced in warp order.
-template <int KWM, typename XF, typename OUT>
+template <int KWM, bool STAGED = false, typename XF, typename OUT>
 __device__ __forceinline__ void gemv_task(int b0, int nb, int n0, int N, int k0, int k1, const float* __restrict__ wT,
                                           float* sx, float* spart, XF xf, OUT out) {
+  // STAGED: sx already holds X[8][k1 - k0] (written and synchronised by the caller)
   // KWM >= rows per warp: every weight load of the warp's K-slice is issued before the first FMA
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int KL = k1 - k0;
@@ -149,11 +161,13 @@ __device__ __forceinline__ void gemv_task(int b0, int nb, int n0, int N, int k0,
   float w[KWM];
 #pragma unroll
   for (int u = 0; u < KWM; ++u) w[u] = (ka + u < kb && n < N) ? __ldg(wT + (int64_t)(k0 + ka + u) * N + n) : 0.f;
-  for (int i = tid; i < 8 * KL; i += NT) {
-    const int it = i / KL, k = k0 + i % KL;
-    sx[i] = it < nb ? xf(b0 + it, k) : 0.f;
+  if (!STAGED) {
+    for (int i = tid; i < 8 * KL; i += NT) {
+      const int it = i / KL, k = k0 + i % KL;
+      sx[i] = it < nb ? xf(b0 + it, k) : 0.f;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   float acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.f;
@@ -188,7 +202,7 @@ struct GateSync {
   uint64_t full[MAXGS], empty[MAXGS], accf, acce, abar[2];
   uint32_t tmem;
 };
-static_assert(2 * ASTAGE <= RING_BYTES, "attention staging exceeds the ring");
+static_assert(2 * ASTAGE <= RING_BYTES && ACH * (ATT + EMB) * 4 <= RING_BYTES, "attention staging exceeds the ring");
 
 // Gate GEMM with the WEIGHTS as the MMA's M operand: CTA c owns unit group ug = c / 4 (32 hidden
 // units = 128 gate rows, ordered [unit][gate]) and K split ks = c % 4.  D[128 gate rows][items] =
@@ -201,6 +215,27 @@ static_assert(2 * ASTAGE <= RING_BYTES, "attention staging exceeds the ring");
 // MODE 1: decoder LSTM   (X = [ctx | att_h(new bank) | dec_h(old bank)], K = 2560)
 constexpr int KSPLIT = 4;
 constexpr uint32_t GW_TILE = 128 * 128;  // weight stage: 128 rows x 64 bf16
+
+// Weight half of the first min(KCS, nst) stages of the next gate phase, issued by one thread
+// during the phase before it (the weights do not depend on the step): the full barrier gets the
+// weight bytes as a pending transaction now and its arrival with the operand tile later.
+template <int MODE>
+__device__ __forceinline__ void gate_prefetch_w(const DecArgs& a, uint8_t* ring, GateSync& gsy, int nst,
+                                                uint32_t g_ring) {
+  constexpr int NKC = (MODE == 0 ? KA : KD) / 64, KCS = NKC / KSPLIT;
+  const int c = blockIdx.x, ug = c >> 2, ks = c & 3;
+  const int npre = min(KCS, nst);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  for (int i = 0; i < npre; ++i) {
+    const uint32_t g = g_ring + i, st = g % nst, ph = (g / nst) & 1;
+    tcg::mbar_wait(&gsy.empty[st], ph ^ 1);
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(tcg::smem_u32(&gsy.full[st])),
+                 "r"(GW_TILE)
+                 : "memory");
+    bulk_g2s(ring + st * GW_TILE, (MODE == 0 ? a.Wa : a.Wd) + ((int64_t)ug * NKC + ks * KCS + i) * 128 * 64,
+             GW_TILE, &gsy.full[st]);
+  }
+}
 
 template <int MODE>
 __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy, uint32_t x_stage_bytes, int nst,
@@ -249,17 +284,22 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       asm volatile("fence.proxy.async.global;" ::: "memory");  // xb tiles written by generic stores
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the ring doubles as PRE scratch
       uint32_t g = g_ring;
+      const int npre = (DEC_PREFETCH & (1 << MODE)) ? min(KCS, nst) : 0;  // weights gate_prefetch_w issued
       for (int i = 0; i < KCS; ++i, ++g) {
         if (g % 3 != pi) continue;
         const uint32_t st = g % nst, ph = (g / nst) & 1;
-        tcg::mbar_wait(&gsy.empty[st], ph ^ 1);
+        if (i >= npre) tcg::mbar_wait(&gsy.empty[st], ph ^ 1);
         const int kc = ks * KCS + i, k0 = kc * 64;
         int col;
         if (MODE == 0) col = k0 < 768 ? k0 : att_off(oldb) + (k0 - 768);
         else col = k0 < 512 ? CTX_OFF + k0 : (k0 < 1536 ? att_off(newb) + (k0 - 512) : dec_off(oldb) + (k0 - 1536));
-        tcg::mbar_expect_tx(&gsy.full[st], GW_TILE + n16 * 128);
-        bulk_g2s(sW + st * GW_TILE, (MODE == 0 ? a.Wa : a.Wd) + ((int64_t)ug * NKC + kc) * 128 * 64, GW_TILE,
-                 &gsy.full[st]);
+        if (i < npre) {
+          tcg::mbar_expect_tx(&gsy.full[st], n16 * 128);
+        } else {
+          tcg::mbar_expect_tx(&gsy.full[st], GW_TILE + n16 * 128);
+          bulk_g2s(sW + st * GW_TILE, (MODE == 0 ? a.Wa : a.Wd) + ((int64_t)ug * NKC + kc) * 128 * 64, GW_TILE,
+                   &gsy.full[st]);
+        }
         const int r0 = min(n16, 128);
         bulk_g2s(sX + st * x_stage_bytes, a.xb + (int64_t)(col >> 6) * 128 * 64, r0 * 128, &gsy.full[st]);
         if (n16 > 128)  // items 128.. live in the next 128-row block of the mirror
@@ -408,9 +448,12 @@ struct AttSmem {
   float scale[MAXCH];
   int tstart[257];             // prefix sum of chunks per item (ATT-A task list), B <= 256
   float wp[ACH + 2 * HALO + 2], wa[ACH + 2 * HALO + 2], e[ACH];
-  __align__(16) float locf[LT * (NF + 1)];   // scratch: gemv / context partials [8][512]
+  // scratch: context partials [8][512] (ATT-A), gate-fixup h (gate phases), PRE's
+  // last frame [8][80] + H1 [8][256] + gemv partials [8 warps][8][32] (so the ring is free for the
+  // prefetch of the attention-gate weights during PRE)
+  __align__(16) float locf[8 * NMEL + 8 * PRE + NW * 8 * 32];
 };
-static_assert(LT * (NF + 1) >= NW * EMB, "context partials alias the location tile");
+static_assert(8 * NMEL + 8 * PRE + NW * 8 * 32 >= NW * EMB, "context partials exceed the scratch");
 
 __device__ __forceinline__ float block_max(float v, float* red) {
   v = itts::warp_max(v);
@@ -439,7 +482,7 @@ __device__ __forceinline__ void att_prefetch(const DecArgs& a, int b, int ta, in
   const int64_t* p = a.plan + b * DPLAN;
   const int n = tb - ta;
   float* sPm = reinterpret_cast<float*>(stage);
-  float* sMem = sPm + ACH * ATT;
+  float* sMem = sPm + n * ATT;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tcg::mbar_expect_tx(bar, (uint32_t)n * (ATT + EMB) * 4);
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -470,7 +513,7 @@ __device__ void att_chunk(const DecArgs& a, AttSmem& sm, int s, int b, int ch, i
   const float* wsrc = reinterpret_cast<const float*>(a.step0 + s == 0 ? p[3] : p[4]);
   const int n = tb - ta, nh = n + 2 * HALO;
   const float* sPm = reinterpret_cast<const float*>(stage);
-  const float* sMem = sPm + ACH * ATT;
+  const float* sMem = sPm + n * ATT;
   if (tid < ATT) {  // q = sum of the 32 unit-group partials, group order (8 loads in flight)
     float qv[NGRP];
 #pragma unroll
@@ -498,8 +541,7 @@ __device__ void att_chunk(const DecArgs& a, AttSmem& sm, int s, int b, int ch, i
     const float4 q4 = reinterpret_cast<const float4*>(sm.q)[lane];
     const float4 v4 = reinterpret_cast<const float4*>(sm.sv)[lane];
     const float4* wl4 = reinterpret_cast<const float4*>(sm.sWl);
-    const int pb = warp * 4;
-    if (pb < n) {  // warp-uniform
+    for (int pb = warp * 4; pb < n; pb += 4 * NW) {  // warp-uniform
       float acc[4][4];
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -696,16 +738,19 @@ __global__ void __launch_bounds__(NT, 1)
   }
   grid_sync(a.bar, gen);
 
-  // position chunking of the attention: about two tasks per CTA
-  // position chunking of the attention: about two tasks per CTA
+  // position chunking of the attention: the smallest multiple of 16 (<= 64) that gives every CTA
+  // at most one chunk; if none does, 32-position chunks in several double-buffered rounds
   int maxL = 1;
   for (int b = 0; b < a.B; ++b) maxL = max(maxL, pc.L[b]);
-  int64_t sumL = 0;
-  for (int b = 0; b < a.B; ++b) sumL += pc.L[b];
-  int chunk = (int)((sumL + G - 1) / G);   // about one task per CTA
-  chunk = max(chunk, (maxL + MAXCH - 1) / MAXCH);
-  chunk = min(ACH, max(16, (chunk + 15) / 16 * 16));
-  if ((maxL + chunk - 1) / chunk > MAXCH) chunk = (maxL + MAXCH - 1) / MAXCH;  // cannot exceed ACH for L <= 8192
+  auto ntask_for = [&](int ch) {
+    int nt = 0;
+    for (int b = 0; b < a.B; ++b) nt += (pc.L[b] + ch - 1) / ch;
+    return nt;
+  };
+  int chunk = 16;
+  while (chunk < ACH && ntask_for(chunk) > G) chunk += 16;
+  if (ntask_for(chunk) > G) chunk = 32;
+  if ((maxL + chunk - 1) / chunk > MAXCH) chunk = (maxL + MAXCH - 1) / MAXCH;  // <= 32 for L <= 8192
   const int nb8 = (a.B + 7) / 8;
 
   unsigned long long tph = gtimer(), tacc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -733,6 +778,7 @@ __global__ void __launch_bounds__(NT, 1)
   for (int s = 0; s < a.nsteps; ++s) {
     const int gs = a.step0 + s;
     // ---- PRE: finish mel(s-1); H1 = relu(W0 . last) for the task's 8 items; p = relu(W1 . H1)
+    if ((DEC_PREFETCH & 1) && gemm_cta && tid == 0) gate_prefetch_w<0>(a, ring, gsy, nst, g_ring);
     for (int task = c; task < nb8 * 8; task += G) {
       const int b0 = (task >> 3) * 8, n0 = (task & 7) * 32, nb = min(8, a.B - b0);
       const bool trp = a.trace && c == 0 && tid == 0;
@@ -744,9 +790,9 @@ __global__ void __launch_bounds__(NT, 1)
           tp0 = t1;
         }
       };
-      float* sx = ringf;                 // [8][80]
+      float* sx = sm.locf;               // [8][80]
       float* sh = sx + 8 * NMEL;         // [8][256]
-      float* gsc = sh + 8 * PRE;         // gemv scratch
+      float* gsc = sh + 8 * PRE;         // gemv partials
 
       {  // warp w: item b0 + w; lane l: mel / gate values k = l, l + 32, l + 64 (< 81), all 3 x 34
          // partial loads in flight before the sums
@@ -813,8 +859,8 @@ __global__ void __launch_bounds__(NT, 1)
       }
       __syncthreads();
       pmark(6);
-      gemv_task<32>(b0, nb, n0, PRE, 0, PRE, a.W1T, gsc, gsc + 8 * PRE,
-                    [&](int b, int k) { return sh[(b - b0) * PRE + k]; },
+      gemv_task<32, true>(b0, nb, n0, PRE, 0, PRE, a.W1T, sh, gsc,
+                    [&](int b, int k) { return 0.f; },
                     [&](int b, int n, float y) {
                       if (!active(pc, b, gs)) return;
                       y = fmaxf(y, 0.f);
@@ -884,7 +930,8 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
     phase_end();
-    // ---- ATT-B
+    // ---- ATT-B (the ring is idle: the decoder-gate weights stream in meanwhile)
+    if ((DEC_PREFETCH & 2) && gemm_cta && tid == 0) gate_prefetch_w<1>(a, ring, gsy, nst, g_ring);
     for (int b = c; b < a.B; b += G)
       if (active(pc, b, gs)) att_combine(a, sm, gs, b, chunk);
     phase_end();

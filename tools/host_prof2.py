@@ -24,6 +24,7 @@ from paper_2211_13939_b200.modules import build_engine, modules_for  # noqa: E40
 ap = argparse.ArgumentParser()
 ap.add_argument("--qps", type=float, default=175)
 ap.add_argument("--seconds", type=float, default=8)
+ap.add_argument("--sort", default="tottime")
 args = ap.parse_args()
 cfg, lex = PipelineConfig(), default_lexicon()
 eng = build_engine(cfg, "r", "cuda:0")
@@ -57,5 +58,8 @@ run = serve(mods, cfg, poisson_trace(args.qps, args.seconds, seed=3, lexicon=lex
 n = len(run.reports)
 print(f"{n} iterations, mean B {sum(len(r.decoder_ids) for r in run.reports) / n:.1f}")
 s = io.StringIO()
-pstats.Stats(prof, stream=s).sort_stats("tottime").print_stats(30)
+pstats.Stats(prof, stream=s).sort_stats(args.sort).print_stats(45)
 print(s.getvalue()[:8000])
+s2 = io.StringIO()
+pstats.Stats(prof, stream=s2).print_callers("acquire|sleep")
+print(s2.getvalue()[:4000])
