@@ -34,6 +34,14 @@
 #ifndef DEC_PREFETCH
 #define DEC_PREFETCH 0
 #endif
+// Pooled batches up to DEC_MERGE_B: the chunk combine (ATT-B) runs at the start of the
+// decoder-gate phase on the CTAs that do not own the context columns of that GEMM; the owners
+// start with their att_h columns and wait for the combined contexts on a counter (one grid
+// barrier fewer per step; same-box A/B: B=1 -4.4%, B=24 -2.7%, B=128 +2.5%, hence the cut-off).
+// Larger batches: separate ATT-B phase.
+#ifndef DEC_MERGE_B
+#define DEC_MERGE_B 96
+#endif
 
 namespace {
 
@@ -100,7 +108,8 @@ struct DecArgs {
   float* U;                        // [B][u_ld] unnormalised attention numerators
   int64_t u_ld;
   float* AP;                       // [B][MAXCH][2 + 512] chunk max, sum, context partial
-  unsigned* bar;                   // [2 + 32] grid barrier + gate-group counters (zeroed before launch)
+  unsigned* bar;                   // [2 + 32 + 1] grid barrier, gate-group counters, combined-context
+                                   // counter (zeroed before launch)
   unsigned long long* trace;       // debug: [16] ns per phase summed over steps (CTA 0), or null
 };
 
@@ -134,6 +143,15 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& gen) {
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
+}
+
+// Spin until a monotonic global counter reaches `target` (relaxed polls, then acquire).
+__device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
+  unsigned seen;
+  do {
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p) : "memory");
+  } while (seen < target);
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
 // L2-coherent loads for data produced inside this kernel by other CTAs (never cached in L1).
@@ -239,7 +257,8 @@ __device__ __forceinline__ void gate_prefetch_w(const DecArgs& a, uint8_t* ring,
 
 template <int MODE>
 __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy, uint32_t x_stage_bytes, int nst,
-                           uint32_t& g_ring, uint32_t& lt_tile, const PlanCache& pc, unsigned& grp_gen, float* hs) {
+                           uint32_t& g_ring, uint32_t& lt_tile, const PlanCache& pc, unsigned& grp_gen, float* hs,
+                           bool merged = false, unsigned ctx_target = 0) {
   constexpr int K = MODE == 0 ? KA : KD;
   constexpr int NKC = K / 64;
   constexpr int KCS = NKC / KSPLIT;
@@ -285,11 +304,20 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the ring doubles as PRE scratch
       uint32_t g = g_ring;
       const int npre = (DEC_PREFETCH & (1 << MODE)) ? min(KCS, nst) : 0;  // weights gate_prefetch_w issued
+      // merged combine: the context columns (decoder gates, split 0, chunks 0..7) go last, after
+      // the combined contexts of every live item are counted in
+      const bool ctx_last = merged && MODE == 1 && ks == 0;
+      bool ctx_ready = !ctx_last;
       for (int i = 0; i < KCS; ++i, ++g) {
         if (g % 3 != pi) continue;
         const uint32_t st = g % nst, ph = (g / nst) & 1;
         if (i >= npre) tcg::mbar_wait(&gsy.empty[st], ph ^ 1);
-        const int kc = ks * KCS + i, k0 = kc * 64;
+        const int kc = ks * KCS + (ctx_last ? (i + 8) % KCS : i), k0 = kc * 64;
+        if (!ctx_ready && k0 < EMB) {
+          wait_count(a.bar + 2 + NGRP, ctx_target);
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // contexts written by generic stores
+          ctx_ready = true;
+        }
         int col;
         if (MODE == 0) col = k0 < 768 ? k0 : att_off(oldb) + (k0 - 768);
         else col = k0 < 512 ? CTX_OFF + k0 : (k0 < 1536 ? att_off(newb) + (k0 - 512) : dec_off(oldb) + (k0 - 1536));
@@ -752,6 +780,7 @@ __global__ void __launch_bounds__(NT, 1)
   if (ntask_for(chunk) > G) chunk = 32;
   if ((maxL + chunk - 1) / chunk > MAXCH) chunk = (maxL + MAXCH - 1) / MAXCH;  // <= 32 for L <= 8192
   const int nb8 = (a.B + 7) / 8;
+  const bool merged = a.B <= DEC_MERGE_B;  // ATT-B folded into the decoder-gate phase
 
   unsigned long long tph = gtimer(), tacc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   int ph_i = 0;
@@ -762,7 +791,7 @@ __global__ void __launch_bounds__(NT, 1)
       tacc[ph_i] += now - tph;
       tph = now;
     }
-    ph_i = ph_i == 4 ? 0 : ph_i + 1;
+    ph_i = ph_i == (merged ? 3 : 4) ? 0 : ph_i + 1;
   };
   // mel / gate value k of item b for the step whose projection partials are in Pp (group order, ctx last)
   auto mel_value = [&](int b, int k) {
@@ -775,6 +804,7 @@ __global__ void __launch_bounds__(NT, 1)
     return m;
   };
   float* ringf = reinterpret_cast<float*>(ring);  // generic scratch outside the gate / staging uses
+  unsigned ctx_target = 0;                         // combined contexts so far (merged ATT-B)
   for (int s = 0; s < a.nsteps; ++s) {
     const int gs = a.step0 + s;
     // ---- PRE: finish mel(s-1); H1 = relu(W0 . last) for the task's 8 items; p = relu(W1 . H1)
@@ -930,15 +960,38 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
     phase_end();
-    // ---- ATT-B (the ring is idle: the decoder-gate weights stream in meanwhile)
+    // ---- ATT-B: combine the chunks of every live item -> context, W, W_acc
     if ((DEC_PREFETCH & 2) && gemm_cta && tid == 0) gate_prefetch_w<1>(a, ring, gsy, nst, g_ring);
-    for (int b = c; b < a.B; b += G)
-      if (active(pc, b, gs)) att_combine(a, sm, gs, b, chunk);
-    phase_end();
+    if (!merged) {
+      for (int b = c; b < a.B; b += G)
+        if (active(pc, b, gs)) att_combine(a, sm, gs, b, chunk);
+      phase_end();
+    } else {
+      // on every CTA but the context-column owners (split 0 of each gate group), before their GEMM
+      for (int b = 0; b < a.B; ++b) ctx_target += active(pc, b, gs) ? 1u : 0u;
+      const bool owner = gemm_cta && (c & 3) == 0;
+      if (!owner) {
+        const int ci = gemm_cta ? (c >> 2) * 3 + (c & 3) - 1 : 3 * (GEMM_CTAS / 4) + (c - GEMM_CTAS);
+        const int ncomb = 3 * (GEMM_CTAS / 4) + (G - GEMM_CTAS);
+        unsigned done = 0;
+        for (int b = ci; b < a.B; b += ncomb)
+          if (active(pc, b, gs)) {
+            att_combine(a, sm, gs, b, chunk);  // ends with __syncthreads
+            ++done;
+          }
+        if (tid == 0 && done)
+          asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.bar + 2 + NGRP), "r"(done) : "memory");
+      }
+    }
     // ---- DEC gates + cell + projection partials of dec_h; the other CTAs project the context
-    if (gemm_cta) gate_phase<1>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen, sm.locf);
+    if (gemm_cta) gate_phase<1>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen, sm.locf,
+                                merged, ctx_target);
     {
       const int c0 = G > GEMM_CTAS ? GEMM_CTAS : 0, nsp = G - c0;
+      if (merged && c >= c0 && c - c0 < nb8 * 3) {  // the contexts of all live items
+        if (tid == 0) wait_count(a.bar + 2 + NGRP, ctx_target);
+        __syncthreads();
+      }
       if (c >= c0)
         for (int task = c - c0; task < nb8 * 3; task += nsp) {
           const int b0 = (task / 3) * 8, n0 = (task % 3) * 32, nb = min(8, a.B - b0);
@@ -1011,7 +1064,7 @@ ITTS_API int itts_r_decode_persistent(int32_t B, int32_t nsteps, const int64_t* 
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
-  cudaError_t e = cudaMemsetAsync(bar, 0, (2 + NGRP) * sizeof(unsigned), st);
+  cudaError_t e = cudaMemsetAsync(bar, 0, (2 + NGRP + 1) * sizeof(unsigned), st);
   if (e != cudaSuccess) return (int)e;
   const int G = tcg::num_sms();
   void* args[] = {&a, &a_box_bytes};

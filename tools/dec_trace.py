@@ -22,7 +22,7 @@ args = ap.parse_args()
 eng = TierREngine(PipelineConfig(), "cuda:0")
 eng.use_graphs = False
 lex = default_lexicon()
-names = ["PRE", "ATT gates+q", "ATT-A", "ATT-B", "DEC gates+proj"]
+names = ["PRE", "ATT gates+q", "ATT-A", "ATT-B (or DEC gates+combine+proj)", "DEC gates+proj"]
 for B in [int(x) for x in args.batches.split(",")]:
     rng = random.Random(B)
     fos = [run_frontend(random_text(rng, 20, 200, lex), lex) for _ in range(B)]
@@ -42,7 +42,7 @@ for B in [int(x) for x in args.batches.split(",")]:
     raw = buf.cpu().tolist()
     t = raw[:5] + [v / REPS for v in raw[5:]]   # phase totals are per launch (last one); the rest accumulate
     print(f"B={B}: chunk {e0.elapsed_time(e1) / REPS:.3f} ms; per step (us): " +
-          ", ".join(f"{n} {t[i] / 32e3:.1f}" for i, n in enumerate(names)))
+          ", ".join(f"{n} {t[i] / 32e3:.1f}" for i, n in enumerate(names) if t[i]))
     print(f"   PRE CTA0 (us): mel partials {t[5] / 32e3:.2f}, H1 {t[6] / 32e3:.2f}, p gemv {t[7] / 32e3:.2f}")
     for m, nm in ((0, "ATT"), (1, "DEC")):
         g = [t[16 + 8 * m + i] / 32e3 for i in range(7)]
