@@ -93,7 +93,7 @@ int itts_s_vocode_chunk(const int64_t* plan, int32_t n_items, int32_t dim, int32
  *          partial at f32_out + z*rows*c_out and only slice 0 adds the bias);
  *          acc_mode 1 store / 2 add / 3 finalize v = (acc + v) / 3 on the bf16
  *          MRF accumulator; act_out = bf16(lrelu(v, slope)); zero_halo writes
- *          zeros into act_out halo rows.
+ *          zeros into act_out halo rows.  0 <= slope <= 1, 0 < res_slope <= 1.
  * c_in and c_out must be multiples of 32; bn = N tile (32/64/128/256) or 0. */
 int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, const void* w,
                    int32_t n_total, int32_t n_taps, const int32_t* host_tap_off, const float* bias,
@@ -109,8 +109,8 @@ int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, cons
  * acc_mode 0: act_out = lrelu(y, slope); 1: acc = y; 2: acc += y;
  * 3: act_out = lrelu((acc + y) / 3, slope).  Exactly one output: act_out is given
  * for modes 0 / 3 and NULL for modes 1 / 2.  Halo rows of the output are written as
- * zeros.  c in {32, 64, 128, 256}, taps odd <= 11, dil <= 5.  act_out / acc must not
- * alias x. */
+ * zeros.  c in {32, 64, 128, 256}, taps odd <= 11, dil <= 5, 0 <= slope <= 1.  act_out /
+ * acc must not alias x. */
 int itts_resblock_tc(const void* x, int64_t rows, int32_t c, const void* w1, const void* w2, const float* b1,
                      const float* b2, int32_t taps, int32_t dil, const int32_t* row_out, void* acc,
                      int32_t acc_mode, void* act_out, float slope, void* stream);
@@ -168,6 +168,14 @@ int itts_r_enc_embed(const int32_t* tok4, int64_t total, const int64_t* plan, in
                      int64_t max_len, const float* Eph, const float* Epw, const float* Epph,
                      const float* Eiph, void* X, void* stream);
 int itts_r_bilstm(const float* PRE, const int64_t* plan, int32_t n, const float* WhhT, void* stream);
+/* The whole encoder launch sequence above (embedding, 3 convs, input projection, BiLSTM,
+ * processed memory, zeroed decoder-state rows) issued from C++ after one H2D copy: pack =
+ * int32 tokens [4][total] (padded to 8 bytes), plan [n][6], row-map plan [n][5], state spans
+ * [n][2] {ptr, floats}; weights = Eph, Epw, Epph, Eiph, (conv w, conv b) x 3, Wih, b_ih, WhhT, WmT;
+ * xa / xb bf16 [rows][512], pre fp32 [rows][2048], rowmap int32 [rows] work buffers. */
+int itts_r_encode(const void* pack, int64_t total, int32_t n, int64_t max_len, int64_t rows, int64_t max_span,
+                  const int64_t* weights, int32_t conv_taps, void* xa, void* xb, float* pre, int32_t* rowmap,
+                  void* stream);
 int itts_r_pmem(const int64_t* plan, int32_t n, int64_t max_len, const float* WmT, void* stream);
 
 /* K7 helpers around the HiFi-GAN conv stack (replaces vocode_batch,

@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(Cfg<C>::THREADS, Cfg<C>::CPS)
   uint64_t* r_full = t_empty + 1;
   uint64_t* t_ready = r_full + 1;  // [NKC]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_ready + NKC);
-  __shared__ float sB1[C], sB2[C];
+  __shared__ __align__(16) float sB1[C], sB2[C];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = a.taps, d = a.dil, h1 = d * (k - 1) / 2, h2 = (k - 1) / 2;
@@ -324,11 +324,14 @@ __global__ void __launch_bounds__(Cfg<C>::THREADS, Cfg<C>::CPS)
           const int col = kc * KT + cw * 32;
           float v[32];
           tmem_ld32(tmem + b * C + ((uint32_t)(q * 32) << 16) + col, v);
+          float bb[32];
+#pragma unroll
+          for (int e4 = 0; e4 < 8; ++e4) *reinterpret_cast<float4*>(&bb[4 * e4]) = reinterpret_cast<const float4*>(sB1 + col)[e4];
           uint32_t w[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            float x0 = lrelu(v[2 * e] + sB1[col + 2 * e], 0.1f);
-            float x1 = lrelu(v[2 * e + 1] + sB1[col + 2 * e + 1], 0.1f);
+            float x0 = lrelu(v[2 * e] + bb[2 * e], 0.1f);
+            float x1 = lrelu(v[2 * e + 1] + bb[2 * e + 1], 0.1f);
             if (!valid) x0 = x1 = 0.f;
             __nv_bfloat162 b2 = __floats2bfloat162_rn(x0, x1);
             w[e] = *reinterpret_cast<uint32_t*>(&b2);
@@ -381,10 +384,12 @@ __global__ void __launch_bounds__(Cfg<C>::THREADS, Cfg<C>::CPS)
         uint4 ru[4];
 #pragma unroll
         for (int c4 = 0; c4 < 4; ++c4) ru[c4] = *reinterpret_cast<const uint4*>(rowp + swz_chunk<SWZ>(o, cw * 4 + c4) * 16);
-        float y[32];
+        float y[32], bb[32];
         unpack_bf16<32>(ru, y);
 #pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] += sB2[c0 + e] + inv_lrelu(y[e], 10.0f);
+        for (int e4 = 0; e4 < 8; ++e4) *reinterpret_cast<float4*>(&bb[4 * e4]) = reinterpret_cast<const float4*>(sB2 + c0)[e4];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] += bb[e] + inv_lrelu(y[e], 10.0f);
         if (a.acc_mode >= 2) {
           float sacc[32];
           unpack_bf16<32>(au[n & 1], sacc);
@@ -484,6 +489,7 @@ ITTS_API int itts_resblock_tc(const void* x, int64_t rows, int32_t c, const void
   if (!x || !w1 || !w2 || !b1 || !b2 || !row_out || rows <= 0) return ITTS_EINVAL;
   if (taps < 1 || taps > kMaxK || taps % 2 == 0 || dil < 1 || dil > 5) return ITTS_EINVAL;
   if (acc_mode < 0 || acc_mode > 3 || (acc_mode && !acc)) return ITTS_EINVAL;
+  if (!(slope >= 0.f && slope <= 1.f)) return ITTS_EINVAL;  // lrelu as max(y, slope * y)
   // exactly one output: act_out for modes 0 / 3, the accumulator for modes 1 / 2
   if ((acc_mode == 0 || acc_mode == 3) != (act_out != nullptr)) return ITTS_EINVAL;
   if ((act_out && act_out == x) || (acc && acc == x)) return ITTS_EINVAL;  // neighbouring tiles still read x

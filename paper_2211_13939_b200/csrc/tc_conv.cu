@@ -276,7 +276,8 @@ ITTS_API int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, int64_t x
   if (!x || !w || !bias || !row_out || !host_tap_off || rows <= 0) return ITTS_EINVAL;
   if (n_taps < 1 || n_taps > kMaxTaps || c_out <= 0 || n_total % c_out) return ITTS_EINVAL;
   if (c_out % 32 || (acc_mode && !acc) || acc_mode < 0 || acc_mode > 3) return ITTS_EINVAL;
-  if (x_ld < c_in || (x_ld * 2) % 16 || res_slope <= 0.f) return ITTS_EINVAL;
+  if (x_ld < c_in || (x_ld * 2) % 16 || res_slope <= 0.f || res_slope > 1.f) return ITTS_EINVAL;
+  if (!(slope >= 0.f && slope <= 1.f)) return ITTS_EINVAL;  // lrelu as max(x, slope * x)
   if (ksplit > 1 && (!f32_out || res_in || acc_mode || act_out)) return ITTS_EINVAL;  // partials are raw fp32
   if (((uintptr_t)x | (uintptr_t)w) & 15) return ITTS_EALIGN;
   Taps taps{};

@@ -118,14 +118,17 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[CW]) {
   if constexpr (CW == 32) tmem_ld32(taddr, v); else tmem_ld16(taddr, v);
 }
 
-__device__ __forceinline__ float lrelu(float x, float s) { return x >= 0.f ? x : x * s; }
+// Leaky ReLU for 0 <= s <= 1 as max(x, s*x): 2 instructions (multiply, max) instead of a
+// compare / multiply / select; identical results (including -0 and NaN) on that slope range.
+__device__ __forceinline__ float lrelu(float x, float s) { return fmaxf(x, x * s); }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // Inverse leaky ReLU given the reciprocal slope (a multiply: an fp32 division here costs ~20 instructions).
-__device__ __forceinline__ float inv_lrelu(float a, float inv_s) { return a >= 0.f ? a : a * inv_s; }
+// (inv_s >= 1: min(a, a * inv_s) selects a for a >= 0 and a * inv_s below zero.)
+__device__ __forceinline__ float inv_lrelu(float a, float inv_s) { return fminf(a, a * inv_s); }
 
 // CW bf16 values (CW/8 x 16-byte vectors) <-> fp32 registers.
 template <int CW>

@@ -816,6 +816,55 @@ ITTS_API int itts_r_pmem(const int64_t* plan, int32_t n, int64_t max_len, const 
   ITTS_RETURN_LAUNCH();
 }
 
+// Zero n spans of fp32 (the fresh decoder-state rows of newly encoded requests): span i =
+// {ptr, count}; one launch instead of one memset per request.
+__global__ void k_zero_spans(const int64_t* __restrict__ spans) {
+  float* p = reinterpret_cast<float*>(spans[2 * blockIdx.y]);
+  const int64_t cnt = spans[2 * blockIdx.y + 1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0.f;
+}
+
+// The whole Tier-R encoder launch sequence of one pooled encoder call (reference encode_batch,
+// acoustic.py:146-160, behind encoder_batch src/modules.py:60-66), issued from C++: embedding
+// sum -> 3 x (conv k5 + ReLU; BN folded) -> BiLSTM input projection (fp32) -> recurrence ->
+// processed memory -> zeroed decoder-state rows.  `pack` holds, after the int32 tokens
+// [4][total] padded to 8 bytes, the item plan [n][6], the row-map plan [n][5] and the state
+// spans [n][2].  weights: Eph, Epw, Epph, Eiph, (conv w, conv b) x 3, Wih, b_ih, WhhT, WmT.
+ITTS_API int itts_r_encode(const void* pack, int64_t total, int32_t n, int64_t max_len, int64_t rows,
+                           int64_t max_span, const int64_t* weights, int32_t conv_taps, void* xa, void* xb,
+                           float* pre, int32_t* rowmap, void* stream) {
+  if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
+  if (conv_taps < 1 || conv_taps > 15 || !pack || !weights || !xa || !xb || !pre || !rowmap) return ITTS_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int32_t* tok4 = static_cast<const int32_t*>(pack);
+  const int64_t* plan = static_cast<const int64_t*>(pack) + (4 * total + 1) / 2;
+  const int64_t* rm_plan = plan + 6 * (int64_t)n;
+  const int64_t* spans = rm_plan + 5 * (int64_t)n;
+  auto W = [&](int i) { return reinterpret_cast<const void*>(weights[i]); };
+  cudaError_t e = cudaMemsetAsync(xa, 0, (size_t)rows * EMB * 2, st);
+  if (e != cudaSuccess) return (int)e;
+  int r = itts_r_enc_embed(tok4, total, plan, n, max_len, (const float*)W(0), (const float*)W(1), (const float*)W(2),
+                           (const float*)W(3), xa, stream);
+  if (r) return r;
+  if ((r = itts_r_rowmap(rm_plan, n, max_span, rowmap, stream))) return r;
+  int32_t offs[16];
+  for (int j = 0; j < conv_taps; ++j) offs[j] = j - (conv_taps - 1) / 2;
+  void* bufs[2] = {xa, xb};
+  for (int i = 0; i < 3; ++i)
+    if ((r = itts_conv1d_tc(bufs[i & 1], rows, EMB, EMB, W(4 + 2 * i), EMB, conv_taps, offs, (const float*)W(5 + 2 * i),
+                            EMB, rowmap, nullptr, 1.0f, nullptr, 1, nullptr, 0, bufs[(i + 1) & 1], 0.0f, 1, 0, stream)))
+      return r;
+  const int32_t off0 = 0;
+  if ((r = itts_conv1d_tc(xb, rows, EMB, EMB, W(10), 8 * EH, 1, &off0, (const float*)W(11), 8 * EH, rowmap, nullptr,
+                          1.0f, pre, 1, nullptr, 0, nullptr, 1.0f, 1, 128, stream)))
+    return r;
+  if ((r = itts_r_bilstm(pre, plan, n, (const float*)W(12), stream))) return r;
+  if ((r = itts_r_pmem(plan, n, max_len, (const float*)W(13), stream))) return r;
+  k_zero_spans<<<dim3(8, n), 256, 0, st>>>(spans);
+  ITTS_RETURN_LAUNCH();
+}
+
 ITTS_API int itts_r_mel_assemble(const int64_t* plan, int32_t n, int64_t max_rows, void* X0, int32_t ld,
                                  void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;

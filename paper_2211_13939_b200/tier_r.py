@@ -43,6 +43,7 @@ from .handles import (DecodeChunkResult, DeviceDecoderState, DeviceEncodedFeatur
 P_OFF, CTX_OFF, ATTH_OFF, DECH_OFF, ATTC_OFF, DECC_OFF, LAST_OFF, ROW = 0, 256, 768, 1792, 2816, 3840, 4864, 4944
 XB_ROW = 2816
 ENC_HALO = 2        # conv k5
+ENC_TAPS = 5
 MEL_HALO = 3        # conv_pre k7
 MRF_HALO = 25       # k11 dilation 5
 UPS = (8, 8, 2, 2)
@@ -130,6 +131,12 @@ class TierREngine:
         self.pcm16 = False               # also produce 16-bit PCM on device in the splice pass (f1)
         self.mrf_streams = True          # run the 3 MRF branches of a stage on 3 streams (fused path)
         self.native_vocoder = True       # issue the fused HiFi-GAN stack from C++ (voc_run.cu)
+        self.native_encoder = True       # issue the encoder launch sequence from C++ (itts_r_encode)
+        enc_w = [*self.E]
+        for wt, _, bias in self.enc_conv:
+            enc_w += [wt, bias]
+        enc_w += [self.enc_ih[0], self.enc_ih[2], self.enc_whhT, self.WmT]
+        self._enc_ptrs = (ctypes.c_int64 * len(enc_w))(*[t.data_ptr() for t in enc_w])
         self._voc = self._create_native_vocoder()
         self._side = [torch.cuda.Stream(self.device) for _ in range(2)]
         self._ev = [torch.cuda.Event() for _ in range(3)]
@@ -327,17 +334,17 @@ class TierREngine:
         lens = [fo.seq_len for fo in fos]
         if min(lens) < 1:
             raise ValueError("frontend output needs at least one phoneme")
-        for fo in fos:
-            if max(fo.phonemes) >= W.N_SYMBOLS or min(fo.phonemes) < 0:
-                raise ValueError("phoneme id outside the embedding table")
-            if max(max(fo.pw), max(fo.pph), max(fo.iph)) > 1 or min(min(fo.pw), min(fo.pph), min(fo.iph)) < 0:
-                raise ValueError("prosody tokens must be 0/1")
         total = sum(lens)
-        tok = np.empty((4, total), dtype=np.int32)
+        tok = np.empty((4, total), dtype=np.int64)
         pos = 0
         for fo, L in zip(fos, lens):
             tok[:, pos:pos + L] = (fo.phonemes, fo.pw, fo.pph, fo.iph)
             pos += L
+        if tok[0].max() >= W.N_SYMBOLS or tok[0].min() < 0:
+            raise ValueError("phoneme id outside the embedding table")
+        if tok[1:].max() > 1 or tok[1:].min() < 0:
+            raise ValueError("prosody tokens must be 0/1")
+        tok = tok.astype(np.int32)
         lay = _Layout(lens, ENC_HALO)
         reqs = []
         for L in lens:
@@ -353,6 +360,8 @@ class TierREngine:
             plan[i] = (tok_off[i], lens[i], lay.first[i], a.ptr(req.extra["mem_off"]),
                        a.ptr(req.extra["pm_off"]), 0)
         st = self._st()
+        if self.native_encoder:
+            return self._encode_native(tok, plan, lay, reqs, total, n, max(lens))
         with torch.cuda.stream(self.stream):
             d_tok, d_plan = self._up(tok), self._up(plan)
             mark = self._mark("encoder", total)
@@ -372,6 +381,31 @@ class TierREngine:
             for req, buf in reqs:
                 a.tensor[buf.off:buf.off + self.state_size(req.seq_len)].zero_()
             mark.__exit__(None, None, None)
+        fpp = self.cfg.frames_per_phoneme
+        return [(DeviceEncodedFeatures(req), DeviceDecoderState(req, buf, 0, fpp * req.seq_len))
+                for req, buf in reqs]
+
+    def _encode_native(self, tok, plan, lay, reqs, total, n, max_len) -> list:
+        """encoder_batch's launch sequence issued from C++ (itts_r_encode) after one H2D copy of
+        tokens, item plan, row-map plan and the state rows to zero."""
+        a = self.arena
+        rm_plan = np.stack([lay.base, np.array(lay.rows, np.int64), np.full(n, lay.halo, np.int64),
+                            lay.first.astype(np.int64), np.ones(n, np.int64)], 1)
+        spans = np.array([(a.ptr(buf.off), self.state_size(req.seq_len)) for req, buf in reqs], np.int64)
+        tok_words = np.zeros((4 * total + 1) // 2 * 2, np.int32)
+        tok_words[:4 * total] = tok.reshape(-1)
+        pack = np.concatenate([tok_words.view(np.int64), plan.reshape(-1), rm_plan.reshape(-1), spans.reshape(-1)])
+        with torch.cuda.stream(self.stream):
+            d_pack = self._up(pack)
+            xa = self._buf("enc_xa", lay.total * W.EMB)
+            xb = self._buf("enc_xb", lay.total * W.EMB)
+            pre = self._buf("enc_pre", lay.total * 2048, torch.float32)
+            rm = self._buf("enc_rm", lay.total, torch.int32)
+            with self._mark("encoder", total):
+                self._call("itts_r_encode", d_pack.data_ptr(), total, n, max_len, lay.total,
+                           int(max(lay.rows)) + 2 * lay.halo, self._enc_ptrs, ENC_TAPS, xa.data_ptr(),
+                           xb.data_ptr(), pre.data_ptr(), rm.data_ptr(), self._st())
+                self.launches += 9   # embed, row map, 3 convs, input projection, BiLSTM, memory, state zero
         fpp = self.cfg.frames_per_phoneme
         return [(DeviceEncodedFeatures(req), DeviceDecoderState(req, buf, 0, fpp * req.seq_len))
                 for req, buf in reqs]
