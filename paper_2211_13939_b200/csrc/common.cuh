@@ -3,6 +3,9 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <utility>
 
 #define ITTS_API extern "C" __attribute__((visibility("default")))
 
@@ -18,6 +21,40 @@
   } while (0)
 
 namespace itts {
+
+// Programmatic dependent launch (PDL): kernels of the vocoder / encoder chains are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's prologue (barrier init, TMEM
+// allocation, tensor-map prefetch, weight loads) overlaps the tail of the kernel before it.
+// Every kernel calls pdl_trigger() on entry (dependents may launch once all its CTAs started) and
+// pdl_wait() before its first access to data a previous kernel produced or still reads.
+// ITTS_NO_PDL=1 launches without the attribute (A/B and race checks).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("ITTS_NO_PDL");
+    on = (e && e[0] == '1') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {

@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(Cfg<C>::THREADS, Cfg<C>::CPS)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  itts::pdl_trigger();  // the weight producer and the MMA warp touch no data of earlier kernels
 
   if (warp == 0) {
     // ---------------- weight producer: c1 in (tap, panel) order, c2 in (panel, tap) order
@@ -194,6 +195,7 @@ __global__ void __launch_bounds__(Cfg<C>::THREADS, Cfg<C>::CPS)
   } else if (warp == 2) {
     // ---------------- X-tile producer; also loads each tile's residual rows into the T region
     // once c2 has consumed it (epilogue 2 then reads x from shared memory, not global).
+    itts::pdl_wait();
     if (lane == 0) {
       uint32_t lt = 0;
       const uint32_t bytes = (uint32_t)NKC * a.nbox * a.box_rows * SWZ;
@@ -285,6 +287,7 @@ __global__ void __launch_bounds__(Cfg<C>::THREADS, Cfg<C>::CPS)
     constexpr int CPP = KT / 32;             // 32-column chunks per panel
     const int q = warp & 3, h = (warp - 3) >> 2;  // h < HP
     const int et = threadIdx.x - 96;
+    itts::pdl_wait();  // row map, output buffers
     for (int i = et; i < C; i += 32 * kEpiWarps) {
       sB1[i] = a.b1[i];
       sB2[i] = a.b2[i];
@@ -469,8 +472,9 @@ int launch(const void* x, int64_t rows, const void* w1, const void* w2, int taps
   a.num_tiles = (int)((rows + a.m_out - 1) / a.m_out);
   const int slots = num_sms() * K::CPS;
   const int grid = a.num_tiles < slots ? a.num_tiles : slots;
-  k_resblock_tc<C><<<grid, K::THREADS, K::SMEM, st>>>(mx, m1, m2, mr, mo, mo2, a);
-  ITTS_RETURN_LAUNCH();
+  const cudaError_t e = itts::launch_pdl(k_resblock_tc<C>, dim3(grid), dim3(K::THREADS), K::SMEM, st, mx, m1, m2,
+                                         mr, mo, mo2, a);
+  return e == cudaSuccess ? ITTS_OK : (int)e;
 }
 
 }  // namespace

@@ -118,8 +118,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  itts::pdl_trigger();
 
   if (warp == 0) {
+    itts::pdl_wait();  // A rows come from the previous kernel
     if (lane == 0) {
       uint32_t g = 0;  // running stage counter across tiles
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -165,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // issued before its tcgen05.ld so their latency overlaps the TMEM read.
     constexpr int CW = BN >= 64 ? 32 : 16;   // columns per chunk
     const int ew = warp - 2;
+    itts::pdl_wait();  // row map, residual, accumulator and output buffers
     const int quarter = warp & 3, half = ew >> 2;
     const int C = epi.c_out;
     const float inv_res = 1.0f / epi.res_slope;
@@ -262,8 +265,9 @@ int launch(const void* x, int64_t rows, int c_in, int64_t x_ld, const void* w, i
   const int m_tiles = (int)((rows + kBlockM - 1) / kBlockM);
   const int tiles = m_tiles * sched.n_tiles * ksplit;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  k_conv_tc<BN, SWZ, STAGES><<<grid, kThreads, smem, st>>>(ma, mb, taps, kchunks, n_total, tiles, sched, epi);
-  ITTS_RETURN_LAUNCH();
+  const cudaError_t e = itts::launch_pdl(k_conv_tc<BN, SWZ, STAGES>, dim3(grid), dim3(kThreads), smem, st, ma, mb,
+                                         taps, kchunks, n_total, tiles, sched, epi);
+  return e == cudaSuccess ? ITTS_OK : (int)e;
 }
 
 }  // namespace

@@ -460,6 +460,8 @@ __global__ void k_enc_embed(const int32_t* __restrict__ tok4, int64_t total, con
                             const float* __restrict__ Eph, const float* __restrict__ Epw,
                             const float* __restrict__ Epph, const float* __restrict__ Eiph,
                             __nv_bfloat16* __restrict__ X) {
+  itts::pdl_trigger();
+  itts::pdl_wait();
   const int64_t* p = plan + blockIdx.y * EPLAN;
   const int64_t L = p[1];
   const int64_t g = (int64_t)blockIdx.x * 256 + threadIdx.x;
@@ -500,10 +502,8 @@ __global__ void __cluster_dims__(BL_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   const int rank = (int)cluster.block_rank();
   const int pair = blockIdx.x / BL_CLUSTER;
   const int item = pair >> 1, dir = pair & 1;
-  const int64_t* p = plan + item * EPLAN;
-  const int64_t L = p[1], row0 = p[2];
-  float* mem = reinterpret_cast<float*>(p[3]);
   const int tid = threadIdx.x;
+  itts::pdl_trigger();
 
   __shared__ __align__(16) float hbuf[2][EH];
   __shared__ float gpart[2][BL_ROWS];
@@ -515,6 +515,10 @@ __global__ void __cluster_dims__(BL_CLUSTER, 1, 1) __launch_bounds__(256, 1)
   float w[128];
 #pragma unroll
   for (int k = 0; k < 128; ++k) w[k] = __ldg(Wd + (int64_t)(half * 128 + k) * (4 * EH) + grow);
+  itts::pdl_wait();  // the input projection PRE comes from the previous kernel
+  const int64_t* p = plan + item * EPLAN;
+  const int64_t L = p[1], row0 = p[2];
+  float* mem = reinterpret_cast<float*>(p[3]);
   for (int i = tid; i < EH; i += 256) hbuf[0][i] = 0.f;
   if (tid < BL_UNITS) cst[tid] = 0.f;
   const uint32_t bar0 = cl_smem_u32(&hbar[0]);
@@ -591,6 +595,8 @@ __global__ void __cluster_dims__(BL_CLUSTER, 1, 1) __launch_bounds__(256, 1)
 
 // pm[t][a] = sum_k mem[t][k] WmT[k][a]; 16 rows per block.
 __global__ void __launch_bounds__(256) k_pmem(const int64_t* __restrict__ plan, const float* __restrict__ WmT) {
+  itts::pdl_trigger();
+  itts::pdl_wait();
   const int64_t* p = plan + blockIdx.y * EPLAN;
   const int64_t L = p[1];
   const float* mem = reinterpret_cast<const float*>(p[3]);
@@ -618,6 +624,8 @@ __global__ void __launch_bounds__(256) k_pmem(const int64_t* __restrict__ plan, 
 constexpr int MPLAN = 5;
 
 __global__ void k_mel_assemble(const int64_t* __restrict__ plan, __nv_bfloat16* __restrict__ X0, int ld) {
+  itts::pdl_trigger();
+  itts::pdl_wait();
   const int64_t* p = plan + blockIdx.y * MPLAN;
   const int64_t m = p[2], nt = p[3];
   const int64_t g = (int64_t)blockIdx.x * 256 + threadIdx.x;
@@ -636,6 +644,8 @@ __global__ void k_mel_assemble(const int64_t* __restrict__ plan, __nv_bfloat16* 
 // rowmap plan[i] = {in_base, in_rows (valid), in_halo, out_first (first valid output row), up}
 // row_out[in_base + r] = (valid ? out_first + up * (r - in_halo) : -1) for r in [0, 2*halo + rows).
 __global__ void k_rowmap(const int64_t* __restrict__ plan, int32_t* __restrict__ row_out) {
+  itts::pdl_trigger();
+  itts::pdl_wait();
   const int64_t* p = plan + blockIdx.y * 5;
   const int64_t span = 2 * p[2] + p[1];
   const int64_t r = (int64_t)blockIdx.x * 256 + threadIdx.x;
@@ -646,6 +656,8 @@ __global__ void k_rowmap(const int64_t* __restrict__ plan, int32_t* __restrict__
 
 // zero plan[i] = {base, rows, halo}: zero [base, base+halo) and [base+halo+rows, base+2halo+rows).
 __global__ void k_zero_halo(const int64_t* __restrict__ plan, __nv_bfloat16* __restrict__ X, int C) {
+  itts::pdl_trigger();
+  itts::pdl_wait();
   const int64_t* p = plan + blockIdx.y * 3;
   const int64_t halo = p[2];
   const int64_t g = (int64_t)blockIdx.x * 256 + threadIdx.x;
@@ -670,6 +682,8 @@ __global__ void __launch_bounds__(256) k_post_splice(const __nv_bfloat16* __rest
                                                      const float* __restrict__ wpost,  // [32][7]
                                                      float bpost, const float* __restrict__ fade, int O, int S,
                                                      float* __restrict__ audio, int16_t* __restrict__ pcm) {
+  itts::pdl_trigger();
+  itts::pdl_wait();
   const int64_t* p = plan + blockIdx.y * PPLAN;
   const int64_t G = p[1];
   const bool has_tail = p[2] & 1, is_last = p[2] & 2;
@@ -798,27 +812,33 @@ ITTS_API int itts_r_enc_embed(const int32_t* tok4, int64_t total, const int64_t*
                               int64_t max_len, const float* Eph, const float* Epw, const float* Epph,
                               const float* Eiph, void* X, void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
-  k_enc_embed<<<grid2(max_len * EMB, n), 256, 0, (cudaStream_t)stream>>>(tok4, total, plan, Eph, Epw, Epph, Eiph,
+  const cudaError_t le_ = itts::launch_pdl(k_enc_embed, dim3(grid2(max_len * EMB, n)), dim3(256), 0, (cudaStream_t)stream,
+                                           tok4, total, plan, Eph, Epw, Epph, Eiph,
                                                                         (__nv_bfloat16*)X);
+  if (le_ != cudaSuccess) return (int)le_;
   ITTS_RETURN_LAUNCH();
 }
 
 ITTS_API int itts_r_bilstm(const float* PRE, const int64_t* plan, int32_t n, const float* WhhT, void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
-  k_bilstm<<<n * 2 * BL_CLUSTER, 256, 0, (cudaStream_t)stream>>>(PRE, plan, WhhT);
-  ITTS_RETURN_LAUNCH();
+  const cudaError_t e = itts::launch_pdl(k_bilstm, dim3(n * 2 * BL_CLUSTER), dim3(256), 0, (cudaStream_t)stream, PRE,
+                                         plan, WhhT);
+  return e == cudaSuccess ? ITTS_OK : (int)e;
 }
 
 ITTS_API int itts_r_pmem(const int64_t* plan, int32_t n, int64_t max_len, const float* WmT, void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
   dim3 grid((unsigned)((max_len + 15) / 16), (unsigned)n);
-  k_pmem<<<grid, 256, 0, (cudaStream_t)stream>>>(plan, WmT);
+  const cudaError_t le_ = itts::launch_pdl(k_pmem, dim3(grid), dim3(256), 0, (cudaStream_t)stream, plan, WmT);
+  if (le_ != cudaSuccess) return (int)le_;
   ITTS_RETURN_LAUNCH();
 }
 
 // Zero n spans of fp32 (the fresh decoder-state rows of newly encoded requests): span i =
 // {ptr, count}; one launch instead of one memset per request.
 __global__ void k_zero_spans(const int64_t* __restrict__ spans) {
+  itts::pdl_trigger();
+  itts::pdl_wait();
   float* p = reinterpret_cast<float*>(spans[2 * blockIdx.y]);
   const int64_t cnt = spans[2 * blockIdx.y + 1];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
@@ -861,20 +881,25 @@ ITTS_API int itts_r_encode(const void* pack, int64_t total, int32_t n, int64_t m
     return r;
   if ((r = itts_r_bilstm(pre, plan, n, (const float*)W(12), stream))) return r;
   if ((r = itts_r_pmem(plan, n, max_len, (const float*)W(13), stream))) return r;
-  k_zero_spans<<<dim3(8, n), 256, 0, st>>>(spans);
+  const cudaError_t le_ = itts::launch_pdl(k_zero_spans, dim3(dim3(8, n)), dim3(256), 0, st, spans);
+  if (le_ != cudaSuccess) return (int)le_;
   ITTS_RETURN_LAUNCH();
 }
 
 ITTS_API int itts_r_mel_assemble(const int64_t* plan, int32_t n, int64_t max_rows, void* X0, int32_t ld,
                                  void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
-  k_mel_assemble<<<grid2(max_rows * ld, n), 256, 0, (cudaStream_t)stream>>>(plan, (__nv_bfloat16*)X0, ld);
+  const cudaError_t le_ = itts::launch_pdl(k_mel_assemble, dim3(grid2(max_rows * ld, n)), dim3(256), 0, (cudaStream_t)stream,
+                                           plan, (__nv_bfloat16*)X0, ld);
+  if (le_ != cudaSuccess) return (int)le_;
   ITTS_RETURN_LAUNCH();
 }
 
 ITTS_API int itts_r_rowmap(const int64_t* plan, int32_t n, int64_t max_span, int32_t* row_out, void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
-  k_rowmap<<<grid2(max_span, n), 256, 0, (cudaStream_t)stream>>>(plan, row_out);
+  const cudaError_t le_ = itts::launch_pdl(k_rowmap, dim3(grid2(max_span, n)), dim3(256), 0, (cudaStream_t)stream,
+                                           plan, row_out);
+  if (le_ != cudaSuccess) return (int)le_;
   ITTS_RETURN_LAUNCH();
 }
 
@@ -884,6 +909,8 @@ ITTS_API int itts_r_rowmap(const int64_t* plan, int32_t n, int64_t max_span, int
 __global__ void __launch_bounds__(256) k_mrf_combine(const uint4* __restrict__ y0, const uint4* __restrict__ y1,
                                                      const uint4* __restrict__ y2, int64_t n8, float slope,
                                                      uint4* __restrict__ out) {
+  itts::pdl_trigger();
+  itts::pdl_wait();
   const float third = 1.0f / 3.0f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     const uint4 a = __ldcs(y0 + i), b = __ldcs(y1 + i), c = __ldcs(y2 + i);
@@ -910,15 +937,19 @@ ITTS_API int itts_r_mrf_combine(const void* y0, const void* y1, const void* y2, 
   if (n == 0) return ITTS_OK;
   const int64_t n8 = n / 8;
   const int blocks = (int)std::min<int64_t>((n8 + 255) / 256, 148 * 8);
-  k_mrf_combine<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4*)y0, (const uint4*)y1, (const uint4*)y2, n8,
+  const cudaError_t le_ = itts::launch_pdl(k_mrf_combine, dim3(blocks), dim3(256), 0, (cudaStream_t)stream,
+                                           (const uint4*)y0, (const uint4*)y1, (const uint4*)y2, n8,
                                                           slope, (uint4*)out);
+  if (le_ != cudaSuccess) return (int)le_;
   ITTS_RETURN_LAUNCH();
 }
 
 ITTS_API int itts_r_zero_halo(const int64_t* plan, int32_t n, int64_t max_halo, void* X, int32_t C,
                               void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
-  k_zero_halo<<<grid2(2 * max_halo * C, n), 256, 0, (cudaStream_t)stream>>>(plan, (__nv_bfloat16*)X, C);
+  const cudaError_t le_ = itts::launch_pdl(k_zero_halo, dim3(grid2(2 * max_halo * C, n)), dim3(256), 0, (cudaStream_t)stream,
+                                           plan, (__nv_bfloat16*)X, C);
+  if (le_ != cudaSuccess) return (int)le_;
   ITTS_RETURN_LAUNCH();
 }
 
@@ -930,8 +961,10 @@ ITTS_API int itts_r_post_splice(const void* X4, const int64_t* plan, int32_t n, 
   cudaError_t e = cudaMemcpyToSymbolAsync(c_wpost, wpost, sizeof(float) * 32 * 7, 0, cudaMemcpyDeviceToDevice,
                                           (cudaStream_t)stream);
   if (e != cudaSuccess) return (int)e;
-  k_post_splice<<<grid2(work, n), 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)X4, plan, wpost, bpost,
+  const cudaError_t le_ = itts::launch_pdl(k_post_splice, dim3(grid2(work, n)), dim3(256), 0, (cudaStream_t)stream,
+                                           (const __nv_bfloat16*)X4, plan, wpost, bpost,
                                                                   fade, overlap_frames, overlap_samples, audio,
                                                                   (int16_t*)pcm16);
+  if (le_ != cudaSuccess) return (int)le_;
   ITTS_RETURN_LAUNCH();
 }

@@ -229,3 +229,20 @@ def test_native_vocoder_large_pool(engine):
     for i in (0, 131, 255):
         (solo, _), = engine.vocoder_batch([triples[i]])
         assert np.array_equal(batched[i][0].samples, solo.samples)
+
+
+def test_programmatic_dependent_launch_changes_nothing():
+    """Encoder + decoder + vocoder outputs are bit-identical with PDL on and off (ITTS_NO_PDL=1)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    digests = []
+    for no_pdl in ("0", "1", "0"):
+        env = dict(os.environ, ITTS_NO_PDL=no_pdl)
+        out = subprocess.run([sys.executable, str(root / "tools" / "pdl_check.py")], env=env, cwd=root,
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        digests.append(out.stdout.strip().splitlines()[-1])
+    assert digests[0] == digests[1] == digests[2], digests
