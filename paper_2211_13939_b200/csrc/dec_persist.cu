@@ -525,7 +525,7 @@ __device__ __forceinline__ void att_prefetch(const DecArgs& a, int b, int ta, in
 
 // ATT-A for one (item b, chunk [ta, tb)) whose rows are (being) staged in `stage`.
 __device__ void att_chunk(const DecArgs& a, AttSmem& sm, int s, int b, int ch, int ta, int tb, const uint8_t* stage,
-                          uint64_t* abar, uint32_t& aphase) {
+                          uint64_t* abar, uint32_t& aphase, bool load_q) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool tr = a.trace && blockIdx.x == 0 && tid == 0;
   unsigned long long t0 = tr ? gtimer() : 0;
@@ -542,7 +542,7 @@ __device__ void att_chunk(const DecArgs& a, AttSmem& sm, int s, int b, int ch, i
   const int n = tb - ta, nh = n + 2 * HALO;
   const float* sPm = reinterpret_cast<const float*>(stage);
   const float* sMem = sPm + n * ATT;
-  if (tid < ATT) {  // q = sum of the 32 unit-group partials, group order (8 loads in flight)
+  if (load_q && tid < ATT) {  // q = sum of the 32 unit-group partials, group order (kept for the item's next chunk)
     float qv[NGRP];
 #pragma unroll
     for (int z = 0; z < NGRP; ++z) qv[z] = ldf(a.Qp + ((int64_t)z * a.B + b) * ATT + tid);
@@ -934,29 +934,32 @@ __global__ void __launch_bounds__(NT, 1)
       auto locate = [&](int task, int& b) {
         while (sm.tstart[b + 1] <= task) ++b;
       };
-      if (c < ntask) {
-        locate(c, bnext);
+      // CTA c takes a contiguous run of tasks, so consecutive chunks of one item share its q
+      const int t0 = (int)((int64_t)c * ntask / G), t1 = (int)((int64_t)(c + 1) * ntask / G);
+      if (t0 < t1) {
+        locate(t0, bnext);
         if (tid == 0) {
-          const int ta = (c - sm.tstart[bnext]) * chunk;
+          const int ta = (t0 - sm.tstart[bnext]) * chunk;
           att_prefetch(a, bnext, ta, min(pc.L[bnext], ta + chunk), ring, &gsy.abar[0]);
         }
       }
       int i = 0;
-      for (int task = c; task < ntask; task += G, ++i) {
+      for (int task = t0; task < t1; ++task, ++i) {
         const int buf = i & 1;
+        const bool load_q = task == t0 || bnext != bcur;
         bcur = bnext;
         const int ch = task - sm.tstart[bcur];
         const int L = pc.L[bcur];
         const int ta = ch * chunk, tb = min(L, ta + chunk);
-        if (task + G < ntask) {  // the next chunk streams into the other buffer during this one
-          locate(task + G, bnext);
+        if (task + 1 < t1) {  // the next chunk streams into the other buffer during this one
+          locate(task + 1, bnext);
           if (tid == 0) {
-            const int ta2 = (task + G - sm.tstart[bnext]) * chunk;
+            const int ta2 = (task + 1 - sm.tstart[bnext]) * chunk;
             att_prefetch(a, bnext, ta2, min(pc.L[bnext], ta2 + chunk), ring + (buf ^ 1) * ASTAGE,
                          &gsy.abar[buf ^ 1]);
           }
         }
-        att_chunk(a, sm, gs, bcur, ch, ta, tb, ring + buf * ASTAGE, &gsy.abar[buf], aphase[buf]);
+        att_chunk(a, sm, gs, bcur, ch, ta, tb, ring + buf * ASTAGE, &gsy.abar[buf], aphase[buf], load_q);
       }
     }
     phase_end();
