@@ -186,6 +186,15 @@ int itts_r_mel_assemble(const int64_t* plan, int32_t n, int64_t max_rows, void* 
                         void* stream);
 int itts_r_rowmap(const int64_t* plan, int32_t n, int64_t max_span, int32_t* row_out, void* stream);
 int itts_r_zero_halo(const int64_t* plan, int32_t n, int64_t max_halo, void* X, int32_t C, void* stream);
+/* f3: chunk-local Tacotron2 PostNet over one decoder call's chunks (mel + PostNet(mel), 5 conv
+ * k5 layers on the tensor cores, tanh after the first four, zero padding at chunk edges).
+ * pack = mel-assembly plan [n][5] {0, mel_ptr, m, 0, first_row}, row-map plan [n][5], residual
+ * plan [n][4] {mel_ptr, out_ptr, m, first_row}; weights = (w bf16 [5][c_out][c_in], b fp32) x 5,
+ * the 80-wide ends padded to 96; x0 bf16 [rows][96], ya / yb bf16 [rows][512], post fp32
+ * [rows][96], rowmap int32 [rows] work buffers. */
+int itts_r_postnet(const int64_t* pack, int32_t n, int64_t max_m, int64_t rows, int64_t max_span,
+                   const int64_t* weights, void* x0, void* ya, void* yb, float* post, int32_t* rowmap,
+                   void* stream);
 /* MRF merge of HiFi-GAN V1 (the xs / num_kernels average of the three ResBlock1 branches):
  * out = bf16(lrelu((y0 + y1 + y2) / 3, slope)) over n bf16 elements (n % 8 == 0). */
 int itts_r_mrf_combine(const void* y0, const void* y1, const void* y2, int64_t n, float slope, void* out,

@@ -123,6 +123,19 @@ def decode_chunk(w, s: RState, memory, pmem, chunk_frames: int):
     return torch.stack(frames), False, s, gates
 
 
+def postnet(pw, mel: np.ndarray | torch.Tensor) -> np.ndarray:
+    """Chunk-local Tacotron2 PostNet: mel + PostNet(mel), 'same' zero padding at
+    the chunk edges; 5 x conv k5 with tanh after the first four (batch norm folded into the
+    weights of ``weights.postnet_weights``).  fp32 torch on the CPU."""
+    x = torch.as_tensor(np.asarray(mel, np.float32)).T[None]          # [1][80][T]
+    y = x
+    for i in range(W.POSTNET_LAYERS):
+        y = F.conv1d(y, pw[f"post.conv{i}.w"], pw[f"post.conv{i}.b"], padding=W.POSTNET_K // 2)
+        if i < W.POSTNET_LAYERS - 1:
+            y = torch.tanh(y)
+    return (x + y)[0].T.numpy().astype(np.float64)
+
+
 def _pad(k: int, d: int) -> int:
     return (k * d - d) // 2
 

@@ -62,6 +62,7 @@ struct Epi {
   int acc_mode;               // 0 none, 1 store, 2 add, 3 finalize: y = (acc + y) / 3
   float slope;                // leaky-ReLU slope for act_out (1.0 = identity, 0.0 = ReLU)
   int zero_halo;              // write zeros into act_out for halo rows (CONV mode only)
+  int act_tanh;               // act_out = bf16(tanh(y)) instead of the leaky ReLU (PostNet)
 };
 
 struct TileSched {
@@ -230,7 +231,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < CW; ++i) v[i] = a[i] * (1.0f / 3.0f);
           }
         }
-        if (epi.act_out) store_bf16<CW>(epi.act_out + o, v, epi.slope);
+        if (epi.act_out) {
+          if (epi.act_tanh) {
+#pragma unroll
+            for (int i = 0; i < CW; ++i) v[i] = tanhf(v[i]);
+          }
+          store_bf16<CW>(epi.act_out + o, v, epi.act_tanh ? 1.0f : epi.slope);
+        }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&tempty[b]);
@@ -272,11 +279,11 @@ int launch(const void* x, int64_t rows, int c_in, int64_t x_ld, const void* w, i
 
 }  // namespace
 
-ITTS_API int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, const void* w,
-                            int32_t n_total, int32_t n_taps, const int32_t* host_tap_off, const float* bias,
-                            int32_t c_out, const int32_t* row_out, const void* res_in, float res_slope,
-                            float* f32_out, int32_t ksplit, void* acc, int32_t acc_mode, void* act_out,
-                            float slope, int32_t zero_halo, int32_t bn, void* stream) {
+int conv1d_tc_impl(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, const void* w, int32_t n_total,
+                   int32_t n_taps, const int32_t* host_tap_off, const float* bias, int32_t c_out,
+                   const int32_t* row_out, const void* res_in, float res_slope, float* f32_out, int32_t ksplit,
+                   void* acc, int32_t acc_mode, void* act_out, float slope, int32_t zero_halo, int32_t bn,
+                   int32_t act_tanh, void* stream) {
   if (!x || !w || !bias || !row_out || !host_tap_off || rows <= 0) return ITTS_EINVAL;
   if (n_taps < 1 || n_taps > kMaxTaps || c_out <= 0 || n_total % c_out) return ITTS_EINVAL;
   if (c_out % 32 || (acc_mode && !acc) || acc_mode < 0 || acc_mode > 3) return ITTS_EINVAL;
@@ -288,7 +295,7 @@ ITTS_API int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, int64_t x
   taps.n = n_taps;
   for (int i = 0; i < n_taps; ++i) taps.off[i] = host_tap_off[i];
   Epi epi{bias, row_out, (const __nv_bfloat16*)res_in, res_slope, f32_out, rows * (int64_t)c_out,
-          (__nv_bfloat16*)acc, (__nv_bfloat16*)act_out, rows, c_out, acc_mode, slope, zero_halo};
+          (__nv_bfloat16*)acc, (__nv_bfloat16*)act_out, rows, c_out, acc_mode, slope, zero_halo, act_tanh};
   if (ksplit < 1) ksplit = 1;
   cudaStream_t st = (cudaStream_t)stream;
   const int swz = (c_in % 64 == 0) ? 128 : (c_in % 32 == 0 ? 64 : 0);
@@ -309,4 +316,13 @@ ITTS_API int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, int64_t x
     }
   }
   return ITTS_EUNSUPPORTED;
+}
+
+ITTS_API int itts_conv1d_tc(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, const void* w,
+                            int32_t n_total, int32_t n_taps, const int32_t* host_tap_off, const float* bias,
+                            int32_t c_out, const int32_t* row_out, const void* res_in, float res_slope,
+                            float* f32_out, int32_t ksplit, void* acc, int32_t acc_mode, void* act_out,
+                            float slope, int32_t zero_halo, int32_t bn, void* stream) {
+  return conv1d_tc_impl(x, rows, c_in, x_ld, w, n_total, n_taps, host_tap_off, bias, c_out, row_out, res_in,
+                        res_slope, f32_out, ksplit, acc, acc_mode, act_out, slope, zero_halo, bn, 0, stream);
 }

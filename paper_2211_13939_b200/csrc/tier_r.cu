@@ -886,6 +886,66 @@ ITTS_API int itts_r_encode(const void* pack, int64_t total, int32_t n, int64_t m
   ITTS_RETURN_LAUNCH();
 }
 
+// PostNet residual: out[t][c] = mel[t][c] + post[first + t][c] (c < 80) per item; plan[i] =
+// {mel_ptr, out_ptr, m, first_row}.
+__global__ void k_postnet_add(const int64_t* __restrict__ plan, const float* __restrict__ post, int32_t ld) {
+  itts::pdl_trigger();
+  itts::pdl_wait();
+  const int64_t* p = plan + 4 * blockIdx.y;
+  const float* mel = reinterpret_cast<const float*>(p[0]);
+  float* out = reinterpret_cast<float*>(p[1]);
+  const int64_t m = p[2], first = p[3];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m * NMEL; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / NMEL, c = i - t * NMEL;
+    out[i] = mel[i] + post[(first + t) * ld + c];
+  }
+}
+
+// Tacotron2 PostNet over the chunks of one decoder call (the paper's decoder
+// "contains ... a PostNet", absorbed as a no-op by the reference): 5 x conv k5
+// (80 -> 512 -> 512 -> 512 -> 512 -> 80, batch norm folded, tanh after the first four), mel_out =
+// mel + PostNet(mel), each chunk zero-padded at its edges (no look-ahead: chunk-local, so it adds
+// no latency; the decoder's fed-back last frame stays the pre-PostNet frame).  Items are packed
+// with 2-row zero halos like the vocoder stages.  pack = mel-assembly plan [n][5], row-map plan
+// [n][5], residual plan [n][4]; weights = (w, b) x 5 in tc_conv layout (c_in / c_out of the mel
+// ends padded to 96); x0 bf16 [rows][96], ya / yb bf16 [rows][512], post fp32 [rows][96].
+ITTS_API int itts_r_postnet(const int64_t* pack, int32_t n, int64_t max_m, int64_t rows, int64_t max_span,
+                            const int64_t* weights, void* x0, void* ya, void* yb, float* post, int32_t* rowmap,
+                            void* stream) {
+  if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
+  if (!pack || !weights || !x0 || !ya || !yb || !post || !rowmap || max_m < 1) return ITTS_EINVAL;
+  constexpr int CP = 96, CH = 512, TAPS = 5;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t* mplan = pack;
+  const int64_t* rm_plan = pack + 5 * (int64_t)n;
+  const int64_t* aplan = rm_plan + 5 * (int64_t)n;
+  auto W = [&](int i) { return reinterpret_cast<const void*>(weights[i]); };
+  cudaError_t e = cudaMemsetAsync(x0, 0, (size_t)rows * CP * 2, st);
+  if (e != cudaSuccess) return (int)e;
+  int r = itts_r_mel_assemble(mplan, n, max_m, x0, CP, stream);
+  if (r) return r;
+  if ((r = itts_r_rowmap(rm_plan, n, max_span, rowmap, stream))) return r;
+  int32_t offs[TAPS];
+  for (int j = 0; j < TAPS; ++j) offs[j] = j - (TAPS - 1) / 2;
+  const void* src = x0;
+  int c_in = CP;
+  void* bufs[2] = {ya, yb};
+  for (int l = 0; l < 4; ++l) {  // conv + tanh; zero halos keep the chunk-edge padding
+    const int bn = c_in % 64 ? 64 : 0;  // the 96-wide input uses the 64B-swizzle path (N tile <= 64)
+    if ((r = conv1d_tc_impl(src, rows, c_in, c_in, W(2 * l), CH, TAPS, offs, (const float*)W(2 * l + 1), CH, rowmap,
+                            nullptr, 1.0f, nullptr, 1, nullptr, 0, bufs[l & 1], 1.0f, 1, bn, 1, stream)))
+      return r;
+    src = bufs[l & 1];
+    c_in = CH;
+  }
+  if ((r = conv1d_tc_impl(src, rows, CH, CH, W(8), CP, TAPS, offs, (const float*)W(9), CP, rowmap, nullptr, 1.0f,
+                          post, 1, nullptr, 0, nullptr, 1.0f, 1, 0, 0, stream)))
+    return r;
+  const cudaError_t le = itts::launch_pdl(k_postnet_add, dim3((unsigned)((max_m * NMEL + 255) / 256), n), dim3(256), 0,
+                                          st, aplan, (const float*)post, CP);
+  return le == cudaSuccess ? ITTS_OK : (int)le;
+}
+
 ITTS_API int itts_r_mel_assemble(const int64_t* plan, int32_t n, int64_t max_rows, void* X0, int32_t ld,
                                  void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;

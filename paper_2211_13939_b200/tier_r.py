@@ -44,6 +44,8 @@ P_OFF, CTX_OFF, ATTH_OFF, DECH_OFF, ATTC_OFF, DECC_OFF, LAST_OFF, ROW = 0, 256, 
 XB_ROW = 2816
 ENC_HALO = 2        # conv k5
 ENC_TAPS = 5
+POST_HALO = 2       # PostNet conv k5 (chunk-local zero padding)
+POST_CP = 96        # PostNet mel channels padded for the tensor-core conv
 MEL_HALO = 3        # conv_pre k7
 MRF_HALO = 25       # k11 dilation 5
 UPS = (8, 8, 2, 2)
@@ -103,7 +105,8 @@ class _Layout:
 class TierREngine:
     dtype = torch.float32
 
-    def __init__(self, cfg: PipelineConfig, device=None, seed: int = 0, weights: dict | None = None):
+    def __init__(self, cfg: PipelineConfig, device=None, seed: int = 0, weights: dict | None = None,
+                 postnet: bool = False, postnet_weights: dict | None = None):
         self.cfg = validate_config(cfg)
         if cfg.hop_samples != 256:
             raise ValueError("HiFi-GAN V1 upsamples by 256: hop_samples must be 256")
@@ -132,6 +135,10 @@ class TierREngine:
         self.mrf_streams = True          # run the 3 MRF branches of a stage on 3 streams (fused path)
         self.native_vocoder = True       # issue the fused HiFi-GAN stack from C++ (voc_run.cu)
         self.native_encoder = True       # issue the encoder launch sequence from C++ (itts_r_encode)
+        # f3: chunk-local Tacotron2 PostNet on the decoder's mel output (off: the reference's no-op)
+        self.postnet = bool(postnet or postnet_weights is not None)
+        if self.postnet:
+            self._prepare_postnet(postnet_weights if postnet_weights is not None else W.postnet_weights(seed))
         enc_w = [*self.E]
         for wt, _, bias in self.enc_conv:
             enc_w += [wt, bias]
@@ -228,6 +235,46 @@ class TierREngine:
             self.res.append(blocks)
         self.wpost = f32(w["hg.conv_post.w"][0])                                        # [32][7]
         self.bpost = float(w["hg.conv_post.b"][0])
+
+    def set_postnet(self, enabled: bool, weights: dict | None = None) -> None:
+        """Turn the chunk-local PostNet (f3) on or off; weights default to postnet_weights(0)."""
+        if enabled and (weights is not None or not hasattr(self, "_post_ptrs")):
+            self._prepare_postnet(weights if weights is not None else W.postnet_weights(0))
+        self.postnet = bool(enabled)
+
+    def _prepare_postnet(self, pw: dict) -> None:
+        """PostNet layers in tc_conv layout; the 80-channel ends padded to 96 (c_in, c_out % 32)."""
+        d, layers = self.device, []
+        for i in range(W.POSTNET_LAYERS):
+            w = pw[f"post.conv{i}.w"].detach().float().to(d)
+            b = pw[f"post.conv{i}.b"].detach().float().to(d)
+            if w.shape[0] == W.N_MEL:   # last layer: 80 outputs -> 96 (zero rows)
+                w = torch.cat([w, w.new_zeros(POST_CP - W.N_MEL, *w.shape[1:])], 0)
+                b = torch.cat([b, b.new_zeros(POST_CP - W.N_MEL)])
+            wt, _ = tc.conv_weights(w, 1, c_in_pad=POST_CP if w.shape[1] == W.N_MEL else None)
+            layers += [wt, b.contiguous()]
+        self._post_layers = layers   # keeps the tensors alive
+        self._post_ptrs = (ctypes.c_int64 * len(layers))(*[t.data_ptr() for t in layers])
+
+    def _apply_postnet(self, src_ptrs: np.ndarray, out_ptrs: np.ndarray, ms: list[int]) -> None:
+        """out_i = mel_i + PostNet(mel_i) for n chunks of ms[i] frames (fp32 [m][80] at the given
+        device addresses), one itts_r_postnet call on the engine stream."""
+        n = len(ms)
+        lay = _Layout(ms, POST_HALO)
+        m_np = np.asarray(ms, np.int64)
+        mplan = np.stack([np.zeros(n, np.int64), src_ptrs, m_np, np.zeros(n, np.int64), lay.first], 1)
+        rm_plan = np.stack([lay.base, m_np, np.full(n, lay.halo, np.int64), lay.first, np.ones(n, np.int64)], 1)
+        aplan = np.stack([src_ptrs, out_ptrs, m_np, lay.first], 1)
+        pack = self._up(np.concatenate([mplan.reshape(-1), rm_plan.reshape(-1), aplan.reshape(-1)]))
+        x0 = self._buf("post_x0", lay.total * POST_CP)
+        ya = self._buf("post_ya", lay.total * W.POSTNET_CH)
+        yb = self._buf("post_yb", lay.total * W.POSTNET_CH)
+        post = self._buf("post_f32", lay.total * POST_CP, torch.float32)
+        rm = self._buf("post_rm", lay.total, torch.int32)
+        self._call("itts_r_postnet", pack.data_ptr(), n, max(ms), lay.total, max(ms) + 2 * lay.halo,
+                   self._post_ptrs, x0.data_ptr(), ya.data_ptr(), yb.data_ptr(), post.data_ptr(), rm.data_ptr(),
+                   self._st())
+        self.launches += 7
 
     def _create_native_vocoder(self) -> int:
         """Handle of the C++ launch sequence (voc_run.cu) over this engine's HiFi-GAN weights."""
@@ -478,6 +525,11 @@ class TierREngine:
                     bk.graph.replay()
                     self.launches += bk.launches
                 mel_all, gate_all = bk.mel[:n].clone(), bk.gate[:n].clone()
+                if self.postnet:
+                    rows = mel_all.data_ptr() + 4 * W.N_MEL * C * np.arange(n, dtype=np.int64)
+                    out = torch.empty_like(mel_all)
+                    self._apply_postnet(rows, out.data_ptr() + (rows - mel_all.data_ptr()), steps)
+                    mel_all = out
                 mels = [DeviceMelChunk.row_of(mel_all, i, steps[i], st.req, gate_all)
                         for i, (st, _) in enumerate(pairs)]
             else:
@@ -497,6 +549,11 @@ class TierREngine:
                 bufs = _DecBuffers(self, n, packed)
                 with self._mark("decoder", dec_bytes):
                     self._enqueue_decoder(bufs, max_L, max_steps)
+                if self.postnet:
+                    rows = mel.data_ptr() + 4 * W.N_MEL * mel_off[:-1]
+                    out = torch.empty_like(mel)
+                    self._apply_postnet(rows, out.data_ptr() + (rows - mel.data_ptr()), steps)
+                    mel = out
                 mels = [DeviceMelChunk(mel[int(mel_off[i]):int(mel_off[i + 1])], st.req)
                         for i, (st, _) in enumerate(pairs)]
                 for i, m in enumerate(mels):

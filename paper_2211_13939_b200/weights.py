@@ -136,5 +136,22 @@ def tier_r_weights(seed: int = 0) -> dict[str, torch.Tensor]:
     return w
 
 
+POSTNET_CH, POSTNET_K, POSTNET_LAYERS = 512, 5, 5
+
+
+def postnet_weights(seed: int = 0) -> dict[str, torch.Tensor]:
+    """Tacotron2 PostNet: 5 x conv k5, 80 -> 512 -> 512 -> 512 -> 512 -> 80, batch
+    norm folded (eval mode, unit running variance), tanh after the first four.  A separate stream
+    (seed + 7919) so the main Tier-R weights do not change."""
+    d, w = _Draw(seed + 7919), {}
+    bn = 1.0 / math.sqrt(1.0 + BN_EPS)
+    chans = [N_MEL] + [POSTNET_CH] * (POSTNET_LAYERS - 1) + [N_MEL]
+    for i in range(POSTNET_LAYERS):
+        gain = "tanh" if i < POSTNET_LAYERS - 1 else "linear"
+        w[f"post.conv{i}.w"] = d.xavier((chans[i + 1], chans[i], POSTNET_K), gain) * bn
+        w[f"post.conv{i}.b"] = d.bias(chans[i + 1], chans[i] * POSTNET_K) * bn
+    return w
+
+
 def parameter_count(w: dict[str, torch.Tensor], prefix: str = "") -> int:
     return sum(t.numel() for k, t in w.items() if k.startswith(prefix))

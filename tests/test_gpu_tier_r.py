@@ -246,3 +246,29 @@ def test_programmatic_dependent_launch_changes_nothing():
         assert out.returncode == 0, out.stderr[-2000:]
         digests.append(out.stdout.strip().splitlines()[-1])
     assert digests[0] == digests[1] == digests[2], digests
+
+
+def test_chunk_postnet_matches_oracle(engine, lexicon):
+    """f3: mel + PostNet(mel) per chunk (tensor-core convs, bf16 activations) vs the fp32 oracle."""
+    from paper_2211_13939_b200.weights import postnet_weights
+    pw = postnet_weights(0)
+    fos = [run_frontend(t, lexicon) for t in random_texts(lexicon, 5, 31, 8, 40)]
+    pairs = [(st, enc) for enc, st in engine.encoder_batch(fos)]
+    for graphs in (True, False):
+        engine.use_graphs = graphs
+        try:
+            engine.set_postnet(False)
+            pre = engine.decoder_batch(pairs)
+            engine.set_postnet(True, pw)
+            post = engine.decoder_batch(pairs)
+        finally:
+            engine.set_postnet(False)
+            engine.use_graphs = True
+        for a, b in zip(pre, post):
+            assert a.mel.frame_count == b.mel.frame_count and a.stop == b.stop
+            want = orc.postnet(pw, a.mel.frames)
+            got = np.asarray(b.mel.frames)
+            assert np.abs(got - want).max() <= 5e-2, np.abs(got - want).max()
+            assert np.sqrt(np.mean((got - want) ** 2)) <= 1e-2 * max(1.0, np.sqrt(np.mean(want ** 2)))
+            # the fed-back state is the pre-PostNet frame: both calls leave the same decoder state
+            assert np.array_equal(a.state.dec_hidden, b.state.dec_hidden)

@@ -55,6 +55,7 @@ def main():
     ap.add_argument("--no-graphs", action="store_true", help="eager decoder (stable kernel order for ncu -s/-c)")
     ap.add_argument("--unfused", action="store_true", help="MRF as two tc_conv launches per layer (A/B)")
     ap.add_argument("--serial-mrf", action="store_true", help="MRF branches one after another on one stream")
+    ap.add_argument("--postnet", action="store_true", help="chunk-local PostNet on the decoder output (f3)")
     args = ap.parse_args()
     cfg = PipelineConfig()
     eng = build_engine(cfg, args.tier, "cuda:0")
@@ -64,6 +65,8 @@ def main():
         eng.fused_mrf = False
     if args.serial_mrf:
         eng.mrf_streams = False
+    if args.postnet:
+        eng.set_postnet(True)
     lex = default_lexicon()
     rows = []
     for B in [int(b) for b in args.batches.split(",")]:
