@@ -195,6 +195,15 @@ int itts_r_zero_halo(const int64_t* plan, int32_t n, int64_t max_halo, void* X, 
 int itts_r_postnet(const int64_t* pack, int32_t n, int64_t max_m, int64_t rows, int64_t max_span,
                    const int64_t* weights, void* x0, void* ya, void* yb, float* post, int32_t* rowmap,
                    void* stream);
+/* f4: BERT prosodic-structure frontend (12 layers, hidden 768, 12 heads, FFN 3072, post-LN,
+ * GELU; three 2-way heads pw / pph / iph) over a pooled batch of texts packed without padding
+ * (csrc/bert.cu).  ids / pos int32 [rows]; plan int64 [n][2] {first row, length <= 256};
+ * weights = 150 device pointers (see bert.cu); row_map int32 [rows] = identity; work buffers
+ * xf fp32 / xb bf16 [rows][768], qkv bf16 [rows][2304], att bf16 [rows][768], y fp32
+ * [rows][768], h bf16 [rows][3072]; outputs logits fp32 [rows][6], tokens int32 [rows][3]. */
+int itts_bert_prosody(const int32_t* ids, const int32_t* pos, const int64_t* plan, int32_t n, int64_t rows,
+                      int32_t max_len, const int64_t* weights, const int32_t* row_map, float* xf, void* xb,
+                      void* qkv, void* att, float* y, void* h, float* logits, int32_t* tokens, void* stream);
 /* MRF merge of HiFi-GAN V1 (the xs / num_kernels average of the three ResBlock1 branches):
  * out = bf16(lrelu((y0 + y1 + y2) / 3, slope)) over n bf16 elements (n % 8 == 0). */
 int itts_r_mrf_combine(const void* y0, const void* y1, const void* y2, int64_t n, float slope, void* out,

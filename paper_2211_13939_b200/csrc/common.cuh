@@ -14,12 +14,13 @@
 // detected before any launch (so nothing is enqueued on failure).
 #include "incrtts_b200.h"
 
-// tc_conv.cu: itts_conv1d_tc with an optional tanh epilogue (act_tanh = 1), for the PostNet.
+// tc_conv.cu: itts_conv1d_tc with a choice of act_out activation: 0 leaky ReLU (slope), 1 tanh
+// (PostNet), 2 GELU tanh form (BERT frontend).
 int conv1d_tc_impl(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, const void* w, int32_t n_total,
                    int32_t n_taps, const int32_t* host_tap_off, const float* bias, int32_t c_out,
                    const int32_t* row_out, const void* res_in, float res_slope, float* f32_out, int32_t ksplit,
                    void* acc, int32_t acc_mode, void* act_out, float slope, int32_t zero_halo, int32_t bn,
-                   int32_t act_tanh, void* stream);
+                   int32_t act, void* stream);
 
 #define ITTS_RETURN_LAUNCH()                        \
   do {                                              \

@@ -62,7 +62,7 @@ struct Epi {
   int acc_mode;               // 0 none, 1 store, 2 add, 3 finalize: y = (acc + y) / 3
   float slope;                // leaky-ReLU slope for act_out (1.0 = identity, 0.0 = ReLU)
   int zero_halo;              // write zeros into act_out for halo rows (CONV mode only)
-  int act_tanh;               // act_out = bf16(tanh(y)) instead of the leaky ReLU (PostNet)
+  int act;                    // act_out activation: 0 leaky ReLU (slope), 1 tanh (PostNet), 2 GELU (tanh form, BERT)
 };
 
 struct TileSched {
@@ -232,11 +232,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (epi.act_out) {
-          if (epi.act_tanh) {
+          if (epi.act == 1) {
 #pragma unroll
             for (int i = 0; i < CW; ++i) v[i] = tanhf(v[i]);
+          } else if (epi.act == 2) {
+#pragma unroll
+            for (int i = 0; i < CW; ++i)
+              v[i] = 0.5f * v[i] * (1.0f + tanhf(0.7978845608f * (v[i] + 0.044715f * v[i] * v[i] * v[i])));
           }
-          store_bf16<CW>(epi.act_out + o, v, epi.act_tanh ? 1.0f : epi.slope);
+          store_bf16<CW>(epi.act_out + o, v, epi.act ? 1.0f : epi.slope);
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -283,7 +287,7 @@ int conv1d_tc_impl(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, cons
                    int32_t n_taps, const int32_t* host_tap_off, const float* bias, int32_t c_out,
                    const int32_t* row_out, const void* res_in, float res_slope, float* f32_out, int32_t ksplit,
                    void* acc, int32_t acc_mode, void* act_out, float slope, int32_t zero_halo, int32_t bn,
-                   int32_t act_tanh, void* stream) {
+                   int32_t act, void* stream) {
   if (!x || !w || !bias || !row_out || !host_tap_off || rows <= 0) return ITTS_EINVAL;
   if (n_taps < 1 || n_taps > kMaxTaps || c_out <= 0 || n_total % c_out) return ITTS_EINVAL;
   if (c_out % 32 || (acc_mode && !acc) || acc_mode < 0 || acc_mode > 3) return ITTS_EINVAL;
@@ -295,7 +299,7 @@ int conv1d_tc_impl(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, cons
   taps.n = n_taps;
   for (int i = 0; i < n_taps; ++i) taps.off[i] = host_tap_off[i];
   Epi epi{bias, row_out, (const __nv_bfloat16*)res_in, res_slope, f32_out, rows * (int64_t)c_out,
-          (__nv_bfloat16*)acc, (__nv_bfloat16*)act_out, rows, c_out, acc_mode, slope, zero_halo, act_tanh};
+          (__nv_bfloat16*)acc, (__nv_bfloat16*)act_out, rows, c_out, acc_mode, slope, zero_halo, act};
   if (ksplit < 1) ksplit = 1;
   cudaStream_t st = (cudaStream_t)stream;
   const int swz = (c_in % 64 == 0) ? 128 : (c_in % 32 == 0 ? 64 : 0);

@@ -32,9 +32,17 @@ def modules_for(engine, lexicon: Lexicon) -> PipelineModules:
 
 
 def build_modules(lexicon: Lexicon, cfg: PipelineConfig, tier: str = "s", device=None,
-                  **kw) -> PipelineModules:
-    """GPU module set behind the reference's plugin boundary."""
+                  frontend: str = "rule", **kw) -> PipelineModules:
+    """GPU module set behind the reference's plugin boundary.  ``frontend="bert"`` swaps the
+    rule-based prosody predictor for the GPU BERT frontend."""
     engine = build_engine(validate_config(cfg), tier, device, **kw)
     mods = modules_for(engine, lexicon)
+    if frontend == "bert":
+        from .bert_frontend import BertProsody
+        bert = BertProsody(lexicon, engine.device if hasattr(engine, "device") else device)
+        mods = PipelineModules(bert.frontend_batch, mods.encoder_batch, mods.decoder_batch, mods.vocoder_batch)
+        object.__setattr__(mods, "bert", bert)
+    elif frontend != "rule":
+        raise ValueError(f"unknown frontend {frontend!r}; expected 'rule' or 'bert'")
     object.__setattr__(mods, "engine", engine)  # for tests / bench introspection
     return mods
