@@ -12,7 +12,7 @@ GPU; the frontend stays on the host.
 from __future__ import annotations
 
 from .domain import PipelineConfig, validate_config
-from .frontend import Lexicon
+from .frontend import Lexicon, run_frontend
 from .scheduler import PipelineModules, frontend_module
 
 
@@ -26,9 +26,51 @@ def build_engine(cfg: PipelineConfig, tier: str = "s", device=None, **kw):
     raise ValueError(f"unknown tier {tier!r}; expected 's' or 'r'")
 
 
+class PrefetchingFrontend:
+    """The host frontend (``run_frontend``, identical outputs) with a bounded memo that the
+    scheduler loop fills for just-submitted texts while it waits on the GPU (the engine's
+    ``idle_hook``), so a request's frontend work is usually done before its admitting iteration
+    starts.  Outputs are immutable, so a memoised value is the value the call would compute."""
+
+    def __init__(self, lexicon: Lexicon, cap: int = 512):
+        self.lexicon, self.cap = lexicon, cap
+        self._memo: dict = {}
+        self._consumed: set = set()
+
+    def __call__(self, texts: list[str]) -> list:
+        out = []
+        for text in texts:
+            fo = self._memo.pop(text, None)
+            if fo is None:
+                fo = run_frontend(text, self.lexicon)   # raises for bad input, as the plain module
+                self._consumed.add(text)
+            out.append(fo)
+        return out
+
+    def prefetch(self, texts: list[str], done=lambda: False) -> None:
+        """Frontend outputs for `texts` until `done()` (the GPU work being waited on finished)."""
+        consumed, self._consumed = self._consumed, set()
+        for text in texts:
+            if done():
+                return
+            if text in consumed or text in self._memo:
+                continue
+            try:
+                fo = run_frontend(text, self.lexicon)
+            except Exception:  # noqa: BLE001 -- the admitting iteration reports it per item
+                continue
+            if len(self._memo) >= self.cap:
+                self._memo.pop(next(iter(self._memo)))
+            self._memo[text] = fo
+
+
 def modules_for(engine, lexicon: Lexicon) -> PipelineModules:
-    return PipelineModules(frontend_module(lexicon), engine.encoder_batch, engine.decoder_batch,
-                           engine.vocoder_batch)
+    fe = PrefetchingFrontend(lexicon) if hasattr(engine, "idle_hook") else frontend_module(lexicon)
+    mods = PipelineModules(fe, engine.encoder_batch, engine.decoder_batch, engine.vocoder_batch)
+    object.__setattr__(mods, "engine", engine)
+    if isinstance(fe, PrefetchingFrontend):
+        object.__setattr__(mods, "frontend_prefetch", fe.prefetch)
+    return mods
 
 
 def build_modules(lexicon: Lexicon, cfg: PipelineConfig, tier: str = "s", device=None,

@@ -135,6 +135,9 @@ class TierREngine:
         self.mrf_streams = True          # run the 3 MRF branches of a stage on 3 streams (fused path)
         self.native_vocoder = True       # issue the fused HiFi-GAN stack from C++ (voc_run.cu)
         self.native_encoder = True       # issue the encoder launch sequence from C++ (itts_r_encode)
+        # host work the scheduler loop runs while vocoder_batch waits on the GPU: idle_hook(done)
+        # with done() -> True once the awaited work finished (set by SchedulerLoop)
+        self.idle_hook = None
         # f3: chunk-local Tacotron2 PostNet on the decoder's mel output (off: the reference's no-op)
         self.postnet = bool(postnet or postnet_weights is not None)
         if self.postnet:
@@ -695,6 +698,10 @@ class TierREngine:
                 self._pin_out = torch.empty(int(audio.numel() * 1.5), dtype=torch.float32, pin_memory=True)
             host = self._pin_out[:audio.numel()]
             host.copy_(audio, non_blocking=True)
+        if self.idle_hook is not None:
+            done = torch.cuda.Event()
+            done.record(self.stream)
+            self.idle_hook(done.query)
         self.stream.synchronize()
         self.d2h_bytes += 4 * int(out_off[-1])
         flat = host.numpy()[:int(out_off[-1])].copy()   # the chunks own their samples
