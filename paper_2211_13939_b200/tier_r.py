@@ -698,23 +698,28 @@ class TierREngine:
                 self._pin_out = torch.empty(int(audio.numel() * 1.5), dtype=torch.float32, pin_memory=True)
             host = self._pin_out[:audio.numel()]
             host.copy_(audio, non_blocking=True)
+        # result objects are built while the GPU works: the chunks are read-only views of `flat`,
+        # which receives the samples after the wait (the chunks own it: no pinned buffer escapes)
+        total = int(out_off[-1])
+        flat = np.empty(total, dtype=np.float32)
+        out = []
+        for i, (req, dst, emitted) in enumerate(results):
+            chunk = AudioChunk.trusted(flat[out_off[i]:out_off[i + 1]], emitted)
+            out.append((chunk, DeviceVocoderState(req, dst, emitted + counts[i])))
         if self.idle_hook is not None:
             done = torch.cuda.Event()
             done.record(self.stream)
             self.idle_hook(done.query)
         self.stream.synchronize()
-        self.d2h_bytes += 4 * int(out_off[-1])
-        flat = host.numpy()[:int(out_off[-1])].copy()   # the chunks own their samples
-        if not np.isfinite(flat[:out_off[-1]]).all():
+        self.d2h_bytes += 4 * total
+        np.copyto(flat, host.numpy()[:total])
+        if not np.isfinite(flat).all():
             raise ValueError("array contains non-finite values")
-        out = []
-        pcm_np = host_pcm.numpy() if self.pcm16 else None
-        for i, (req, dst, emitted) in enumerate(results):
-            chunk = AudioChunk.trusted(flat[out_off[i]:out_off[i + 1]], emitted)
-            if pcm_np is not None:
+        if self.pcm16:
+            pcm_np = host_pcm.numpy()
+            for i, (chunk, _) in enumerate(out):
                 object.__setattr__(chunk, "_pcm16", pcm_np[out_off[i]:out_off[i + 1]].astype("<i2").tobytes())
                 self.d2h_bytes += 2 * counts[i]
-            out.append((chunk, DeviceVocoderState(req, dst, emitted + counts[i])))
         return out
 
     def _mrf_branches(self, s: int, XA, OA_next, scratch, outs, rm, slope_out: float) -> None:
