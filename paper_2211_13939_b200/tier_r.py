@@ -102,6 +102,37 @@ class _Layout:
         self.first = self.base + halo   # first valid row per item
 
 
+class _Mark:
+    __slots__ = ("engine", "kind", "units", "e0")
+
+    def __init__(self, engine, kind, units):
+        self.engine, self.kind, self.units = engine, kind, units
+
+    def __enter__(self):
+        self.e0 = torch.cuda.Event(enable_timing=True)
+        self.e0.record(self.engine.stream)
+        return self
+
+    def __exit__(self, *exc):
+        if exc[0] is None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(self.engine.stream)
+            units = self.units() if callable(self.units) else self.units
+            self.engine.timers.append((self.kind, self.e0, e1, units))
+        return False
+
+
+class _NoMark:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+_NO_MARK = _NoMark()
+
+
 class TierREngine:
     dtype = torch.float32
 
@@ -138,6 +169,8 @@ class TierREngine:
         # host work the scheduler loop runs while vocoder_batch waits on the GPU: idle_hook(done)
         # with done() -> True once the awaited work finished (set by SchedulerLoop)
         self.idle_hook = None
+        self._spec_src = None            # continuing (state, features) of the last decoder call
+        self._spec = None                # their precomputed plan fields (see _speculate_next_decoder)
         # f3: chunk-local Tacotron2 PostNet on the decoder's mel output (off: the reference's no-op)
         self.postnet = bool(postnet or postnet_weights is not None)
         if self.postnet:
@@ -155,25 +188,10 @@ class TierREngine:
         self._pin_out = torch.empty(1 << 22, dtype=torch.float32, pin_memory=True)  # audio D2H
         self._graph_warm = False
 
-    def _mark(self, kind: str, units: float):
-        """Context manager recording CUDA events on the engine stream around a region."""
-        engine = self
-
-        class _M:
-            def __enter__(self):
-                if engine.timers is not None:
-                    self.e0 = torch.cuda.Event(enable_timing=True)
-                    self.e0.record(engine.stream)
-                return self
-
-            def __exit__(self, *exc):
-                if engine.timers is not None and exc[0] is None:
-                    e1 = torch.cuda.Event(enable_timing=True)
-                    e1.record(engine.stream)
-                    engine.timers.append((kind, self.e0, e1, units))
-                return False
-
-        return _M()
+    def _mark(self, kind: str, units):
+        """Context manager recording CUDA events on the engine stream around a region (timers on);
+        `units` may be a callable, evaluated only then."""
+        return _Mark(self, kind, units) if self.timers is not None else _NO_MARK
 
     def _up(self, arr: np.ndarray) -> torch.Tensor:
         self.h2d_bytes += arr.nbytes
@@ -461,14 +479,12 @@ class TierREngine:
                 for req, buf in reqs]
 
     # ------------------------------------------------------------ decoder
-    def decoder_batch(self, pairs) -> list:
-        n = len(pairs)
-        if n == 0:
-            return []
+    def _dec_items(self, pairs, taken: set, cols=None) -> list:
+        """Per-item decoder plan fields (steps, L, dst buffer, mem / pm / src / dst offsets) --
+        the host work between the previous vocoder wait and the decoder launch."""
         C = self.cfg.chunk_frames
-        a = self.arena
-        # one pass over the items (host work here delays the decoder launch)
-        steps, dsts, Ls, mem_off, pm_off, src_off, dst_off, taken = [], [], [], [], [], [], [], set()
+        cols = cols if cols is not None else ([], [], [], [], [], [], [])
+        steps, dsts, Ls, mem_off, pm_off, src_off, dst_off = cols
         for state, enc in pairs:
             if type(state) is not DeviceDecoderState or type(enc) is not DeviceEncodedFeatures:
                 if not isinstance(state, DeviceDecoderState) or not isinstance(enc, DeviceEncodedFeatures):
@@ -489,13 +505,47 @@ class TierREngine:
             pm_off.append(ex["pm_off"])
             src_off.append(state.buf.off)
             dst_off.append(d.off)
+        return cols
+
+    def _speculate_next_decoder(self) -> None:
+        """While the vocoder runs: the plan fields of the items that continue (the last decoder
+        call's non-stopped results, in order -- the next call's batch prefix unless the
+        scheduler drops an item).  decoder_batch uses them only if its pairs start with exactly
+        these state / feature objects; the buffer claims are the ones it would make (the previous
+        states are gone by now, so the free ping-pong buffer is determined)."""
+        src, self._spec_src = self._spec_src, None
+        self._spec = None
+        if not src:
+            return
+        taken: set = set()
+        try:
+            cols = self._dec_items(src, taken)
+        except Exception:  # noqa: BLE001 -- the real call raises (and is retried per item) itself
+            return
+        self._spec = (src, taken, cols)
+
+    def decoder_batch(self, pairs) -> list:
+        n = len(pairs)
+        if n == 0:
+            return []
+        C = self.cfg.chunk_frames
+        a = self.arena
+        spec, self._spec = self._spec, None
+        if (spec is not None and len(spec[0]) <= n
+                and all(p[0] is q[0] and p[1] is q[1] for p, q in zip(pairs, spec[0]))):
+            taken, cols = spec[1], tuple(list(c) for c in spec[2])
+            self._dec_items(pairs[len(spec[0]):], taken, cols)   # the newly admitted items
+        else:
+            taken = set()
+            cols = self._dec_items(pairs, taken)
+        steps, dsts, Ls, mem_off, pm_off, src_off, dst_off = cols
         base = a.ptr(0)
         max_L, max_steps = max(Ls), max(steps)
         steps_np = np.array(steps, dtype=np.int64)
         Ls_np = np.array(Ls, dtype=np.int64)
         src = base + 4 * np.array(src_off, dtype=np.int64)
         dstp = base + 4 * np.array(dst_off, dtype=np.int64)
-        dec_bytes = max_steps * DEC_WEIGHT_BYTES + int(
+        dec_bytes = lambda: max_steps * DEC_WEIGHT_BYTES + int(  # algorithmic bytes (timers only)
             (steps_np * (2 * 4 * ROW + Ls_np * (4 * 512 + 4 * 128 + 16) + 4 * 81)).sum())
         with torch.cuda.stream(self.stream):
             if self.use_graphs and max_steps == C and max_L <= GRAPH_MAX_L:
@@ -566,6 +616,7 @@ class TierREngine:
             emitted = state.frames_emitted + k
             out.append(DecodeChunkResult(m, emitted >= state.target_frames,
                                          DeviceDecoderState(state.req, dst, emitted, state.target_frames)))
+        self._spec_src = [(r.state, enc) for r, (_, enc) in zip(out, pairs) if not r.stop]
         return out
 
     def _enqueue_decoder(self, b: "_DecBuffers", max_L: int, nsteps: int) -> None:
@@ -706,6 +757,7 @@ class TierREngine:
         for i, (req, dst, emitted) in enumerate(results):
             chunk = AudioChunk.trusted(flat[out_off[i]:out_off[i + 1]], emitted)
             out.append((chunk, DeviceVocoderState(req, dst, emitted + counts[i])))
+        self._speculate_next_decoder()
         if self.idle_hook is not None:
             done = torch.cuda.Event()
             done.record(self.stream)
