@@ -175,7 +175,7 @@ ITTS_API int itts_bert_prosody(const int32_t* ids, const int32_t* pos, const int
   auto P = [&](int i) { return reinterpret_cast<const void*>(weights[i]); };
   auto F = [&](int i) { return reinterpret_cast<const float*>(weights[i]); };
   const dim3 rgrid((unsigned)((rows + 7) / 8));
-  cudaError_t e = itts::launch_pdl(k_bert_embed_ln, rgrid, dim3(256), 0, st, ids, pos, rows, F(0), F(1), F(2), F(3),
+  cudaError_t e = itts::launch_pdl_cls(itts::PDL_BERT, k_bert_embed_ln, rgrid, dim3(256), 0, st, ids, pos, rows, F(0), F(1), F(2), F(3),
                                    xf, (__nv_bfloat16*)xb);
   if (e != cudaSuccess) return (int)e;
   const size_t att_smem = sizeof(float) * (MAXLEN * (HD + 1) + MAXLEN * HD + 8 * MAXLEN + 8 * HD);
@@ -194,14 +194,14 @@ ITTS_API int itts_bert_prosody(const int32_t* ids, const int32_t* pos, const int
     if ((r = conv1d_tc_impl(xb, rows, HB, HB, P(w), 3 * HB, 1, &off0, F(w + 1), 3 * HB, row_map, nullptr, 1.0f,
                             nullptr, 1, nullptr, 0, qkv, 1.0f, 0, 0, 0, stream)))
       return r;
-    if ((e = itts::launch_pdl(k_bert_attn, dim3(n, NH), dim3(256), att_smem, st, (const __nv_bfloat16*)qkv, plan,
+    if ((e = itts::launch_pdl_cls(itts::PDL_BERT, k_bert_attn, dim3(n, NH), dim3(256), att_smem, st, (const __nv_bfloat16*)qkv, plan,
                               (__nv_bfloat16*)att)) != cudaSuccess)
       return (int)e;
     // y = att Wo^T + bo (fp32); x = LN(x + y)
     if ((r = conv1d_tc_impl(att, rows, HB, HB, P(w + 2), HB, 1, &off0, F(w + 3), HB, row_map, nullptr, 1.0f, y, 1,
                             nullptr, 0, nullptr, 1.0f, 0, 0, 0, stream)))
       return r;
-    if ((e = itts::launch_pdl(k_bert_add_ln, rgrid, dim3(256), 0, st, (const float*)y, rows, F(w + 4), F(w + 5), xf,
+    if ((e = itts::launch_pdl_cls(itts::PDL_BERT, k_bert_add_ln, rgrid, dim3(256), 0, st, (const float*)y, rows, F(w + 4), F(w + 5), xf,
                               (__nv_bfloat16*)xb)) != cudaSuccess)
       return (int)e;
     // h = GELU(x W1^T + b1) (bf16); y = h W2^T + b2; x = LN(x + y)
@@ -211,11 +211,11 @@ ITTS_API int itts_bert_prosody(const int32_t* ids, const int32_t* pos, const int
     if ((r = conv1d_tc_impl(h, rows, FF, FF, P(w + 8), HB, 1, &off0, F(w + 9), HB, row_map, nullptr, 1.0f, y, 1,
                             nullptr, 0, nullptr, 1.0f, 0, 0, 0, stream)))
       return r;
-    if ((e = itts::launch_pdl(k_bert_add_ln, rgrid, dim3(256), 0, st, (const float*)y, rows, F(w + 10), F(w + 11), xf,
+    if ((e = itts::launch_pdl_cls(itts::PDL_BERT, k_bert_add_ln, rgrid, dim3(256), 0, st, (const float*)y, rows, F(w + 10), F(w + 11), xf,
                               (__nv_bfloat16*)xb)) != cudaSuccess)
       return (int)e;
   }
-  e = itts::launch_pdl(k_bert_heads, rgrid, dim3(256), 0, st, (const float*)xf, rows, F(4 + 12 * NL),
+  e = itts::launch_pdl_cls(itts::PDL_BERT, k_bert_heads, rgrid, dim3(256), 0, st, (const float*)xf, rows, F(4 + 12 * NL),
                        F(5 + 12 * NL), logits, tokens);
   return e == cudaSuccess ? ITTS_OK : (int)e;
 }

@@ -304,8 +304,8 @@ __global__ void __launch_bounds__(Cfg<C>::THREADS, Cfg<C>::CPS)
       for (int b = 0; b < NB; ++b) {
         const int i = b * 128 + q * 32 + lane;
         const int64_t gt = r0 - h2 + i, go = r0 + i;
-        if (gt >= 0 && gt < a.rows && __ldg(a.row_out + gt) >= 0) vT |= 1u << b;
-        if (i < a.m_out && go < a.rows && __ldg(a.row_out + go) >= 0) vO |= 1u << b;
+        if (gt >= 0 && gt < a.rows && __ldcg(a.row_out + gt) >= 0) vT |= 1u << b;
+        if (i < a.m_out && go < a.rows && __ldcg(a.row_out + go) >= 0) vO |= 1u << b;
       }
       // ---- epilogue 1: acc1 -> T tile (bf16, swizzled), panel-major
       tw.wait(a1_full, ph, 0);
@@ -472,7 +472,7 @@ int launch(const void* x, int64_t rows, const void* w1, const void* w2, int taps
   a.num_tiles = (int)((rows + a.m_out - 1) / a.m_out);
   const int slots = num_sms() * K::CPS;
   const int grid = a.num_tiles < slots ? a.num_tiles : slots;
-  const cudaError_t e = itts::launch_pdl(k_resblock_tc<C>, dim3(grid), dim3(K::THREADS), K::SMEM, st, mx, m1, m2,
+  const cudaError_t e = itts::launch_pdl_cls(itts::PDL_RESBLOCK, k_resblock_tc<C>, dim3(grid), dim3(K::THREADS), K::SMEM, st, mx, m1, m2,
                                          mr, mo, mo2, a);
   return e == cudaSuccess ? ITTS_OK : (int)e;
 }

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t b = lt & 1, tph = (lt >> 1) & 1;
       const int64_t r = (int64_t)mt * kBlockM + quarter * 32 + lane;
       const bool in_range = r < epi.rows;
-      const int out_row = in_range ? __ldg(epi.row_out + r) : -1;
+      const int out_row = in_range ? __ldcg(epi.row_out + r) : -1;
       mbar_wait(&tfull[b], tph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
@@ -276,7 +276,7 @@ int launch(const void* x, int64_t rows, int c_in, int64_t x_ld, const void* w, i
   const int m_tiles = (int)((rows + kBlockM - 1) / kBlockM);
   const int tiles = m_tiles * sched.n_tiles * ksplit;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  const cudaError_t e = itts::launch_pdl(k_conv_tc<BN, SWZ, STAGES>, dim3(grid), dim3(kThreads), smem, st, ma, mb,
+  const cudaError_t e = itts::launch_pdl_cls(itts::PDL_CONV, k_conv_tc<BN, SWZ, STAGES>, dim3(grid), dim3(kThreads), smem, st, ma, mb,
                                          taps, kchunks, n_total, tiles, sched, epi);
   return e == cudaSuccess ? ITTS_OK : (int)e;
 }

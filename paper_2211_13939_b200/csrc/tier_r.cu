@@ -821,7 +821,7 @@ ITTS_API int itts_r_enc_embed(const int32_t* tok4, int64_t total, const int64_t*
 
 ITTS_API int itts_r_bilstm(const float* PRE, const int64_t* plan, int32_t n, const float* WhhT, void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
-  const cudaError_t e = itts::launch_pdl(k_bilstm, dim3(n * 2 * BL_CLUSTER), dim3(256), 0, (cudaStream_t)stream, PRE,
+  const cudaError_t e = itts::launch_pdl_cls(itts::PDL_BILSTM, k_bilstm, dim3(n * 2 * BL_CLUSTER), dim3(256), 0, (cudaStream_t)stream, PRE,
                                          plan, WhhT);
   return e == cudaSuccess ? ITTS_OK : (int)e;
 }

@@ -43,6 +43,8 @@ class PrefetchingFrontend:
             fo = self._memo.pop(text, None)
             if fo is None:
                 fo = run_frontend(text, self.lexicon)   # raises for bad input, as the plain module
+                if len(self._consumed) >= 4 * self.cap:   # no prefetcher draining it
+                    self._consumed.clear()
                 self._consumed.add(text)
             out.append(fo)
         return out

@@ -169,6 +169,7 @@ class TierREngine:
         # host work the scheduler loop runs while vocoder_batch waits on the GPU: idle_hook(done)
         # with done() -> True once the awaited work finished (set by SchedulerLoop)
         self.idle_hook = None
+        self.speculate = False           # precompute the next decoder call's item fields during V waits (off: see DESIGN §10)
         self._spec_src = None            # continuing (state, features) of the last decoder call
         self._spec = None                # their precomputed plan fields (see _speculate_next_decoder)
         # f3: chunk-local Tacotron2 PostNet on the decoder's mel output (off: the reference's no-op)
@@ -515,7 +516,7 @@ class TierREngine:
         states are gone by now, so the free ping-pong buffer is determined)."""
         src, self._spec_src = self._spec_src, None
         self._spec = None
-        if not src:
+        if not src or not self.speculate:
             return
         taken: set = set()
         try:
