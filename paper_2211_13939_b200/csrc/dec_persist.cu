@@ -39,6 +39,12 @@
 // start with their att_h columns and wait for the combined contexts on a counter (one grid
 // barrier fewer per step; same-box A/B: B=1 -4.4%, B=24 -2.7%, B=128 +2.5%, hence the cut-off).
 // Larger batches: separate ATT-B phase.
+#ifndef DEC_QREUSE
+#define DEC_QREUSE 1  // contiguous runs keep q across chunks of the same item
+#endif
+#ifndef DEC_CONTIG
+#define DEC_CONTIG 0  // ATT-A: 1 = contiguous task runs per CTA (q reused; off: see DESIGN §10), 0 = round-robin
+#endif
 #ifndef DEC_MERGE_B
 #define DEC_MERGE_B 96
 #endif
@@ -935,7 +941,11 @@ __global__ void __launch_bounds__(NT, 1)
         while (sm.tstart[b + 1] <= task) ++b;
       };
       // CTA c takes a contiguous run of tasks, so consecutive chunks of one item share its q
-      const int t0 = (int)((int64_t)c * ntask / G), t1 = (int)((int64_t)(c + 1) * ntask / G);
+#if DEC_CONTIG
+      const int t0 = (int)((int64_t)c * ntask / G), t1 = (int)((int64_t)(c + 1) * ntask / G), tstep = 1;
+#else
+      const int t0 = c, t1 = ntask, tstep = G;
+#endif
       if (t0 < t1) {
         locate(t0, bnext);
         if (tid == 0) {
@@ -944,17 +954,17 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
       int i = 0;
-      for (int task = t0; task < t1; ++task, ++i) {
+      for (int task = t0; task < t1; task += tstep, ++i) {
         const int buf = i & 1;
-        const bool load_q = task == t0 || bnext != bcur;
+        const bool load_q = DEC_CONTIG == 0 || !DEC_QREUSE || task == t0 || bnext != bcur;
         bcur = bnext;
         const int ch = task - sm.tstart[bcur];
         const int L = pc.L[bcur];
         const int ta = ch * chunk, tb = min(L, ta + chunk);
-        if (task + 1 < t1) {  // the next chunk streams into the other buffer during this one
-          locate(task + 1, bnext);
+        if (task + tstep < t1) {  // the next chunk streams into the other buffer during this one
+          locate(task + tstep, bnext);
           if (tid == 0) {
-            const int ta2 = (task + 1 - sm.tstart[bnext]) * chunk;
+            const int ta2 = (task + tstep - sm.tstart[bnext]) * chunk;
             att_prefetch(a, bnext, ta2, min(pc.L[bnext], ta2 + chunk), ring + (buf ^ 1) * ASTAGE,
                          &gsy.abar[buf ^ 1]);
           }

@@ -169,6 +169,9 @@ class TierREngine:
         # host work the scheduler loop runs while vocoder_batch waits on the GPU: idle_hook(done)
         # with done() -> True once the awaited work finished (set by SchedulerLoop)
         self.idle_hook = None
+        self.diagnose = True             # on a non-finite chunk, record which inputs were already bad
+        self.plan_staging = True         # decoder graph plans: rewrite only the rows that changed
+        self.failures: list = []
         self.speculate = False           # precompute the next decoder call's item fields during V waits (off: see DESIGN §10)
         self._spec_src = None            # continuing (state, features) of the last decoder call
         self._spec = None                # their precomputed plan fields (see _speculate_next_decoder)
@@ -555,6 +558,9 @@ class TierREngine:
                 hn = bk.host_np
                 if bk.pending:  # the previous H2D out of the staging buffer must have finished
                     bk.copied.synchronize()
+                if not self.plan_staging:   # whole template rewritten (A/B of the row-wise staging)
+                    hn[:] = bk.template
+                    bk.dirty = 0
                 if bk.dirty > n:  # rows [n, dirty) go back to the idle template
                     for lo, hi in ((0, 8 * B), (8 * B, 9 * B), (9 * B, 10 * B)):
                         step = 8 if hi - lo == 8 * B else 1
@@ -767,6 +773,8 @@ class TierREngine:
         self.d2h_bytes += 4 * total
         np.copyto(flat, host.numpy()[:total])
         if not np.isfinite(flat).all():
+            if self.diagnose:
+                self._diagnose_nonfinite(triples, flat, out_off)
             raise ValueError("array contains non-finite values")
         if self.pcm16:
             pcm_np = host_pcm.numpy()
@@ -774,6 +782,22 @@ class TierREngine:
                 object.__setattr__(chunk, "_pcm16", pcm_np[out_off[i]:out_off[i + 1]].astype("<i2").tobytes())
                 self.d2h_bytes += 2 * counts[i]
         return out
+
+    def _diagnose_nonfinite(self, triples, flat, out_off) -> None:
+        """Failure path only: which inputs of the non-finite chunks are already non-finite."""
+        import sys
+        for i, (vstate, mel, last) in enumerate(triples):
+            if np.isfinite(flat[out_off[i]:out_off[i + 1]]).all():
+                continue
+            req = getattr(mel, "req", None)
+            info = {"item": i, "batch": len(triples), "frames": mel.frame_count, "last": bool(last),
+                    "mel_finite": bool(np.isfinite(np.asarray(mel.frames)).all())}
+            if req is not None:
+                info["L"] = req.seq_len
+                info["enc_finite"] = bool(np.isfinite(self.read_features(req)).all())
+                info["pmem_finite"] = bool(np.isfinite(self.read_processed_memory(req)).all())
+            self.failures.append(info)
+            print("itts non-finite chunk:", info, file=sys.stderr, flush=True)
 
     def _mrf_branches(self, s: int, XA, OA_next, scratch, outs, rm, slope_out: float) -> None:
         """One MRF stage: the three ResBlock1 branches each write their own y (last layer in

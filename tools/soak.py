@@ -21,11 +21,13 @@ ap.add_argument("--seconds", type=float, default=60)
 ap.add_argument("--no-spec", action="store_true")
 ap.add_argument("--no-prefetch", action="store_true", help="no frontend prefetch in the vocoder wait")
 ap.add_argument("--no-diag", action="store_true")
+ap.add_argument("--no-staging", action="store_true")
 args = ap.parse_args()
 cfg, lex = PipelineConfig(), default_lexicon()
 eng = build_engine(cfg, "r", "cuda:0")
 eng.prepare_graphs(max_batch=512)
 eng.speculate = not args.no_spec
+eng.plan_staging = not args.no_staging
 mods = modules_for(eng, lex)
 diag = []
 _voc = eng.vocoder_batch
@@ -81,3 +83,5 @@ print(f"torch allocated {mem0 / 2**20:.0f} -> {torch.cuda.memory_allocated() / 2
       f"{eng.arena.used * 4 / 2**20:.1f} MiB (peak {eng.arena.peak * 4 / 2**20:.1f} MiB)")
 for d in diag:
     print("diag:", d)
+for f in eng.failures[:8]:
+    print("engine failure:", f)
