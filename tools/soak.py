@@ -22,6 +22,7 @@ ap.add_argument("--no-spec", action="store_true")
 ap.add_argument("--no-prefetch", action="store_true", help="no frontend prefetch in the vocoder wait")
 ap.add_argument("--no-diag", action="store_true")
 ap.add_argument("--no-staging", action="store_true")
+ap.add_argument("--gc-like-bench", action="store_true", help="gc.freeze + high thresholds as bench.py")
 args = ap.parse_args()
 cfg, lex = PipelineConfig(), default_lexicon()
 eng = build_engine(cfg, "r", "cuda:0")
@@ -58,6 +59,11 @@ for k in ("engine",) + (() if args.no_prefetch else ("frontend_prefetch",)):
 mods = mods2
 serve(mods, cfg, poisson_trace(50, 1.0, seed=7, lexicon=lex), warmup_iters=0, timed_iters=2, drain_seconds=0.0)
 torch.cuda.synchronize()
+if args.gc_like_bench:
+    import gc
+    gc.collect()
+    gc.freeze()
+    gc.set_threshold(200000, 100, 100)
 mem0 = torch.cuda.memory_allocated()
 arena0 = eng.arena.tensor.numel()
 run = serve(mods, cfg, poisson_trace(args.qps, args.seconds, seed=11, lexicon=lex), warmup_iters=3,
