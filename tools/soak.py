@@ -23,6 +23,7 @@ ap.add_argument("--no-prefetch", action="store_true", help="no frontend prefetch
 ap.add_argument("--no-diag", action="store_true")
 ap.add_argument("--no-staging", action="store_true")
 ap.add_argument("--gc-like-bench", action="store_true", help="gc.freeze + high thresholds as bench.py")
+ap.add_argument("--gc-after", default="", help="force gc.collect() after this module call (E, D or V)")
 args = ap.parse_args()
 cfg, lex = PipelineConfig(), default_lexicon()
 eng = build_engine(cfg, "r", "cuda:0")
@@ -51,8 +52,22 @@ def vocoder_diag(triples):
 
 
 from paper_2211_13939_b200.scheduler import PipelineModules  # noqa: E402
-mods2 = PipelineModules(mods.frontend_batch, mods.encoder_batch, mods.decoder_batch,
-                        mods.vocoder_batch if args.no_diag else vocoder_diag)
+import gc  # noqa: E402
+
+
+def after_gc(fn, tag):
+    if tag not in args.gc_after:
+        return fn
+
+    def inner(x):
+        out = fn(x)
+        gc.collect()
+        return out
+    return inner
+
+
+mods2 = PipelineModules(mods.frontend_batch, after_gc(mods.encoder_batch, "E"), after_gc(mods.decoder_batch, "D"),
+                        after_gc(mods.vocoder_batch if args.no_diag else vocoder_diag, "V"))
 for k in ("engine",) + (() if args.no_prefetch else ("frontend_prefetch",)):
     if hasattr(mods, k):
         object.__setattr__(mods2, k, getattr(mods, k))
