@@ -28,6 +28,7 @@ ap.add_argument("--serial", action="store_true")
 ap.add_argument("--no-streams", action="store_true")
 ap.add_argument("--no-spec", action="store_true")
 ap.add_argument("--spec", action="store_true")
+ap.add_argument("--no-graphs", action="store_true")
 ap.add_argument("--iters", type=int, default=300)
 ap.add_argument("--heavy", action="store_true", help="~2.5 arrivals per iteration (pooled batch ~100)")
 args = ap.parse_args()
@@ -40,6 +41,8 @@ if args.serial or args.no_spec:
     eng.speculate = False
 if args.spec:
     eng.speculate = True
+if args.no_graphs:
+    eng.use_graphs = False
 mods = modules_for(eng, lex)
 rng = random.Random(1234)
 pool = RequestPool()

@@ -24,12 +24,14 @@ ap.add_argument("--no-diag", action="store_true")
 ap.add_argument("--no-staging", action="store_true")
 ap.add_argument("--gc-like-bench", action="store_true", help="gc.freeze + high thresholds as bench.py")
 ap.add_argument("--gc-after", default="", help="force gc.collect() after this module call (E, D or V)")
+ap.add_argument("--no-graphs", action="store_true", help="eager decoder launches (no CUDA-graph buckets)")
 args = ap.parse_args()
 cfg, lex = PipelineConfig(), default_lexicon()
 eng = build_engine(cfg, "r", "cuda:0")
 eng.prepare_graphs(max_batch=512)
 eng.speculate = not args.no_spec
 eng.plan_staging = not args.no_staging
+eng.use_graphs = not args.no_graphs
 mods = modules_for(eng, lex)
 diag = []
 _voc = eng.vocoder_batch
