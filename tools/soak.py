@@ -25,6 +25,7 @@ ap.add_argument("--no-staging", action="store_true")
 ap.add_argument("--gc-like-bench", action="store_true", help="gc.freeze + high thresholds as bench.py")
 ap.add_argument("--gc-after", default="", help="force gc.collect() after this module call (E, D or V)")
 ap.add_argument("--no-graphs", action="store_true", help="eager decoder launches (no CUDA-graph buckets)")
+ap.add_argument("--no-consumers", action="store_true", help="no client poller thread (server-side timing)")
 args = ap.parse_args()
 cfg, lex = PipelineConfig(), default_lexicon()
 eng = build_engine(cfg, "r", "cuda:0")
@@ -84,7 +85,8 @@ if args.gc_like_bench:
 mem0 = torch.cuda.memory_allocated()
 arena0 = eng.arena.tensor.numel()
 run = serve(mods, cfg, poisson_trace(args.qps, args.seconds, seed=11, lexicon=lex), warmup_iters=3,
-            warmup_seconds=1.0, timed_iters=None, timed_seconds=args.seconds - 2, drain_seconds=5.0, tail_seconds=30)
+            warmup_seconds=1.0, timed_iters=None, timed_seconds=args.seconds - 2, drain_seconds=5.0, tail_seconds=30,
+            consumers=not args.no_consumers)
 torch.cuda.synchronize()
 recs = sorted((r for r in run.timings if r.fcl is not None), key=lambda r: r.send_time)
 t0 = recs[0].send_time
