@@ -14,6 +14,7 @@ across calls and rebuild pointers from :attr:`base_ptr` per call.
 from __future__ import annotations
 
 import bisect
+import collections
 import threading
 
 import torch
@@ -29,15 +30,25 @@ class RaggedArena:
         self.align = max(1, _ALIGN_BYTES // self.itemsize)
         self.stream = stream
         self._lock = threading.Lock()
+        # frees from weakref finalizers: those can run inside a cyclic collection on ANY thread,
+        # including this one while alloc() holds the lock, so they only append here (atomic, no
+        # lock, no allocation-triggered re-entry) and the owning thread's next alloc() applies them
+        self._deferred: collections.deque = collections.deque()
         cap = self._round(capacity)
         self.tensor = torch.empty(cap, dtype=dtype, device=device)
         self._free_starts = [0]
         self._free_sizes = {0: cap}
-        self.used = 0
+        self._used = 0
         self.peak = 0
 
     def _round(self, n: int) -> int:
         return max(self.align, -(-int(n) // self.align) * self.align)
+
+    @property
+    def used(self) -> int:
+        """Elements in use (queued finalizer frees applied first)."""
+        self.drain()
+        return self._used
 
     @property
     def capacity(self) -> int:
@@ -50,18 +61,38 @@ class RaggedArena:
     def ptr(self, off: int) -> int:
         return self.tensor.data_ptr() + off * self.itemsize
 
+    def release(self, off: int, n: int) -> None:
+        """Finalizer-safe free: queued, applied by the next alloc() / free() / drain()."""
+        self._deferred.append((off, n))
+
+    def drain(self) -> None:
+        with self._lock:
+            self._drain_locked()
+
+    def _drain_locked(self) -> None:
+        while True:
+            try:
+                off, n = self._deferred.popleft()
+            except IndexError:
+                return
+            size = self._round(n)
+            self._used -= size
+            self._insert_free(off, size)
+
     def alloc(self, n: int) -> int:
         size = self._round(n)
         with self._lock:
-            for i, start in enumerate(self._free_starts):
+            self._drain_locked()
+            for i in range(len(self._free_starts)):
+                start = self._free_starts[i]
                 have = self._free_sizes[start]
                 if have >= size:
                     del self._free_sizes[start]
                     self._free_starts.pop(i)
                     if have > size:
                         self._insert_free(start + size, have - size)
-                    self.used += size
-                    self.peak = max(self.peak, self.used)
+                    self._used += size
+                    self.peak = max(self.peak, self._used)
                     return start
             self._grow(size)
         return self.alloc(n)
@@ -69,7 +100,8 @@ class RaggedArena:
     def free(self, off: int, n: int) -> None:
         size = self._round(n)
         with self._lock:
-            self.used -= size
+            self._drain_locked()
+            self._used -= size
             self._insert_free(off, size)
 
     def _insert_free(self, start: int, size: int) -> None:

@@ -179,12 +179,12 @@ ITTS_API int itts_bert_prosody(const int32_t* ids, const int32_t* pos, const int
                                    xf, (__nv_bfloat16*)xb);
   if (e != cudaSuccess) return (int)e;
   const size_t att_smem = sizeof(float) * (MAXLEN * (HD + 1) + MAXLEN * HD + 8 * MAXLEN + 8 * HD);
-  static bool configured = false;
-  if (!configured) {
+  static uint64_t configured = 0;
+  if (!(configured & itts::device_bit())) {
     if ((e = cudaFuncSetAttribute(k_bert_attn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)att_smem)) !=
         cudaSuccess)
       return (int)e;
-    configured = true;
+    configured |= itts::device_bit();
   }
   const int32_t off0 = 0;
   int r;

@@ -30,6 +30,14 @@ int conv1d_tc_impl(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, cons
 
 namespace itts {
 
+// Bit of the calling thread's current device: one-time per-device setup (cudaFuncSetAttribute
+// applies to the current device only) is tracked in a 64-bit mask per call site.
+inline uint64_t device_bit() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return 1ull << (d & 63);
+}
+
 // Programmatic dependent launch (PDL): kernels of the vocoder / encoder chains can be launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's prologue (barrier init, TMEM
 // allocation, tensor-map prefetch, weight loads) overlaps the tail of the kernel before it.

@@ -1071,11 +1071,11 @@ ITTS_API int itts_r_decode_persistent(int32_t B, int32_t nsteps, const int64_t* 
   const size_t smem = 1024 + RING_BYTES + sizeof(AttSmem);
   const int b16 = (B + 15) / 16 * 16;
   uint32_t a_box_bytes = (uint32_t)b16 * 128;  // X stage: all items x 64 columns
-  static bool configured = false;
-  if (!configured) {
+  static uint64_t configured = 0;
+  if (!(configured & itts::device_bit())) {
     cudaError_t e = cudaFuncSetAttribute(k_dec_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
-    configured = true;
+    configured |= itts::device_bit();
   }
   cudaError_t e = cudaMemsetAsync(bar, 0, (2 + NGRP + 1) * sizeof(unsigned), st);
   if (e != cudaSuccess) return (int)e;

@@ -457,11 +457,11 @@ int launch(const void* x, int64_t rows, const void* w1, const void* w2, int taps
   if (!encode_2d(&mr, x, C, (uint64_t)rows, C, K::KT, 128, K::SWZ)) return ITTS_EINVAL;
   if (!encode_2d(&m1, w1, C, (uint64_t)taps * C, C, K::KT, C, K::SWZ)) return ITTS_EINVAL;
   if (!encode_2d(&m2, w2, C, (uint64_t)taps * C, C, K::KT, C, K::SWZ)) return ITTS_EINVAL;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_set = 0;
+  if (!(attr_set & itts::device_bit())) {
     cudaError_t e = cudaFuncSetAttribute(k_resblock_tc<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM);
     if (e != cudaSuccess) return (int)e;
-    attr_set = true;
+    attr_set |= itts::device_bit();
   }
   a.m_out = 128 * K::NB - (taps - 1);
   void* out = (a.acc_mode == 1 || a.acc_mode == 2) ? (void*)a.acc : (void*)a.act_out;

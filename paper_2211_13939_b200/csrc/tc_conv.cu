@@ -267,10 +267,10 @@ int launch(const void* x, int64_t rows, int c_in, int64_t x_ld, const void* w, i
   const int total_iters = taps.n * kchunks;
   if (ksplit < 1 || total_iters % ksplit) return ITTS_EINVAL;
   const size_t smem = 1024 + STAGES * (kBlockM + BN) * SWZ + (2 * STAGES + 4) * 8 + 16;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_set = 0;
+  if (!(attr_set & itts::device_bit())) {
     cudaFuncSetAttribute(k_conv_tc<BN, SWZ, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
+    attr_set |= itts::device_bit();
   }
   TileSched sched{n_total / BN, ksplit, total_iters / ksplit};
   const int m_tiles = (int)((rows + kBlockM - 1) / kBlockM);

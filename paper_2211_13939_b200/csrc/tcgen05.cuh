@@ -199,11 +199,12 @@ inline bool encode_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64
   return r == CUDA_SUCCESS;
 }
 
-inline int num_sms() {
-  static int n = 0;
+inline int num_sms() {  // of the current device (cached per device)
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& n = cache[dev & 63];
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
   }

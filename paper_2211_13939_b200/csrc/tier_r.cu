@@ -193,10 +193,10 @@ int launch_gemv(const GemvIO& io, int B, int KS, float* part, bool finish, cudaS
   const int K = io.len0 + io.len1;
   const int KL = (K + KS - 1) / KS + 1;
   const size_t smem = (size_t)(IT * KL + GW * IT * NPL * 32) * 4;
-  static bool configured = false;
-  if (!configured) {
+  static uint64_t configured = 0;
+  if (!(configured & itts::device_bit())) {
     cudaFuncSetAttribute(k_gemv<NPL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
+    configured |= itts::device_bit();
   }
   dim3 grid((B + IT - 1) / IT, (io.N + 32 * NPL - 1) / (32 * NPL), KS);
   k_gemv<NPL, MODE><<<grid, GW * 32, smem, st>>>(io, B, part);
@@ -781,10 +781,10 @@ int launch_attention(float* state, void* xb, const int64_t* plan, int32_t B, int
   const size_t smem = ((size_t)(2 * lh + ls + 4) + (size_t)LT * (NF + 1)) * sizeof(float);
   static_assert(LT * (NF + 1) >= AT_WARPS * EMB, "context partials alias the location tile");
   if (smem > 150 * 1024) return ITTS_EUNSUPPORTED;
-  static bool configured = false;
-  if (!configured) {
+  static uint64_t configured = 0;
+  if (!(configured & itts::device_bit())) {
     cudaFuncSetAttribute(k_attention<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024);
-    configured = true;
+    configured |= itts::device_bit();
   }
   k_attention<CL><<<B * CL, AT_WARPS * 32, smem, st>>>(state, (__nv_bfloat16*)xb, plan, Q, Wloc, WdT, v, step);
   ITTS_RETURN_LAUNCH();

@@ -39,10 +39,11 @@ class _Buf:
 
 
 def _release_all(arena, regions, state_bufs, voc_bufs) -> None:
+    # a finalizer: may run inside a cyclic collection on any thread, so the arena only queues it
     for off, size in regions:
-        arena.free(off, size)
+        arena.release(off, size)
     for b in state_bufs + voc_bufs:
-        arena.free(b.off, b.size)
+        arena.release(b.off, b.size)
 
 
 class DeviceRequest:

@@ -25,6 +25,7 @@ in Tier S; the gate logit is computed and returned but not used.
 from __future__ import annotations
 
 import ctypes
+import functools
 import weakref
 
 import numpy as np
@@ -72,6 +73,16 @@ HIFIGAN_MACS_PER_FRAME = _hifigan_macs_per_frame()
 # Decoder-step weight bytes as stored here (bf16 gate GEMMs, fp32 elsewhere).
 DEC_WEIGHT_BYTES = (4096 * 1792 + 4096 * 2560) * 2 + (80 * 256 + 256 * 256 + 1024 * 128 + 32 * 62 + 32 * 128
                                                       + 128 + 1536 * 81 + 81) * 4
+
+
+def _on_device(fn):
+    """Run a module entry point with the engine's device current (the calling thread may be on
+    another device, e.g. a router worker or a test on cuda:1)."""
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kw):
+        with torch.cuda.device(self.device):
+            return fn(self, *args, **kw)
+    return wrapper
 
 
 def _h2d(arr: np.ndarray, device) -> torch.Tensor:
@@ -145,6 +156,15 @@ class TierREngine:
         if self.device.type != "cuda":
             raise RuntimeError("Tier-R GPU modules need a CUDA device (no CPU fallback)")
         _native.lib()
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        # everything below -- torch allocations, the native vocoder's streams / events, its
+        # cudaMalloc'd work buffers -- lives on self.device, whatever the calling thread's device
+        with torch.cuda.device(self.device):
+            self._init_on_device(seed, weights, postnet, postnet_weights)
+
+    def _init_on_device(self, seed, weights, postnet, postnet_weights) -> None:
+        cfg = self.cfg
         self.stream = torch.cuda.Stream(self.device)
         w = weights if weights is not None else W.tier_r_weights(seed)
         with torch.cuda.stream(self.stream):
@@ -172,6 +192,11 @@ class TierREngine:
         self.diagnose = True             # on a non-finite chunk, record which inputs were already bad
         self.plan_staging = True         # decoder graph plans: rewrite only the rows that changed
         self.failures: list = []
+        # diagnostics: keep the last decoder call's inputs / outputs so a non-finite chunk can be
+        # traced to a transient (re-run differs) or an input fault (re-run reproduces it)
+        self.keep_last_decoder = False
+        self._last_dec = None
+        self.bisect_dir: str | None = None   # with keep_last_decoder: shrink + dump failing decoder batches here
         self.speculate = False           # precompute the next decoder call's item fields during V waits (off: see DESIGN §10)
         self._spec_src = None            # continuing (state, features) of the last decoder call
         self._spec = None                # their precomputed plan fields (see _speculate_next_decoder)
@@ -261,6 +286,7 @@ class TierREngine:
         self.wpost = f32(w["hg.conv_post.w"][0])                                        # [32][7]
         self.bpost = float(w["hg.conv_post.b"][0])
 
+    @_on_device
     def set_postnet(self, enabled: bool, weights: dict | None = None) -> None:
         """Turn the chunk-local PostNet (f3) on or off; weights default to postnet_weights(0)."""
         if enabled and (weights is not None or not hasattr(self, "_post_ptrs")):
@@ -268,7 +294,14 @@ class TierREngine:
         self.postnet = bool(enabled)
 
     def _prepare_postnet(self, pw: dict) -> None:
-        """PostNet layers in tc_conv layout; the 80-channel ends padded to 96 (c_in, c_out % 32)."""
+        """PostNet layers in tc_conv layout; the 80-channel ends padded to 96 (c_in, c_out % 32).
+        Built on the engine stream (and waited for), so the first itts_r_postnet launch is ordered
+        after these writes."""
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            self._prepare_postnet_layers(pw)
+        self.stream.synchronize()
+
+    def _prepare_postnet_layers(self, pw: dict) -> None:
         d, layers = self.device, []
         for i in range(W.POSTNET_LAYERS):
             w = pw[f"post.conv{i}.w"].detach().float().to(d)
@@ -399,6 +432,7 @@ class TierREngine:
         return self.cfg.overlap_frames * W.N_MEL + self.cfg.overlap_samples
 
     # ------------------------------------------------------------ encoder
+    @_on_device
     def encoder_batch(self, fos) -> list:
         n = len(fos)
         if n == 0:
@@ -528,6 +562,7 @@ class TierREngine:
             return
         self._spec = (src, taken, cols)
 
+    @_on_device
     def decoder_batch(self, pairs) -> list:
         n = len(pairs)
         if n == 0:
@@ -624,6 +659,8 @@ class TierREngine:
             out.append(DecodeChunkResult(m, emitted >= state.target_frames,
                                          DeviceDecoderState(state.req, dst, emitted, state.target_frames)))
         self._spec_src = [(r.state, enc) for r, (_, enc) in zip(out, pairs) if not r.stop]
+        if self.keep_last_decoder:
+            self._last_dec = (list(pairs), out)
         return out
 
     def _enqueue_decoder(self, b: "_DecBuffers", max_L: int, nsteps: int) -> None:
@@ -666,6 +703,7 @@ class TierREngine:
             self._dec_buckets[B] = _DecBucket(self, B, GRAPH_MAX_L)
         return self._dec_buckets[B]
 
+    @_on_device
     def prepare_graphs(self, max_batch: int = 256) -> None:
         """Capture the decoder-chunk graph of every 16-row bucket up to ``max_batch`` now, and
         grow the vocoder work buffers for that batch, so no capture or cudaMalloc happens on
@@ -681,6 +719,7 @@ class TierREngine:
         self.stream.synchronize()
 
     # ------------------------------------------------------------ vocoder
+    @_on_device
     def vocoder_batch(self, triples) -> list:
         n = len(triples)
         if n == 0:
@@ -798,6 +837,117 @@ class TierREngine:
                 info["pmem_finite"] = bool(np.isfinite(self.read_processed_memory(req)).all())
             self.failures.append(info)
             print("itts non-finite chunk:", info, file=sys.stderr, flush=True)
+        if self._last_dec is not None and any(getattr(m, "req", None) is not None and
+                                              any(m is r.mel for r in self._last_dec[1]) for _, m, _ in triples):
+            info = self._rerun_last_decoder()
+            self.failures.append(info)
+            print("itts decoder re-run:", info, file=sys.stderr, flush=True)
+
+    def _rerun_last_decoder(self) -> dict:
+        """Failure path only: decode the last decoder call's inputs again (graph and eager) and
+        compare bit for bit with what that call produced."""
+        pairs, out = self._last_dec
+        self._last_dec = None
+        keep, spec_src, graphs = self.keep_last_decoder, self._spec_src, self.use_graphs
+        self.keep_last_decoder = False
+        bad = lambda fr: [i for i, f in enumerate(fr) if not np.isfinite(f).all()]
+        info: dict = {"batch": len(pairs)}
+        try:
+            orig = [r.mel.frames for r in out]
+            info["orig_nonfinite"] = bad(orig)
+            info["src_nonfinite"] = [i for i, (st, _) in enumerate(pairs)
+                                     if not np.isfinite(self._read(st.buf.off, self.state_size(st.req.seq_len))).all()]
+            info["steps"] = [r.mel.frame_count for r in out]
+            info["L"] = [st.req.seq_len for st, _ in pairs]
+            for use_graphs in (graphs, False):
+                self.use_graphs = use_graphs
+                again = [r.mel.frames for r in self.decoder_batch(pairs)]
+                tag = "graph" if use_graphs else "eager"
+                info[f"{tag}_nonfinite"] = bad(again)
+                info[f"{tag}_differs"] = [i for i, (a, b) in enumerate(zip(orig, again))
+                                          if not np.array_equal(a, b, equal_nan=True)]
+            if self.bisect_dir is not None and info.get("eager_nonfinite"):
+                info["bisect"] = self._bisect_decoder(pairs)
+        except Exception as exc:  # noqa: BLE001 -- diagnostics must not mask the failure
+            info["error"] = repr(exc)
+        finally:
+            self.keep_last_decoder, self._spec_src, self.use_graphs = keep, spec_src, graphs
+        return info
+
+    # ------------------------------------------------------------ failure reproduction (debug only)
+    def _bisect_decoder(self, pairs) -> dict:
+        """Shrink a decoder batch whose eager re-run gives non-finite mel to a small failing subset
+        (delta debugging on the item list), dump it with debug_dump_decoder_case."""
+        import os
+        self.use_graphs = False
+        tries = {"n": 0}
+
+        def fails(sub) -> bool:
+            tries["n"] += 1
+            return any(not np.isfinite(r.mel.frames).all() for r in self.decoder_batch(list(sub)))
+
+        out: dict = {"solo_fails": [i for i in range(min(len(pairs), 8)) if fails([pairs[i]])]}
+        cur, k = list(range(len(pairs))), 2
+        while len(cur) > 1 and tries["n"] < 80:
+            size = -(-len(cur) // k)
+            parts = [cur[i:i + size] for i in range(0, len(cur), size)]
+            for part in parts:   # a failing part
+                if fails([pairs[i] for i in part]):
+                    cur, k = part, 2
+                    break
+            else:
+                for part in parts:   # a failing complement
+                    rest = [i for i in cur if i not in part]
+                    if len(parts) > 2 and fails([pairs[i] for i in rest]):
+                        cur, k = rest, max(k - 1, 2)
+                        break
+                else:
+                    if k >= len(cur):
+                        break
+                    k = min(len(cur), 2 * k)
+        out["minimal"] = cur
+        out["minimal_fails_again"] = [fails([pairs[i] for i in cur]) for _ in range(3)]
+        out["tries"] = tries["n"]
+        os.makedirs(self.bisect_dir, exist_ok=True)
+        path = os.path.join(self.bisect_dir, f"dec_case_{len(self.failures)}.npz")
+        self.debug_dump_decoder_case([pairs[i] for i in cur], path)
+        out["dump"] = path
+        return out
+
+    def debug_dump_decoder_case(self, pairs, path: str) -> None:
+        """Inputs of a decoder call (per item: state row + W / W_acc, memory, processed memory,
+        counters) -> npz, replayable with debug_load_decoder_case on any engine."""
+        arrs: dict = {"n": np.array(len(pairs))}
+        for i, (st, enc) in enumerate(pairs):
+            req = st.req
+            arrs[f"state{i}"] = self._read(st.buf.off, self.state_size(req.seq_len))
+            arrs[f"mem{i}"] = np.asarray(self.read_features(req))
+            arrs[f"pm{i}"] = self.read_processed_memory(req)
+            arrs[f"cnt{i}"] = np.array([st.frames_emitted, st.target_frames, req.seq_len])
+        np.savez(path, **arrs)
+
+    @_on_device
+    def debug_load_decoder_case(self, path: str) -> list:
+        """(state, features) handles holding exactly the dumped inputs."""
+        from .frontend import FrontendOutput
+        z = np.load(path)
+        n = int(z["n"])
+        Ls = [int(z[f"cnt{i}"][2]) for i in range(n)]
+        fos = [FrontendOutput((1,) * L, (1,) * L, (0,) * L, (0,) * L, (0,) * L) for L in Ls]
+        encs = self.encoder_batch(fos)
+        self.stream.synchronize()
+        pairs = []
+        t = self.arena.tensor
+        for i, (enc, st) in enumerate(encs):
+            req = enc.req
+            put = lambda off, arr: t[off:off + arr.size].copy_(torch.from_numpy(np.ascontiguousarray(arr.reshape(-1))))
+            put(st.buf.off, z[f"state{i}"])
+            put(req.extra["mem_off"], z[f"mem{i}"])
+            put(req.extra["pm_off"], z[f"pm{i}"])
+            fe, tf, _ = (int(v) for v in z[f"cnt{i}"])
+            pairs.append((DeviceDecoderState(req, st.buf, fe, tf), enc))
+        torch.cuda.synchronize(self.device)
+        return pairs
 
     def _mrf_branches(self, s: int, XA, OA_next, scratch, outs, rm, slope_out: float) -> None:
         """One MRF stage: the three ResBlock1 branches each write their own y (last layer in
