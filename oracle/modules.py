@@ -117,3 +117,18 @@ class EncodedR:
     @property
     def seq_len(self) -> int:
         return int(self.memory.shape[0])
+
+
+def crashing_modules(lexicon, cfg: PipelineConfig) -> PipelineModules:
+    """Tier-S oracle modules whose decoder kills the process on a text that maps to >= 40
+    phonemes (router liveness tests: a worker dying mid-stream)."""
+    import os
+
+    base = cpu_modules(lexicon, cfg)
+
+    def decoder(pairs):
+        if any(enc.seq_len >= 40 for _, enc in pairs):
+            os._exit(3)
+        return base.decoder_batch(pairs)
+
+    return PipelineModules(base.frontend_batch, base.encoder_batch, decoder, base.vocoder_batch)

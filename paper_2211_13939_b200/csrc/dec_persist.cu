@@ -48,6 +48,17 @@
 #ifndef DEC_MERGE_B
 #define DEC_MERGE_B 96
 #endif
+#ifndef DEC_WFENCE
+#define DEC_WFENCE 0
+#endif
+// generic-proxy stores to the bf16 operand mirror are read by bulk copies (async proxy) of other
+// CTAs: with DEC_WFENCE every writing thread fences its stores to the async proxy before the
+// release that publishes them
+#if DEC_WFENCE
+#define WFENCE() asm volatile("fence.proxy.async.global;" ::: "memory")
+#else
+#define WFENCE() ((void)0)
+#endif
 
 namespace {
 
@@ -442,6 +453,7 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
         hs[e] = hn;
       }
     }
+    WFENCE();
     __syncthreads();
     if (threadIdx.x == 0) mark(6);
     // this group's share of the next linear layer: query (MODE 0, 128 outputs) or the mel/gate
@@ -557,9 +569,13 @@ __device__ void att_chunk(const DecArgs& a, AttSmem& sm, int s, int b, int ch, i
     for (int z = 1; z < NGRP; ++z) qa += qv[z];
     sm.q[tid] = qa;
   }
-  for (int i = tid; i < nh; i += NT) {
+  // The whole window buffer, not just the nh entries the 31 taps use: the 4-position sliding
+  // window also multiplies the zero tap 31 (and loads ahead) up to index n + 34, and stale shared
+  // memory there (another kernel's bytes, possibly an Inf / NaN pattern) would give 0 * NaN = NaN
+  // in the chunk's last energy.
+  for (int i = tid; i < ACH + 2 * HALO + 2; i += NT) {
     const int t = ta - HALO + i;
-    const bool in = t >= 0 && t < L;
+    const bool in = i < nh && t >= 0 && t < L;
     sm.wp[i] = in ? ldf(wsrc + t) : 0.f;
     sm.wa[i] = in ? ldf(wsrc + L + t) : 0.f;
   }
@@ -709,6 +725,7 @@ __device__ void att_combine(const DecArgs& a, AttSmem& sm, int s, int b, int chu
     st[CTX_OFF + d] = c;
     a.xb[xb_off(b, CTX_OFF + d)] = __float2bfloat16_rn(c);
   }
+  WFENCE();
   for (int t = tid; t < L; t += NT) {
     const float w = ldf(a.U + (int64_t)b * a.u_ld + t) * scale[t / chunk];
     const float acc = ldf(wsrc + L + t);
@@ -770,6 +787,7 @@ __global__ void __launch_bounds__(NT, 1)
     const float* st = a.work + (int64_t)b * ROW;
     for (int i = tid; i < ATTC_OFF; i += NT) a.xb[xb_off(b, i)] = __float2bfloat16_rn(ldf(st + i));
   }
+  WFENCE();
   grid_sync(a.bar, gen);
 
   // position chunking of the attention: the smallest multiple of 16 (<= 64) that gives every CTA
@@ -903,6 +921,7 @@ __global__ void __launch_bounds__(NT, 1)
                       a.work[(int64_t)b * ROW + P_OFF + n] = y;
                       a.xb[xb_off(b, P_OFF + n)] = __float2bfloat16_rn(y);
                     });
+      WFENCE();
       pmark(7);
     }
     phase_end();

@@ -196,6 +196,7 @@ class TierREngine:
         # traced to a transient (re-run differs) or an input fault (re-run reproduces it)
         self.keep_last_decoder = False
         self._last_dec = None
+        self.poison_scratch = False          # debug: NaN-fill decoder scratch (eager path; True or a set of buffer names)
         self.bisect_dir: str | None = None   # with keep_last_decoder: shrink + dump failing decoder batches here
         self.speculate = False           # precompute the next decoder call's item fields during V waits (off: see DESIGN §10)
         self._spec_src = None            # continuing (state, features) of the last decoder call
@@ -631,6 +632,10 @@ class TierREngine:
                 mel_off = np.concatenate([[0], np.cumsum(steps_np)]).astype(np.int64)
                 mel = torch.empty(int(mel_off[-1]), W.N_MEL, dtype=torch.float32, device=self.device)
                 gate = torch.empty(int(mel_off[-1]), dtype=torch.float32, device=self.device)
+                if self.poison_scratch is True or (self.poison_scratch and "mel" in self.poison_scratch):
+                    v = self.poison_scratch["mel"] if isinstance(self.poison_scratch, dict) else float("nan")
+                    mel.fill_(v)
+                    gate.fill_(v)
                 plan = np.zeros((n, 8), dtype=np.int64)
                 plan[:, 0] = base + 4 * np.array(mem_off, dtype=np.int64)
                 plan[:, 1] = base + 4 * np.array(pm_off, dtype=np.int64)
@@ -642,6 +647,8 @@ class TierREngine:
                 plan[:, 7] = gate.data_ptr() + 4 * mel_off[:-1]
                 packed = self._up(np.concatenate([plan.reshape(-1), src, dstp]))
                 bufs = _DecBuffers(self, n, packed)
+                if self.poison_scratch:
+                    self._last_bufs = bufs   # debug: the scratch of the last poisoned call
                 with self._mark("decoder", dec_bytes):
                     self._enqueue_decoder(bufs, max_L, max_steps)
                 if self.postnet:
@@ -859,10 +866,13 @@ class TierREngine:
                                      if not np.isfinite(self._read(st.buf.off, self.state_size(st.req.seq_len))).all()]
             info["steps"] = [r.mel.frame_count for r in out]
             info["L"] = [st.req.seq_len for st, _ in pairs]
-            for use_graphs in (graphs, False):
-                self.use_graphs = use_graphs
-                again = [r.mel.frames for r in self.decoder_batch(pairs)]
-                tag = "graph" if use_graphs else "eager"
+            for tag, use_graphs, poison in (("first", graphs, False), ("eager", False, False),
+                                            ("eager_poisoned", False, True)):
+                self.use_graphs, self.poison_scratch = use_graphs, poison
+                try:
+                    again = [r.mel.frames for r in self.decoder_batch(pairs)]
+                finally:
+                    self.poison_scratch = False
                 info[f"{tag}_nonfinite"] = bad(again)
                 info[f"{tag}_differs"] = [i for i, (a, b) in enumerate(zip(orig, again))
                                           if not np.array_equal(a, b, equal_nan=True)]
@@ -1077,29 +1087,44 @@ class _DecBuffers:
 
     def __init__(self, eng: TierREngine, n: int, packed: torch.Tensor):
         dev = eng.device
+        self.dev = dev
         self.n = n
         self.packed = packed
         self.d_plan, self.d_src, self.d_dst = packed[:8 * n], packed[8 * n:9 * n], packed[9 * n:10 * n]
-        self.work = torch.empty(n, ROW, dtype=torch.float32, device=dev)
-        self.xbm = torch.empty(n, XB_ROW, dtype=torch.bfloat16, device=dev)
-        self.G = torch.empty(DEC_KSPLIT, n, 4096, dtype=torch.float32, device=dev)
+        # scratch is never read before the kernels write it: eng.poison_scratch fills it with NaN
+        # (debug / tests: the outputs must not change)
+        self.poison = getattr(eng, "poison_scratch", False)
+        self.work = self._empty((n, ROW), torch.float32, "work")
+        self.xbm = self._empty((n, XB_ROW), torch.bfloat16, "xbm")
+        self.G = self._empty((DEC_KSPLIT, n, 4096), torch.float32, "G")
         # query / projection partials: 8 K-slices (per-kernel chain) or 32 unit groups (+1 context
         # projection) in the persistent decoder
-        self.Q = torch.empty(32, n, 128, dtype=torch.float32, device=dev)
-        self.P = torch.empty(33, n, 81, dtype=torch.float32, device=dev)
-        self.H1 = torch.empty(n, 256, dtype=torch.float32, device=dev)
+        self.Q = self._empty((32, n, 128), torch.float32, "Q")
+        self.P = self._empty((33, n, 81), torch.float32, "P")
+        self.H1 = self._empty((n, 256), torch.float32, "H1")
         self.dev, self.xb2, self.U, self.AP, self.bar, self.Gp = dev, None, None, None, None, None
+
+    def _poisoned(self, name: str) -> bool:
+        return self.poison is True or (bool(self.poison) and name in self.poison)
+
+    def _empty(self, shape, dtype, name: str) -> torch.Tensor:
+        t = torch.empty(shape, dtype=dtype, device=self.dev)
+        if self._poisoned(name):   # True / a set: NaN; a dict: that buffer's fill value
+            t.fill_(self.poison[name] if isinstance(self.poison, dict) else float("nan"))
+        return t
 
     def ensure_persistent(self, max_L: int) -> None:
         """Scratch of the persistent decoder kernel (allocated once per buffer set)."""
         if self.U is not None and self.U.shape[1] >= max_L:
             return
         nblk = -(-self.n // 128)
-        self.xb2 = torch.zeros(nblk * (XB2 // 64) * 128 * 64, dtype=torch.bfloat16, device=self.dev)
-        self.U = torch.empty(self.n, max(max_L, 256), dtype=torch.float32, device=self.dev)
-        self.AP = torch.empty(self.n, 256, 2 + 512, dtype=torch.float32, device=self.dev)
+        self.xb2 = self._empty((nblk * (XB2 // 64) * 128 * 64,), torch.bfloat16, "xb2")
+        if not self._poisoned("xb2"):
+            self.xb2.zero_()
+        self.U = self._empty((self.n, max(max_L, 256)), torch.float32, "U")
+        self.AP = self._empty((self.n, 256, 2 + 512), torch.float32, "AP")
         self.bar = torch.zeros(64, dtype=torch.int32, device=self.dev)
-        self.Gp = torch.empty(4 * 32 * (-(-self.n // 16) * 16) * 128, dtype=torch.float32, device=self.dev)
+        self.Gp = self._empty((4 * 32 * (-(-self.n // 16) * 16) * 128,), torch.float32, "Gp")
 
 
 class _DecBucket(_DecBuffers):

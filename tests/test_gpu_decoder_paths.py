@@ -54,3 +54,53 @@ def test_persistent_matches_chain(engine, B):
     for sa, sb in zip(outs[True][1], outs[False][1]):
         for key in ("attn_weights", "attn_weights_sum", "attn_context", "dec_hidden", "dec_cell"):
             assert np.abs(sa[key] - sb[key]).max() <= 2e-4, key
+
+
+def _ragged_pairs(engine, B, seed, lefts):
+    """B fresh requests whose next chunk has `lefts[i % len]` frames left (mid-chunk stops)."""
+    from paper_2211_13939_b200.handles import DeviceDecoderState
+    lex = default_lexicon()
+    encs = engine.encoder_batch([run_frontend(t, lex) for t in texts(B, seed)])
+    pairs = []
+    for i, (enc, st) in enumerate(encs):
+        left = min(lefts[i % len(lefts)], st.target_frames)
+        pairs.append((DeviceDecoderState(st.req, st.buf, st.target_frames - left, st.target_frames), enc))
+    return pairs
+
+
+@pytest.mark.parametrize("B", [3, 84, 120])
+def test_scratch_is_written_before_read(engine, B):
+    """NaN-filled decoder scratch (partials, attention numerators, operand mirror, outputs) must
+    not change a single bit of the result: every scratch element the kernel reads was written
+    earlier in the same launch.  Ragged stops (8 / 16 / 32 frames left) exercise the inactive-item
+    paths of both the merged (B <= 96) and the separate chunk-combine schedule."""
+    pairs = _ragged_pairs(engine, B, 100 + B, [8, 40, 64, 64, 16, 64, 48])
+    got = {}
+    for poison in (False, True):
+        engine.poison_scratch = poison
+        try:
+            r1 = engine.decoder_batch(pairs)
+            r2 = engine.decoder_batch([(r.state, enc) for r, (_, enc) in zip(r1, pairs) if not r.stop])
+            got[poison] = ([r.mel.frames for r in r1] + [r.mel.frames for r in r2],
+                           [engine.read_state(r.state.req, r.state.buf)["attn_weights_sum"] for r in r2])
+        finally:
+            engine.poison_scratch = False
+    for a, b in zip(got[False][0], got[True][0]):
+        assert np.isfinite(a).all() and np.array_equal(a, b)
+    for a, b in zip(got[False][1], got[True][1]):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("B", [5, 84, 120])
+def test_graph_bucket_equals_eager(engine, B):
+    """The CUDA-graph bucket (B padded to 16 with idle rows) gives the eager launch's bits."""
+    pairs = _ragged_pairs(engine, B, 200 + B, [64, 64, 8, 40, 16])
+    out = {}
+    for graphs in (False, True):
+        engine.use_graphs = graphs
+        try:
+            out[graphs] = [r.mel.frames for r in engine.decoder_batch(pairs)]
+        finally:
+            engine.use_graphs = False
+    for a, b in zip(out[False], out[True]):
+        assert np.array_equal(a, b)

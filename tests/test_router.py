@@ -54,3 +54,27 @@ def test_router_two_workers(policy):
         recorded = [(d, c) for _, d, c in router.reports[w]]
         assert replay == recorded[:len(replay)]
         assert all(not d for d, _ in recorded[len(replay):])
+
+
+def test_dead_worker_fails_its_streams():
+    """A worker process that dies mid-stream: its open streams fail (no hang), the other
+    worker's requests still complete."""
+    from paper_2211_13939_b200.scheduler import RequestFailed
+    cfg, lex = PipelineConfig(), default_lexicon()
+    specs = [WorkerSpec("oracle.modules:cpu_modules", None, cfg),
+             WorkerSpec("oracle.modules:crashing_modules", None, cfg)]
+    rng = random.Random(9)
+    short = [random_text(rng, 2, 6, lex) for _ in range(4)]
+    long_text = random_text(rng, 40, 40, lex)
+    with Router(specs, policy="mod") as router:
+        streams = [router.submit(t)[1] for t in short[:3]] + [router.submit(long_text)[1]]  # ids 1..4
+        ok = []
+        for i, s in enumerate(streams):
+            try:
+                ok.append(len(wait_all([s], timeout=60)[0]) > 0)
+            except RequestFailed as exc:
+                assert "died" in str(exc)
+                ok.append(False)
+    assert router.dead == [1]
+    assert ok[0] and ok[2]            # worker 0 (ids 1, 3) unaffected
+    assert not ok[3]                  # the crash request (id 4 -> worker 1) failed, no hang
