@@ -135,13 +135,17 @@ int itts_resblock_debug_trace(void* buf);
  * W0T [80][256], W1T [256][256], WqT [1024][128], v [128], WpT [1536][81], bp [81] fp32;
  * WlocD [2][31][128] = the location conv composed with the location dense layer
  * (sum_f Wloc[f][c][k] WdT[f][a]).  Scratch: H1 [B][256], Q [8][B][128], P [8][B][81],
- * U [B][u_ld >= max L], AP [B][256][514], bar = 34 x u32.  B <= 256, texts <= 8192 phonemes. */
+ * U [B][u_ld >= max L], AP [B][256][514], bar = 34 x u32.  B <= 256, texts <= 8192 phonemes.
+ * Split-bf16 parity mode: Wa_lo / Wd_lo = the low bf16 parts (W - bf16(W)) in the same layout;
+ * the gate products are then Wh.Xh + Wh.Xl + Wl.Xh with fp32 accumulation (about 16 significant
+ * bits per operand) and xb must hold 2 x the mirror (high parts, then low parts).  Both null: plain
+ * bf16 products. */
 int itts_r_decode_persistent(int32_t B, int32_t nsteps, const int64_t* plan, float* work, void* xb,
                              const float* W0T, const float* W1T, const void* Wa, const float* ba,
                              const void* Wd, const float* bd, const float* WqT, const float* WlocD,
                              const float* v, const float* WpT, const float* bp,
                              float* Gp, float* H1, float* Q, float* P, float* U, int64_t u_ld, float* AP,
-                             unsigned* bar, void* stream);
+                             unsigned* bar, const void* Wa_lo, const void* Wd_lo, void* stream);
 /* Profiling aid: per-phase wall time of later persistent-decoder launches ([8] u64 ns). */
 int itts_r_decode_debug_trace(void* buf);
 int itts_r_dec_prepare(const float* state, void* xb, int32_t B, void* stream);
@@ -176,6 +180,14 @@ int itts_r_bilstm(const float* PRE, const int64_t* plan, int32_t n, const float*
 int itts_r_encode(const void* pack, int64_t total, int32_t n, int64_t max_len, int64_t rows, int64_t max_span,
                   const int64_t* weights, int32_t conv_taps, void* xa, void* xb, float* pre, int32_t* rowmap,
                   void* stream);
+/* The same encoder in the split-bf16 parity mode: every tensor-core product on [hi | lo | hi]
+ * bf16 operands against [Wh | Wh | Wl] weights (Wh.Xh + Wh.Xl + Wl.Xh, fp32 accumulation), fp32
+ * activations between layers.  weights3 = the itts_r_encode table with entries 4, 6, 8 (convs,
+ * [5][512][1536]) and 10 (input projection, [1][2048][1536]) replaced; x3 bf16 [rows][1536],
+ * f32 fp32 [rows][512] scratch.  Replaces the same reference functions as itts_r_encode. */
+int itts_r_encode_split(const void* pack, int64_t total, int32_t n, int64_t max_len, int64_t rows,
+                        int64_t max_span, const int64_t* weights3, int32_t conv_taps, void* x3, float* f32,
+                        float* pre, int32_t* rowmap, void* stream);
 int itts_r_pmem(const int64_t* plan, int32_t n, int64_t max_len, const float* WmT, void* stream);
 
 /* K7 helpers around the HiFi-GAN conv stack (replaces vocode_batch,

@@ -48,6 +48,9 @@
 #ifndef DEC_MERGE_B
 #define DEC_MERGE_B 96
 #endif
+#ifndef DEC_ADAPTIVE_CHUNK
+#define DEC_ADAPTIVE_CHUNK 0  // 1: batch-dependent chunk sizes (not batch-invariant; A/B only)
+#endif
 #ifndef DEC_WFENCE
 #define DEC_WFENCE 0
 #endif
@@ -75,6 +78,9 @@ __device__ __forceinline__ int64_t xb_off(int r, int col) {
   const int cc = col >> 6, j = (col >> 3) & 7, e = col & 7;
   return ((int64_t)((r >> 7) * NCC + cc) * 128 + (r & 127)) * 64 + ((j ^ (r & 7)) << 3) + e;
 }
+
+struct DecArgs;
+__device__ __forceinline__ void xb_store(const DecArgs& a, int b, int col, float v);
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -107,11 +113,15 @@ struct DecArgs {
   const int64_t* plan;             // [B][8]
   float* work;                     // [B][ROW]
   __nv_bfloat16* xb;               // [ceil(B/128)][NCC][128][64] swizzled tiles (see xb_off)
+  __nv_bfloat16* xbl;              // split mode: the low bf16 parts v - bf16(v) of the mirror, same layout
   const float* W0T;                // [80][256]
   const float* W1T;                // [256][256]
   const __nv_bfloat16* Wa;         // [128 CTAs][28 chunks][32 rows][64] swizzled tiles, unit-interleaved rows
   const float* ba;                 // [128][32]
   const __nv_bfloat16* Wd;         // [128][40][32][64]
+  const __nv_bfloat16* Wal;        // split mode: low bf16 parts of Wa / Wd (null: plain bf16 products)
+  const __nv_bfloat16* Wdl;
+  int split;                       // 1: gates = Wh.Xh + Wh.Xl + Wl.Xh (fp32-level products, fp32 accumulation)
   const float* bd;                 // [128][32]
   const float* WqT;                // [1024][128]
   const float* WlocD;              // [2][31][128] = location conv composed with the location dense layer
@@ -131,6 +141,15 @@ struct DecArgs {
 };
 
 unsigned long long* g_dec_trace = nullptr;
+
+// One value of the operand mirror: bf16(v), and in split mode also the remainder bf16(v - bf16(v))
+// (together ~16 significant bits; the gate products then match fp32 GEMV to ~1e-5 relative).
+__device__ __forceinline__ void xb_store(const DecArgs& a, int b, int col, float v) {
+  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+  const int64_t o = xb_off(b, col);
+  a.xb[o] = hi;
+  if (a.split) a.xbl[o] = __float2bfloat16_rn(v - __bfloat162float(hi));
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -320,13 +339,18 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       asm volatile("fence.proxy.async.global;" ::: "memory");  // xb tiles written by generic stores
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the ring doubles as PRE scratch
       uint32_t g = g_ring;
-      const int npre = (DEC_PREFETCH & (1 << MODE)) ? min(KCS, nst) : 0;  // weights gate_prefetch_w issued
-      // merged combine: the context columns (decoder gates, split 0, chunks 0..7) go last, after
-      // the combined contexts of every live item are counted in
-      const bool ctx_last = merged && MODE == 1 && ks == 0;
-      bool ctx_ready = !ctx_last;
-      for (int i = 0; i < KCS; ++i, ++g) {
+      // split mode: three virtual stages per K-chunk, (Wh, Xh), (Wh, Xl), (Wl, Xh)
+      const int nsub = a.split ? 3 : 1;
+      const int npre = (!a.split && (DEC_PREFETCH & (1 << MODE))) ? min(KCS, nst) : 0;  // weights prefetched
+      // decoder gates, split 0: the context columns (chunks 0..7) go last -- in the merged-combine
+      // schedule after the combined contexts of every live item are counted in.  The order is the
+      // same in both schedules, so the fp32 accumulation (and the result bits) do not depend on
+      // which schedule the batch size selects.
+      const bool ctx_last = MODE == 1 && ks == 0;
+      bool ctx_ready = !(ctx_last && merged);
+      for (int v = 0; v < KCS * nsub; ++v, ++g) {
         if (g % 3 != pi) continue;
+        const int i = v / nsub, sub = v - i * nsub;
         const uint32_t st = g % nst, ph = (g / nst) & 1;
         if (i >= npre) tcg::mbar_wait(&gsy.empty[st], ph ^ 1);
         const int kc = ks * KCS + (ctx_last ? (i + 8) % KCS : i), k0 = kc * 64;
@@ -338,17 +362,18 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
         int col;
         if (MODE == 0) col = k0 < 768 ? k0 : att_off(oldb) + (k0 - 768);
         else col = k0 < 512 ? CTX_OFF + k0 : (k0 < 1536 ? att_off(newb) + (k0 - 512) : dec_off(oldb) + (k0 - 1536));
+        const __nv_bfloat16* wsrc = sub == 2 ? (MODE == 0 ? a.Wal : a.Wdl) : (MODE == 0 ? a.Wa : a.Wd);
+        const __nv_bfloat16* xsrc = sub == 1 ? a.xbl : a.xb;
         if (i < npre) {
           tcg::mbar_expect_tx(&gsy.full[st], n16 * 128);
         } else {
           tcg::mbar_expect_tx(&gsy.full[st], GW_TILE + n16 * 128);
-          bulk_g2s(sW + st * GW_TILE, (MODE == 0 ? a.Wa : a.Wd) + ((int64_t)ug * NKC + kc) * 128 * 64, GW_TILE,
-                   &gsy.full[st]);
+          bulk_g2s(sW + st * GW_TILE, wsrc + ((int64_t)ug * NKC + kc) * 128 * 64, GW_TILE, &gsy.full[st]);
         }
         const int r0 = min(n16, 128);
-        bulk_g2s(sX + st * x_stage_bytes, a.xb + (int64_t)(col >> 6) * 128 * 64, r0 * 128, &gsy.full[st]);
+        bulk_g2s(sX + st * x_stage_bytes, xsrc + (int64_t)(col >> 6) * 128 * 64, r0 * 128, &gsy.full[st]);
         if (n16 > 128)  // items 128.. live in the next 128-row block of the mirror
-          bulk_g2s(sX + st * x_stage_bytes + 128 * 128, a.xb + (int64_t)(NCC + (col >> 6)) * 128 * 64,
+          bulk_g2s(sX + st * x_stage_bytes + 128 * 128, xsrc + (int64_t)(NCC + (col >> 6)) * 128 * 64,
                    (n16 - 128) * 128, &gsy.full[st]);
       }
       if (pi == 0) mark(0);
@@ -360,7 +385,8 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       uint32_t g = g_ring;
       tcg::mbar_wait(&gsy.acce, (lt_tile & 1) ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      for (int i = 0; i < KCS; ++i, ++g) {
+      const int nv = KCS * (a.split ? 3 : 1);
+      for (int i = 0; i < nv; ++i, ++g) {
         const uint32_t st = g % nst, ph = (g / nst) & 1;
         tcg::mbar_wait(&gsy.full[st], ph);
         if (i == 0) mark(1);
@@ -448,7 +474,7 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
           float* st = a.work + (int64_t)b * ROW;
           st[c_off + j] = cn;
           st[h_off + j] = hn;
-          a.xb[xb_off(b, hb_off + j)] = __float2bfloat16_rn(hn);
+          xb_store(a, b, hb_off + j, hn);
         }
         hs[e] = hn;
       }
@@ -482,7 +508,7 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
     __syncthreads();
     if (threadIdx.x == 0) mark(5);
   }
-  g_ring += KCS;
+  g_ring += KCS * (a.split ? 3 : 1);
   lt_tile += 1;
 }
 
@@ -723,7 +749,7 @@ __device__ void att_combine(const DecArgs& a, AttSmem& sm, int s, int b, int chu
     }
     for (; k < nch; ++k) c = fmaf(scale[k], ldf(ap + k * (2 + EMB) + 2 + d), c);
     st[CTX_OFF + d] = c;
-    a.xb[xb_off(b, CTX_OFF + d)] = __float2bfloat16_rn(c);
+    xb_store(a, b, CTX_OFF + d, c);
   }
   WFENCE();
   for (int t = tid; t < L; t += NT) {
@@ -785,7 +811,7 @@ __global__ void __launch_bounds__(NT, 1)
   // bf16 operand mirror, bank 0, from the gathered fp32 state rows
   for (int b = c; b < a.B; b += G) {
     const float* st = a.work + (int64_t)b * ROW;
-    for (int i = tid; i < ATTC_OFF; i += NT) a.xb[xb_off(b, i)] = __float2bfloat16_rn(ldf(st + i));
+    for (int i = tid; i < ATTC_OFF; i += NT) xb_store(a, b, i, ldf(st + i));
   }
   WFENCE();
   grid_sync(a.bar, gen);
@@ -799,10 +825,19 @@ __global__ void __launch_bounds__(NT, 1)
     for (int b = 0; b < a.B; ++b) nt += (pc.L[b] + ch - 1) / ch;
     return nt;
   };
+#if DEC_ADAPTIVE_CHUNK
   int chunk = 16;
   while (chunk < ACH && ntask_for(chunk) > G) chunk += 16;
   if (ntask_for(chunk) > G) chunk = 32;
   if ((maxL + chunk - 1) / chunk > MAXCH) chunk = (maxL + MAXCH - 1) / MAXCH;  // <= 32 for L <= 8192
+#else
+  // Fixed 32-position chunks: an item's softmax / context reduction order then depends on its own
+  // L only, so a request decodes to the same bits in any pooled batch (batch transparency,
+  // reference SPEC.md:232); 32 positions = 8 warps x 4 in the energy pass.
+  constexpr int chunk = 32;
+  (void)maxL;
+  (void)ntask_for;
+#endif
   const int nb8 = (a.B + 7) / 8;
   const bool merged = a.B <= DEC_MERGE_B;  // ATT-B folded into the decoder-gate phase
 
@@ -919,7 +954,7 @@ __global__ void __launch_bounds__(NT, 1)
                       if (!active(pc, b, gs)) return;
                       y = fmaxf(y, 0.f);
                       a.work[(int64_t)b * ROW + P_OFF + n] = y;
-                      a.xb[xb_off(b, P_OFF + n)] = __float2bfloat16_rn(y);
+                      xb_store(a, b, P_OFF + n, y);
                     });
       WFENCE();
       pmark(7);
@@ -1078,15 +1113,21 @@ ITTS_API int itts_r_decode_persistent(int32_t B, int32_t nsteps, const int64_t* 
                                       const void* Wd, const float* bd, const float* WqT, const float* WlocD,
                                       const float* v, const float* WpT, const float* bp,
                                       float* Gp, float* H1, float* Qp, float* Pp, float* U, int64_t u_ld,
-                                      float* AP, unsigned* bar, void* stream) {
+                                      float* AP, unsigned* bar, const void* Wa_lo, const void* Wd_lo,
+                                      void* stream) {
   if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
   if (B > 256) return ITTS_EUNSUPPORTED;  // attention task table in shared memory; MMA N <= 256
   if (nsteps <= 0 || !plan || !work || !xb || !Wa || !Wd || !bar) return ITTS_EINVAL;
   if (tcg::num_sms() < GEMM_CTAS) return ITTS_EUNSUPPORTED;
   cudaStream_t st = (cudaStream_t)stream;
-  DecArgs a{B, nsteps, 0, plan, work, (__nv_bfloat16*)xb, W0T, W1T, (const __nv_bfloat16*)Wa, ba,
-            (const __nv_bfloat16*)Wd, bd, WqT, WlocD, v, WpT, bp, Gp, H1, Qp, Pp, U, u_ld, AP, bar,
-            g_dec_trace};
+  if ((Wa_lo == nullptr) != (Wd_lo == nullptr)) return ITTS_EINVAL;
+  const int split = Wa_lo != nullptr;
+  // split mode: the mirror buffer holds the high parts, then the low parts (same tile layout)
+  __nv_bfloat16* xbh = (__nv_bfloat16*)xb;
+  __nv_bfloat16* xbl = split ? xbh + (int64_t)((B + 127) / 128) * NCC * 128 * 64 : nullptr;
+  DecArgs a{B, nsteps, 0, plan, work, xbh, xbl, W0T, W1T, (const __nv_bfloat16*)Wa, ba,
+            (const __nv_bfloat16*)Wd, (const __nv_bfloat16*)Wa_lo, (const __nv_bfloat16*)Wd_lo, split, bd,
+            WqT, WlocD, v, WpT, bp, Gp, H1, Qp, Pp, U, u_ld, AP, bar, g_dec_trace};
   const size_t smem = 1024 + RING_BYTES + sizeof(AttSmem);
   const int b16 = (B + 15) / 16 * 16;
   uint32_t a_box_bytes = (uint32_t)b16 * 128;  // X stage: all items x 64 columns

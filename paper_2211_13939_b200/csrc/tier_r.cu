@@ -456,10 +456,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(AT_WARPS * 32, 3)
 // plan[i] = {tok_off, L, row_base (first valid row), mem_ptr, pm_ptr, 0}
 constexpr int EPLAN = 6;
 
+template <typename OutT>
 __global__ void k_enc_embed(const int32_t* __restrict__ tok4, int64_t total, const int64_t* __restrict__ plan,
                             const float* __restrict__ Eph, const float* __restrict__ Epw,
                             const float* __restrict__ Epph, const float* __restrict__ Eiph,
-                            __nv_bfloat16* __restrict__ X) {
+                            OutT* __restrict__ X) {
   itts::pdl_trigger();
   itts::pdl_wait();
   const int64_t* p = plan + blockIdx.y * EPLAN;
@@ -471,7 +472,32 @@ __global__ void k_enc_embed(const int32_t* __restrict__ tok4, int64_t total, con
   const int64_t idx = p[0] + t;
   const float v = ((Eph[(int64_t)tok4[idx] * EMB + c] + Epw[(int64_t)tok4[total + idx] * EMB + c]) +
                    Epph[(int64_t)tok4[2 * total + idx] * EMB + c]) + Eiph[(int64_t)tok4[3 * total + idx] * EMB + c];
-  X[(p[2] + t) * EMB + c] = __float2bfloat16_rn(v);
+  if constexpr (sizeof(OutT) == 4) X[(p[2] + t) * EMB + c] = v;
+  else X[(p[2] + t) * EMB + c] = __float2bfloat16_rn(v);
+}
+
+// Split-bf16 parity encoder: fp32 activations [rows][512] (valid rows of each item) -> the bf16
+// operand [rows][1536] = [hi | lo | hi] (hi = bf16(v), lo = bf16(v - hi)), so one tensor-core conv
+// against weights [Wh | Wh | Wl] computes Wh.Xh + Wh.Xl + Wl.Xh (fp32-level products, fp32
+// accumulation).  relu: apply max(v, 0) first.  Halo rows are never written (zero from a memset).
+__global__ void k_split3(const float* __restrict__ src, const int64_t* __restrict__ plan, int relu,
+                         __nv_bfloat16* __restrict__ dst) {
+  itts::pdl_trigger();
+  itts::pdl_wait();
+  const int64_t* p = plan + blockIdx.y * EPLAN;
+  const int64_t L = p[1];
+  const int64_t g = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (g >= L * EMB) return;
+  const int64_t row = p[2] + g / EMB;
+  const int c = (int)(g % EMB);
+  float v = src[row * EMB + c];
+  if (relu) v = fmaxf(v, 0.f);
+  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+  const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+  __nv_bfloat16* d = dst + row * (3 * EMB) + c;
+  d[0] = hi;
+  d[EMB] = lo;
+  d[2 * EMB] = hi;
 }
 
 // One 8-CTA cluster per (item, direction).  CTA r owns hidden units
@@ -812,9 +838,9 @@ ITTS_API int itts_r_enc_embed(const int32_t* tok4, int64_t total, const int64_t*
                               int64_t max_len, const float* Eph, const float* Epw, const float* Epph,
                               const float* Eiph, void* X, void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
-  const cudaError_t le_ = itts::launch_pdl(k_enc_embed, dim3(grid2(max_len * EMB, n)), dim3(256), 0, (cudaStream_t)stream,
-                                           tok4, total, plan, Eph, Epw, Epph, Eiph,
-                                                                        (__nv_bfloat16*)X);
+  const cudaError_t le_ = itts::launch_pdl(k_enc_embed<__nv_bfloat16>, dim3(grid2(max_len * EMB, n)), dim3(256), 0,
+                                           (cudaStream_t)stream, tok4, total, plan, Eph, Epw, Epph, Eiph,
+                                           (__nv_bfloat16*)X);
   if (le_ != cudaSuccess) return (int)le_;
   ITTS_RETURN_LAUNCH();
 }
@@ -878,6 +904,54 @@ ITTS_API int itts_r_encode(const void* pack, int64_t total, int32_t n, int64_t m
   const int32_t off0 = 0;
   if ((r = itts_conv1d_tc(xb, rows, EMB, EMB, W(10), 8 * EH, 1, &off0, (const float*)W(11), 8 * EH, rowmap, nullptr,
                           1.0f, pre, 1, nullptr, 0, nullptr, 1.0f, 1, 128, stream)))
+    return r;
+  if ((r = itts_r_bilstm(pre, plan, n, (const float*)W(12), stream))) return r;
+  if ((r = itts_r_pmem(plan, n, max_len, (const float*)W(13), stream))) return r;
+  const cudaError_t le_ = itts::launch_pdl(k_zero_spans, dim3(dim3(8, n)), dim3(256), 0, st, spans);
+  if (le_ != cudaSuccess) return (int)le_;
+  ITTS_RETURN_LAUNCH();
+}
+
+// The encoder of the split-bf16 parity mode: the same launch sequence as itts_r_encode with every
+// tensor-core product (3 convs, the BiLSTM input projection) on [hi | lo | hi] operands against
+// [Wh | Wh | Wl] weights (weights3: the itts_r_encode weight table with the conv / input-projection
+// entries replaced by those [.][C_out][3 x 512] tensors); activations stay fp32 between layers
+// (f32 [rows][512]), x3 = bf16 [rows][1536] operand buffer.
+ITTS_API int itts_r_encode_split(const void* pack, int64_t total, int32_t n, int64_t max_len, int64_t rows,
+                                 int64_t max_span, const int64_t* weights3, int32_t conv_taps, void* x3, float* f32,
+                                 float* pre, int32_t* rowmap, void* stream) {
+  if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
+  if (conv_taps < 1 || conv_taps > 15 || !pack || !weights3 || !x3 || !f32 || !pre || !rowmap) return ITTS_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int32_t* tok4 = static_cast<const int32_t*>(pack);
+  const int64_t* plan = static_cast<const int64_t*>(pack) + (4 * total + 1) / 2;
+  const int64_t* rm_plan = plan + 6 * (int64_t)n;
+  const int64_t* spans = rm_plan + 5 * (int64_t)n;
+  auto W = [&](int i) { return reinterpret_cast<const void*>(weights3[i]); };
+  cudaError_t e = cudaMemsetAsync(x3, 0, (size_t)rows * 3 * EMB * 2, st);
+  if (e != cudaSuccess) return (int)e;
+  const dim3 g2 = grid2(max_len * EMB, n);
+  if ((e = itts::launch_pdl(k_enc_embed<float>, g2, dim3(256), 0, st, tok4, total, plan, (const float*)W(0),
+                            (const float*)W(1), (const float*)W(2), (const float*)W(3), f32)) != cudaSuccess)
+    return (int)e;
+  if ((e = itts::launch_pdl(k_split3, g2, dim3(256), 0, st, (const float*)f32, plan, 0, (__nv_bfloat16*)x3)) !=
+      cudaSuccess)
+    return (int)e;
+  int r;
+  if ((r = itts_r_rowmap(rm_plan, n, max_span, rowmap, stream))) return r;
+  int32_t offs[16];
+  for (int j = 0; j < conv_taps; ++j) offs[j] = j - (conv_taps - 1) / 2;
+  for (int i = 0; i < 3; ++i) {
+    if ((r = itts_conv1d_tc(x3, rows, 3 * EMB, 3 * EMB, W(4 + 2 * i), EMB, conv_taps, offs, (const float*)W(5 + 2 * i),
+                            EMB, rowmap, nullptr, 1.0f, f32, 1, nullptr, 0, nullptr, 0.0f, 0, 0, stream)))
+      return r;
+    if ((e = itts::launch_pdl(k_split3, g2, dim3(256), 0, st, (const float*)f32, plan, 1, (__nv_bfloat16*)x3)) !=
+        cudaSuccess)
+      return (int)e;
+  }
+  const int32_t off0 = 0;
+  if ((r = itts_conv1d_tc(x3, rows, 3 * EMB, 3 * EMB, W(10), 8 * EH, 1, &off0, (const float*)W(11), 8 * EH, rowmap,
+                          nullptr, 1.0f, pre, 1, nullptr, 0, nullptr, 1.0f, 1, 128, stream)))
     return r;
   if ((r = itts_r_bilstm(pre, plan, n, (const float*)W(12), stream))) return r;
   if ((r = itts_r_pmem(plan, n, max_len, (const float*)W(13), stream))) return r;

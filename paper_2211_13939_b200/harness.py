@@ -266,3 +266,90 @@ def merge_rank_stats(local: dict, dist=None) -> dict | None:
         merged[k] = sum(g.get(k, 0) for g in gathered)
     merged["per_rank_window"] = [g["window"] for g in gathered]
     return merged
+
+
+def serve_router(router, trace: list[TimedRequest], *, warmup_seconds: float, timed_seconds: float,
+                 drain_seconds: float = 5.0, tail_seconds: float = 60.0) -> ServeRun:
+    """``serve`` for the multi-GPU path: plays ``trace`` against a :class:`router.Router` (one pool
+    per GPU worker process).  The window is ``[warmup_seconds, warmup_seconds + timed_seconds)``
+    after the first send; every request sent inside it is measured.  ``first_push`` is the
+    worker-side time its first chunk became visible (CLOCK_MONOTONIC, same clock as here),
+    ``first_recv`` the time this process's poller received it from the router."""
+    run = ServeRun(timings=[])
+    lock = threading.Lock()
+    live: list = []
+    stop_poll = threading.Event()
+
+    def poller() -> None:
+        pending: list = []
+        while not (stop_poll.is_set() and not pending and not live):
+            time.sleep(0.001)
+            with lock:
+                pending.extend(live)
+                live.clear()
+            keep = []
+            for rec, stream in pending:
+                try:
+                    while True:
+                        chunk = stream.get(timeout=0)
+                        now = time.perf_counter()
+                        if chunk is None:
+                            rec.done = True
+                            break
+                        if rec.first_recv is None:
+                            rec.first_recv = now
+                        rec.last_recv = now
+                        rec.samples += chunk.sample_count
+                        rec.chunks += 1
+                except queue.Empty:
+                    keep.append((rec, stream))
+                except Exception as exc:  # noqa: BLE001 -- recorded, reported by the caller
+                    rec.error = str(exc)
+                    rec.done = True
+            pending = keep
+            if stop_poll.is_set():   # one last pass after the stop; later chunks are not measured
+                return
+
+    th = threading.Thread(target=poller, name="router-client-poller", daemon=True)
+    th.start()
+    origin = time.perf_counter()
+    w0, w1 = origin + warmup_seconds, origin + warmup_seconds + timed_seconds
+    run.window = (w0, w1)
+    for req in trace:
+        _wait_until(origin + req.send_at)
+        now = time.perf_counter()
+        if now >= w1:
+            inside = [r for r in run.timings if w0 <= r.send_time < w1]
+            if all(r.done for r in inside) or now - w1 > drain_seconds:
+                break
+        rid, stream = router.submit(req.text)
+        rec = RequestTiming(rid, req.text, time.perf_counter())
+        with lock:
+            run.timings.append(rec)
+            live.append((rec, stream))
+    else:
+        end = time.perf_counter() + tail_seconds
+        while time.perf_counter() < end and not all(r.done for r in run.timings):
+            time.sleep(0.005)
+    stop_poll.set()
+    th.join(timeout=10.0)
+    for rec in run.timings:
+        rec.first_push = router.first_push.get(rec.request_id)
+    return run
+
+
+def warm_up(modules: PipelineModules, cfg, seed: int = 7, max_batch: int = 512) -> None:
+    """Untimed warm-up of every serving code path before a measurement: decoder CUDA graphs of
+    every batch bucket, vocoder work buffers, pinned host blocks (engine.prepare_graphs), then a
+    Poisson second and bursts of simultaneous arrivals (large encoder batches, tensor maps, lazy
+    module loading, allocator pools).  Also the router workers' ``WorkerSpec.warmup``."""
+    engine = getattr(modules, "engine", None)
+    if engine is not None and hasattr(engine, "prepare_graphs"):
+        engine.prepare_graphs(max_batch=max_batch)
+    lex = default_lexicon()
+    serve(modules, cfg, poisson_trace(50, 1.0, seed=seed, lexicon=lex), warmup_iters=0, timed_iters=2,
+          drain_seconds=0.0)
+    rng = random.Random(seed + 1)
+    for burst in (8, 32, 64):
+        serve(modules, cfg, [TimedRequest(0.0, random_text(rng, 20, 200, lex)) for _ in range(burst)],
+              warmup_iters=0, timed_iters=None, drain_seconds=0.0)

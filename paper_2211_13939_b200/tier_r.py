@@ -71,8 +71,10 @@ def _hifigan_macs_per_frame() -> int:
 
 HIFIGAN_MACS_PER_FRAME = _hifigan_macs_per_frame()
 # Decoder-step weight bytes as stored here (bf16 gate GEMMs, fp32 elsewhere).
-DEC_WEIGHT_BYTES = (4096 * 1792 + 4096 * 2560) * 2 + (80 * 256 + 256 * 256 + 1024 * 128 + 32 * 62 + 32 * 128
-                                                      + 128 + 1536 * 81 + 81) * 4
+_DEC_GEMV_BYTES = (80 * 256 + 256 * 256 + 1024 * 128 + 32 * 62 + 32 * 128 + 128 + 1536 * 81 + 81) * 4
+DEC_WEIGHT_BYTES = (4096 * 1792 + 4096 * 2560) * 2 + _DEC_GEMV_BYTES
+# parity mode: the gate weights carry fp32-level values (high + low bf16 parts = 4 bytes per weight)
+DEC_WEIGHT_BYTES_SPLIT = (4096 * 1792 + 4096 * 2560) * 4 + _DEC_GEMV_BYTES
 
 
 def _on_device(fn):
@@ -182,6 +184,9 @@ class TierREngine:
         self.use_graphs = True           # CUDA-graph the 32-step decoder chunk per (batch, L) bucket
         self.fused_mrf = True            # one fused c1->c2 kernel per ResBlock1 layer (resblock_tc.cu)
         self.persistent_decoder = True   # whole decoder chunk in one grid-synchronised kernel (dec_persist.cu)
+        # decoder gate products: "parity" = split bf16 (Wh.Xh + Wh.Xl + Wl.Xh, fp32 accumulate: fp32-level
+        # mel, north_star's parity mode); "bf16" = single bf16 products (reported separately)
+        self.precision = "parity"
         self.pcm16 = False               # also produce 16-bit PCM on device in the splice pass (f1)
         self.mrf_streams = True          # run the 3 MRF branches of a stage on 3 streams (fused path)
         self.native_vocoder = True       # issue the fused HiFi-GAN stack from C++ (voc_run.cu)
@@ -210,6 +215,11 @@ class TierREngine:
             enc_w += [wt, bias]
         enc_w += [self.enc_ih[0], self.enc_ih[2], self.enc_whhT, self.WmT]
         self._enc_ptrs = (ctypes.c_int64 * len(enc_w))(*[t.data_ptr() for t in enc_w])
+        # parity mode: conv / input-projection weights as [Wh | Wh | Wl] along C_in (itts_r_encode_split)
+        enc_w3 = list(enc_w)
+        for i, t in enumerate(self._enc_split_w):
+            enc_w3[4 + 2 * i] = t
+        self._enc_ptrs3 = (ctypes.c_int64 * len(enc_w3))(*[t.data_ptr() for t in enc_w3])
         self._voc = self._create_native_vocoder()
         self._side = [torch.cuda.Stream(self.device) for _ in range(2)]
         self._ev = [torch.cuda.Event() for _ in range(3)]
@@ -217,6 +227,24 @@ class TierREngine:
         self._pool: dict = {}
         self._pin_out = torch.empty(1 << 22, dtype=torch.float32, pin_memory=True)  # audio D2H
         self._graph_warm = False
+
+    PRECISIONS = ("parity", "bf16")
+
+    def set_precision(self, mode: str) -> None:
+        """Decoder gate-product arithmetic for later calls (drops captured decoder graphs)."""
+        if mode not in self.PRECISIONS:
+            raise ValueError(f"precision must be one of {self.PRECISIONS}")
+        if mode != self.precision:
+            self.stream.synchronize()
+            self._dec_buckets = {}
+            self._graph_warm = False
+        self.precision = mode
+
+    def precision_label(self) -> str:
+        if self.precision == "parity":
+            return ("fp32-level decoder: split-bf16 (x3) tcgen05 gate products, fp32 accumulate / attention / "
+                    "cells; bf16-operand encoder convs and HiFi-GAN (fp32 accumulate)")
+        return "bf16 decoder gate products; bf16-operand encoder convs and HiFi-GAN (fp32 accumulate)"
 
     def _mark(self, kind: str, units):
         """Context manager recording CUDA events on the engine stream around a region (timers on);
@@ -241,6 +269,13 @@ class TierREngine:
                        f32(torch.cat([w["enc.lstm_fwd.b_ih"] + w["enc.lstm_fwd.b_hh"],
                                       w["enc.lstm_bwd.b_ih"] + w["enc.lstm_bwd.b_hh"]])))
         self.enc_whhT = f32(torch.stack([w["enc.lstm_fwd.w_hh"].T, w["enc.lstm_bwd.w_hh"].T]))  # [2][256][1024]
+
+        def split3(t):   # fp32 [k][C_out][C_in] -> bf16 [k][C_out][3 C_in] = [Wh | Wh | Wl]
+            hi = t.to(torch.bfloat16)
+            lo = (t - hi.float()).to(torch.bfloat16)
+            return torch.cat([hi, hi, lo], 2).contiguous()
+        self._enc_split_w = [split3(f32(w[f"enc.conv{i}.w"]).permute(2, 0, 1)) for i in range(3)]
+        self._enc_split_w.append(split3(wih.to(d).float()[None]))
         self.WmT = f32(w["att.memory_layer"].T)                                          # [512][128]
         # decoder
         self.W0T, self.W1T = f32(w["prenet.0"].T), f32(w["prenet.1"].T)
@@ -255,9 +290,13 @@ class TierREngine:
         # persistent decoder: gate rows regrouped per 32-unit group g as [unit u][gate q]
         # (row 128g + 4u + q <- original row q*1024 + 32g + u), then UMMA-swizzled 64-column tiles
         perm = lambda t: t.reshape(4, HID // 32, 32, -1).permute(1, 2, 0, 3).reshape(4 * HID, -1)
-        self.Wa_p = _swizzle_tiles(perm(wa.to(d)).to(torch.bfloat16), 128)
+        # split-bf16 parity mode: W = Wh + Wl with Wh = bf16(W), Wl = bf16(W - Wh) (same layout)
+        split = lambda t: (t.to(torch.bfloat16), (t - t.to(torch.bfloat16).float()).to(torch.bfloat16))
+        wa_h, wa_l = split(perm(wa.to(d).float()))
+        wd_h, wd_l = split(perm(wd.to(d).float()))
+        self.Wa_p, self.Wal_p = _swizzle_tiles(wa_h, 128), _swizzle_tiles(wa_l, 128)
+        self.Wd_p, self.Wdl_p = _swizzle_tiles(wd_h, 128), _swizzle_tiles(wd_l, 128)
         self.ba_p = perm(self.att_bias[:, None]).reshape(-1).contiguous()
-        self.Wd_p = _swizzle_tiles(perm(wd.to(d)).to(torch.bfloat16), 128)
         self.bd_p = perm(self.dec_bias[:, None]).reshape(-1).contiguous()
         self.WqT = f32(w["att.query_layer"].T)                                           # [1024][128]
         self.Wloc = f32(w["att.location_conv"])                                          # [32][2][31]
@@ -504,15 +543,24 @@ class TierREngine:
         pack = np.concatenate([tok_words.view(np.int64), plan.reshape(-1), rm_plan.reshape(-1), spans.reshape(-1)])
         with torch.cuda.stream(self.stream):
             d_pack = self._up(pack)
-            xa = self._buf("enc_xa", lay.total * W.EMB)
-            xb = self._buf("enc_xb", lay.total * W.EMB)
             pre = self._buf("enc_pre", lay.total * 2048, torch.float32)
             rm = self._buf("enc_rm", lay.total, torch.int32)
+            span = int(max(lay.rows)) + 2 * lay.halo
             with self._mark("encoder", total):
-                self._call("itts_r_encode", d_pack.data_ptr(), total, n, max_len, lay.total,
-                           int(max(lay.rows)) + 2 * lay.halo, self._enc_ptrs, ENC_TAPS, xa.data_ptr(),
-                           xb.data_ptr(), pre.data_ptr(), rm.data_ptr(), self._st())
-                self.launches += 9   # embed, row map, 3 convs, input projection, BiLSTM, memory, state zero
+                if self.precision == "parity":
+                    x3 = self._buf("enc_x3", lay.total * 3 * W.EMB)
+                    f32 = self._buf("enc_f32", lay.total * W.EMB, torch.float32)
+                    self._call("itts_r_encode_split", d_pack.data_ptr(), total, n, max_len, lay.total, span,
+                               self._enc_ptrs3, ENC_TAPS, x3.data_ptr(), f32.data_ptr(), pre.data_ptr(),
+                               rm.data_ptr(), self._st())
+                    self.launches += 13  # embed, 4 splits, row map, 3 convs, input projection, BiLSTM, memory, zero
+                else:
+                    xa = self._buf("enc_xa", lay.total * W.EMB)
+                    xb = self._buf("enc_xb", lay.total * W.EMB)
+                    self._call("itts_r_encode", d_pack.data_ptr(), total, n, max_len, lay.total, span,
+                               self._enc_ptrs, ENC_TAPS, xa.data_ptr(), xb.data_ptr(), pre.data_ptr(),
+                               rm.data_ptr(), self._st())
+                    self.launches += 9   # embed, row map, 3 convs, input projection, BiLSTM, memory, state zero
         fpp = self.cfg.frames_per_phoneme
         return [(DeviceEncodedFeatures(req), DeviceDecoderState(req, buf, 0, fpp * req.seq_len))
                 for req, buf in reqs]
@@ -585,7 +633,8 @@ class TierREngine:
         Ls_np = np.array(Ls, dtype=np.int64)
         src = base + 4 * np.array(src_off, dtype=np.int64)
         dstp = base + 4 * np.array(dst_off, dtype=np.int64)
-        dec_bytes = lambda: max_steps * DEC_WEIGHT_BYTES + int(  # algorithmic bytes (timers only)
+        wbytes = DEC_WEIGHT_BYTES_SPLIT if self.precision == "parity" else DEC_WEIGHT_BYTES
+        dec_bytes = lambda: max_steps * wbytes + int(  # algorithmic bytes (timers only)
             (steps_np * (2 * 4 * ROW + Ls_np * (4 * 512 + 4 * 128 + 16) + 4 * 81)).sum())
         with torch.cuda.stream(self.stream):
             if self.use_graphs and max_steps == C and max_L <= GRAPH_MAX_L:
@@ -675,14 +724,16 @@ class TierREngine:
         st, n = self._st(), b.n
         self._call("itts_gather_rows", b.work.data_ptr(), b.d_src.data_ptr(), n, 4 * ROW, st)
         if self.persistent_decoder and max_L <= PERSIST_MAX_L and n <= PERSIST_MAX_B:
-            b.ensure_persistent(max_L)
+            split = self.precision == "parity"
+            b.ensure_persistent(max_L, split)
             self._call("itts_r_decode_persistent", n, nsteps, b.d_plan.data_ptr(), b.work.data_ptr(),
                        b.xb2.data_ptr(), self.W0T.data_ptr(), self.W1T.data_ptr(), self.Wa_p.data_ptr(),
                        self.ba_p.data_ptr(), self.Wd_p.data_ptr(), self.bd_p.data_ptr(), self.WqT.data_ptr(),
                        self.WlocD.data_ptr(), self.v.data_ptr(), self.WpT.data_ptr(),
                        self.bp.data_ptr(), b.Gp.data_ptr(), b.H1.data_ptr(), b.Q.data_ptr(), b.P.data_ptr(),
                        b.U.data_ptr(),
-                       b.U.shape[1], b.AP.data_ptr(), b.bar.data_ptr(), st)
+                       b.U.shape[1], b.AP.data_ptr(), b.bar.data_ptr(),
+                       self.Wal_p.data_ptr() if split else 0, self.Wdl_p.data_ptr() if split else 0, st)
             self._call("itts_scatter_rows", b.d_dst.data_ptr(), b.work.data_ptr(), n, 4 * ROW, st)
             return
         self._call("itts_r_dec_prepare", b.work.data_ptr(), b.xbm.data_ptr(), n, st)
@@ -1103,6 +1154,7 @@ class _DecBuffers:
         self.P = self._empty((33, n, 81), torch.float32, "P")
         self.H1 = self._empty((n, 256), torch.float32, "H1")
         self.dev, self.xb2, self.U, self.AP, self.bar, self.Gp = dev, None, None, None, None, None
+        self.split = False
 
     def _poisoned(self, name: str) -> bool:
         return self.poison is True or (bool(self.poison) and name in self.poison)
@@ -1113,12 +1165,14 @@ class _DecBuffers:
             t.fill_(self.poison[name] if isinstance(self.poison, dict) else float("nan"))
         return t
 
-    def ensure_persistent(self, max_L: int) -> None:
-        """Scratch of the persistent decoder kernel (allocated once per buffer set)."""
-        if self.U is not None and self.U.shape[1] >= max_L:
+    def ensure_persistent(self, max_L: int, split: bool = False) -> None:
+        """Scratch of the persistent decoder kernel (allocated once per buffer set); the split-bf16
+        mode keeps a second (low-part) operand mirror after the first."""
+        if self.U is not None and self.U.shape[1] >= max_L and self.split == split:
             return
+        self.split = split
         nblk = -(-self.n // 128)
-        self.xb2 = self._empty((nblk * (XB2 // 64) * 128 * 64,), torch.bfloat16, "xb2")
+        self.xb2 = self._empty(((2 if split else 1) * nblk * (XB2 // 64) * 128 * 64,), torch.bfloat16, "xb2")
         if not self._poisoned("xb2"):
             self.xb2.zero_()
         self.U = self._empty((self.n, max(max_L, 256)), torch.float32, "U")

@@ -35,6 +35,8 @@ def texts(n, seed, lo=20, hi=200):
 
 @pytest.mark.parametrize("B", [1, 16, 100, 192, 256])
 def test_persistent_matches_chain(engine, B):
+    """Same (bf16) gate arithmetic on both paths; the split-bf16 parity mode is persistent-only."""
+    engine.set_precision("bf16")
     lex = default_lexicon()
     encs = engine.encoder_batch([run_frontend(t, lex) for t in texts(B, B)])
     pairs = [(st, enc) for enc, st in encs]
@@ -48,6 +50,7 @@ def test_persistent_matches_chain(engine, B):
         outs[persistent] = ([r.mel.frames for r in r1] + [r.mel.frames for r in r2],
                             [engine.read_state(r.state.req, r.state.buf) for r in r2])
     engine.persistent_decoder = True
+    engine.set_precision("parity")
     for a, b in zip(outs[True][0], outs[False][0]):
         assert np.isfinite(a).all()
         assert np.abs(a - b).max() <= 2e-4
@@ -104,3 +107,23 @@ def test_graph_bucket_equals_eager(engine, B):
             engine.use_graphs = False
     for a, b in zip(out[False], out[True]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("B", [24, 96, 97, 100])
+def test_pooled_decode_equals_solo_bitwise(engine, B):
+    """Batch transparency (reference SPEC.md:232, acceptance 1): a request's mel and state are the
+    same bits whether it decodes alone or inside a pooled ragged batch (merged-combine B <= 96 and
+    separate-combine schedules), over two consecutive chunks."""
+    pairs = _ragged_pairs(engine, B, 300 + B, [64, 40, 8, 64, 16, 64])
+    r1 = engine.decoder_batch(pairs)
+    r2 = engine.decoder_batch([(r.state, enc) for r, (_, enc) in zip(r1, pairs) if not r.stop])
+    pooled = [r.mel.frames for r in r1] + [r.mel.frames for r in r2]
+    for i in sorted({0, 1, 2, B // 2, B - 1}):
+        s1 = engine.decoder_batch([pairs[i]])[0]
+        solo = [s1.mel.frames]
+        if not s1.stop:
+            solo.append(engine.decoder_batch([(s1.state, pairs[i][1])])[0].mel.frames)
+        assert np.array_equal(solo[0], pooled[i])
+        if len(solo) > 1:
+            k = [j for j, r in enumerate(r1) if not r.stop].index(i)
+            assert np.array_equal(solo[1], pooled[len(r1) + k])

@@ -30,7 +30,8 @@ from paper_2211_13939_b200.scheduler import ChunkStream, CostModel, PipelineModu
 from paper_2211_13939_b200.weights import tier_r_weights
 
 pytestmark = pytest.mark.gpu
-MEL_TOL = 1e-3
+MEL_TOL = 1e-3          # north_star's fp32 tolerance (mel max-abs)
+PARITY_TOL = 2e-5       # what the default split-bf16 parity mode actually holds (measured ~3e-6 to 16k steps)
 SNR_DB = 40.0
 
 
@@ -71,6 +72,7 @@ def check_request(got_chunks, got_mel, want_chunks, want_mel):
     assert got_mel.shape == want_mel.shape
     err = float(np.abs(got_mel - want_mel).max())
     assert err <= MEL_TOL, err
+    assert err <= PARITY_TOL, err
     snr = orc.snr_db(np.concatenate([s for s, _ in want_chunks]), np.concatenate([c.samples for c in got_chunks]))
     assert snr >= SNR_DB, snr
     return err, snr
@@ -93,7 +95,7 @@ def test_pooled_requests_match_single_request_oracle(mods, weights, lexicon):
         rep = run_iteration(pool, wrapped, CostModel.zero(), cfg, step_index=it)
         assert not rep.failed_ids
         it += 1
-    # the decoder log is keyed by request handle; map back through each stream's chunk count
+    # the decoder log is keyed by request handle, in first-decoded order (= FIFO admission order)
     logs = list(mel_log.values())
     assert len(logs) == len(texts)
     errs = []
@@ -152,7 +154,7 @@ def test_long_paragraph_c5(mods, weights, lexicon):
     assert got_mel.shape == want_mel.shape
     err = float(np.abs(got_mel - want_mel).max())
     print(f"C5: {len(want)} chunks, {want_mel.shape[0]} frames, mel max-abs {err:.3e}")
-    assert err <= MEL_TOL, err
+    assert err <= PARITY_TOL, err
     first, _, _ = orc.synthesize(weights, fo.phonemes, fo.pw, fo.pph, fo.iph, max_chunks=8)
     for k, (samples, off) in enumerate(first):
         assert got_chunks[k].sample_offset == off
@@ -177,3 +179,26 @@ def test_non_incremental_twin_matches_oracle(mods, weights, lexicon, texts):
         want = orc.hifigan(weights, mel)
         assert chunk.sample_offset == 0 and chunk.sample_count == want.size
         assert orc.snr_db(want, chunk.samples) >= SNR_DB
+
+
+def test_bf16_mode_reported_separately(weights, lexicon):
+    """The single-bf16-product decoder / encoder mode (``set_precision("bf16")``): still inside
+    north_star's fp32 tolerance at the C1 length, about 100x looser than the parity mode."""
+    from paper_2211_13939_b200.modules import build_modules
+    cfg = PipelineConfig()
+    mods = build_modules(lexicon, cfg, tier="r", device="cuda:0", weights=weights)
+    mods.engine.set_precision("bf16")
+    wrapped, mel_log = recording(mods)
+    text = random_text(random.Random(5), 50, 50, lexicon)
+    pool = RequestPool()
+    _, stream = pool.submit(text)
+    while pool.pending():
+        run_iteration(pool, wrapped, CostModel.zero(), cfg)
+    fo = run_frontend(text, lexicon)
+    want_chunks, want_mel = oracle_request(weights, fo)
+    got_mel = np.concatenate(next(iter(mel_log.values())))
+    err = float(np.abs(got_mel - want_mel).max())
+    print(f"bf16 mode: mel max-abs {err:.3e}")
+    assert err <= MEL_TOL, err
+    snr = orc.snr_db(np.concatenate([s for s, _ in want_chunks]), np.concatenate([c.samples for c in stream]))
+    assert snr >= SNR_DB, snr

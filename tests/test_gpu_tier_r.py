@@ -74,9 +74,10 @@ def test_encoder_matches_oracle(engine, weights, lexicon):
         mem, pm = orc.encode(weights, fo.phonemes, fo.pw, fo.pph, fo.iph)
         got = enc.rows
         assert got.shape == tuple(mem.shape)
-        assert np.abs(got - mem.numpy()).max() <= 5e-3, np.abs(got - mem.numpy()).max()
+        # default split-bf16 parity mode: fp32-level products (measured ~6e-6 / 1e-5); bf16 mode ~1e-3
+        assert np.abs(got - mem.numpy()).max() <= 5e-5, np.abs(got - mem.numpy()).max()
         gpm = engine.read_processed_memory(enc.req)
-        assert np.abs(gpm - pm.numpy()).max() <= 5e-3
+        assert np.abs(gpm - pm.numpy()).max() <= 5e-5
         assert st.frames_emitted == 0 and st.target_frames == 8 * fo.seq_len
 
 

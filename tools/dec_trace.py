@@ -18,9 +18,11 @@ from paper_2211_13939_b200.tier_r import TierREngine  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--batches", default="16,64,128")
+ap.add_argument("--precision", default="parity")
 args = ap.parse_args()
 eng = TierREngine(PipelineConfig(), "cuda:0")
 eng.use_graphs = False
+eng.set_precision(args.precision)
 lex = default_lexicon()
 names = ["PRE", "ATT gates+q", "ATT-A", "ATT-B (or DEC gates+combine+proj)", "DEC gates+proj"]
 for B in [int(x) for x in args.batches.split(",")]:

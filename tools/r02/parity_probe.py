@@ -22,6 +22,7 @@ from paper_2211_13939_b200.weights import tier_r_weights  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--chars", default="50,200,1000")
 ap.add_argument("--precision", default=None)
+ap.add_argument("--oracle-encoder", action="store_true", help="feed the oracle's fp32 memory / processed memory")
 args = ap.parse_args()
 torch.set_num_threads(len(__import__("os").sched_getaffinity(0)))
 w = tier_r_weights(0)
@@ -34,6 +35,16 @@ for n in [int(x) for x in args.chars.split(",")]:
     text = random_text(rng, n, n, lex)
     fo = run_frontend(text, lex)
     (enc, st), = eng.encoder_batch([fo])
+    m_o, pm_o = orc.encode(w, fo.phonemes, fo.pw, fo.pph, fo.iph)
+    print(f"  encoder max-abs: memory {np.abs(enc.rows - m_o.numpy()).max():.3e} processed "
+          f"{np.abs(eng.read_processed_memory(enc.req) - pm_o.numpy()).max():.3e}", flush=True)
+    if args.oracle_encoder:
+        m_o, pm_o = orc.encode(w, fo.phonemes, fo.pw, fo.pph, fo.iph)
+        t = eng.arena.tensor
+        eng.stream.synchronize()
+        t[enc.req.extra["mem_off"]:enc.req.extra["mem_off"] + m_o.numel()].copy_(m_o.reshape(-1).to(t.device))
+        t[enc.req.extra["pm_off"]:enc.req.extra["pm_off"] + pm_o.numel()].copy_(pm_o.reshape(-1).to(t.device))
+        torch.cuda.synchronize()
     gpu = []
     while True:
         r, = eng.decoder_batch([(st, enc)])
