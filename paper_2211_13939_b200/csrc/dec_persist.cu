@@ -307,8 +307,15 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
   auto mark = [&](int slot) {
     if (tr) a.trace[16 + MODE * 8 + slot] += gtimer() - t_in;
   };
-  uint8_t* sW = ring;
-  uint8_t* sX = ring + nst * GW_TILE;
+  const bool comb = a.split && n16 <= 128;   // combined split stages (see k_dec_persist)
+  const uint32_t sbytes = 2 * (GW_TILE + (uint32_t)n16 * 128);
+  // stage st: the weight tile and the operand tile (combined split stages: Wh, Wl, Xh, Xl)
+  auto sW = [&](uint32_t st) { return comb ? ring + st * sbytes : ring + st * GW_TILE; };
+  auto sX = [&](uint32_t st) {
+    return comb ? ring + st * sbytes + 2 * GW_TILE : ring + nst * GW_TILE + st * x_stage_bytes;
+  };
+  // producer lanes: stage g goes to lane g % np; np <= nst keeps the empty-barrier parity unambiguous
+  const int np = min(3, nst);
   ++grp_gen;
   // Loads that do not depend on this phase's GEMM, issued now so their latency hides behind the
   // GEMM and the group sync: the group's slice of the next linear layer (query / projection)
@@ -339,8 +346,8 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       asm volatile("fence.proxy.async.global;" ::: "memory");  // xb tiles written by generic stores
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the ring doubles as PRE scratch
       uint32_t g = g_ring;
-      // split mode: three virtual stages per K-chunk, (Wh, Xh), (Wh, Xl), (Wl, Xh)
-      const int nsub = a.split ? 3 : 1;
+      // split mode, > 128 rows: three virtual stages per K-chunk, (Wh, Xh), (Wh, Xl), (Wl, Xh)
+      const int nsub = (a.split && !comb) ? 3 : 1;
       const int npre = (!a.split && (DEC_PREFETCH & (1 << MODE))) ? min(KCS, nst) : 0;  // weights prefetched
       // decoder gates, split 0: the context columns (chunks 0..7) go last -- in the merged-combine
       // schedule after the combined contexts of every live item are counted in.  The order is the
@@ -349,7 +356,7 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       const bool ctx_last = MODE == 1 && ks == 0;
       bool ctx_ready = !(ctx_last && merged);
       for (int v = 0; v < KCS * nsub; ++v, ++g) {
-        if (g % 3 != pi) continue;
+        if ((int)(g % np) != (int)pi) continue;
         const int i = v / nsub, sub = v - i * nsub;
         const uint32_t st = g % nst, ph = (g / nst) & 1;
         if (i >= npre) tcg::mbar_wait(&gsy.empty[st], ph ^ 1);
@@ -362,19 +369,28 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
         int col;
         if (MODE == 0) col = k0 < 768 ? k0 : att_off(oldb) + (k0 - 768);
         else col = k0 < 512 ? CTX_OFF + k0 : (k0 < 1536 ? att_off(newb) + (k0 - 512) : dec_off(oldb) + (k0 - 1536));
+        const int64_t wofs = ((int64_t)ug * NKC + kc) * 128 * 64, xofs = (int64_t)(col >> 6) * 128 * 64;
+        if (comb) {   // [Wh | Wl | Xh | Xl]
+          tcg::mbar_expect_tx(&gsy.full[st], sbytes);
+          bulk_g2s(sW(st), (MODE == 0 ? a.Wa : a.Wd) + wofs, GW_TILE, &gsy.full[st]);
+          bulk_g2s(sW(st) + GW_TILE, (MODE == 0 ? a.Wal : a.Wdl) + wofs, GW_TILE, &gsy.full[st]);
+          bulk_g2s(sX(st), a.xb + xofs, n16 * 128, &gsy.full[st]);
+          bulk_g2s(sX(st) + n16 * 128, a.xbl + xofs, n16 * 128, &gsy.full[st]);
+          continue;
+        }
         const __nv_bfloat16* wsrc = sub == 2 ? (MODE == 0 ? a.Wal : a.Wdl) : (MODE == 0 ? a.Wa : a.Wd);
         const __nv_bfloat16* xsrc = sub == 1 ? a.xbl : a.xb;
         if (i < npre) {
           tcg::mbar_expect_tx(&gsy.full[st], n16 * 128);
         } else {
           tcg::mbar_expect_tx(&gsy.full[st], GW_TILE + n16 * 128);
-          bulk_g2s(sW + st * GW_TILE, wsrc + ((int64_t)ug * NKC + kc) * 128 * 64, GW_TILE, &gsy.full[st]);
+          bulk_g2s(sW(st), wsrc + wofs, GW_TILE, &gsy.full[st]);
         }
         const int r0 = min(n16, 128);
-        bulk_g2s(sX + st * x_stage_bytes, xsrc + (int64_t)(col >> 6) * 128 * 64, r0 * 128, &gsy.full[st]);
+        bulk_g2s(sX(st), xsrc + xofs, r0 * 128, &gsy.full[st]);
         if (n16 > 128)  // items 128.. live in the next 128-row block of the mirror
-          bulk_g2s(sX + st * x_stage_bytes + 128 * 128, xsrc + (int64_t)(NCC + (col >> 6)) * 128 * 64,
-                   (n16 - 128) * 128, &gsy.full[st]);
+          bulk_g2s(sX(st) + 128 * 128, xsrc + (int64_t)(NCC + (col >> 6)) * 128 * 64, (n16 - 128) * 128,
+                   &gsy.full[st]);
       }
       if (pi == 0) mark(0);
     }
@@ -385,16 +401,24 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       uint32_t g = g_ring;
       tcg::mbar_wait(&gsy.acce, (lt_tile & 1) ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int nv = KCS * (a.split ? 3 : 1);
+      const int nv = KCS * ((a.split && !comb) ? 3 : 1);
       for (int i = 0; i < nv; ++i, ++g) {
         const uint32_t st = g % nst, ph = (g / nst) & 1;
         tcg::mbar_wait(&gsy.full[st], ph);
         if (i == 0) mark(1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t dw = tcg::make_desc<128>(tcg::smem_u32(sW + st * GW_TILE));
-        const uint64_t dx = tcg::make_desc<128>(tcg::smem_u32(sX + st * x_stage_bytes));
+        const uint64_t dw = tcg::make_desc<128>(tcg::smem_u32(sW(st)));
+        const uint64_t dx = tcg::make_desc<128>(tcg::smem_u32(sX(st)));
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, dw + 2 * kk, dx + 2 * kk, idesc, (i | kk) != 0);
+        if (comb) {   // + Wh.Xl + Wl.Xh from the same stage
+          const uint64_t dwl = tcg::make_desc<128>(tcg::smem_u32(sW(st) + GW_TILE));
+          const uint64_t dxl = tcg::make_desc<128>(tcg::smem_u32(sX(st) + n16 * 128));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, dw + 2 * kk, dxl + 2 * kk, idesc, 1);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, dwl + 2 * kk, dx + 2 * kk, idesc, 1);
+        }
         tcg::umma_commit(&gsy.empty[st]);
       }
       tcg::umma_commit(&gsy.accf);
@@ -508,7 +532,7 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
     __syncthreads();
     if (threadIdx.x == 0) mark(5);
   }
-  g_ring += KCS * (a.split ? 3 : 1);
+  g_ring += KCS * ((a.split && !comb) ? 3 : 1);
   lt_tile += 1;
 }
 
@@ -767,7 +791,10 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = tcg::align_smem_1024(smem_raw);
   AttSmem& sm = *reinterpret_cast<AttSmem*>(ring + RING_BYTES);  // ring = gate pipeline / attention staging
-  const int nst = min(MAXGS, (int)(RING_BYTES / (GW_TILE + a_box_bytes)));
+  // Split mode with <= 128 pooled rows: one ring stage holds [Wh | Wl | Xh | Xl] and feeds all three
+  // products (no tile loaded twice); larger batches use three (W, X) stages per K-chunk.
+  const bool comb = a.split && a_box_bytes <= 128u * 128u;
+  const int nst = min(MAXGS, (int)(RING_BYTES / (comb ? 2 * (GW_TILE + a_box_bytes) : GW_TILE + a_box_bytes)));
   float* scratch = reinterpret_cast<float*>(&sm.locf[0]);                       // gemv reductions
   __shared__ GateSync gsy;
   __shared__ PlanCache pc;

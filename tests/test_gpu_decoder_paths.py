@@ -71,7 +71,7 @@ def _ragged_pairs(engine, B, seed, lefts):
     return pairs
 
 
-@pytest.mark.parametrize("B", [3, 84, 120])
+@pytest.mark.parametrize("B", [3, 84, 120, 140])
 def test_scratch_is_written_before_read(engine, B):
     """NaN-filled decoder scratch (partials, attention numerators, operand mirror, outputs) must
     not change a single bit of the result: every scratch element the kernel reads was written
@@ -109,7 +109,7 @@ def test_graph_bucket_equals_eager(engine, B):
         assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("B", [24, 96, 97, 100])
+@pytest.mark.parametrize("B", [24, 96, 97, 100, 136])
 def test_pooled_decode_equals_solo_bitwise(engine, B):
     """Batch transparency (reference SPEC.md:232, acceptance 1): a request's mel and state are the
     same bits whether it decodes alone or inside a pooled ragged batch (merged-combine B <= 96 and

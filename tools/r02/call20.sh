@@ -1,0 +1,3 @@
+mkdir -p gpurun_out/c20
+timeout 900 python -m pytest tests/test_gpu_decoder_paths.py tests/test_gpu_parity_r.py -q -rf > gpurun_out/c20/pytest.txt 2>&1; echo "rc $?" >> gpurun_out/c20/pytest.txt
+timeout 300 python tools/dec_trace.py --batches 1,24,128,200 --precision parity > gpurun_out/c20/trace_parity.txt 2>&1
