@@ -275,7 +275,7 @@ def _flush_wrapped(mods, engine, device):
         return dec_fn(pairs)
 
     out = PipelineModules(mods.frontend_batch, mods.encoder_batch, decoder_with_flush, mods.vocoder_batch)
-    for k in ("engine", "frontend_prefetch"):
+    for k in ("engine", "frontend_prefetch", "decoder_steps", "concat_mels"):
         if hasattr(mods, k):
             object.__setattr__(out, k, getattr(mods, k))
     return out
@@ -355,9 +355,10 @@ def run_multi(args, world: int) -> dict:
 
     cfg, lex = PipelineConfig(), default_lexicon()
     log(f"starting router with {world} GPU workers")
-    router = gpu_router(world, cfg, tier="r", warmup="paper_2211_13939_b200.harness:warm_up")
+    devices = args.router_devices.split(",") if args.router_devices else [f"cuda:{i}" for i in range(world)]
+    router = gpu_router(world, cfg, tier="r", warmup="paper_2211_13939_b200.harness:warm_up", devices=devices)
     log("workers ready")
-    sampler = ClockSampler(",".join(str(i) for i in range(world)))
+    sampler = ClockSampler(",".join(sorted({d.split(":")[-1] for d in devices})))
     try:
         qps = args.qps * world
         sampler.start()
@@ -510,7 +511,7 @@ def side_configs(mods, cfg, lex, args) -> dict:
     log("C5 done")
     out["incr_vs_non_incr"] = incr_vs_non_incr(mods, cfg, lex, args)
     log("INCR vs Non-INCR done")
-    if hasattr(mods, "engine") and hasattr(mods.engine, "admission"):
+    if hasattr(mods, "decoder_steps"):
         out["step_admission"] = step_admission_compare(mods, cfg, lex, args)
         log("step-granular admission done")
     return out
@@ -521,14 +522,12 @@ def step_admission_compare(mods, cfg, lex, args) -> dict:
     same Poisson trace with per-iteration admission (the reference's parity mode) and with
     step-granular admission."""
     from paper_2211_13939_b200.harness import poisson_trace, serve
-    eng, out = mods.engine, {}
+    out = {"sub_steps": 8}
     for mode in ("iteration", "step"):
-        eng.admission = mode
         run = serve(mods, cfg, poisson_trace(args.qps, 3600.0, seed=args.seed + 55, lexicon=lex), warmup_iters=3,
-                    warmup_seconds=2.0, timed_iters=None, timed_seconds=10.0, drain_seconds=2.0)
+                    warmup_seconds=2.0, timed_iters=None, timed_seconds=10.0, drain_seconds=2.0, admission=mode)
         st = _window_stats(run)
-        out[mode] = {"p50_ms": st["p50"], "p99_ms": st["p99"], "requests": st["requests"]}
-    eng.admission = "iteration"
+        out[mode] = {"p50_ms": st["p50"], "p99_ms": st["p99"], "requests": st["requests"], "failed": st["failed"]}
     return out
 
 
@@ -616,6 +615,9 @@ def main() -> None:
     ap.add_argument("--side-configs", type=int, default=1, help="also run C1, C2, C5, INCR vs Non-INCR (1 = on)")
     ap.add_argument("--c5-qps", type=float, default=50.0)
     ap.add_argument("--twin-qps", type=float, default=30.0, help="QPS of the INCR vs Non-INCR comparison")
+    ap.add_argument("--router-devices", default="",
+                    help="N > 1: comma-separated worker devices (default cuda:0..N-1; e.g. cuda:0,cuda:0 to test "
+                         "the router path on one GPU)")
     ap.add_argument("--l2-flush", type=int, default=1,
                     help="1: write a 256 MB buffer on the engine stream before every decoder call, so each "
                          "serving iteration starts with a cold L2 (timing rule); 0: steady-state caches")

@@ -63,7 +63,19 @@ def cpu_modules(lexicon, cfg: PipelineConfig) -> PipelineModules:
             out.append((AudioChunk(samples, off), new))
         return out
 
-    return PipelineModules(frontend_module(lexicon), encoder, decoder, vocoder)
+    mods = PipelineModules(frontend_module(lexicon), encoder, decoder, vocoder)
+
+    def decoder_steps(triples):   # step-granular admission: <= limit steps of the current chunk
+        out = []
+        for state, enc, limit in triples:
+            mel, stop, new = tier_s.decode_chunk(state, enc.rows, min(int(limit), cfg.chunk_frames),
+                                                 cfg.attention_penalty, cfg.stop_threshold)
+            out.append(DecodeResult(MelChunk(mel), stop, new))
+        return out
+
+    object.__setattr__(mods, "decoder_steps", decoder_steps)
+    object.__setattr__(mods, "concat_mels", lambda parts: MelChunk(np.concatenate([p.frames for p in parts], 0)))
+    return mods
 
 
 def cpu_modules_r(lexicon, cfg: PipelineConfig, weights, deadline: float | None = None) -> PipelineModules:

@@ -111,7 +111,8 @@ def serve(modules: PipelineModules, cfg, trace: list[TimedRequest], *, warmup_it
           warmup_seconds: float = 0.0, timed_iters: int | None = None, drain_seconds: float = 30.0,
           on_window=None, max_clients: int = 4096, sample_rate: int = 22050,
           tail_seconds: float = 120.0, timed_seconds: float | None = None,
-          consumers: bool = True, client: str = "poller") -> ServeRun:
+          consumers: bool = True, client: str = "poller", admission: str = "iteration",
+          sub_steps: int = 8) -> ServeRun:
     """Plays ``trace`` against a fresh SchedulerLoop and records every request.
 
     The timed window is iterations ``[w, w + timed_iters)`` where ``w`` is the
@@ -152,7 +153,8 @@ def serve(modules: PipelineModules, cfg, trace: list[TimedRequest], *, warmup_it
         sink(rep)
         wake.set()
 
-    loop = SchedulerLoop(modules, CostModel.zero(), cfg, report_sink=sink_and_wake if client == "poller" else sink)
+    loop = SchedulerLoop(modules, CostModel.zero(), cfg, report_sink=sink_and_wake if client == "poller" else sink,
+                         admission=admission, sub_steps=sub_steps)
     stop_poll = threading.Event()
 
     def poller() -> None:

@@ -70,6 +70,9 @@ def modules_for(engine, lexicon: Lexicon) -> PipelineModules:
     fe = PrefetchingFrontend(lexicon) if hasattr(engine, "idle_hook") else frontend_module(lexicon)
     mods = PipelineModules(fe, engine.encoder_batch, engine.decoder_batch, engine.vocoder_batch)
     object.__setattr__(mods, "engine", engine)
+    for name in ("decoder_steps", "concat_mels"):   # step-granular admission (scheduler.run_iteration_steps)
+        if hasattr(engine, name):
+            object.__setattr__(mods, name, getattr(engine, name))
     if isinstance(fe, PrefetchingFrontend):
         object.__setattr__(mods, "frontend_prefetch", fe.prefetch)
     return mods

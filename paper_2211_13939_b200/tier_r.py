@@ -566,13 +566,13 @@ class TierREngine:
                 for req, buf in reqs]
 
     # ------------------------------------------------------------ decoder
-    def _dec_items(self, pairs, taken: set, cols=None) -> list:
+    def _dec_items(self, pairs, taken: set, cols=None, limits=None) -> list:
         """Per-item decoder plan fields (steps, L, dst buffer, mem / pm / src / dst offsets) --
         the host work between the previous vocoder wait and the decoder launch."""
         C = self.cfg.chunk_frames
         cols = cols if cols is not None else ([], [], [], [], [], [], [])
         steps, dsts, Ls, mem_off, pm_off, src_off, dst_off = cols
-        for state, enc in pairs:
+        for k, (state, enc) in enumerate(pairs):
             if type(state) is not DeviceDecoderState or type(enc) is not DeviceEncodedFeatures:
                 if not isinstance(state, DeviceDecoderState) or not isinstance(enc, DeviceEncodedFeatures):
                     raise TypeError("Tier-R GPU decoder needs handles produced by its own encoder")
@@ -582,7 +582,12 @@ class TierREngine:
             left = state.target_frames - state.frames_emitted
             if left <= 0:
                 raise ValueError("decode past stop")
-            steps.append(C if left > C else left)
+            n_steps = C if left > C else left
+            if limits is not None:
+                n_steps = min(n_steps, int(limits[k]))
+                if n_steps < 1:
+                    raise ValueError("step limit must be >= 1")
+            steps.append(n_steps)
             L = req.seq_len
             Ls.append(L)
             d = req.claim(req.state_bufs, ROW + 2 * L, taken)
@@ -612,14 +617,35 @@ class TierREngine:
         self._spec = (src, taken, cols)
 
     @_on_device
+    def decoder_steps(self, triples) -> list:
+        """Step-granular decoding (the opt-in admission mode, ``scheduler.run_iteration_steps``):
+        (state, features, limit) -> DecodeChunkResult of min(limit, frames left in the chunk) steps."""
+        return self._decode([(s, e) for s, e, _ in triples], [lim for _, _, lim in triples])
+
+    @_on_device
+    def concat_mels(self, parts: list) -> DeviceMelChunk:
+        """One mel chunk from consecutive partial decodes of the same request (engine stream)."""
+        if len(parts) == 1:
+            return parts[0]
+        with torch.cuda.stream(self.stream):
+            return DeviceMelChunk(torch.cat([m.data for m in parts], 0), parts[0].req)
+
+    @_on_device
     def decoder_batch(self, pairs) -> list:
+        return self._decode(pairs)
+
+    def _decode(self, pairs, limits=None) -> list:
         n = len(pairs)
         if n == 0:
             return []
         C = self.cfg.chunk_frames
         a = self.arena
         spec, self._spec = self._spec, None
-        if (spec is not None and len(spec[0]) <= n
+        if limits is not None:
+            spec = None
+            taken = set()
+            cols = self._dec_items(pairs, taken, limits=limits)
+        elif (spec is not None and len(spec[0]) <= n
                 and all(p[0] is q[0] and p[1] is q[1] for p, q in zip(pairs, spec[0]))):
             taken, cols = spec[1], tuple(list(c) for c in spec[2])
             self._dec_items(pairs[len(spec[0]):], taken, cols)   # the newly admitted items

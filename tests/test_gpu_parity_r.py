@@ -202,3 +202,34 @@ def test_bf16_mode_reported_separately(weights, lexicon):
     assert err <= MEL_TOL, err
     snr = orc.snr_db(np.concatenate([s for s, _ in want_chunks]), np.concatenate([c.samples for c in stream]))
     assert snr >= SNR_DB, snr
+
+
+def test_step_granular_admission_same_audio(mods, lexicon):
+    """The opt-in step-granular admission (run_iteration_steps: requests join the pooled decode at
+    the next 8-step boundary, the persistent decoder runs 8-step launches) produces every request's
+    audio bit for bit as the reference's per-iteration admission does: the decoder and vocoder
+    are batch-invariant and the chunk boundaries are unchanged."""
+    from paper_2211_13939_b200.scheduler import run_iteration_steps
+    cfg = PipelineConfig()
+    rng = random.Random(99)
+    texts = [random_text(rng, 20, 80, lexicon) for _ in range(6)]
+    admit_at = [0, 1, 3, 3, 9, 14]
+    audio = {}
+    for mode in ("iteration", "step"):
+        pool, streams, partial, it = RequestPool(), {}, {}, 0
+        while it <= max(admit_at) * (4 if mode == "step" else 1) or pool.pending():
+            for k, t in enumerate(texts):
+                if admit_at[k] * (4 if mode == "step" else 1) == it:
+                    streams[k] = pool.submit(t)[1]
+            if mode == "step":
+                rep = run_iteration_steps(pool, mods, CostModel.zero(), cfg, step_index=it, sub_steps=8,
+                                          partial=partial)
+            else:
+                rep = run_iteration(pool, mods, CostModel.zero(), cfg, step_index=it)
+            assert not rep.failed_ids
+            it += 1
+        audio[mode] = [[(c.sample_offset, c.samples.copy()) for c in streams[k]] for k in range(len(texts))]
+    for a, b in zip(audio["iteration"], audio["step"]):
+        assert [o for o, _ in a] == [o for o, _ in b]
+        for (_, x), (_, y) in zip(a, b):
+            assert np.array_equal(x, y)

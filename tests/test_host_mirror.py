@@ -211,3 +211,38 @@ def test_config_validation():
     assert config_from_mapping(parse_kv("overlap_frames = 8  # x\n\n")).overlap_frames == 8
     with pytest.raises(ConfigError):
         parse_kv("novalue\n")
+
+
+def test_step_granular_admission_preserves_chunks(lexicon, cfg):
+    """The opt-in step-granular mode (run_iteration_steps): requests join the decode at the next
+    8-step sub-iteration, yet every request's chunks (offsets, counts, samples) equal single-request
+    synthesis exactly -- only batch composition and timing change (Tier-S oracle modules)."""
+    import random
+
+    from oracle import tier_s as orc
+    from oracle.modules import cpu_modules
+    from paper_2211_13939_b200.frontend import run_frontend
+    from paper_2211_13939_b200.harness import random_text
+    from paper_2211_13939_b200.scheduler import CostModel, RequestPool, run_iteration_steps
+    rng = random.Random(12)
+    texts = [random_text(rng, 2, 30, lexicon) for _ in range(12)]
+    admit_at = sorted(rng.randrange(0, 40) for _ in texts)
+    mods = cpu_modules(lexicon, cfg)
+    pool, streams, partial, it = RequestPool(), {}, {}, 0
+    joined_mid_chunk = False
+    while it <= max(admit_at) or pool.pending():
+        for k, t in enumerate(texts):
+            if admit_at[k] == it:
+                streams[k] = pool.submit(t)[1]
+                joined_mid_chunk |= bool(partial)
+        rep = run_iteration_steps(pool, mods, CostModel.zero(), cfg, step_index=it, sub_steps=8, partial=partial)
+        assert not rep.failed_ids
+        it += 1
+    assert joined_mid_chunk   # some request was admitted while others were mid-chunk
+    for k, t in enumerate(texts):
+        fo = run_frontend(t, lexicon)
+        want, _ = orc.synthesize(fo.phonemes, fo.pw, fo.pph, fo.iph)
+        got = list(streams[k])
+        assert [c.sample_offset for c in got] == [o for _, o in want]
+        for c, (w, _) in zip(got, want):
+            np.testing.assert_allclose(c.samples, w, rtol=0, atol=1e-12)
