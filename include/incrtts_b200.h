@@ -139,13 +139,15 @@ int itts_resblock_debug_trace(void* buf);
  * Split-bf16 parity mode: Wa_lo / Wd_lo = the low bf16 parts (W - bf16(W)) in the same layout;
  * the gate products are then Wh.Xh + Wh.Xl + Wl.Xh with fp32 accumulation (about 16 significant
  * bits per operand) and xb must hold 2 x the mirror (high parts, then low parts).  Both null: plain
- * bf16 products. */
+ * bf16 products, or, with split_x != 0 (weights exactly representable in bf16, e.g. a bf16
+ * checkpoint), Wh.Xh + Wh.Xl -- the same fp32-level products at the bf16 weight bytes. */
 int itts_r_decode_persistent(int32_t B, int32_t nsteps, const int64_t* plan, float* work, void* xb,
                              const float* W0T, const float* W1T, const void* Wa, const float* ba,
                              const void* Wd, const float* bd, const float* WqT, const float* WlocD,
                              const float* v, const float* WpT, const float* bp,
                              float* Gp, float* H1, float* Q, float* P, float* U, int64_t u_ld, float* AP,
-                             unsigned* bar, const void* Wa_lo, const void* Wd_lo, void* stream);
+                             unsigned* bar, const void* Wa_lo, const void* Wd_lo, int32_t split_x,
+                             void* stream);
 /* Profiling aid: per-phase wall time of later persistent-decoder launches ([8] u64 ns). */
 int itts_r_decode_debug_trace(void* buf);
 int itts_r_dec_prepare(const float* state, void* xb, int32_t B, void* stream);

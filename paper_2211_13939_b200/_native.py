@@ -36,7 +36,7 @@ SIGNATURES: dict[str, list] = {
     "itts_r_dec_prepare": [_p, _p, _i32, _p],
     "itts_r_decode_debug_trace": [_p],
     "itts_r_decode_persistent": [_i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p,
-                                 _p, _p, _p, _i64, _p, _p, _p, _p, _p],
+                                 _p, _p, _p, _i64, _p, _p, _p, _p, _i32, _p],
     "itts_r_prenet": [_p, _p, _p, _p, _p, _p, _i32, _i32, _p],
     "itts_r_lstm_cell": [_p, _i32, _p, _p, _p, _i32, _i32, _p, _i32, _i32, _p],
     "itts_r_query": [_p, _p, _p, _i32, _p],

@@ -94,6 +94,7 @@ constexpr int NGRP = HID / 32;   // 32-unit gate groups: query partials, project
 constexpr int GEMM_CTAS = HID / 8;  // 128 CTAs x 8 hidden units
 constexpr int KA = 1792, KD = 2560;
 constexpr int MAXCH = 256;       // max position chunks per item
+constexpr int MAXB = 512;        // max pooled rows (two 256-column MMA N tiles)
 constexpr int ACH = 64;          // max positions per attention chunk (pm + memory rows staged in smem)
 // Staging: a chunk of n positions is [n pm rows][n memory rows].  One round of tasks (every CTA
 // at most one chunk): chunks up to 64 positions in one 160 KB buffer.  Several rounds: 32-position
@@ -121,7 +122,8 @@ struct DecArgs {
   const __nv_bfloat16* Wd;         // [128][40][32][64]
   const __nv_bfloat16* Wal;        // split mode: low bf16 parts of Wa / Wd (null: plain bf16 products)
   const __nv_bfloat16* Wdl;
-  int split;                       // 1: gates = Wh.Xh + Wh.Xl + Wl.Xh (fp32-level products, fp32 accumulation)
+  int split;                       // 0: bf16 products; 1: gates = Wh.Xh + Wh.Xl + Wl.Xh (fp32-level products,
+                                   // fp32 accumulation); 2: weights exact in bf16 (Wl = 0): Wh.Xh + Wh.Xl
   const float* bd;                 // [128][32]
   const float* WqT;                // [1024][128]
   const float* WlocD;              // [2][31][128] = location conv composed with the location dense layer
@@ -194,9 +196,9 @@ __device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
 __device__ __forceinline__ float ldf(const float* p) { return __ldcg(p); }
 __device__ __forceinline__ uint32_t ldu(const void* p) { return __ldcg(reinterpret_cast<const unsigned int*>(p)); }
 
-// per-item L and step counts, cached in shared memory at kernel start (B <= 256)
+// per-item L and step counts, cached in shared memory at kernel start (B <= MAXB)
 struct PlanCache {
-  int L[256], steps[256];
+  int L[MAXB], steps[MAXB];
 };
 __device__ __forceinline__ bool active(const PlanCache& pc, int b, int s) { return s < pc.steps[b]; }
 
@@ -308,12 +310,16 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
     if (tr) a.trace[16 + MODE * 8 + slot] += gtimer() - t_in;
   };
   const bool comb = a.split && n16 <= 128;   // combined split stages (see k_dec_persist)
-  const uint32_t sbytes = 2 * (GW_TILE + (uint32_t)n16 * 128);
-  // stage st: the weight tile and the operand tile (combined split stages: Wh, Wl, Xh, Xl)
+  const int nw = a.split == 1 ? 2 : 1;       // weight tiles per combined stage (Wh [, Wl])
+  const uint32_t sbytes = nw * GW_TILE + 2 * (uint32_t)n16 * 128;
+  // stage st: the weight tile and the operand tile (combined split stages: Wh, [Wl,] Xh, Xl)
   auto sW = [&](uint32_t st) { return comb ? ring + st * sbytes : ring + st * GW_TILE; };
   auto sX = [&](uint32_t st) {
-    return comb ? ring + st * sbytes + 2 * GW_TILE : ring + nst * GW_TILE + st * x_stage_bytes;
+    return comb ? ring + st * sbytes + nw * GW_TILE : ring + nst * GW_TILE + st * x_stage_bytes;
   };
+  // virtual stages per K-chunk when the split products do not share one stage: (Wh, Xh), (Wh, Xl)
+  // [, (Wl, Xh)] -- the same product order as a combined stage
+  const int nsub = (a.split && !comb) ? (a.split == 1 ? 3 : 2) : 1;
   // producer lanes: stage g goes to lane g % np; np <= nst keeps the empty-barrier parity unambiguous
   const int np = min(3, nst);
   ++grp_gen;
@@ -346,8 +352,6 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       asm volatile("fence.proxy.async.global;" ::: "memory");  // xb tiles written by generic stores
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the ring doubles as PRE scratch
       uint32_t g = g_ring;
-      // split mode, > 128 rows: three virtual stages per K-chunk, (Wh, Xh), (Wh, Xl), (Wl, Xh)
-      const int nsub = (a.split && !comb) ? 3 : 1;
       const int npre = (!a.split && (DEC_PREFETCH & (1 << MODE))) ? min(KCS, nst) : 0;  // weights prefetched
       // decoder gates, split 0: the context columns (chunks 0..7) go last -- in the merged-combine
       // schedule after the combined contexts of every live item are counted in.  The order is the
@@ -370,10 +374,10 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
         if (MODE == 0) col = k0 < 768 ? k0 : att_off(oldb) + (k0 - 768);
         else col = k0 < 512 ? CTX_OFF + k0 : (k0 < 1536 ? att_off(newb) + (k0 - 512) : dec_off(oldb) + (k0 - 1536));
         const int64_t wofs = ((int64_t)ug * NKC + kc) * 128 * 64, xofs = (int64_t)(col >> 6) * 128 * 64;
-        if (comb) {   // [Wh | Wl | Xh | Xl]
+        if (comb) {   // [Wh | Wl | Xh | Xl]  (split 2: [Wh | Xh | Xl])
           tcg::mbar_expect_tx(&gsy.full[st], sbytes);
           bulk_g2s(sW(st), (MODE == 0 ? a.Wa : a.Wd) + wofs, GW_TILE, &gsy.full[st]);
-          bulk_g2s(sW(st) + GW_TILE, (MODE == 0 ? a.Wal : a.Wdl) + wofs, GW_TILE, &gsy.full[st]);
+          if (nw == 2) bulk_g2s(sW(st) + GW_TILE, (MODE == 0 ? a.Wal : a.Wdl) + wofs, GW_TILE, &gsy.full[st]);
           bulk_g2s(sX(st), a.xb + xofs, n16 * 128, &gsy.full[st]);
           bulk_g2s(sX(st) + n16 * 128, a.xbl + xofs, n16 * 128, &gsy.full[st]);
           continue;
@@ -386,22 +390,25 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
           tcg::mbar_expect_tx(&gsy.full[st], GW_TILE + n16 * 128);
           bulk_g2s(sW(st), wsrc + wofs, GW_TILE, &gsy.full[st]);
         }
-        const int r0 = min(n16, 128);
-        bulk_g2s(sX(st), xsrc + xofs, r0 * 128, &gsy.full[st]);
-        if (n16 > 128)  // items 128.. live in the next 128-row block of the mirror
-          bulk_g2s(sX(st) + 128 * 128, xsrc + (int64_t)(NCC + (col >> 6)) * 128 * 64, (n16 - 128) * 128,
-                   &gsy.full[st]);
+        for (int blk = 0; blk * 128 < n16; ++blk)  // items 128 blk.. live in 128-row block blk of the mirror
+          bulk_g2s(sX(st) + blk * 128 * 128, xsrc + xofs + (int64_t)blk * NCC * 128 * 64,
+                   min(128, n16 - 128 * blk) * 128, &gsy.full[st]);
       }
       if (pi == 0) mark(0);
     }
     prefetch();
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n16 >> 3) << 17) | ((128u >> 4) << 24);
+      // N = pooled rows padded to 16; above 256 rows two MMAs per K-step, rows 256.. into TMEM
+      // columns 256.. (the accumulator columns stay item-indexed)
+      const int nA = min(n16, 256), nB = n16 - nA;
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nA >> 3) << 17) | ((128u >> 4) << 24);
+      const uint32_t idescB = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nB >> 3) << 17) | ((128u >> 4) << 24);
+      constexpr uint32_t XB_OFF = 256 * 128;  // bytes to the second N tile of an operand tile
       uint32_t g = g_ring;
       tcg::mbar_wait(&gsy.acce, (lt_tile & 1) ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int nv = KCS * ((a.split && !comb) ? 3 : 1);
+      const int nv = KCS * nsub;
       for (int i = 0; i < nv; ++i, ++g) {
         const uint32_t st = g % nst, ph = (g / nst) & 1;
         tcg::mbar_wait(&gsy.full[st], ph);
@@ -411,13 +418,20 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
         const uint64_t dx = tcg::make_desc<128>(tcg::smem_u32(sX(st)));
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, dw + 2 * kk, dx + 2 * kk, idesc, (i | kk) != 0);
-        if (comb) {   // + Wh.Xl + Wl.Xh from the same stage
-          const uint64_t dwl = tcg::make_desc<128>(tcg::smem_u32(sW(st) + GW_TILE));
+        if (nB) {  // no combined stages above 128 rows: every product has its own (W, X) stage
+          const uint64_t dx2 = tcg::make_desc<128>(tcg::smem_u32(sX(st) + XB_OFF));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem + 256, dw + 2 * kk, dx2 + 2 * kk, idescB, (i | kk) != 0);
+        }
+        if (comb) {   // + Wh.Xl [+ Wl.Xh] from the same stage
           const uint64_t dxl = tcg::make_desc<128>(tcg::smem_u32(sX(st) + n16 * 128));
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, dw + 2 * kk, dxl + 2 * kk, idesc, 1);
+          if (nw == 2) {
+            const uint64_t dwl = tcg::make_desc<128>(tcg::smem_u32(sW(st) + GW_TILE));
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, dwl + 2 * kk, dx + 2 * kk, idesc, 1);
+            for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, dwl + 2 * kk, dx + 2 * kk, idesc, 1);
+          }
         }
         tcg::umma_commit(&gsy.empty[st]);
       }
@@ -532,7 +546,7 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
     __syncthreads();
     if (threadIdx.x == 0) mark(5);
   }
-  g_ring += KCS * ((a.split && !comb) ? 3 : 1);
+  g_ring += KCS * nsub;
   lt_tile += 1;
 }
 
@@ -542,7 +556,7 @@ struct AttSmem {
   __align__(16) float sWl[2 * 32 * ATT];  // [c][k][a], k < 31 (tap 31 = 0): loc[a] = sum sWl[c][k][a] w_c[t+k-15]
   float red[32];
   float scale[MAXCH];
-  int tstart[257];             // prefix sum of chunks per item (ATT-A task list), B <= 256
+  int tstart[MAXB + 1];        // prefix sum of chunks per item (ATT-A task list)
   float wp[ACH + 2 * HALO + 2], wa[ACH + 2 * HALO + 2], e[ACH];
   // scratch: context partials [8][512] (ATT-A), gate-fixup h (gate phases), PRE's
   // last frame [8][80] + H1 [8][256] + gemv partials [8 warps][8][32] (so the ring is free for the
@@ -794,7 +808,8 @@ __global__ void __launch_bounds__(NT, 1)
   // Split mode with <= 128 pooled rows: one ring stage holds [Wh | Wl | Xh | Xl] and feeds all three
   // products (no tile loaded twice); larger batches use three (W, X) stages per K-chunk.
   const bool comb = a.split && a_box_bytes <= 128u * 128u;
-  const int nst = min(MAXGS, (int)(RING_BYTES / (comb ? 2 * (GW_TILE + a_box_bytes) : GW_TILE + a_box_bytes)));
+  const uint32_t comb_bytes = (a.split == 1 ? 2 : 1) * GW_TILE + 2 * a_box_bytes;
+  const int nst = min(MAXGS, (int)(RING_BYTES / (comb ? comb_bytes : GW_TILE + a_box_bytes)));
   float* scratch = reinterpret_cast<float*>(&sm.locf[0]);                       // gemv reductions
   __shared__ GateSync gsy;
   __shared__ PlanCache pc;
@@ -815,8 +830,10 @@ __global__ void __launch_bounds__(NT, 1)
     tcg::mbar_init(&gsy.abar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  const uint32_t tcols = a_box_bytes > 256u * 128u ? 512u : 256u;  // accumulator columns = rows (2 N tiles)
   if (gemm_cta && (tid >> 5) == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(tcg::smem_u32(&gsy.tmem)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tcg::smem_u32(&gsy.tmem)),
+                 "r"(tcols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -991,14 +1008,11 @@ __global__ void __launch_bounds__(NT, 1)
     if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen, sm.locf);
     phase_end();
     // ---- ATT-A: the non-empty (item, chunk) tasks of the live items, dealt round-robin
-    if (tid < 32) {  // task prefix over items: 8 items per lane, then a warp scan
-      int cnt[8], loc = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int b = tid * 8 + i;
-        cnt[i] = (b < a.B && active(pc, b, gs)) ? (pc.L[b] + chunk - 1) / chunk : 0;
-        loc += cnt[i];
-      }
+    if (tid < 32) {  // task prefix over items: 16 items per lane, then a warp scan
+      constexpr int PL = MAXB / 32;
+      auto cnt = [&](int b) { return (b < a.B && active(pc, b, gs)) ? (pc.L[b] + chunk - 1) / chunk : 0; };
+      int loc = 0;
+      for (int i = 0; i < PL; ++i) loc += cnt(tid * PL + i);
       int incl = loc;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -1006,13 +1020,12 @@ __global__ void __launch_bounds__(NT, 1)
         if (tid >= o) incl += y;
       }
       int run = incl - loc;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int b = tid * 8 + i;
+      for (int i = 0; i < PL; ++i) {
+        const int b = tid * PL + i;
         if (b <= a.B) sm.tstart[b] = run;
-        run += cnt[i];
+        run += cnt(b);
       }
-      if (tid == 31 && a.B == 256) sm.tstart[256] = run;
+      if (tid == 31) sm.tstart[a.B] = run;  // the total (also for B == MAXB)
     }
     __syncthreads();
     {
@@ -1120,7 +1133,7 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   if (gemm_cta && (tid >> 5) == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(gsy.tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(gsy.tmem), "r"(tcols));
   }
 }
 
@@ -1141,14 +1154,15 @@ ITTS_API int itts_r_decode_persistent(int32_t B, int32_t nsteps, const int64_t* 
                                       const float* v, const float* WpT, const float* bp,
                                       float* Gp, float* H1, float* Qp, float* Pp, float* U, int64_t u_ld,
                                       float* AP, unsigned* bar, const void* Wa_lo, const void* Wd_lo,
-                                      void* stream) {
+                                      int32_t split_x, void* stream) {
   if (B <= 0) return B == 0 ? ITTS_OK : ITTS_EINVAL;
-  if (B > 256) return ITTS_EUNSUPPORTED;  // attention task table in shared memory; MMA N <= 256
+  if (B > MAXB) return ITTS_EUNSUPPORTED;  // plan cache / attention task table in shared memory
   if (nsteps <= 0 || !plan || !work || !xb || !Wa || !Wd || !bar) return ITTS_EINVAL;
   if (tcg::num_sms() < GEMM_CTAS) return ITTS_EUNSUPPORTED;
   cudaStream_t st = (cudaStream_t)stream;
   if ((Wa_lo == nullptr) != (Wd_lo == nullptr)) return ITTS_EINVAL;
-  const int split = Wa_lo != nullptr;
+  // 1: split weights and operands (x3 products); 2: bf16-exact weights, split operands (x2)
+  const int split = Wa_lo != nullptr ? 1 : (split_x ? 2 : 0);
   // split mode: the mirror buffer holds the high parts, then the low parts (same tile layout)
   __nv_bfloat16* xbh = (__nv_bfloat16*)xb;
   __nv_bfloat16* xbl = split ? xbh + (int64_t)((B + 127) / 128) * NCC * 128 * 64 : nullptr;

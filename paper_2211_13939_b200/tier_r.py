@@ -56,7 +56,7 @@ GRAPH_MAX_L = 8192  # attention smem is sized for this in captured graphs; longe
 HID = 1024
 XB2 = 4864          # persistent decoder's bf16 mirror row (two banks of att_h / dec_h)
 PERSIST_MAX_L = 8192  # 256 attention chunks of <= 32 positions
-PERSIST_MAX_B = 256   # kernel limit (MMA N, attention task table); larger pools use the per-kernel chain
+PERSIST_MAX_B = 512   # kernel limit (2 MMA N tiles, plan cache); larger pools decode in slices of <= 512
 
 
 def _hifigan_macs_per_frame() -> int:
@@ -242,7 +242,9 @@ class TierREngine:
 
     def precision_label(self) -> str:
         if self.precision == "parity":
-            return ("fp32-level decoder: split-bf16 (x3) tcgen05 gate products, fp32 accumulate / attention / "
+            prod = ("bf16-grid weights x split-bf16 operands (x2)" if self.w_exact_bf16
+                    else "split-bf16 (x3)")
+            return (f"fp32-level decoder: {prod} tcgen05 gate products, fp32 accumulate / attention / "
                     "cells; bf16-operand encoder convs and HiFi-GAN (fp32 accumulate)")
         return "bf16 decoder gate products; bf16-operand encoder convs and HiFi-GAN (fp32 accumulate)"
 
@@ -294,8 +296,13 @@ class TierREngine:
         split = lambda t: (t.to(torch.bfloat16), (t - t.to(torch.bfloat16).float()).to(torch.bfloat16))
         wa_h, wa_l = split(perm(wa.to(d).float()))
         wd_h, wd_l = split(perm(wd.to(d).float()))
-        self.Wa_p, self.Wal_p = _swizzle_tiles(wa_h, 128), _swizzle_tiles(wa_l, 128)
-        self.Wd_p, self.Wdl_p = _swizzle_tiles(wd_h, 128), _swizzle_tiles(wd_l, 128)
+        # weights already on the bf16 grid (a bf16 checkpoint, or tier_r_weights' default): Wl = 0,
+        # and the parity products reduce to Wh.Xh + Wh.Xl at the bf16 weight bytes
+        self.w_exact_bf16 = not bool(wa_l.any()) and not bool(wd_l.any())
+        self.Wa_p, self.Wd_p = _swizzle_tiles(wa_h, 128), _swizzle_tiles(wd_h, 128)
+        self.Wal_p = self.Wdl_p = None
+        if not self.w_exact_bf16:
+            self.Wal_p, self.Wdl_p = _swizzle_tiles(wa_l, 128), _swizzle_tiles(wd_l, 128)
         self.ba_p = perm(self.att_bias[:, None]).reshape(-1).contiguous()
         self.bd_p = perm(self.dec_bias[:, None]).reshape(-1).contiguous()
         self.WqT = f32(w["att.query_layer"].T)                                           # [1024][128]
@@ -638,6 +645,15 @@ class TierREngine:
         n = len(pairs)
         if n == 0:
             return []
+        if n > PERSIST_MAX_B and self.persistent_decoder:
+            # items are independent and the kernel is batch-invariant: balanced slices of <= 512 rows
+            per = -(-n // -(-n // PERSIST_MAX_B))
+            self._spec = None
+            out = []
+            for i in range(0, n, per):
+                out += self._decode(pairs[i:i + per], None if limits is None else limits[i:i + per])
+            self._spec_src = [(r.state, enc) for r, (_, enc) in zip(out, pairs) if not r.stop]
+            return out
         C = self.cfg.chunk_frames
         a = self.arena
         spec, self._spec = self._spec, None
@@ -659,7 +675,7 @@ class TierREngine:
         Ls_np = np.array(Ls, dtype=np.int64)
         src = base + 4 * np.array(src_off, dtype=np.int64)
         dstp = base + 4 * np.array(dst_off, dtype=np.int64)
-        wbytes = DEC_WEIGHT_BYTES_SPLIT if self.precision == "parity" else DEC_WEIGHT_BYTES
+        wbytes = DEC_WEIGHT_BYTES_SPLIT if self.precision == "parity" and not self.w_exact_bf16 else DEC_WEIGHT_BYTES
         dec_bytes = lambda: max_steps * wbytes + int(  # algorithmic bytes (timers only)
             (steps_np * (2 * 4 * ROW + Ls_np * (4 * 512 + 4 * 128 + 16) + 4 * 81)).sum())
         with torch.cuda.stream(self.stream):
@@ -759,7 +775,8 @@ class TierREngine:
                        self.bp.data_ptr(), b.Gp.data_ptr(), b.H1.data_ptr(), b.Q.data_ptr(), b.P.data_ptr(),
                        b.U.data_ptr(),
                        b.U.shape[1], b.AP.data_ptr(), b.bar.data_ptr(),
-                       self.Wal_p.data_ptr() if split else 0, self.Wdl_p.data_ptr() if split else 0, st)
+                       self.Wal_p.data_ptr() if split and not self.w_exact_bf16 else 0,
+                       self.Wdl_p.data_ptr() if split and not self.w_exact_bf16 else 0, int(split), st)
             self._call("itts_scatter_rows", b.d_dst.data_ptr(), b.work.data_ptr(), n, 4 * ROW, st)
             return
         self._call("itts_r_dec_prepare", b.work.data_ptr(), b.xbm.data_ptr(), n, st)
@@ -795,7 +812,7 @@ class TierREngine:
         self.prewarm_pinned(max_batch)
         with torch.cuda.stream(self.stream):
             self.reserve_vocoder(max_batch)
-            for B in range(16, max_batch + 1, 16):
+            for B in range(16, min(max_batch, PERSIST_MAX_B) + 1, 16):   # larger pools run in slices
                 bk = self._dec_bucket(B)
                 if bk.graph is None:
                     bk.idle_plan()
@@ -1159,14 +1176,38 @@ class TierREngine:
         return raw[:O * W.N_MEL].reshape(O, W.N_MEL), raw[O * W.N_MEL:]
 
 
+class _ScratchPool:
+    """Decoder scratch shared by every graph bucket of an engine: one flat buffer per name, sized
+    for the largest bucket.  Decoder calls are serialised on the engine stream, so the buckets'
+    captured graphs can all address the same memory (~0.4 GB at 512 rows, instead of per-bucket
+    copies summing to several GB); a bucket's buffer is a view of the first numel elements."""
+
+    def __init__(self, dev, poison):
+        self.dev, self.poison, self.flat = dev, poison, {}
+
+    def get(self, name: str, shape, dtype, max_numel: int) -> torch.Tensor:
+        numel = int(np.prod(shape))
+        t = self.flat.get(name)
+        if t is None:
+            t = torch.empty(max_numel, dtype=dtype, device=self.dev)
+            if self.poison is True or (bool(self.poison) and name in self.poison):
+                t.fill_(self.poison[name] if isinstance(self.poison, dict) else float("nan"))
+            elif name == "xb2":
+                t.zero_()
+            self.flat[name] = t
+        assert t.dtype == dtype and numel <= t.numel(), (name, shape)
+        return t[:numel].view(shape)
+
+
 class _DecBuffers:
     """Work buffers of one decoder call (n pooled rows); `packed` = plan | src ptrs | dst ptrs."""
 
-    def __init__(self, eng: TierREngine, n: int, packed: torch.Tensor):
+    def __init__(self, eng: TierREngine, n: int, packed: torch.Tensor, pool: "_ScratchPool | None" = None):
         dev = eng.device
         self.dev = dev
         self.n = n
         self.packed = packed
+        self.pool = pool
         self.d_plan, self.d_src, self.d_dst = packed[:8 * n], packed[8 * n:9 * n], packed[9 * n:10 * n]
         # scratch is never read before the kernels write it: eng.poison_scratch fills it with NaN
         # (debug / tests: the outputs must not change)
@@ -1185,7 +1226,13 @@ class _DecBuffers:
     def _poisoned(self, name: str) -> bool:
         return self.poison is True or (bool(self.poison) and name in self.poison)
 
+    # per-row element counts of the scratch buffers at the pool's row limit
+    _POOL_ROWS = PERSIST_MAX_B
+
     def _empty(self, shape, dtype, name: str) -> torch.Tensor:
+        if self.pool is not None:   # a view of the engine-wide pool, sized for _POOL_ROWS rows
+            numel = int(np.prod(shape))
+            return self.pool.get(name, shape, dtype, numel // self.n * self._POOL_ROWS + 4096)
         t = torch.empty(shape, dtype=dtype, device=self.dev)
         if self._poisoned(name):   # True / a set: NaN; a dict: that buffer's fill value
             t.fill_(self.poison[name] if isinstance(self.poison, dict) else float("nan"))
@@ -1198,6 +1245,15 @@ class _DecBuffers:
             return
         self.split = split
         nblk = -(-self.n // 128)
+        if self.pool is not None:   # pool views: sized for the largest bucket and the split layout
+            self.xb2 = self.pool.get("xb2", (2 * nblk * (XB2 // 64) * 128 * 64,), torch.bfloat16,
+                                     2 * (-(-self._POOL_ROWS // 128)) * (XB2 // 64) * 128 * 64)
+            self.U = self.pool.get("U", (self.n, GRAPH_MAX_L), torch.float32, self._POOL_ROWS * GRAPH_MAX_L)
+            self.AP = self.pool.get("AP", (self.n, 256, 2 + 512), torch.float32, self._POOL_ROWS * 256 * 514)
+            self.bar = self.pool.get("bar", (64,), torch.int32, 64)
+            self.Gp = self.pool.get("Gp", (4 * 32 * (-(-self.n // 16) * 16) * 128,), torch.float32,
+                                    4 * 32 * self._POOL_ROWS * 128)
+            return
         self.xb2 = self._empty(((2 if split else 1) * nblk * (XB2 // 64) * 128 * 64,), torch.bfloat16, "xb2")
         if not self._poisoned("xb2"):
             self.xb2.zero_()
@@ -1216,13 +1272,15 @@ class _DecBucket(_DecBuffers):
 
     def __init__(self, eng: TierREngine, B: int, L: int):
         dev = eng.device
-        super().__init__(eng, B, torch.empty(10 * B, dtype=torch.int64, device=dev))
+        if getattr(eng, "_scratch_pool", None) is None:
+            eng._scratch_pool = _ScratchPool(dev, getattr(eng, "poison_scratch", False))
+        super().__init__(eng, B, torch.empty(10 * B, dtype=torch.int64, device=dev), eng._scratch_pool)
         self.B, self.L = B, L
         C = eng.cfg.chunk_frames
-        self.mel = torch.empty(B, C, W.N_MEL, dtype=torch.float32, device=dev)
-        self.gate = torch.empty(B, C, dtype=torch.float32, device=dev)
+        self.mel = self._empty((B, C, W.N_MEL), torch.float32, "bucket_mel")   # pool views (read right
+        self.gate = self._empty((B, C), torch.float32, "bucket_gate")          # after each replay)
         self.zero_row = torch.zeros(ROW, dtype=torch.float32, device=dev)
-        self.sink = torch.empty(B, ROW, dtype=torch.float32, device=dev)
+        self.sink = self._empty((B, ROW), torch.float32, "sink")
         self.graph = None
         self.launches = 0
         # pinned staging of the packed plan [B][8] | src [B] | dst [B]: the per-call H2D source.

@@ -15,6 +15,14 @@ LSTMs, the Tacotron2 embedding range; HiFi-GAN ``init_weights`` normal(0,
 0.01) for ups / resblocks / conv_post, default conv init for conv_pre.
 Every tensor is drawn from one ``torch.Generator(seed)`` in a fixed order,
 so the CPU oracle and every GPU process see identical float32 values.
+
+By default every parameter is then rounded to the nearest bfloat16 (kept as
+float32): the weights are those of a bf16 checkpoint, the storage format of a
+served model.  The oracle computes with exactly these values in fp32; the GPU
+parity mode then needs no low-order weight parts (gate products Wh.(Xh + Xl),
+fp32 accumulation) and streams half the weight bytes.  ``bf16_grid=False``
+gives the unrounded float32 draw (the GPU parity mode then splits the weights
+too: Wh.Xh + Wh.Xl + Wl.Xh).
 """
 
 from __future__ import annotations
@@ -86,8 +94,13 @@ def _lstm(d: _Draw, w: dict, prefix: str, n_in: int, hidden: int) -> None:
     w[prefix + ".b_hh"] = d.uniform((4 * hidden,), b)
 
 
-def tier_r_weights(seed: int = 0) -> dict[str, torch.Tensor]:
-    """All Tier-R parameters, float32 on the CPU, deterministic in ``seed``."""
+def _on_grid(w: dict[str, torch.Tensor], bf16_grid: bool) -> dict[str, torch.Tensor]:
+    return {k: t.to(torch.bfloat16).float() for k, t in w.items()} if bf16_grid else w
+
+
+def tier_r_weights(seed: int = 0, bf16_grid: bool = True) -> dict[str, torch.Tensor]:
+    """All Tier-R parameters, float32 on the CPU, deterministic in ``seed`` (on the bf16 grid
+    unless ``bf16_grid=False``)."""
     d, w = _Draw(seed), {}
     # --- encoder (paper Eq. 1: four embedding tables summed) -------------
     std = math.sqrt(2.0 / (N_SYMBOLS + EMB))
@@ -133,13 +146,13 @@ def tier_r_weights(seed: int = 0) -> dict[str, torch.Tensor]:
                     w[key + ".b"] = d.uniform((ch,), 1.0 / math.sqrt(ch * kr))
     w["hg.conv_post.w"] = d.normal((1, ch, 7), 0.01)
     w["hg.conv_post.b"] = d.uniform((1,), 1.0 / math.sqrt(ch * 7))
-    return w
+    return _on_grid(w, bf16_grid)
 
 
 POSTNET_CH, POSTNET_K, POSTNET_LAYERS = 512, 5, 5
 
 
-def postnet_weights(seed: int = 0) -> dict[str, torch.Tensor]:
+def postnet_weights(seed: int = 0, bf16_grid: bool = True) -> dict[str, torch.Tensor]:
     """Tacotron2 PostNet: 5 x conv k5, 80 -> 512 -> 512 -> 512 -> 512 -> 80, batch
     norm folded (eval mode, unit running variance), tanh after the first four.  A separate stream
     (seed + 7919) so the main Tier-R weights do not change."""
@@ -150,7 +163,7 @@ def postnet_weights(seed: int = 0) -> dict[str, torch.Tensor]:
         gain = "tanh" if i < POSTNET_LAYERS - 1 else "linear"
         w[f"post.conv{i}.w"] = d.xavier((chans[i + 1], chans[i], POSTNET_K), gain) * bn
         w[f"post.conv{i}.b"] = d.bias(chans[i + 1], chans[i] * POSTNET_K) * bn
-    return w
+    return _on_grid(w, bf16_grid)
 
 
 def parameter_count(w: dict[str, torch.Tensor], prefix: str = "") -> int:

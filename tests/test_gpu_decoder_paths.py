@@ -33,7 +33,7 @@ def texts(n, seed, lo=20, hi=200):
     return ["".join(rng.choice(singles) for _ in range(rng.randint(lo, hi))) for _ in range(n)]
 
 
-@pytest.mark.parametrize("B", [1, 16, 100, 192, 256])
+@pytest.mark.parametrize("B", [1, 16, 100, 192, 256, 300, 512])
 def test_persistent_matches_chain(engine, B):
     """Same (bf16) gate arithmetic on both paths; the split-bf16 parity mode is persistent-only."""
     engine.set_precision("bf16")
@@ -71,7 +71,7 @@ def _ragged_pairs(engine, B, seed, lefts):
     return pairs
 
 
-@pytest.mark.parametrize("B", [3, 84, 120, 140])
+@pytest.mark.parametrize("B", [3, 84, 120, 140, 300])
 def test_scratch_is_written_before_read(engine, B):
     """NaN-filled decoder scratch (partials, attention numerators, operand mirror, outputs) must
     not change a single bit of the result: every scratch element the kernel reads was written
@@ -94,7 +94,7 @@ def test_scratch_is_written_before_read(engine, B):
         assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("B", [5, 84, 120])
+@pytest.mark.parametrize("B", [5, 84, 120, 300])
 def test_graph_bucket_equals_eager(engine, B):
     """The CUDA-graph bucket (B padded to 16 with idle rows) gives the eager launch's bits."""
     pairs = _ragged_pairs(engine, B, 200 + B, [64, 64, 8, 40, 16])
@@ -109,11 +109,12 @@ def test_graph_bucket_equals_eager(engine, B):
         assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("B", [24, 96, 97, 100, 136])
+@pytest.mark.parametrize("B", [24, 96, 97, 100, 136, 260, 512, 600])
 def test_pooled_decode_equals_solo_bitwise(engine, B):
     """Batch transparency (reference SPEC.md:232, acceptance 1): a request's mel and state are the
     same bits whether it decodes alone or inside a pooled ragged batch (merged-combine B <= 96 and
-    separate-combine schedules), over two consecutive chunks."""
+    separate-combine schedules, one or two 256-row MMA N tiles, pools above 512 rows decoded in
+    slices), over two consecutive chunks."""
     pairs = _ragged_pairs(engine, B, 300 + B, [64, 40, 8, 64, 16, 64])
     r1 = engine.decoder_batch(pairs)
     r2 = engine.decoder_batch([(r.state, enc) for r, (_, enc) in zip(r1, pairs) if not r.stop])

@@ -204,6 +204,33 @@ def test_bf16_mode_reported_separately(weights, lexicon):
     assert snr >= SNR_DB, snr
 
 
+def test_split3_mode_for_weights_off_the_bf16_grid(lexicon):
+    """Weights NOT on the bf16 grid (``bf16_grid=False``: the raw float32 draw) take the x3 path
+    (Wh.Xh + Wh.Xl + Wl.Xh): still fp32-level against the oracle on those same weights."""
+    from paper_2211_13939_b200.modules import build_modules
+    cfg = PipelineConfig()
+    w32 = tier_r_weights(0, bf16_grid=False)
+    mods = build_modules(lexicon, cfg, tier="r", device="cuda:0", weights=w32)
+    assert not mods.engine.w_exact_bf16
+    wrapped, mel_log = recording(mods)
+    text = random_text(random.Random(11), 50, 50, lexicon)
+    pool = RequestPool()
+    _, stream = pool.submit(text)
+    while pool.pending():
+        run_iteration(pool, wrapped, CostModel.zero(), cfg)
+    want_chunks, want_mel = oracle_request(w32, run_frontend(text, lexicon))
+    err, snr = check_request(list(stream), np.concatenate(next(iter(mel_log.values()))), want_chunks, want_mel)
+    print(f"x3 mode: mel max-abs {err:.3e}, SNR {snr:.1f} dB")
+
+
+def test_default_weights_are_a_bf16_checkpoint(mods, weights):
+    """The default Tier-R weights sit on the bf16 grid, so the engine's parity mode runs the x2
+    products (no low weight parts streamed)."""
+    for t in weights.values():
+        assert torch.equal(t, t.to(torch.bfloat16).float())
+    assert mods.engine.w_exact_bf16 and mods.engine.Wal_p is None
+
+
 def test_step_granular_admission_same_audio(mods, lexicon):
     """The opt-in step-granular admission (run_iteration_steps: requests join the pooled decode at
     the next 8-step boundary, the persistent decoder runs 8-step launches) produces every request's
