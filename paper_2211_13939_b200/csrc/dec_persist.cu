@@ -43,7 +43,7 @@
 #define DEC_QREUSE 1  // contiguous runs keep q across chunks of the same item
 #endif
 #ifndef DEC_CONTIG
-#define DEC_CONTIG 0  // ATT-A: 1 = contiguous task runs per CTA (q reused; off: see DESIGN §10), 0 = round-robin
+#define DEC_CONTIG 1  // ATT-A: 1 = contiguous task runs per CTA (q reused across an item's chunks), 0 = round-robin
 #endif
 #ifndef DEC_MERGE_B
 #define DEC_MERGE_B 96
@@ -255,7 +255,7 @@ constexpr uint32_t RING_BYTES = 160 * 1024;   // gate bulk-copy ring / attention
 constexpr int MAXGS = 10;                      // ring stages (W tile 16 KB + X tile items x 128 B)
 
 struct GateSync {
-  uint64_t full[MAXGS], empty[MAXGS], accf, acce, abar[2];
+  uint64_t full[MAXGS], empty[MAXGS], accf, acce, abar[2], amma;
   uint32_t tmem;
 };
 static_assert(2 * ASTAGE <= RING_BYTES && ACH * (ATT + EMB) * 4 <= RING_BYTES, "attention staging exceeds the ring");
@@ -527,20 +527,30 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
     if (n < N) {
       float* out = (MODE == 0 ? a.Qp : a.Pp) + (int64_t)ug * a.B * N + n;
       const float* w = wq;
-      for (int i = half; i < nmine; i += 2) {
-        const int b = ks + KSPLIT * i;
-        if (!active(pc, b, s)) continue;
-        const float4* h4 = reinterpret_cast<const float4*>(hs + i * 32);
-        float acc = 0.f;
+      // 4 items per pass (independent FMA chains; each item's sum stays in unit order)
+      for (int i0 = half; i0 < nmine; i0 += 8) {
+        const float4* h4[4];
+        float acc[4];
 #pragma unroll
-        for (int u4 = 0; u4 < 8; ++u4) {
-          const float4 h = h4[u4];
-          acc = fmaf(w[4 * u4], h.x, acc);
-          acc = fmaf(w[4 * u4 + 1], h.y, acc);
-          acc = fmaf(w[4 * u4 + 2], h.z, acc);
-          acc = fmaf(w[4 * u4 + 3], h.w, acc);
+        for (int j = 0; j < 4; ++j) {
+          h4[j] = reinterpret_cast<const float4*>(hs + min(i0 + 2 * j, nmine - 1) * 32);
+          acc[j] = 0.f;
         }
-        out[(int64_t)b * N] = acc;
+#pragma unroll
+        for (int u4 = 0; u4 < 8; ++u4)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 h = h4[j][u4];
+            acc[j] = fmaf(w[4 * u4], h.x, acc[j]);
+            acc[j] = fmaf(w[4 * u4 + 1], h.y, acc[j]);
+            acc[j] = fmaf(w[4 * u4 + 2], h.z, acc[j]);
+            acc[j] = fmaf(w[4 * u4 + 3], h.w, acc[j]);
+          }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = i0 + 2 * j, b = ks + KSPLIT * i;
+          if (i < nmine && active(pc, b, s)) out[(int64_t)b * N] = acc[j];
+        }
       }
     }
     __syncthreads();
@@ -552,18 +562,24 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
 
 // ------------------------------------------------------------------ attention
 struct AttSmem {
+  // location features on the tensor cores: loc[a][t] = sum_k WL[a][k] . WIN[t][k], k = 32 c + tap
+  // (tap 31 = 0), WL = the location conv composed with the location dense layer; both operands as
+  // bf16 high / low parts in the UMMA 128B-swizzled K-major layout (A: 128 rows x 128 B, B: 32 x 128 B)
+  __align__(1024) uint8_t wl[2][ATT * 128];
+  __align__(1024) uint8_t win[2][32 * 128];
   float q[ATT], sv[ATT];
-  __align__(16) float sWl[2 * 32 * ATT];  // [c][k][a], k < 31 (tap 31 = 0): loc[a] = sum sWl[c][k][a] w_c[t+k-15]
   float red[32];
+  float ered[NW][16];          // per-warp position partials of the energies (ATT-A)
   float scale[MAXCH];
   int tstart[MAXB + 1];        // prefix sum of chunks per item (ATT-A task list)
   float wp[ACH + 2 * HALO + 2], wa[ACH + 2 * HALO + 2], e[ACH];
-  // scratch: context partials [8][512] (ATT-A), gate-fixup h (gate phases), PRE's
-  // last frame [8][80] + H1 [8][256] + gemv partials [8 warps][8][32] (so the ring is free for the
-  // prefetch of the attention-gate weights during PRE)
-  __align__(16) float locf[8 * NMEL + 8 * PRE + NW * 8 * 32];
 };
-static_assert(8 * NMEL + 8 * PRE + NW * 8 * 32 >= NW * EMB, "context partials exceed the scratch");
+// Generic scratch in the ring (free outside the gate pipeline / attention staging): the gate fixup's
+// h values [32 x B/4] and PRE's last frame [8][80] + H1 [8][256] + gemv partials [8 warps][8][32]
+constexpr int SCRATCH_F = 8 * NMEL + 8 * PRE + NW * 8 * 32;
+static_assert(SCRATCH_F * 4 <= RING_BYTES && 32 * (MAXB / 4) * 4 <= RING_BYTES, "ring scratch");
+static_assert(DEC_PREFETCH == 0, "gate-weight prefetch would overwrite the PRE scratch in the ring");
+
 
 __device__ __forceinline__ float block_max(float v, float* red) {
   v = itts::warp_max(v);
@@ -605,9 +621,19 @@ __device__ __forceinline__ void att_prefetch(const DecArgs& a, int b, int ta, in
                : "memory");
 }
 
+// 128B-swizzled K-major UMMA tile element (row r, k < 64) of a [rows][64] bf16 tile
+__device__ __forceinline__ int swz128(int r, int k) { return r * 64 + ((((k >> 3) ^ (r & 7))) << 3) + (k & 7); }
+
 // ATT-A for one (item b, chunk [ta, tb)) whose rows are (being) staged in `stage`.
-__device__ void att_chunk(const DecArgs& a, AttSmem& sm, int s, int b, int ch, int ta, int tb, const uint8_t* stage,
-                          uint64_t* abar, uint32_t& aphase, bool load_q) {
+// Energies: the location term of the 32 positions is one tcgen05 MMA chain D[128 dims][32 pos] =
+// WL . WIN^T (bf16 hi/lo x3 products, fp32 accumulation, in TMEM columns [0, 32)); each thread
+// then owns one dim a and 16 positions: v[a] tanh(q[a] + D[a][t] + pm[t][a]), summed over the 32
+// dims of its warp by a shuffle reduce-scatter (lane t % 16 ends with position t) and over the 4
+// warps of its position half in warp order.  Softmax statistics of the chunk on one warp; context
+// partial: thread d sums its 2 dims over the chunk's positions in order.  Every reduction order
+// depends only on the chunk (batch transparency).
+__device__ void att_chunk(const DecArgs& a, AttSmem& sm, GateSync& gsy, int s, int b, int ch, int ta, int tb,
+                          const uint8_t* stage, uint64_t* abar, uint32_t& aphase, uint32_t& mphase, bool load_q) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool tr = a.trace && blockIdx.x == 0 && tid == 0;
   unsigned long long t0 = tr ? gtimer() : 0;
@@ -633,10 +659,7 @@ __device__ void att_chunk(const DecArgs& a, AttSmem& sm, int s, int b, int ch, i
     for (int z = 1; z < NGRP; ++z) qa += qv[z];
     sm.q[tid] = qa;
   }
-  // The whole window buffer, not just the nh entries the 31 taps use: the 4-position sliding
-  // window also multiplies the zero tap 31 (and loads ahead) up to index n + 34, and stale shared
-  // memory there (another kernel's bytes, possibly an Inf / NaN pattern) would give 0 * NaN = NaN
-  // in the chunk's last energy.
+  // window w_c[ta - 15 + i], zero outside [0, L) and beyond the chunk's taps
   for (int i = tid; i < ACH + 2 * HALO + 2; i += NT) {
     const int t = ta - HALO + i;
     const bool in = i < nh && t >= 0 && t < L;
@@ -645,112 +668,94 @@ __device__ void att_chunk(const DecArgs& a, AttSmem& sm, int s, int b, int ch, i
   }
   __syncthreads();
   mark(8);
-  tcg::mbar_wait(abar, aphase);
+  {  // WIN rows t < 32: [wp[t .. t+30], 0, wa[t .. t+30], 0]; thread -> (row t, 8-column group j)
+    const int t = tid >> 3, j = tid & 7, c = j >> 2;
+    const float* wv = c ? sm.wa : sm.wp;
+    alignas(16) __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int tap = (j & 3) * 8 + e;
+      const float x = (t < n && tap < KLOC) ? wv[t + tap] : 0.f;
+      hi[e] = __float2bfloat16_rn(x);
+      lo[e] = __float2bfloat16_rn(x - __bfloat162float(hi[e]));
+    }
+    const int o = swz128(t, 8 * j);
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(sm.win[0]) + o) = *reinterpret_cast<const uint4*>(hi);
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(sm.win[1]) + o) = *reinterpret_cast<const uint4*>(lo);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (tid == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+    const uint64_t dwh = tcg::make_desc<128>(tcg::smem_u32(sm.wl[0])), dwl = tcg::make_desc<128>(tcg::smem_u32(sm.wl[1]));
+    const uint64_t dxh = tcg::make_desc<128>(tcg::smem_u32(sm.win[0])), dxl = tcg::make_desc<128>(tcg::smem_u32(sm.win[1]));
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, dwh + 2 * kk, dxh + 2 * kk, idesc, kk != 0);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, dwh + 2 * kk, dxl + 2 * kk, idesc, 1);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, dwl + 2 * kk, dxh + 2 * kk, idesc, 1);
+    tcg::umma_commit(&gsy.amma);
+  }
+  tcg::mbar_wait(abar, aphase);   // the chunk's pm / memory rows
   aphase ^= 1;
   mark(9);
-  // energies: warp w takes positions [4w, 4w+4) of the (<= 32-position) chunk, lane l dims 4l..4l+3.
-  // The location conv and dense layer are one 62-tap x 128 filter (composed on the host); each
-  // filter tap is loaded once per lane and applied to 4 positions held in a sliding register window.
   {
-    const float4 q4 = reinterpret_cast<const float4*>(sm.q)[lane];
-    const float4 v4 = reinterpret_cast<const float4*>(sm.sv)[lane];
-    const float4* wl4 = reinterpret_cast<const float4*>(sm.sWl);
-    for (int pb = warp * 4; pb < n; pb += 4 * NW) {  // warp-uniform
-      float acc[4][4];
+    const int qd = warp & 3, h = warp >> 2, ad = qd * 32 + lane;
+    tcg::mbar_wait(&gsy.amma, mphase);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float x[16];
+    tcg::tmem_ld16(gsy.tmem + ((uint32_t)(qd * 32) << 16) + 16 * h, x);
+    const float qa = sm.q[ad], va = sm.sv[ad];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+    for (int i = 0; i < 16; ++i) {
+      const int t = 16 * h + i;
+      x[i] = t < n ? va * tanh_fast((qa + x[i]) + sPm[t * ATT + ad]) : 0.f;
+    }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) acc[q][u] = 0.f;
+    for (int i = 0; i < 16; ++i) x[i] += __shfl_xor_sync(0xffffffffu, x[i], 16);
 #pragma unroll
-      for (int cch = 0; cch < 2; ++cch) {
-        const float* wv = (cch ? sm.wa : sm.wp) + pb;
-        // slot (q + k) & 3 holds w[pb + q + k]; unrolled by 4 taps so the rotation is static
-        float win[4];
+    for (int st = 8; st >= 1; st >>= 1) {
+      const bool up = lane & st;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) win[q] = wv[q];
-        const float4* wl = wl4 + cch * 32 * (ATT / 4) + lane;
-#pragma unroll 2
-        for (int k0 = 0; k0 < 32; k0 += 4) {
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const float4 w4 = wl[(k0 + kk) * (ATT / 4)];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float x = win[(q + kk) & 3];
-              acc[q][0] = fmaf(w4.x, x, acc[q][0]);
-              acc[q][1] = fmaf(w4.y, x, acc[q][1]);
-              acc[q][2] = fmaf(w4.z, x, acc[q][2]);
-              acc[q][3] = fmaf(w4.w, x, acc[q][3]);
-            }
-            win[kk] = wv[k0 + kk + 4];
-          }
-        }
-      }
-      float en[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float4 pv = reinterpret_cast<const float4*>(sPm + (pb + q) * ATT)[lane];
-        en[q] = v4.x * tanh_fast((q4.x + acc[q][0]) + pv.x);
-        en[q] = fmaf(v4.y, tanh_fast((q4.y + acc[q][1]) + pv.y), en[q]);
-        en[q] = fmaf(v4.z, tanh_fast((q4.z + acc[q][2]) + pv.z), en[q]);
-        en[q] = fmaf(v4.w, tanh_fast((q4.w + acc[q][3]) + pv.w), en[q]);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) en[q] = itts::warp_sum(en[q]);
-      if (lane < 4 && pb + lane < n) {
-        float mine = en[0];
-#pragma unroll
-        for (int q = 1; q < 4; ++q) mine = lane == q ? en[q] : mine;
-        sm.e[pb + lane] = mine;
+      for (int i = 0; i < st; ++i) {
+        const float send = up ? x[i] : x[i + st], keep = up ? x[i + st] : x[i];
+        x[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
       }
     }
+    if (lane < 16) sm.ered[warp][lane] = x[0];
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
+  mphase ^= 1;
   __syncthreads();
   mark(10);
-  float lmax = -INFINITY;
-  for (int t = tid; t < n; t += NT) lmax = fmaxf(lmax, sm.e[t]);
-  const float M = block_max(lmax, sm.red);
-  float lsum = 0.f;
-  for (int t = tid; t < n; t += NT) {
-    const float x = expf(sm.e[t] - M);
-    sm.e[t] = x;
-    lsum += x;
-    a.U[(int64_t)b * a.u_ld + ta + t] = x;
-  }
-  const float Ssum = block_sum(lsum, sm.red);
-  mark(11);
-  // unnormalised context partial: warp w takes positions t = w (mod 8), lane 16 dims
-  float4 acc[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float4* mem4 = reinterpret_cast<const float4*>(sMem);
-#pragma unroll 4
-  for (int t = warp; t < n; t += NW) {
-    const float w = sm.e[t];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float4 m4 = mem4[t * (EMB / 4) + lane + 32 * j];
-      acc[j].x = fmaf(w, m4.x, acc[j].x);
-      acc[j].y = fmaf(w, m4.y, acc[j].y);
-      acc[j].z = fmaf(w, m4.z, acc[j].z);
-      acc[j].w = fmaf(w, m4.w, acc[j].w);
+  if (warp == 0) {  // chunk softmax statistics: lane t = position t
+    const int h = lane >> 4, i = lane & 15;
+    const float e = ((sm.ered[4 * h][i] + sm.ered[4 * h + 1][i]) + sm.ered[4 * h + 2][i]) + sm.ered[4 * h + 3][i];
+    const float M = itts::warp_max(lane < n ? e : -INFINITY);
+    const float xv = lane < n ? expf(e - M) : 0.f;
+    const float Ssum = itts::warp_sum(xv);
+    sm.e[lane] = xv;
+    if (lane < n) a.U[(int64_t)b * a.u_ld + ta + lane] = xv;
+    if (lane == 0) {
+      float* ap = a.AP + ((int64_t)b * MAXCH + ch) * (2 + EMB);
+      ap[0] = M;
+      ap[1] = Ssum;
     }
   }
-  float4(*cpart)[EMB / 4] = reinterpret_cast<float4(*)[EMB / 4]>(sm.locf);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) cpart[warp][lane + 32 * j] = acc[j];
   __syncthreads();
-  float* ap = a.AP + ((int64_t)b * MAXCH + ch) * (2 + EMB);
-  const float* cp = reinterpret_cast<const float*>(cpart);
-  for (int d = tid; d < EMB; d += NT) {
-    float c = cp[d];
-#pragma unroll
-    for (int w = 1; w < NW; ++w) c += cp[w * EMB + d];
-    ap[2 + d] = c;
-  }
-  if (tid == 0) {
-    ap[0] = M;
-    ap[1] = Ssum;
+  mark(11);
+  {  // unnormalised context partial: thread -> dims tid, tid + 256, positions in order
+    float c0 = 0.f, c1 = 0.f;
+    for (int t = 0; t < n; ++t) {
+      const float w = sm.e[t];
+      c0 = fmaf(w, sMem[t * EMB + tid], c0);
+      c1 = fmaf(w, sMem[t * EMB + tid + NT], c1);
+    }
+    float* ap = a.AP + ((int64_t)b * MAXCH + ch) * (2 + EMB);
+    ap[2 + tid] = c0;
+    ap[2 + NT + tid] = c1;
   }
   __syncthreads();
   mark(12);
@@ -810,13 +815,12 @@ __global__ void __launch_bounds__(NT, 1)
   const bool comb = a.split && a_box_bytes <= 128u * 128u;
   const uint32_t comb_bytes = (a.split == 1 ? 2 : 1) * GW_TILE + 2 * a_box_bytes;
   const int nst = min(MAXGS, (int)(RING_BYTES / (comb ? comb_bytes : GW_TILE + a_box_bytes)));
-  float* scratch = reinterpret_cast<float*>(&sm.locf[0]);                       // gemv reductions
   __shared__ GateSync gsy;
   __shared__ PlanCache pc;
   const int tid = threadIdx.x, G = gridDim.x, c = blockIdx.x;
   const bool gemm_cta = c < GEMM_CTAS;
   unsigned gen = 0;
-  uint32_t g_ring = 0, lt_tile = 0, aphase[2] = {0, 0};
+  uint32_t g_ring = 0, lt_tile = 0, aphase[2] = {0, 0}, mphase = 0;
   unsigned grp_gen = 0;
 
   if (tid == 0) {
@@ -828,10 +832,13 @@ __global__ void __launch_bounds__(NT, 1)
     tcg::mbar_init(&gsy.acce, 4);
     tcg::mbar_init(&gsy.abar[0], 1);
     tcg::mbar_init(&gsy.abar[1], 1);
+    tcg::mbar_init(&gsy.amma, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const uint32_t tcols = a_box_bytes > 256u * 128u ? 512u : 256u;  // accumulator columns = rows (2 N tiles)
-  if (gemm_cta && (tid >> 5) == 1) {
+  // gate CTAs: accumulator columns = rows (2 N tiles above 256); every CTA: ATT-A location features
+  // in columns [0, 32) (free between gate phases)
+  const uint32_t tcols = !gemm_cta ? 32u : a_box_bytes > 256u * 128u ? 512u : 256u;
+  if ((tid >> 5) == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tcg::smem_u32(&gsy.tmem)),
                  "r"(tcols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -843,13 +850,15 @@ __global__ void __launch_bounds__(NT, 1)
     pc.L[b] = (int)a.plan[b * DPLAN + 2];
     pc.steps[b] = (int)a.plan[b * DPLAN + 5];
   }
-  // attention constants (resident for the whole chunk)
-  for (int i = tid; i < 2 * 32 * ATT / 4; i += NT) {
-    const int cch = i / (32 * ATT / 4), r = i - cch * (32 * ATT / 4), k = r / (ATT / 4);
-    reinterpret_cast<float4*>(sm.sWl)[i] =
-        k < KLOC ? __ldg(reinterpret_cast<const float4*>(a.WlocD) + (cch * KLOC + k) * (ATT / 4) + r % (ATT / 4))
-                 : make_float4(0.f, 0.f, 0.f, 0.f);
+  // attention constants (resident for the whole chunk): WL[a][32 c + tap] as bf16 hi / lo UMMA tiles
+  for (int i = tid; i < ATT * 64; i += NT) {
+    const int ad = i >> 6, k = i & 63, cch = k >> 5, tap = k & 31;
+    const float x = tap < KLOC ? __ldg(a.WlocD + (cch * KLOC + tap) * ATT + ad) : 0.f;
+    const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+    reinterpret_cast<__nv_bfloat16*>(sm.wl[0])[swz128(ad, k)] = hi;
+    reinterpret_cast<__nv_bfloat16*>(sm.wl[1])[swz128(ad, k)] = __float2bfloat16_rn(x - __bfloat162float(hi));
   }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (tid < ATT) sm.sv[tid] = __ldg(a.v + tid);
   __syncthreads();
   // bf16 operand mirror, bank 0, from the gathered fp32 state rows
@@ -923,7 +932,7 @@ __global__ void __launch_bounds__(NT, 1)
           tp0 = t1;
         }
       };
-      float* sx = sm.locf;               // [8][80]
+      float* sx = ringf;                 // [8][80]
       float* sh = sx + 8 * NMEL;         // [8][256]
       float* gsc = sh + 8 * PRE;         // gemv partials
 
@@ -1005,7 +1014,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
     phase_end();
     // ---- ATT gates + cell + query partials
-    if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen, sm.locf);
+    if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen, ringf);
     phase_end();
     // ---- ATT-A: the non-empty (item, chunk) tasks of the live items, dealt round-robin
     if (tid < 32) {  // task prefix over items: 16 items per lane, then a warp scan
@@ -1063,7 +1072,7 @@ __global__ void __launch_bounds__(NT, 1)
                          &gsy.abar[buf ^ 1]);
           }
         }
-        att_chunk(a, sm, gs, bcur, ch, ta, tb, ring + buf * ASTAGE, &gsy.abar[buf], aphase[buf], load_q);
+        att_chunk(a, sm, gsy, gs, bcur, ch, ta, tb, ring + buf * ASTAGE, &gsy.abar[buf], aphase[buf], mphase, load_q);
       }
     }
     phase_end();
@@ -1091,7 +1100,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
     // ---- DEC gates + cell + projection partials of dec_h; the other CTAs project the context
-    if (gemm_cta) gate_phase<1>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen, sm.locf,
+    if (gemm_cta) gate_phase<1>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen, ringf,
                                 merged, ctx_target);
     {
       const int c0 = G > GEMM_CTAS ? GEMM_CTAS : 0, nsp = G - c0;
@@ -1131,7 +1140,7 @@ __global__ void __launch_bounds__(NT, 1)
     for (int i = 0; i < 5; ++i) a.trace[i] = tacc[i];
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (gemm_cta && (tid >> 5) == 1) {
+  if ((tid >> 5) == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(gsy.tmem), "r"(tcols));
   }
