@@ -25,7 +25,7 @@ ap.add_argument("--batch", type=int, default=24)
 ap.add_argument("--reps", type=int, default=50)
 args = ap.parse_args()
 eng = TierREngine(PipelineConfig(), "cuda:0")
-eng.prepare_graphs(64)
+eng.prepare_graphs(max(64, args.batch))
 lex = default_lexicon()
 rng = random.Random(0)
 fos = [run_frontend(random_text(rng, 150, 200, lex), lex) for _ in range(args.batch)]
