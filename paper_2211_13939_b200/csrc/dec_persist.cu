@@ -39,12 +39,6 @@
 // start with their att_h columns and wait for the combined contexts on a counter (one grid
 // barrier fewer per step; same-box A/B: B=1 -4.4%, B=24 -2.7%, B=128 +2.5%, hence the cut-off).
 // Larger batches: separate ATT-B phase.
-#ifndef DEC_QREUSE
-#define DEC_QREUSE 1  // contiguous runs keep q across chunks of the same item
-#endif
-#ifndef DEC_CONTIG
-#define DEC_CONTIG 1  // ATT-A: 1 = contiguous task runs per CTA (q reused across an item's chunks), 0 = round-robin
-#endif
 #ifndef DEC_MERGE_B
 #define DEC_MERGE_B 96
 #endif
@@ -255,7 +249,7 @@ constexpr uint32_t RING_BYTES = 160 * 1024;   // gate bulk-copy ring / attention
 constexpr int MAXGS = 10;                      // ring stages (W tile 16 KB + X tile items x 128 B)
 
 struct GateSync {
-  uint64_t full[MAXGS], empty[MAXGS], accf, acce, abar[2], amma;
+  uint64_t full[MAXGS], empty[MAXGS], accf, acce, abar[2], amma[2];
   uint32_t tmem;
 };
 static_assert(2 * ASTAGE <= RING_BYTES && ACH * (ATT + EMB) * 4 <= RING_BYTES, "attention staging exceeds the ring");
@@ -566,13 +560,13 @@ struct AttSmem {
   // (tap 31 = 0), WL = the location conv composed with the location dense layer; both operands as
   // bf16 high / low parts in the UMMA 128B-swizzled K-major layout (A: 128 rows x 128 B, B: 32 x 128 B)
   __align__(1024) uint8_t wl[2][ATT * 128];
-  __align__(1024) uint8_t win[2][32 * 128];
-  float q[ATT], sv[ATT];
+  __align__(1024) uint8_t win[2][2][32 * 128];   // [pipeline buffer][hi / lo]
+  float q[2][ATT], sv[ATT];
   float red[32];
   float ered[NW][16];          // per-warp position partials of the energies (ATT-A)
   float scale[MAXCH];
   int tstart[MAXB + 1];        // prefix sum of chunks per item (ATT-A task list)
-  float wp[ACH + 2 * HALO + 2], wa[ACH + 2 * HALO + 2], e[ACH];
+  float wp[2][ACH + 2 * HALO + 2], wa[2][ACH + 2 * HALO + 2], e[ACH];
 };
 // Generic scratch in the ring (free outside the gate pipeline / attention staging): the gate fixup's
 // h values [32 x B/4] and PRE's last frame [8][80] + H1 [8][256] + gemv partials [8 warps][8][32]
@@ -624,53 +618,64 @@ __device__ __forceinline__ void att_prefetch(const DecArgs& a, int b, int ta, in
 // 128B-swizzled K-major UMMA tile element (row r, k < 64) of a [rows][64] bf16 tile
 __device__ __forceinline__ int swz128(int r, int k) { return r * 64 + ((((k >> 3) ^ (r & 7))) << 3) + (k & 7); }
 
-// ATT-A for one (item b, chunk [ta, tb)) whose rows are (being) staged in `stage`.
-// Energies: the location term of the 32 positions is one tcgen05 MMA chain D[128 dims][32 pos] =
-// WL . WIN^T (bf16 hi/lo x3 products, fp32 accumulation, in TMEM columns [0, 32)); each thread
-// then owns one dim a and 16 positions: v[a] tanh(q[a] + D[a][t] + pm[t][a]), summed over the 32
-// dims of its warp by a shuffle reduce-scatter (lane t % 16 ends with position t) and over the 4
-// warps of its position half in warp order.  Softmax statistics of the chunk on one warp; context
-// partial: thread d sums its 2 dims over the chunk's positions in order.  Every reduction order
-// depends only on the chunk (batch transparency).
-__device__ void att_chunk(const DecArgs& a, AttSmem& sm, GateSync& gsy, int s, int b, int ch, int ta, int tb,
-                          const uint8_t* stage, uint64_t* abar, uint32_t& aphase, uint32_t& mphase, bool load_q) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool tr = a.trace && blockIdx.x == 0 && tid == 0;
-  unsigned long long t0 = tr ? gtimer() : 0;
-  auto mark = [&](int slot) {
-    if (tr) {
-      const unsigned long long t1 = gtimer();
-      a.trace[slot] += t1 - t0;
-      t0 = t1;
-    }
-  };
+// ATT-A, software-pipelined over a CTA's run of (item, 32-position chunk) tasks.  Task i:
+//   load    the q partials (new item only) and the location window, into registers, issued before
+//           task i-1's energies so their latency hides behind them; stored to smem buffer i & 1;
+//   mma     WIN[i & 1] (rows t < 32: [wp[t .. t+30], 0, wa[t .. t+30], 0], bf16 hi / lo) built from
+//           the window; the location term D[128 dims][32 pos] = WL . WIN^T as one tcgen05 chain
+//           (x3 hi/lo products, fp32) into TMEM columns [32 (i & 1), +32) -- it runs during task
+//           i-1's context pass;
+//   energy  thread (dim a, position half h): v_a tanh(q_a + D[a][t] + pm[t][a]) for 16 positions,
+//           summed over the warp's 32 dims by a shuffle reduce-scatter (lane t % 16 keeps
+//           position t) and over the 4 warps of the half in warp order;
+//   softmax chunk max / exp / sum on one warp (lane = position);
+//   context thread d: dims d, d + 256 summed over the chunk's positions in order.
+// The pm / memory rows of task i stream into ring buffer i & 1 (bulk copies issued one task
+// ahead).  Every reduction order depends only on the chunk (batch transparency).
+struct AttNext {
+  float wpv, wav;       // window values w_c[ta - 15 + tid] of the next task
+  float qv[NGRP];       // its q partials (tid < 128, new item only)
+};
+
+__device__ __forceinline__ const float* att_wsrc(const DecArgs& a, int s, int b) {
   const int64_t* p = a.plan + b * DPLAN;
-  const int L = (int)p[2];
-  const float* wsrc = reinterpret_cast<const float*>(a.step0 + s == 0 ? p[3] : p[4]);
-  const int n = tb - ta, nh = n + 2 * HALO;
-  const float* sPm = reinterpret_cast<const float*>(stage);
-  const float* sMem = sPm + n * ATT;
-  if (load_q && tid < ATT) {  // q = sum of the 32 unit-group partials, group order (kept for the item's next chunk)
-    float qv[NGRP];
+  return reinterpret_cast<const float*>(a.step0 + s == 0 ? p[3] : p[4]);
+}
+
+__device__ __forceinline__ void att_load(const DecArgs& a, int s, int b, int L, int ta, int n, bool load_q,
+                                         AttNext& r) {
+  const int tid = threadIdx.x;
+  if (load_q && tid < ATT) {
 #pragma unroll
-    for (int z = 0; z < NGRP; ++z) qv[z] = ldf(a.Qp + ((int64_t)z * a.B + b) * ATT + tid);
-    float qa = qv[0];
+    for (int z = 0; z < NGRP; ++z) r.qv[z] = ldf(a.Qp + ((int64_t)z * a.B + b) * ATT + tid);
+  }
+  const float* wsrc = att_wsrc(a, s, b);
+  const int t = ta - HALO + tid;
+  const bool in = tid < ACH + 2 * HALO + 2 && tid < n + 2 * HALO && t >= 0 && t < L;
+  r.wpv = in ? ldf(wsrc + t) : 0.f;
+  r.wav = in ? ldf(wsrc + L + t) : 0.f;
+}
+
+__device__ __forceinline__ void att_store(AttSmem& sm, int wb, int qb, bool load_q, const AttNext& r) {
+  const int tid = threadIdx.x;
+  if (load_q && tid < ATT) {  // q = sum of the 32 unit-group partials, group order
+    float qa = r.qv[0];
 #pragma unroll
-    for (int z = 1; z < NGRP; ++z) qa += qv[z];
-    sm.q[tid] = qa;
+    for (int z = 1; z < NGRP; ++z) qa += r.qv[z];
+    sm.q[qb][tid] = qa;
   }
-  // window w_c[ta - 15 + i], zero outside [0, L) and beyond the chunk's taps
-  for (int i = tid; i < ACH + 2 * HALO + 2; i += NT) {
-    const int t = ta - HALO + i;
-    const bool in = i < nh && t >= 0 && t < L;
-    sm.wp[i] = in ? ldf(wsrc + t) : 0.f;
-    sm.wa[i] = in ? ldf(wsrc + L + t) : 0.f;
+  if (tid < ACH + 2 * HALO + 2) {
+    sm.wp[wb][tid] = r.wpv;   // zero past the chunk's taps: the WIN build reads only t < n rows,
+    sm.wa[wb][tid] = r.wav;   // but the buffer never holds another launch's bytes
   }
-  __syncthreads();
-  mark(8);
-  {  // WIN rows t < 32: [wp[t .. t+30], 0, wa[t .. t+30], 0]; thread -> (row t, 8-column group j)
-    const int t = tid >> 3, j = tid & 7, c = j >> 2;
-    const float* wv = c ? sm.wa : sm.wp;
+}
+
+// WIN[wb] from the window buffer wb (all threads), then (thread 0) the location-term MMA chain.
+__device__ __forceinline__ void att_build_mma(AttSmem& sm, GateSync& gsy, int wb, int n) {
+  const int tid = threadIdx.x;
+  {
+    const int t = tid >> 3, j = tid & 7, cch = j >> 2;
+    const float* wv = cch ? sm.wa[wb] : sm.wp[wb];
     alignas(16) __nv_bfloat16 hi[8], lo[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -680,8 +685,8 @@ __device__ void att_chunk(const DecArgs& a, AttSmem& sm, GateSync& gsy, int s, i
       lo[e] = __float2bfloat16_rn(x - __bfloat162float(hi[e]));
     }
     const int o = swz128(t, 8 * j);
-    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(sm.win[0]) + o) = *reinterpret_cast<const uint4*>(hi);
-    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(sm.win[1]) + o) = *reinterpret_cast<const uint4*>(lo);
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(sm.win[wb][0]) + o) = *reinterpret_cast<const uint4*>(hi);
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(sm.win[wb][1]) + o) = *reinterpret_cast<const uint4*>(lo);
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
@@ -689,77 +694,80 @@ __device__ void att_chunk(const DecArgs& a, AttSmem& sm, GateSync& gsy, int s, i
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
     const uint64_t dwh = tcg::make_desc<128>(tcg::smem_u32(sm.wl[0])), dwl = tcg::make_desc<128>(tcg::smem_u32(sm.wl[1]));
-    const uint64_t dxh = tcg::make_desc<128>(tcg::smem_u32(sm.win[0])), dxl = tcg::make_desc<128>(tcg::smem_u32(sm.win[1]));
+    const uint64_t dxh = tcg::make_desc<128>(tcg::smem_u32(sm.win[wb][0]));
+    const uint64_t dxl = tcg::make_desc<128>(tcg::smem_u32(sm.win[wb][1]));
+    const uint32_t d = gsy.tmem + 32 * wb;
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, dwh + 2 * kk, dxh + 2 * kk, idesc, kk != 0);
+    for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(d, dwh + 2 * kk, dxh + 2 * kk, idesc, kk != 0);
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, dwh + 2 * kk, dxl + 2 * kk, idesc, 1);
+    for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(d, dwh + 2 * kk, dxl + 2 * kk, idesc, 1);
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, dwl + 2 * kk, dxh + 2 * kk, idesc, 1);
-    tcg::umma_commit(&gsy.amma);
+    for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(d, dwl + 2 * kk, dxh + 2 * kk, idesc, 1);
+    tcg::umma_commit(&gsy.amma[wb]);
   }
-  tcg::mbar_wait(abar, aphase);   // the chunk's pm / memory rows
-  aphase ^= 1;
-  mark(9);
-  {
-    const int qd = warp & 3, h = warp >> 2, ad = qd * 32 + lane;
-    tcg::mbar_wait(&gsy.amma, mphase);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    float x[16];
-    tcg::tmem_ld16(gsy.tmem + ((uint32_t)(qd * 32) << 16) + 16 * h, x);
-    const float qa = sm.q[ad], va = sm.sv[ad];
+}
+
+// Energies of the task in pipeline buffer wb (q buffer qb, rows staged in `stage`) -> sm.ered.
+__device__ __forceinline__ void att_energy(AttSmem& sm, GateSync& gsy, int wb, int qb, int n, const float* sPm,
+                                           uint32_t& mph) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int qd = warp & 3, h = warp >> 2, ad = qd * 32 + lane;
+  tcg::mbar_wait(&gsy.amma[wb], mph);
+  mph ^= 1;
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  float x[16];
+  tcg::tmem_ld16(gsy.tmem + ((uint32_t)(qd * 32) << 16) + 32 * wb + 16 * h, x);
+  const float qa = sm.q[qb][ad], va = sm.sv[ad];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int t = 16 * h + i;
-      x[i] = t < n ? va * tanh_fast((qa + x[i]) + sPm[t * ATT + ad]) : 0.f;
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) x[i] += __shfl_xor_sync(0xffffffffu, x[i], 16);
-#pragma unroll
-    for (int st = 8; st >= 1; st >>= 1) {
-      const bool up = lane & st;
-#pragma unroll
-      for (int i = 0; i < st; ++i) {
-        const float send = up ? x[i] : x[i + st], keep = up ? x[i + st] : x[i];
-        x[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
-      }
-    }
-    if (lane < 16) sm.ered[warp][lane] = x[0];
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  for (int i = 0; i < 16; ++i) {
+    const int t = 16 * h + i;
+    x[i] = t < n ? va * tanh_fast((qa + x[i]) + sPm[t * ATT + ad]) : 0.f;
   }
-  mphase ^= 1;
-  __syncthreads();
-  mark(10);
-  if (warp == 0) {  // chunk softmax statistics: lane t = position t
-    const int h = lane >> 4, i = lane & 15;
-    const float e = ((sm.ered[4 * h][i] + sm.ered[4 * h + 1][i]) + sm.ered[4 * h + 2][i]) + sm.ered[4 * h + 3][i];
-    const float M = itts::warp_max(lane < n ? e : -INFINITY);
-    const float xv = lane < n ? expf(e - M) : 0.f;
-    const float Ssum = itts::warp_sum(xv);
-    sm.e[lane] = xv;
-    if (lane < n) a.U[(int64_t)b * a.u_ld + ta + lane] = xv;
-    if (lane == 0) {
-      float* ap = a.AP + ((int64_t)b * MAXCH + ch) * (2 + EMB);
-      ap[0] = M;
-      ap[1] = Ssum;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] += __shfl_xor_sync(0xffffffffu, x[i], 16);
+#pragma unroll
+  for (int st = 8; st >= 1; st >>= 1) {
+    const bool up = lane & st;
+#pragma unroll
+    for (int i = 0; i < st; ++i) {
+      const float send = up ? x[i] : x[i + st], keep = up ? x[i + st] : x[i];
+      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
     }
   }
-  __syncthreads();
-  mark(11);
-  {  // unnormalised context partial: thread -> dims tid, tid + 256, positions in order
-    float c0 = 0.f, c1 = 0.f;
-    for (int t = 0; t < n; ++t) {
-      const float w = sm.e[t];
-      c0 = fmaf(w, sMem[t * EMB + tid], c0);
-      c1 = fmaf(w, sMem[t * EMB + tid + NT], c1);
-    }
+  if (lane < 16) sm.ered[warp][lane] = x[0];
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// Chunk softmax statistics (warp 0; lane = position) -> U numerators, AP[0..1], sm.e.
+__device__ __forceinline__ void att_softmax(const DecArgs& a, AttSmem& sm, int b, int ch, int ta, int n) {
+  const int lane = threadIdx.x & 31;
+  const int h = lane >> 4, i = lane & 15;
+  const float e = ((sm.ered[4 * h][i] + sm.ered[4 * h + 1][i]) + sm.ered[4 * h + 2][i]) + sm.ered[4 * h + 3][i];
+  const float M = itts::warp_max(lane < n ? e : -INFINITY);
+  const float xv = lane < n ? expf(e - M) : 0.f;
+  const float Ssum = itts::warp_sum(xv);
+  sm.e[lane] = xv;
+  if (lane < n) a.U[(int64_t)b * a.u_ld + ta + lane] = xv;
+  if (lane == 0) {
     float* ap = a.AP + ((int64_t)b * MAXCH + ch) * (2 + EMB);
-    ap[2 + tid] = c0;
-    ap[2 + NT + tid] = c1;
+    ap[0] = M;
+    ap[1] = Ssum;
   }
-  __syncthreads();
-  mark(12);
-  if (tr) a.trace[13] += 1;
+}
+
+// Unnormalised context partial: thread -> dims tid, tid + 256, positions in order.
+__device__ __forceinline__ void att_context(const DecArgs& a, const AttSmem& sm, int b, int ch, int n,
+                                            const float* sMem) {
+  const int tid = threadIdx.x;
+  float c0 = 0.f, c1 = 0.f;
+  for (int t = 0; t < n; ++t) {
+    const float w = sm.e[t];
+    c0 = fmaf(w, sMem[t * EMB + tid], c0);
+    c1 = fmaf(w, sMem[t * EMB + tid + NT], c1);
+  }
+  float* ap = a.AP + ((int64_t)b * MAXCH + ch) * (2 + EMB);
+  ap[2 + tid] = c0;
+  ap[2 + NT + tid] = c1;
 }
 
 // ATT-B for item b: combine the chunks (max, sum, context partial; chunk order) -> context, W, W_acc.
@@ -820,7 +828,7 @@ __global__ void __launch_bounds__(NT, 1)
   const int tid = threadIdx.x, G = gridDim.x, c = blockIdx.x;
   const bool gemm_cta = c < GEMM_CTAS;
   unsigned gen = 0;
-  uint32_t g_ring = 0, lt_tile = 0, aphase[2] = {0, 0}, mphase = 0;
+  uint32_t g_ring = 0, lt_tile = 0, aphase[2] = {0, 0}, mphase[2] = {0, 0};
   unsigned grp_gen = 0;
 
   if (tid == 0) {
@@ -832,12 +840,13 @@ __global__ void __launch_bounds__(NT, 1)
     tcg::mbar_init(&gsy.acce, 4);
     tcg::mbar_init(&gsy.abar[0], 1);
     tcg::mbar_init(&gsy.abar[1], 1);
-    tcg::mbar_init(&gsy.amma, 1);
+    tcg::mbar_init(&gsy.amma[0], 1);
+    tcg::mbar_init(&gsy.amma[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // gate CTAs: accumulator columns = rows (2 N tiles above 256); every CTA: ATT-A location features
-  // in columns [0, 32) (free between gate phases)
-  const uint32_t tcols = !gemm_cta ? 32u : a_box_bytes > 256u * 128u ? 512u : 256u;
+  // in columns [0, 64) (two pipeline buffers; free between gate phases)
+  const uint32_t tcols = !gemm_cta ? 64u : a_box_bytes > 256u * 128u ? 512u : 256u;
   if ((tid >> 5) == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tcg::smem_u32(&gsy.tmem)),
                  "r"(tcols));
@@ -892,6 +901,16 @@ __global__ void __launch_bounds__(NT, 1)
   (void)ntask_for;
 #endif
   const int nb8 = (a.B + 7) / 8;
+  // PRE tasks: column blocks per task minimising rounds x (mel + H1 + cpt x p-block) (~5 + 3 cpt us);
+  // the arithmetic of every value is the same for any choice
+  int pre_cpt = 1;
+  {
+    int best = 1 << 30;
+    for (int cpt = 1; cpt <= 8; cpt *= 2) {
+      const int cost = ((nb8 * (8 / cpt) + G - 1) / G) * (5 + 3 * cpt);
+      if (cost < best) best = cost, pre_cpt = cpt;
+    }
+  }
   const bool merged = a.B <= DEC_MERGE_B;  // ATT-B folded into the decoder-gate phase
 
   unsigned long long tph = gtimer(), tacc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -921,8 +940,10 @@ __global__ void __launch_bounds__(NT, 1)
     const int gs = a.step0 + s;
     // ---- PRE: finish mel(s-1); H1 = relu(W0 . last) for the task's 8 items; p = relu(W1 . H1)
     if ((DEC_PREFETCH & 1) && gemm_cta && tid == 0) gate_prefetch_w<0>(a, ring, gsy, nst, g_ring);
-    for (int task = c; task < nb8 * 8; task += G) {
-      const int b0 = (task >> 3) * 8, n0 = (task & 7) * 32, nb = min(8, a.B - b0);
+    // task = (8 items, pre_cpt blocks of 32 prenet columns): mel and H1 are computed once per task
+    for (int task = c; task < nb8 * (8 / pre_cpt); task += G) {
+      const int b0 = (task / (8 / pre_cpt)) * 8, cb0 = (task % (8 / pre_cpt)) * pre_cpt, nb = min(8, a.B - b0);
+      const int n0 = cb0 * 32;
       const bool trp = a.trace && c == 0 && tid == 0;
       unsigned long long tp0 = trp ? gtimer() : 0;
       auto pmark = [&](int slot) {
@@ -1001,14 +1022,15 @@ __global__ void __launch_bounds__(NT, 1)
       }
       __syncthreads();
       pmark(6);
-      gemv_task<32, true>(b0, nb, n0, PRE, 0, PRE, a.W1T, sh, gsc,
-                    [&](int b, int k) { return 0.f; },
-                    [&](int b, int n, float y) {
-                      if (!active(pc, b, gs)) return;
-                      y = fmaxf(y, 0.f);
-                      a.work[(int64_t)b * ROW + P_OFF + n] = y;
-                      xb_store(a, b, P_OFF + n, y);
-                    });
+      for (int cb = cb0; cb < cb0 + pre_cpt; ++cb)
+        gemv_task<32, true>(b0, nb, cb * 32, PRE, 0, PRE, a.W1T, sh, gsc,
+                      [&](int b, int k) { return 0.f; },
+                      [&](int b, int n, float y) {
+                        if (!active(pc, b, gs)) return;
+                        y = fmaxf(y, 0.f);
+                        a.work[(int64_t)b * ROW + P_OFF + n] = y;
+                        xb_store(a, b, P_OFF + n, y);
+                      });
       WFENCE();
       pmark(7);
     }
@@ -1039,40 +1061,65 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();
     {
       const int ntask = sm.tstart[a.B];
-      int bcur = 0, bnext = 0;
-      auto locate = [&](int task, int& b) {
-        while (sm.tstart[b + 1] <= task) ++b;
-      };
       // CTA c takes a contiguous run of tasks, so consecutive chunks of one item share its q
-#if DEC_CONTIG
-      const int t0 = (int)((int64_t)c * ntask / G), t1 = (int)((int64_t)(c + 1) * ntask / G), tstep = 1;
-#else
-      const int t0 = c, t1 = ntask, tstep = G;
-#endif
+      const int t0 = (int)((int64_t)c * ntask / G), t1 = (int)((int64_t)(c + 1) * ntask / G);
+      const bool tr = a.trace && c == 0 && tid == 0;
+      unsigned long long tq = tr ? gtimer() : 0;
+      auto mark = [&](int slot) {
+        if (tr) {
+          const unsigned long long t2 = gtimer();
+          a.trace[slot] += t2 - tq;
+          tq = t2;
+        }
+      };
+      int bi = 0;  // item of the task being located (monotonic)
+      auto locate = [&](int task) {
+        while (sm.tstart[bi + 1] <= task) ++bi;
+        return bi;
+      };
       if (t0 < t1) {
-        locate(t0, bnext);
-        if (tid == 0) {
-          const int ta = (t0 - sm.tstart[bnext]) * chunk;
-          att_prefetch(a, bnext, ta, min(pc.L[bnext], ta + chunk), ring, &gsy.abar[0]);
-        }
-      }
-      int i = 0;
-      for (int task = t0; task < t1; task += tstep, ++i) {
-        const int buf = i & 1;
-        const bool load_q = DEC_CONTIG == 0 || !DEC_QREUSE || task == t0 || bnext != bcur;
-        bcur = bnext;
-        const int ch = task - sm.tstart[bcur];
-        const int L = pc.L[bcur];
-        const int ta = ch * chunk, tb = min(L, ta + chunk);
-        if (task + tstep < t1) {  // the next chunk streams into the other buffer during this one
-          locate(task + tstep, bnext);
-          if (tid == 0) {
-            const int ta2 = (task + tstep - sm.tstart[bnext]) * chunk;
-            att_prefetch(a, bnext, ta2, min(pc.L[bnext], ta2 + chunk), ring + (buf ^ 1) * ASTAGE,
-                         &gsy.abar[buf ^ 1]);
+        // prologue: task t0's rows (ring buffer 0), q and window (buffers 0), its MMA
+        int b = locate(t0);
+        int ta = (t0 - sm.tstart[b]) * chunk, n = min(pc.L[b], ta + chunk) - ta;
+        if (tid == 0) att_prefetch(a, b, ta, ta + n, ring, &gsy.abar[0]);
+        AttNext r;
+        att_load(a, gs, b, pc.L[b], ta, n, true, r);
+        att_store(sm, 0, 0, true, r);
+        __syncthreads();
+        att_build_mma(sm, gsy, 0, n);
+        int qb = 0;
+        for (int task = t0, i = 0; task < t1; ++task, ++i) {
+          const int buf = i & 1;
+          const int bc = b, tac = ta, nc = n, ch = task - sm.tstart[bc];
+          const bool more = task + 1 < t1;
+          bool new_q = false;
+          if (more) {  // task + 1: rows into the other ring buffer, q / window into registers
+            b = locate(task + 1);
+            ta = (task + 1 - sm.tstart[b]) * chunk;
+            n = min(pc.L[b], ta + chunk) - ta;
+            new_q = b != bc;
+            if (tid == 0) att_prefetch(a, b, ta, ta + n, ring + (buf ^ 1) * ASTAGE, &gsy.abar[buf ^ 1]);
+            att_load(a, gs, b, pc.L[b], ta, n, new_q, r);
           }
+          mark(8);
+          const float* sPm = reinterpret_cast<const float*>(ring + buf * ASTAGE);
+          tcg::mbar_wait(&gsy.abar[buf], aphase[buf]);   // task's pm / memory rows
+          aphase[buf] ^= 1;
+          mark(9);
+          att_energy(sm, gsy, buf, qb, nc, sPm, mphase[buf]);
+          if (more) att_store(sm, buf ^ 1, new_q ? qb ^ 1 : qb, new_q, r);
+          __syncthreads();
+          mark(10);
+          if (tid < 32) att_softmax(a, sm, bc, ch, tac, nc);
+          if (more) att_build_mma(sm, gsy, buf ^ 1, n);   // ends in a __syncthreads (softmax visible)
+          else __syncthreads();
+          mark(11);
+          att_context(a, sm, bc, ch, nc, sPm + nc * ATT);
+          __syncthreads();   // ring buffer / e reuse
+          mark(12);
+          if (tr) a.trace[13] += 1;
+          if (new_q) qb ^= 1;
         }
-        att_chunk(a, sm, gsy, gs, bcur, ch, ta, tb, ring + buf * ASTAGE, &gsy.abar[buf], aphase[buf], mphase, load_q);
       }
     }
     phase_end();

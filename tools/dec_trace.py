@@ -51,6 +51,6 @@ for B in [int(x) for x in args.batches.split(",")]:
         print(f"   {nm} gates CTA0 (us from phase start): producer issued {g[0]:.1f}, first stage {g[1]:.1f}, "
               f"MMA done {g[2]:.1f}, acc ready {g[3]:.1f}, group synced {g[4]:.1f}, cells {g[6]:.1f}, partials {g[5]:.1f}")
     if t[13]:
-        sub = ["q/w loads", "bulk wait", "energies", "softmax", "context+store"]
+        sub = ["next-task issue", "bulk wait", "energies", "softmax+next MMA", "context"]
         print(f"   ATT-A CTA0: {t[13] / 32:.1f} tasks/step; per task (us): " +
               ", ".join(f"{n} {t[8 + i] / t[13] / 1e3:.2f}" for i, n in enumerate(sub)))
