@@ -223,10 +223,12 @@ int itts_bert_prosody(const int32_t* ids, const int32_t* pos, const int64_t* pla
 int itts_r_mrf_combine(const void* y0, const void* y1, const void* y2, int64_t n, float slope, void* out,
                        void* stream);
 /* pcm16 (optional, may be NULL): int16 [total] 16-bit PCM of `audio` as the reference
- * pcm16_encode (src/vocoder.py:146-149), produced in the same pass. */
+ * pcm16_encode (src/vocoder.py:146-149), produced in the same pass.
+ * nonfinite (optional): int32 [n], zeroed here, item i's count of non-finite emitted samples
+ * (the finite-audio guard of AudioChunk, domain.py:_frozen_array, without a host scan). */
 int itts_r_post_splice(const void* X4, const int64_t* plan, int32_t n, int64_t max_g, const float* wpost,
                        float bpost, const float* fade, int32_t overlap_frames, int32_t overlap_samples,
-                       float* audio, void* pcm16, void* stream);
+                       float* audio, void* pcm16, int32_t* nonfinite, void* stream);
 
 /* K7 native launch sequence: the whole HiFi-GAN V1 stack of one pooled vocoder
  * call (replaces the per-layer host loop over vocode_batch's conv stack,

@@ -2,9 +2,11 @@
 
 Every live request owns a handful of variable-length regions (encoder
 memory, two ping-pong decoder-state buffers, two vocoder-state buffers).
-They are carved out of a single growable torch tensor by a first-fit
-allocator with coalescing, so kernels address them with plain base+offset
-pointers and no per-request cudaMalloc ever happens on the serving path.
+They are carved out of a single growable torch tensor by a best-fit
+allocator with coalescing (free blocks indexed by start for coalescing and by
+(size, start) for an O(log n) fit), so kernels address them with plain
+base+offset pointers and no per-request cudaMalloc ever happens on the serving
+path.
 
 Offsets are in elements and 128-byte aligned.  Growth reallocates and
 copies on the owning stream; callers keep offsets (never raw pointers)
@@ -38,6 +40,7 @@ class RaggedArena:
         self.tensor = torch.empty(cap, dtype=dtype, device=device)
         self._free_starts = [0]
         self._free_sizes = {0: cap}
+        self._by_size = [(cap, 0)]   # sorted (size, start) of the free blocks
         self._used = 0
         self.peak = 0
 
@@ -83,19 +86,24 @@ class RaggedArena:
         size = self._round(n)
         with self._lock:
             self._drain_locked()
-            for i in range(len(self._free_starts)):
-                start = self._free_starts[i]
-                have = self._free_sizes[start]
-                if have >= size:
-                    del self._free_sizes[start]
-                    self._free_starts.pop(i)
-                    if have > size:
-                        self._insert_free(start + size, have - size)
-                    self._used += size
-                    self.peak = max(self.peak, self._used)
-                    return start
+            j = bisect.bisect_left(self._by_size, (size, -1))   # smallest block that fits
+            if j < len(self._by_size):
+                have, start = self._by_size[j]
+                self._remove_free(start, have, j)
+                if have > size:
+                    self._insert_free(start + size, have - size)
+                self._used += size
+                self.peak = max(self.peak, self._used)
+                return start
             self._grow(size)
         return self.alloc(n)
+
+    def _remove_free(self, start: int, size: int, j: int | None = None) -> None:
+        del self._free_sizes[start]
+        self._free_starts.pop(bisect.bisect_left(self._free_starts, start))
+        if j is None:
+            j = bisect.bisect_left(self._by_size, (size, start))
+        self._by_size.pop(j)
 
     def free(self, off: int, n: int) -> None:
         size = self._round(n)
@@ -108,15 +116,21 @@ class RaggedArena:
         i = bisect.bisect_left(self._free_starts, start)
         # coalesce with right neighbour
         if i < len(self._free_starts) and start + size == self._free_starts[i]:
-            size += self._free_sizes.pop(self._free_starts.pop(i))
+            right = self._free_starts[i]
+            rsize = self._free_sizes[right]
+            self._remove_free(right, rsize)
+            size += rsize
         # coalesce with left neighbour
         if i > 0:
             left = self._free_starts[i - 1]
-            if left + self._free_sizes[left] == start:
-                self._free_sizes[left] += size
-                return
+            lsize = self._free_sizes[left]
+            if left + lsize == start:
+                self._remove_free(left, lsize)
+                start, size = left, lsize + size
+                i -= 1
         self._free_starts.insert(i, start)
         self._free_sizes[start] = size
+        bisect.insort(self._by_size, (size, start))
 
     def _grow(self, need: int) -> None:
         old = self.tensor

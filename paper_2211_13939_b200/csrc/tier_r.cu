@@ -707,7 +707,8 @@ __global__ void __launch_bounds__(256) k_post_splice(const __nv_bfloat16* __rest
                                                      const int64_t* __restrict__ plan,
                                                      const float* __restrict__ wpost,  // [32][7]
                                                      float bpost, const float* __restrict__ fade, int O, int S,
-                                                     float* __restrict__ audio, int16_t* __restrict__ pcm) {
+                                                     float* __restrict__ audio, int16_t* __restrict__ pcm,
+                                                     int32_t* __restrict__ nonfinite) {
   itts::pdl_trigger();
   itts::pdl_wait();
   const int64_t* p = plan + blockIdx.y * PPLAN;
@@ -753,6 +754,7 @@ __global__ void __launch_bounds__(256) k_post_splice(const __nv_bfloat16* __rest
   if (g < count) {
     if (has_tail && g < S) v = fade[g] * v + fade[S + g] * reinterpret_cast<const float*>(p[3])[g];
     audio[p[5] + g] = v;
+    if (nonfinite && !isfinite(v)) atomicAdd(nonfinite + blockIdx.y, 1);  // per-item guard (host reads n ints)
     if (pcm)  // f1: 16-bit PCM as pcm16_encode (src/vocoder.py:146-149): clamp, x 32767, round half to even
       pcm[p[5] + g] = (int16_t)__double2int_rn(fmin(fmax((double)v, -1.0), 1.0) * 32767.0);
   } else {
@@ -1089,16 +1091,19 @@ ITTS_API int itts_r_zero_halo(const int64_t* plan, int32_t n, int64_t max_halo, 
 
 ITTS_API int itts_r_post_splice(const void* X4, const int64_t* plan, int32_t n, int64_t max_g,
                                 const float* wpost, float bpost, const float* fade, int32_t overlap_frames,
-                                int32_t overlap_samples, float* audio, void* pcm16, void* stream) {
+                                int32_t overlap_samples, float* audio, void* pcm16, int32_t* nonfinite,
+                                void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
   const int64_t work = max(max_g, (int64_t)overlap_frames * NMEL);
   cudaError_t e = cudaMemcpyToSymbolAsync(c_wpost, wpost, sizeof(float) * 32 * 7, 0, cudaMemcpyDeviceToDevice,
                                           (cudaStream_t)stream);
   if (e != cudaSuccess) return (int)e;
+  if (nonfinite && (e = cudaMemsetAsync(nonfinite, 0, sizeof(int32_t) * n, (cudaStream_t)stream)) != cudaSuccess)
+    return (int)e;
   const cudaError_t le_ = itts::launch_pdl(k_post_splice, dim3(grid2(work, n)), dim3(256), 0, (cudaStream_t)stream,
                                            (const __nv_bfloat16*)X4, plan, wpost, bpost,
                                                                   fade, overlap_frames, overlap_samples, audio,
-                                                                  (int16_t*)pcm16);
+                                                                  (int16_t*)pcm16, nonfinite);
   if (le_ != cudaSuccess) return (int)le_;
   ITTS_RETURN_LAUNCH();
 }

@@ -22,7 +22,7 @@ from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
 from .frontend import Lexicon, default_lexicon, default_texts
-from .scheduler import CostModel, IterationReport, PipelineModules, SchedulerLoop, _wait_until
+from .scheduler import CostModel, IterationReport, PipelineModules, RequestCancelled, SchedulerLoop, _wait_until
 
 
 @dataclass(frozen=True)
@@ -76,6 +76,7 @@ class RequestTiming:
     samples: int = 0
     chunks: int = 0
     error: str | None = None
+    cancelled: bool = False              # cancelled by the server's shutdown (after the window)
     done: bool = False
 
     @property
@@ -187,6 +188,9 @@ def serve(modules: PipelineModules, cfg, trace: list[TimedRequest], *, warmup_it
                         rec.chunks += 1
                 except queue.Empty:
                     pass
+                except RequestCancelled:   # the loop stopped after the window: not a failure
+                    rec.cancelled = True
+                    rec.done = True
                 except Exception as exc:  # noqa: BLE001 -- recorded, reported by the caller
                     rec.error = str(exc)
                     rec.done = True

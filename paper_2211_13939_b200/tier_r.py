@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes
 import functools
+import sys
 import weakref
 
 import numpy as np
@@ -203,7 +204,7 @@ class TierREngine:
         self._last_dec = None
         self.poison_scratch = False          # debug: NaN-fill decoder scratch (eager path; True or a set of buffer names)
         self.bisect_dir: str | None = None   # with keep_last_decoder: shrink + dump failing decoder batches here
-        self.speculate = False           # precompute the next decoder call's item fields during V waits (off: see DESIGN §10)
+        self.speculate = True            # precompute the next decoder call's item fields during V waits
         self._spec_src = None            # continuing (state, features) of the last decoder call
         self._spec = None                # their precomputed plan fields (see _speculate_next_decoder)
         # f3: chunk-local Tacotron2 PostNet on the decoder's mel output (off: the reference's no-op)
@@ -225,7 +226,11 @@ class TierREngine:
         self._ev = [torch.cuda.Event() for _ in range(3)]
         self._dec_buckets: dict = {}
         self._pool: dict = {}
-        self._pin_out = torch.empty(1 << 22, dtype=torch.float32, pin_memory=True)  # audio D2H
+        self._pin_out = torch.empty(1 << 22, dtype=torch.float32, pin_memory=True)  # audio D2H (fallback)
+        self._nf_pin = torch.empty(1024, dtype=torch.int32, pin_memory=True)     # per-chunk non-finite counts
+        self._out_ring: list = [None] * 6    # pinned (tensor, ndarray) audio slots; chunks view them
+        self._out_next = 0
+        self.host_finite_check = False      # also scan the samples on the host (the device count is the guard)
         self._graph_warm = False
 
     PRECISIONS = ("parity", "bf16")
@@ -886,20 +891,31 @@ class TierREngine:
             with self._mark("vocoder", 2.0 * HIFIGAN_MACS_PER_FRAME * sum(Ts)):
                 x4 = self._hifigan(Ts, lay0, d_mplan)
             pcm = self._buf("pcm16", max(int(out_off[-1]), 1), torch.int16) if self.pcm16 else None
+            nonfinite = self._buf("voc_nonfinite", n, torch.int32)
             self._call("itts_r_post_splice", x4 if isinstance(x4, int) else x4.data_ptr(), d_pplan.data_ptr(), n, max(mt[4] for mt in metas),
                        self.wpost.data_ptr(), self.bpost, self.fade.data_ptr(), O, S, audio.data_ptr(),
-                       0 if pcm is None else pcm.data_ptr(), st)
+                       0 if pcm is None else pcm.data_ptr(), nonfinite.data_ptr(), st)
             if pcm is not None:
                 host_pcm = torch.empty(pcm.numel(), dtype=torch.int16, pin_memory=True)
                 host_pcm.copy_(pcm, non_blocking=True)
-            if self._pin_out.numel() < audio.numel():   # grow-only persistent D2H buffer
-                self._pin_out = torch.empty(int(audio.numel() * 1.5), dtype=torch.float32, pin_memory=True)
-            host = self._pin_out[:audio.numel()]
-            host.copy_(audio, non_blocking=True)
-        # result objects are built while the GPU works: the chunks are read-only views of `flat`,
-        # which receives the samples after the wait (the chunks own it: no pinned buffer escapes)
-        total = int(out_off[-1])
-        flat = np.empty(total, dtype=np.float32)
+            total = int(out_off[-1])
+            # D2H straight into a pinned ring slot whose earlier chunks are all gone; the new chunks
+            # are read-only views of it (no host copy).  No free slot (a client holding chunks of
+            # several iterations): the persistent buffer, copied out after the wait.
+            slot = self._out_slot(total)
+            if slot is not None:
+                host = slot[0][:total]
+            else:
+                if self._pin_out.numel() < total:   # grow-only persistent D2H buffer
+                    self._pin_out = torch.empty(int(total * 1.5), dtype=torch.float32, pin_memory=True)
+                host = self._pin_out[:total]
+            host.copy_(audio[:total], non_blocking=True)
+            if self._nf_pin.numel() < n:
+                self._nf_pin = torch.empty(2 * n, dtype=torch.int32, pin_memory=True)
+            nf_host = self._nf_pin[:n]
+            nf_host.copy_(nonfinite, non_blocking=True)
+        # result objects are built while the GPU works: the chunks are read-only views of `flat`
+        flat = slot[1][:total] if slot is not None else np.empty(total, dtype=np.float32)
         out = []
         for i, (req, dst, emitted) in enumerate(results):
             chunk = AudioChunk.trusted(flat[out_off[i]:out_off[i + 1]], emitted)
@@ -910,9 +926,10 @@ class TierREngine:
             done.record(self.stream)
             self.idle_hook(done.query)
         self.stream.synchronize()
-        self.d2h_bytes += 4 * total
-        np.copyto(flat, host.numpy()[:total])
-        if not np.isfinite(flat).all():
+        self.d2h_bytes += 4 * total + 4 * n
+        if slot is None:
+            np.copyto(flat, host.numpy())
+        if nf_host.numpy().any() or (self.host_finite_check and not np.isfinite(flat).all()):
             if self.diagnose:
                 self._diagnose_nonfinite(triples, flat, out_off)
             raise ValueError("array contains non-finite values")
@@ -922,6 +939,22 @@ class TierREngine:
                 object.__setattr__(chunk, "_pcm16", pcm_np[out_off[i]:out_off[i + 1]].astype("<i2").tobytes())
                 self.d2h_bytes += 2 * counts[i]
         return out
+
+    def _out_slot(self, total: int):
+        """A pinned audio slot for `total` samples no live chunk views (None: all in use)."""
+        ring = self._out_ring
+        for _ in range(len(ring)):
+            k = self._out_next
+            self._out_next = (k + 1) % len(ring)
+            if ring[k] is None or ring[k][0].numel() < total:
+                if ring[k] is not None and sys.getrefcount(ring[k][1]) > 2:
+                    continue   # too small AND still viewed: leave it to its chunks
+                t = torch.empty(max(int(total * 1.25), 1 << 20), dtype=torch.float32, pin_memory=True)
+                ring[k] = (t, t.numpy())
+                return ring[k]
+            if sys.getrefcount(ring[k][1]) == 2:   # only the ring (and the call) reference the array
+                return ring[k]
+        return None
 
     def _diagnose_nonfinite(self, triples, flat, out_off) -> None:
         """Failure path only: which inputs of the non-finite chunks are already non-finite."""

@@ -232,6 +232,32 @@ def test_native_vocoder_large_pool(engine):
         assert np.array_equal(batched[i][0].samples, solo.samples)
 
 
+def test_nonfinite_audio_is_caught_on_device(engine):
+    """The finite-audio guard (reference _frozen_array, domain.py:170-178) now counts non-finite
+    samples per chunk in the splice kernel: an overflowing mel chunk fails its batch (the
+    scheduler then isolates it per item) and a good chunk alone still passes."""
+    good = (VocoderState.initial(), MelChunk(np.zeros((32, 80))), False)
+    bad = (VocoderState.initial(), MelChunk(np.full((32, 80), 3e38)), False)
+    with pytest.raises(ValueError, match="non-finite"):
+        engine.vocoder_batch([good, bad])
+    (chunk, _), = engine.vocoder_batch([good])
+    assert np.isfinite(chunk.samples).all()
+
+
+def test_chunks_stay_valid_while_held(engine):
+    """Chunks are read-only views of pinned D2H slots; a slot is reused only once no chunk views
+    it, so chunks held across many later calls keep their samples."""
+    rng = np.random.default_rng(3)
+    held = []
+    for it in range(10):
+        triples = [(VocoderState.initial(), MelChunk(rng.uniform(-0.3, 0.3, (32, 80))), False) for _ in range(3)]
+        out = engine.vocoder_batch(triples)
+        held += [(c, c.samples.copy()) for c, _ in out]
+    for c, ref in held:
+        assert np.array_equal(c.samples, ref)
+        assert not c.samples.flags.writeable
+
+
 def test_serving_replay_matches_serialized_launches():
     """A deterministic serving replay (arrivals, stops, pooled batches) gives bit-identical chunks
     with the default launch configuration (MRF branches on 3 streams, decoder speculation) and a

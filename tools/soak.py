@@ -18,7 +18,7 @@ from paper_2211_13939_b200.modules import build_engine, modules_for  # noqa: E40
 ap = argparse.ArgumentParser()
 ap.add_argument("--qps", type=float, default=200)
 ap.add_argument("--seconds", type=float, default=60)
-ap.add_argument("--spec", action="store_true", help="decoder speculation on (engine default: off)")
+ap.add_argument("--no-spec", action="store_true", help="decoder speculation off (engine default: on)")
 ap.add_argument("--diag-rerun", action="store_true", help="re-run the last decoder call on a non-finite chunk")
 ap.add_argument("--bisect-dir", default=None, help="with --diag-rerun: shrink failing decoder batches, dump them here")
 ap.add_argument("--no-prefetch", action="store_true", help="no frontend prefetch in the vocoder wait")
@@ -32,7 +32,7 @@ args = ap.parse_args()
 cfg, lex = PipelineConfig(), default_lexicon()
 eng = build_engine(cfg, "r", "cuda:0")
 eng.prepare_graphs(max_batch=512)
-eng.speculate = args.spec
+eng.speculate = not args.no_spec
 eng.keep_last_decoder = args.diag_rerun
 eng.bisect_dir = args.bisect_dir
 eng.plan_staging = not args.no_staging
