@@ -560,13 +560,13 @@ struct AttSmem {
   // (tap 31 = 0), WL = the location conv composed with the location dense layer; both operands as
   // bf16 high / low parts in the UMMA 128B-swizzled K-major layout (A: 128 rows x 128 B, B: 32 x 128 B)
   __align__(1024) uint8_t wl[2][ATT * 128];
-  __align__(1024) uint8_t win[2][2][32 * 128];   // [pipeline buffer][hi / lo]
+  __align__(1024) uint8_t win[2][2][32 * 128];   // [half-CTA][hi / lo]
   float q[2][ATT], sv[ATT];
   float red[32];
-  float ered[NW][16];          // per-warp position partials of the energies (ATT-A)
+  float ered[2][4][32];        // [half][warp][position] partials of the energies (ATT-A)
   float scale[MAXCH];
   int tstart[MAXB + 1];        // prefix sum of chunks per item (ATT-A task list)
-  float wp[2][ACH + 2 * HALO + 2], wa[2][ACH + 2 * HALO + 2], e[ACH];
+  float wp[2][ACH + 2 * HALO + 2], wa[2][ACH + 2 * HALO + 2], e[2][32];
 };
 // Generic scratch in the ring (free outside the gate pipeline / attention staging): the gate fixup's
 // h values [32 x B/4] and PRE's last frame [8][80] + H1 [8][256] + gemv partials [8 warps][8][32]
@@ -618,64 +618,60 @@ __device__ __forceinline__ void att_prefetch(const DecArgs& a, int b, int ta, in
 // 128B-swizzled K-major UMMA tile element (row r, k < 64) of a [rows][64] bf16 tile
 __device__ __forceinline__ int swz128(int r, int k) { return r * 64 + ((((k >> 3) ^ (r & 7))) << 3) + (k & 7); }
 
-// ATT-A, software-pipelined over a CTA's run of (item, 32-position chunk) tasks.  Task i:
-//   load    the q partials (new item only) and the location window, into registers, issued before
-//           task i-1's energies so their latency hides behind them; stored to smem buffer i & 1;
-//   mma     WIN[i & 1] (rows t < 32: [wp[t .. t+30], 0, wa[t .. t+30], 0], bf16 hi / lo) built from
-//           the window; the location term D[128 dims][32 pos] = WL . WIN^T as one tcgen05 chain
-//           (x3 hi/lo products, fp32) into TMEM columns [32 (i & 1), +32) -- it runs during task
-//           i-1's context pass;
-//   energy  thread (dim a, position half h): v_a tanh(q_a + D[a][t] + pm[t][a]) for 16 positions,
-//           summed over the warp's 32 dims by a shuffle reduce-scatter (lane t % 16 keeps
-//           position t) and over the 4 warps of the half in warp order;
-//   softmax chunk max / exp / sum on one warp (lane = position);
-//   context thread d: dims d, d + 256 summed over the chunk's positions in order.
-// The pm / memory rows of task i stream into ring buffer i & 1 (bulk copies issued one task
-// ahead).  Every reduction order depends only on the chunk (batch transparency).
-struct AttNext {
-  float wpv, wav;       // window values w_c[ta - 15 + tid] of the next task
-  float qv[NGRP];       // its q partials (tid < 128, new item only)
-};
+// ATT-A: the CTA's contiguous run of (item, 32-position chunk) tasks is dealt alternately to its
+// two half-CTAs (4 warps each, own named barrier, ring buffer, mbarriers, TMEM columns and
+// operand tiles), so the latency chains of two chunks -- row / q / window loads, the MMA round
+// trip, the reductions -- overlap.  One task on half h:
+//   rows    the chunk's pm / memory rows -> ring half h (bulk copies, issued first);
+//   load    q (new item: the 32 unit-group partials, group order) and the location window;
+//   mma     WIN (rows t < 32: [wp[t .. t+30], 0, wa[t .. t+30], 0], bf16 hi / lo) built from the
+//           window; the location term D[128 dims][32 pos] = WL . WIN^T as one tcgen05 chain (x3
+//           hi/lo products, fp32) into TMEM columns [32 h, 32 h + 32);
+//   energy  thread (dim a): v_a tanh(q_a + D[a][t] + pm[t][a]) for the 32 positions, summed over
+//           the warp's 32 dims by a shuffle reduce-scatter (lane t keeps position t) and over the
+//           half's 4 warps in warp order;
+//   softmax chunk max / exp / sum on the half's first warp (lane = position);
+//   context thread d: dims d + 128 j summed over the chunk's positions in order.
+// Every reduction order depends only on the chunk (batch transparency).
+__device__ __forceinline__ void half_sync(int h) { asm volatile("bar.sync %0, 128;" ::"r"(3 + h) : "memory"); }
 
-__device__ __forceinline__ const float* att_wsrc(const DecArgs& a, int s, int b) {
-  const int64_t* p = a.plan + b * DPLAN;
-  return reinterpret_cast<const float*>(a.step0 + s == 0 ? p[3] : p[4]);
-}
-
-__device__ __forceinline__ void att_load(const DecArgs& a, int s, int b, int L, int ta, int n, bool load_q,
-                                         AttNext& r) {
-  const int tid = threadIdx.x;
-  if (load_q && tid < ATT) {
+__device__ __forceinline__ void att_task(const DecArgs& a, AttSmem& sm, GateSync& gsy, uint8_t* ring, int s, int h,
+                                         int b, int L, int ch, bool load_q, uint32_t& aph, uint32_t& mph,
+                                         unsigned long long* tr_t) {
+  const int tid = threadIdx.x & 127, lane = tid & 31, qd = tid >> 5;
+  const int ta = ch * 32, n = min(L, ta + 32) - ta;
+  auto mark = [&](int slot) {
+    if (tr_t) {
+      const unsigned long long t2 = gtimer();
+      a.trace[slot] += t2 - *tr_t;
+      *tr_t = t2;
+    }
+  };
+  uint8_t* stage = ring + h * ASTAGE;
+  if (tid == 0) att_prefetch(a, b, ta, ta + n, stage, &gsy.abar[h]);
+  if (load_q) {  // q = sum of the 32 unit-group partials, group order (kept for the item's next chunk)
+    float qv[NGRP];
 #pragma unroll
-    for (int z = 0; z < NGRP; ++z) r.qv[z] = ldf(a.Qp + ((int64_t)z * a.B + b) * ATT + tid);
-  }
-  const float* wsrc = att_wsrc(a, s, b);
-  const int t = ta - HALO + tid;
-  const bool in = tid < ACH + 2 * HALO + 2 && tid < n + 2 * HALO && t >= 0 && t < L;
-  r.wpv = in ? ldf(wsrc + t) : 0.f;
-  r.wav = in ? ldf(wsrc + L + t) : 0.f;
-}
-
-__device__ __forceinline__ void att_store(AttSmem& sm, int wb, int qb, bool load_q, const AttNext& r) {
-  const int tid = threadIdx.x;
-  if (load_q && tid < ATT) {  // q = sum of the 32 unit-group partials, group order
-    float qa = r.qv[0];
+    for (int z = 0; z < NGRP; ++z) qv[z] = ldf(a.Qp + ((int64_t)z * a.B + b) * ATT + tid);
+    float qa = qv[0];
 #pragma unroll
-    for (int z = 1; z < NGRP; ++z) qa += r.qv[z];
-    sm.q[qb][tid] = qa;
+    for (int z = 1; z < NGRP; ++z) qa += qv[z];
+    sm.q[h][tid] = qa;
   }
-  if (tid < ACH + 2 * HALO + 2) {
-    sm.wp[wb][tid] = r.wpv;   // zero past the chunk's taps: the WIN build reads only t < n rows,
-    sm.wa[wb][tid] = r.wav;   // but the buffer never holds another launch's bytes
+  if (tid < ACH + 2 * HALO + 2) {  // window w_c[ta - 15 + i]: zero outside [0, L) and past the chunk's taps
+    const int64_t* p = a.plan + b * DPLAN;
+    const float* wsrc = reinterpret_cast<const float*>(a.step0 + s == 0 ? p[3] : p[4]);
+    const int t = ta - HALO + tid;
+    const bool in = tid < n + 2 * HALO && t >= 0 && t < L;
+    sm.wp[h][tid] = in ? ldf(wsrc + t) : 0.f;
+    sm.wa[h][tid] = in ? ldf(wsrc + L + t) : 0.f;
   }
-}
-
-// WIN[wb] from the window buffer wb (all threads), then (thread 0) the location-term MMA chain.
-__device__ __forceinline__ void att_build_mma(AttSmem& sm, GateSync& gsy, int wb, int n) {
-  const int tid = threadIdx.x;
-  {
-    const int t = tid >> 3, j = tid & 7, cch = j >> 2;
-    const float* wv = cch ? sm.wa[wb] : sm.wp[wb];
+  half_sync(h);
+  mark(8);
+#pragma unroll
+  for (int r2 = 0; r2 < 2; ++r2) {  // WIN: thread -> (row t, 8-column group j), two per thread
+    const int idx = tid + 128 * r2, t = idx >> 3, j = idx & 7, cch = j >> 2;
+    const float* wv = cch ? sm.wa[h] : sm.wp[h];
     alignas(16) __nv_bfloat16 hi[8], lo[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -685,89 +681,84 @@ __device__ __forceinline__ void att_build_mma(AttSmem& sm, GateSync& gsy, int wb
       lo[e] = __float2bfloat16_rn(x - __bfloat162float(hi[e]));
     }
     const int o = swz128(t, 8 * j);
-    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(sm.win[wb][0]) + o) = *reinterpret_cast<const uint4*>(hi);
-    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(sm.win[wb][1]) + o) = *reinterpret_cast<const uint4*>(lo);
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(sm.win[h][0]) + o) = *reinterpret_cast<const uint4*>(hi);
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(sm.win[h][1]) + o) = *reinterpret_cast<const uint4*>(lo);
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncthreads();
+  half_sync(h);
   if (tid == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
     const uint64_t dwh = tcg::make_desc<128>(tcg::smem_u32(sm.wl[0])), dwl = tcg::make_desc<128>(tcg::smem_u32(sm.wl[1]));
-    const uint64_t dxh = tcg::make_desc<128>(tcg::smem_u32(sm.win[wb][0]));
-    const uint64_t dxl = tcg::make_desc<128>(tcg::smem_u32(sm.win[wb][1]));
-    const uint32_t d = gsy.tmem + 32 * wb;
+    const uint64_t dxh = tcg::make_desc<128>(tcg::smem_u32(sm.win[h][0]));
+    const uint64_t dxl = tcg::make_desc<128>(tcg::smem_u32(sm.win[h][1]));
+    const uint32_t d = gsy.tmem + 32 * h;
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(d, dwh + 2 * kk, dxh + 2 * kk, idesc, kk != 0);
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(d, dwh + 2 * kk, dxl + 2 * kk, idesc, 1);
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(d, dwl + 2 * kk, dxh + 2 * kk, idesc, 1);
-    tcg::umma_commit(&gsy.amma[wb]);
+    tcg::umma_commit(&gsy.amma[h]);
   }
-}
-
-// Energies of the task in pipeline buffer wb (q buffer qb, rows staged in `stage`) -> sm.ered.
-__device__ __forceinline__ void att_energy(AttSmem& sm, GateSync& gsy, int wb, int qb, int n, const float* sPm,
-                                           uint32_t& mph) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int qd = warp & 3, h = warp >> 2, ad = qd * 32 + lane;
-  tcg::mbar_wait(&gsy.amma[wb], mph);
-  mph ^= 1;
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  float x[16];
-  tcg::tmem_ld16(gsy.tmem + ((uint32_t)(qd * 32) << 16) + 32 * wb + 16 * h, x);
-  const float qa = sm.q[qb][ad], va = sm.sv[ad];
+  const float* sPm = reinterpret_cast<const float*>(stage);
+  tcg::mbar_wait(&gsy.abar[h], aph);   // the chunk's pm / memory rows
+  aph ^= 1;
+  mark(9);
+  {
+    const int ad = qd * 32 + lane;
+    tcg::mbar_wait(&gsy.amma[h], mph);
+    mph ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float x[32];
+    tcg::tmem_ld32(gsy.tmem + ((uint32_t)(qd * 32) << 16) + 32 * h, x);
+    const float qa = sm.q[h][ad], va = sm.sv[ad];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int t = 16 * h + i;
-    x[i] = t < n ? va * tanh_fast((qa + x[i]) + sPm[t * ATT + ad]) : 0.f;
+    for (int i = 0; i < 32; ++i) x[i] = i < n ? va * tanh_fast((qa + x[i]) + sPm[i * ATT + ad]) : 0.f;
+#pragma unroll
+    for (int st = 16; st >= 1; st >>= 1) {  // reduce-scatter: lane t ends with position t
+      const bool up = lane & st;
+#pragma unroll
+      for (int i = 0; i < st; ++i) {
+        const float send = up ? x[i] : x[i + st], keep = up ? x[i + st] : x[i];
+        x[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+      }
+    }
+    sm.ered[h][qd][lane] = x[0];
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
-#pragma unroll
-  for (int i = 0; i < 16; ++i) x[i] += __shfl_xor_sync(0xffffffffu, x[i], 16);
-#pragma unroll
-  for (int st = 8; st >= 1; st >>= 1) {
-    const bool up = lane & st;
-#pragma unroll
-    for (int i = 0; i < st; ++i) {
-      const float send = up ? x[i] : x[i + st], keep = up ? x[i + st] : x[i];
-      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+  half_sync(h);
+  mark(10);
+  if (qd == 0) {  // chunk softmax statistics: lane = position
+    const float e = ((sm.ered[h][0][lane] + sm.ered[h][1][lane]) + sm.ered[h][2][lane]) + sm.ered[h][3][lane];
+    const float M = itts::warp_max(lane < n ? e : -INFINITY);
+    const float xv = lane < n ? expf(e - M) : 0.f;
+    const float Ssum = itts::warp_sum(xv);
+    sm.e[h][lane] = xv;
+    if (lane < n) a.U[(int64_t)b * a.u_ld + ta + lane] = xv;
+    if (lane == 0) {
+      float* ap = a.AP + ((int64_t)b * MAXCH + ch) * (2 + EMB);
+      ap[0] = M;
+      ap[1] = Ssum;
     }
   }
-  if (lane < 16) sm.ered[warp][lane] = x[0];
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-
-// Chunk softmax statistics (warp 0; lane = position) -> U numerators, AP[0..1], sm.e.
-__device__ __forceinline__ void att_softmax(const DecArgs& a, AttSmem& sm, int b, int ch, int ta, int n) {
-  const int lane = threadIdx.x & 31;
-  const int h = lane >> 4, i = lane & 15;
-  const float e = ((sm.ered[4 * h][i] + sm.ered[4 * h + 1][i]) + sm.ered[4 * h + 2][i]) + sm.ered[4 * h + 3][i];
-  const float M = itts::warp_max(lane < n ? e : -INFINITY);
-  const float xv = lane < n ? expf(e - M) : 0.f;
-  const float Ssum = itts::warp_sum(xv);
-  sm.e[lane] = xv;
-  if (lane < n) a.U[(int64_t)b * a.u_ld + ta + lane] = xv;
-  if (lane == 0) {
+  half_sync(h);
+  mark(11);
+  {  // unnormalised context partial: thread -> dims tid + 128 j, positions in order
+    const float* sMem = sPm + n * ATT;
+    float c[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int t = 0; t < n; ++t) {
+      const float w = sm.e[h][t];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c[j] = fmaf(w, sMem[t * EMB + tid + 128 * j], c[j]);
+    }
     float* ap = a.AP + ((int64_t)b * MAXCH + ch) * (2 + EMB);
-    ap[0] = M;
-    ap[1] = Ssum;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ap[2 + tid + 128 * j] = c[j];
   }
-}
-
-// Unnormalised context partial: thread -> dims tid, tid + 256, positions in order.
-__device__ __forceinline__ void att_context(const DecArgs& a, const AttSmem& sm, int b, int ch, int n,
-                                            const float* sMem) {
-  const int tid = threadIdx.x;
-  float c0 = 0.f, c1 = 0.f;
-  for (int t = 0; t < n; ++t) {
-    const float w = sm.e[t];
-    c0 = fmaf(w, sMem[t * EMB + tid], c0);
-    c1 = fmaf(w, sMem[t * EMB + tid + NT], c1);
-  }
-  float* ap = a.AP + ((int64_t)b * MAXCH + ch) * (2 + EMB);
-  ap[2 + tid] = c0;
-  ap[2 + NT + tid] = c1;
+  half_sync(h);   // ring half / e / q reuse
+  mark(12);
+  if (tr_t) a.trace[13] += 1;
 }
 
 // ATT-B for item b: combine the chunks (max, sum, context partial; chunk order) -> context, W, W_acc.
@@ -1061,65 +1052,17 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();
     {
       const int ntask = sm.tstart[a.B];
-      // CTA c takes a contiguous run of tasks, so consecutive chunks of one item share its q
+      // CTA c takes a contiguous run of tasks (consecutive chunks of one item share its q), dealt
+      // alternately to its two half-CTAs
       const int t0 = (int)((int64_t)c * ntask / G), t1 = (int)((int64_t)(c + 1) * ntask / G);
-      const bool tr = a.trace && c == 0 && tid == 0;
-      unsigned long long tq = tr ? gtimer() : 0;
-      auto mark = [&](int slot) {
-        if (tr) {
-          const unsigned long long t2 = gtimer();
-          a.trace[slot] += t2 - tq;
-          tq = t2;
-        }
-      };
-      int bi = 0;  // item of the task being located (monotonic)
-      auto locate = [&](int task) {
+      const int h = tid >> 7;
+      unsigned long long tq = (a.trace && c == 0 && tid == 0) ? gtimer() : 0;
+      int bi = 0, bprev = -1;
+      for (int task = t0 + h; task < t1; task += 2) {
         while (sm.tstart[bi + 1] <= task) ++bi;
-        return bi;
-      };
-      if (t0 < t1) {
-        // prologue: task t0's rows (ring buffer 0), q and window (buffers 0), its MMA
-        int b = locate(t0);
-        int ta = (t0 - sm.tstart[b]) * chunk, n = min(pc.L[b], ta + chunk) - ta;
-        if (tid == 0) att_prefetch(a, b, ta, ta + n, ring, &gsy.abar[0]);
-        AttNext r;
-        att_load(a, gs, b, pc.L[b], ta, n, true, r);
-        att_store(sm, 0, 0, true, r);
-        __syncthreads();
-        att_build_mma(sm, gsy, 0, n);
-        int qb = 0;
-        for (int task = t0, i = 0; task < t1; ++task, ++i) {
-          const int buf = i & 1;
-          const int bc = b, tac = ta, nc = n, ch = task - sm.tstart[bc];
-          const bool more = task + 1 < t1;
-          bool new_q = false;
-          if (more) {  // task + 1: rows into the other ring buffer, q / window into registers
-            b = locate(task + 1);
-            ta = (task + 1 - sm.tstart[b]) * chunk;
-            n = min(pc.L[b], ta + chunk) - ta;
-            new_q = b != bc;
-            if (tid == 0) att_prefetch(a, b, ta, ta + n, ring + (buf ^ 1) * ASTAGE, &gsy.abar[buf ^ 1]);
-            att_load(a, gs, b, pc.L[b], ta, n, new_q, r);
-          }
-          mark(8);
-          const float* sPm = reinterpret_cast<const float*>(ring + buf * ASTAGE);
-          tcg::mbar_wait(&gsy.abar[buf], aphase[buf]);   // task's pm / memory rows
-          aphase[buf] ^= 1;
-          mark(9);
-          att_energy(sm, gsy, buf, qb, nc, sPm, mphase[buf]);
-          if (more) att_store(sm, buf ^ 1, new_q ? qb ^ 1 : qb, new_q, r);
-          __syncthreads();
-          mark(10);
-          if (tid < 32) att_softmax(a, sm, bc, ch, tac, nc);
-          if (more) att_build_mma(sm, gsy, buf ^ 1, n);   // ends in a __syncthreads (softmax visible)
-          else __syncthreads();
-          mark(11);
-          att_context(a, sm, bc, ch, nc, sPm + nc * ATT);
-          __syncthreads();   // ring buffer / e reuse
-          mark(12);
-          if (tr) a.trace[13] += 1;
-          if (new_q) qb ^= 1;
-        }
+        att_task(a, sm, gsy, ring, gs, h, bi, pc.L[bi], task - sm.tstart[bi], bi != bprev, aphase[h], mphase[h],
+                 (a.trace && c == 0 && tid == 0) ? &tq : nullptr);
+        bprev = bi;
       }
     }
     phase_end();
