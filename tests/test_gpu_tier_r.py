@@ -81,6 +81,19 @@ def test_encoder_matches_oracle(engine, weights, lexicon):
         assert st.frames_emitted == 0 and st.target_frames == 8 * fo.seq_len
 
 
+@pytest.mark.parametrize("n", [12, 40, 128])
+def test_pooled_encoder_is_bitwise_transparent(engine, lexicon, n):
+    """Each item's encoder memory in a pooled ragged batch (packed rows, shared convs, one BiLSTM
+    cluster per item) is the same bits as when it is encoded alone (batch transparency,
+    SPEC.md:232)."""
+    fos = [run_frontend(t, lexicon) for t in random_texts(lexicon, n, 100 + n, 20, 200)]
+    encs = engine.encoder_batch(fos)
+    pooled = {i: encs[i][0].rows.copy() for i in sorted({0, 1, n // 2, n - 1})}
+    for i, rows in pooled.items():
+        (enc, _), = engine.encoder_batch([fos[i]])
+        assert np.array_equal(enc.rows, rows), i
+
+
 def test_vocoder_chunks_match_oracle(engine, weights):
     rng = np.random.default_rng(3)
     for lens, last_short in (((32, 32, 8), False), ((16,), False), ((32, 2), True)):

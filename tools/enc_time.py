@@ -18,12 +18,13 @@ from paper_2211_13939_b200.tier_r import TierREngine  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--batches", default="1,3,8")
 ap.add_argument("--chars", type=int, default=200)
+ap.add_argument("--lo", type=int, default=None, help="ragged texts: U{lo..chars} characters")
 args = ap.parse_args()
 eng = TierREngine(PipelineConfig(), "cuda:0")
 lex = default_lexicon()
 for B in [int(x) for x in args.batches.split(",")]:
     rng = random.Random(B)
-    fos = [run_frontend(random_text(rng, args.chars, args.chars, lex), lex) for _ in range(B)]
+    fos = [run_frontend(random_text(rng, args.lo or args.chars, args.chars, lex), lex) for _ in range(B)]
     eng.encoder_batch(fos)
     ts = []
     for _ in range(5):
