@@ -762,7 +762,10 @@ __device__ __forceinline__ void att_task(const DecArgs& a, AttSmem& sm, GateSync
 }
 
 // ATT-B for item b: combine the chunks (max, sum, context partial; chunk order) -> context, W, W_acc.
-__device__ void att_combine(const DecArgs& a, AttSmem& sm, int s, int b, int chunk) {
+// Part `part` of `nparts`: context dims [part, part + 1) x 512 / nparts and attention positions
+// [part, part + 1) x ceil(L / nparts) (the chunk statistics are recomputed by every part); every
+// value is computed the same way for any nparts.
+__device__ void att_combine(const DecArgs& a, AttSmem& sm, int s, int b, int chunk, int part = 0, int nparts = 1) {
   const int tid = threadIdx.x;
   const int64_t* p = a.plan + b * DPLAN;
   const int L = (int)p[2];
@@ -779,7 +782,8 @@ __device__ void att_combine(const DecArgs& a, AttSmem& sm, int s, int b, int chu
   if (tid < nch) scale[tid] = ec / Z;
   __syncthreads();
   float* st = a.work + (int64_t)b * ROW;
-  for (int d = tid; d < EMB; d += NT) {
+  const int d0 = part * (EMB / nparts), d1 = d0 + EMB / nparts;
+  for (int d = d0 + tid; d < d1; d += NT) {
     float c = 0.f;
     int k = 0;
     for (; k + 4 <= nch; k += 4) {  // 4 partial loads in flight, summed in chunk order
@@ -794,7 +798,8 @@ __device__ void att_combine(const DecArgs& a, AttSmem& sm, int s, int b, int chu
     xb_store(a, b, CTX_OFF + d, c);
   }
   WFENCE();
-  for (int t = tid; t < L; t += NT) {
+  const int lp = (L + nparts - 1) / nparts, t1 = min(L, (part + 1) * lp);
+  for (int t = part * lp + tid; t < t1; t += NT) {
     const float w = ldf(a.U + (int64_t)b * a.u_ld + t) * scale[t / chunk];
     const float acc = ldf(wsrc + L + t);
     wdst[t] = w;
@@ -1073,18 +1078,22 @@ __global__ void __launch_bounds__(NT, 1)
         if (active(pc, b, gs)) att_combine(a, sm, gs, b, chunk);
       phase_end();
     } else {
-      // on every CTA but the context-column owners (split 0 of each gate group), before their GEMM
-      for (int b = 0; b < a.B; ++b) ctx_target += active(pc, b, gs) ? 1u : 0u;
+      // on every CTA but the context-column owners (split 0 of each gate group), before their
+      // GEMM; small batches split each item's combine into up to 4 parts so more CTAs share it
+      const int ncomb = 3 * (GEMM_CTAS / 4) + (G - GEMM_CTAS);
+      const int nparts = a.B * 4 <= ncomb ? 4 : a.B * 2 <= ncomb ? 2 : 1;
+      for (int b = 0; b < a.B; ++b) ctx_target += active(pc, b, gs) ? (unsigned)nparts : 0u;
       const bool owner = gemm_cta && (c & 3) == 0;
       if (!owner) {
         const int ci = gemm_cta ? (c >> 2) * 3 + (c & 3) - 1 : 3 * (GEMM_CTAS / 4) + (c - GEMM_CTAS);
-        const int ncomb = 3 * (GEMM_CTAS / 4) + (G - GEMM_CTAS);
         unsigned done = 0;
-        for (int b = ci; b < a.B; b += ncomb)
+        for (int task = ci; task < a.B * nparts; task += ncomb) {
+          const int b = task / nparts;
           if (active(pc, b, gs)) {
-            att_combine(a, sm, gs, b, chunk);  // ends with __syncthreads
+            att_combine(a, sm, gs, b, chunk, task % nparts, nparts);  // ends with __syncthreads
             ++done;
           }
+        }
         if (tid == 0 && done)
           asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.bar + 2 + NGRP), "r"(done) : "memory");
       }
