@@ -14,6 +14,10 @@
 // detected before any launch (so nothing is enqueued on failure).
 #include "incrtts_b200.h"
 
+// tier_r.cu: several row maps (as itts_r_rowmap) in one launch (vocoder call setup, voc_run.cu).
+int itts_r_rowmaps(int32_t count, const int64_t* const* plans, int32_t* const* outs, const int64_t* spans, int32_t n,
+                   void* stream);
+
 // tc_conv.cu: itts_conv1d_tc with a choice of act_out activation: 0 leaky ReLU (slope), 1 tanh
 // (PostNet), 2 GELU tanh form (BERT frontend).
 int conv1d_tc_impl(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, const void* w, int32_t n_total,

@@ -680,6 +680,25 @@ __global__ void k_rowmap(const int64_t* __restrict__ plan, int32_t* __restrict__
   row_out[p[0] + r] = (q >= 0 && q < p[1]) ? (int32_t)(p[3] + p[4] * q) : -1;
 }
 
+// Up to 9 row maps of one vocoder call in one launch (blockIdx.z = map); map k as k_rowmap with
+// its own plan rows, output buffer and span.
+struct RowMaps {
+  const int64_t* plan[9];
+  int32_t* out[9];
+  int64_t span[9];
+};
+__global__ void k_rowmaps(const __grid_constant__ RowMaps m) {
+  itts::pdl_trigger();
+  itts::pdl_wait();
+  const int k = blockIdx.z;
+  const int64_t r = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (r >= m.span[k]) return;
+  const int64_t* p = m.plan[k] + blockIdx.y * 5;
+  if (r >= 2 * p[2] + p[1]) return;
+  const int64_t q = r - p[2];
+  m.out[k][p[0] + r] = (q >= 0 && q < p[1]) ? (int32_t)(p[3] + p[4] * q) : -1;
+}
+
 // zero plan[i] = {base, rows, halo}: zero [base, base+halo) and [base+halo+rows, base+2halo+rows).
 __global__ void k_zero_halo(const int64_t* __restrict__ plan, __nv_bfloat16* __restrict__ X, int C) {
   itts::pdl_trigger();
@@ -1027,6 +1046,25 @@ ITTS_API int itts_r_mel_assemble(const int64_t* plan, int32_t n, int64_t max_row
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
   const cudaError_t le_ = itts::launch_pdl(k_mel_assemble, dim3(grid2(max_rows * ld, n)), dim3(256), 0, (cudaStream_t)stream,
                                            plan, (__nv_bfloat16*)X0, ld);
+  if (le_ != cudaSuccess) return (int)le_;
+  ITTS_RETURN_LAUNCH();
+}
+
+// `count` (<= 9) row maps in one launch: plans[k] (n items x 5, as itts_r_rowmap), outs[k], spans[k].
+int itts_r_rowmaps(int32_t count, const int64_t* const* plans, int32_t* const* outs, const int64_t* spans, int32_t n,
+                   void* stream) {
+  if (n <= 0 || count <= 0) return (n == 0 || count == 0) ? ITTS_OK : ITTS_EINVAL;
+  if (count > 9) return ITTS_EINVAL;
+  RowMaps m{};
+  int64_t max_span = 1;
+  for (int k = 0; k < count; ++k) {
+    m.plan[k] = plans[k];
+    m.out[k] = outs[k];
+    m.span[k] = spans[k];
+    max_span = max(max_span, spans[k]);
+  }
+  const dim3 grid((unsigned)((max_span + 255) / 256), (unsigned)n, (unsigned)count);
+  const cudaError_t le_ = itts::launch_pdl(k_rowmaps, grid, dim3(256), 0, (cudaStream_t)stream, m);
   if (le_ != cudaSuccess) return (int)le_;
   ITTS_RETURN_LAUNCH();
 }

@@ -236,10 +236,8 @@ struct Vocoder {
     plan_pending = true;
 
     int32_t* rm[9];
-    for (int k = 0; k < 9; ++k) {
-      rm[k] = rowmaps.p + rm_off[k];
-      if ((st = itts_r_rowmap(rm_plan[k], n, rm_span[k], rm[k], stream))) return FAIL_AT(st);
-    }
+    for (int k = 0; k < 9; ++k) rm[k] = rowmaps.p + rm_off[k];
+    if ((st = itts_r_rowmaps(9, rm_plan, rm, rm_span, n, stream))) return FAIL_AT(st);   // one launch
     // spliced mel -> conv_pre -> lrelu(0.1)
     if ((e = cudaMemsetAsync(x0.p, 0, (size_t)lay[0].total * 128 * sizeof(uint16_t), stream)) != cudaSuccess)
       return FAIL_AT((int)e);
