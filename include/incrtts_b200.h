@@ -186,10 +186,12 @@ int itts_r_encode(const void* pack, int64_t total, int32_t n, int64_t max_len, i
  * bf16 operands against [Wh | Wh | Wl] weights (Wh.Xh + Wh.Xl + Wl.Xh, fp32 accumulation), fp32
  * activations between layers.  weights3 = the itts_r_encode table with entries 4, 6, 8 (convs,
  * [5][512][1536]) and 10 (input projection, [1][2048][1536]) replaced; x3 bf16 [rows][1536],
- * f32 fp32 [rows][512] scratch.  Replaces the same reference functions as itts_r_encode. */
+ * f32 fp32 [rows][512] scratch.  Replaces the same reference functions as itts_r_encode.
+ * parts = 3, or 2 when the weights are exact in bf16: entries [Wh | Wh] ([.][.][1024]) against the
+ * first two operand thirds [hi | lo] (Wh.Xh + Wh.Xl). */
 int itts_r_encode_split(const void* pack, int64_t total, int32_t n, int64_t max_len, int64_t rows,
                         int64_t max_span, const int64_t* weights3, int32_t conv_taps, void* x3, float* f32,
-                        float* pre, int32_t* rowmap, void* stream);
+                        float* pre, int32_t* rowmap, int32_t parts, void* stream);
 int itts_r_pmem(const int64_t* plan, int32_t n, int64_t max_len, const float* WmT, void* stream);
 
 /* K7 helpers around the HiFi-GAN conv stack (replaces vocode_batch,

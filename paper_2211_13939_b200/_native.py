@@ -49,7 +49,7 @@ SIGNATURES: dict[str, list] = {
     "itts_r_rowmap": [_p, _i32, _i64, _p, _p],
     "itts_r_zero_halo": [_p, _i32, _i64, _p, _i32, _p],
     "itts_r_encode": [_p, _i64, _i32, _i64, _i64, _i64, _p, _i32, _p, _p, _p, _p, _p],
-    "itts_r_encode_split": [_p, _i64, _i32, _i64, _i64, _i64, _p, _i32, _p, _p, _p, _p, _p],
+    "itts_r_encode_split": [_p, _i64, _i32, _i64, _i64, _i64, _p, _i32, _p, _p, _p, _p, _i32, _p],
     "itts_bert_prosody": [_p, _p, _p, _i32, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "itts_r_postnet": [_p, _i32, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _p],
     "itts_r_mrf_combine": [_p, _p, _p, _i64, ctypes.c_float, _p, _p],

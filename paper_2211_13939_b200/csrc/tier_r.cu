@@ -940,8 +940,10 @@ ITTS_API int itts_r_encode(const void* pack, int64_t total, int32_t n, int64_t m
 // (f32 [rows][512]), x3 = bf16 [rows][1536] operand buffer.
 ITTS_API int itts_r_encode_split(const void* pack, int64_t total, int32_t n, int64_t max_len, int64_t rows,
                                  int64_t max_span, const int64_t* weights3, int32_t conv_taps, void* x3, float* f32,
-                                 float* pre, int32_t* rowmap, void* stream) {
+                                 float* pre, int32_t* rowmap, int32_t parts, void* stream) {
   if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
+  if (parts != 2 && parts != 3) return ITTS_EINVAL;
+  const int32_t kin = parts * EMB;   // [hi | lo (| hi)] columns of the [rows][1536] operand
   if (conv_taps < 1 || conv_taps > 15 || !pack || !weights3 || !x3 || !f32 || !pre || !rowmap) return ITTS_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   const int32_t* tok4 = static_cast<const int32_t*>(pack);
@@ -963,7 +965,7 @@ ITTS_API int itts_r_encode_split(const void* pack, int64_t total, int32_t n, int
   int32_t offs[16];
   for (int j = 0; j < conv_taps; ++j) offs[j] = j - (conv_taps - 1) / 2;
   for (int i = 0; i < 3; ++i) {
-    if ((r = itts_conv1d_tc(x3, rows, 3 * EMB, 3 * EMB, W(4 + 2 * i), EMB, conv_taps, offs, (const float*)W(5 + 2 * i),
+    if ((r = itts_conv1d_tc(x3, rows, kin, 3 * EMB, W(4 + 2 * i), EMB, conv_taps, offs, (const float*)W(5 + 2 * i),
                             EMB, rowmap, nullptr, 1.0f, f32, 1, nullptr, 0, nullptr, 0.0f, 0, 0, stream)))
       return r;
     if ((e = itts::launch_pdl(k_split3, g2, dim3(256), 0, st, (const float*)f32, plan, 1, (__nv_bfloat16*)x3)) !=
@@ -971,7 +973,7 @@ ITTS_API int itts_r_encode_split(const void* pack, int64_t total, int32_t n, int
       return (int)e;
   }
   const int32_t off0 = 0;
-  if ((r = itts_conv1d_tc(x3, rows, 3 * EMB, 3 * EMB, W(10), 8 * EH, 1, &off0, (const float*)W(11), 8 * EH, rowmap,
+  if ((r = itts_conv1d_tc(x3, rows, kin, 3 * EMB, W(10), 8 * EH, 1, &off0, (const float*)W(11), 8 * EH, rowmap,
                           nullptr, 1.0f, pre, 1, nullptr, 0, nullptr, 1.0f, 1, 128, stream)))
     return r;
   if ((r = itts_r_bilstm(pre, plan, n, (const float*)W(12), stream))) return r;

@@ -277,12 +277,16 @@ class TierREngine:
                                       w["enc.lstm_bwd.b_ih"] + w["enc.lstm_bwd.b_hh"]])))
         self.enc_whhT = f32(torch.stack([w["enc.lstm_fwd.w_hh"].T, w["enc.lstm_bwd.w_hh"].T]))  # [2][256][1024]
 
-        def split3(t):   # fp32 [k][C_out][C_in] -> bf16 [k][C_out][3 C_in] = [Wh | Wh | Wl]
+        # fp32 [k][C_out][C_in] -> bf16 [k][C_out][3 C_in] = [Wh | Wh | Wl], or [Wh | Wh] when every
+        # encoder weight is exact in bf16 (Wl = 0: two products instead of three)
+        enc_src = [f32(w[f"enc.conv{i}.w"]).permute(2, 0, 1) for i in range(3)] + [wih.to(d).float()[None]]
+        self.enc_parts = 2 if all(bool((t.to(torch.bfloat16).float() == t).all()) for t in enc_src) else 3
+
+        def split(t):
             hi = t.to(torch.bfloat16)
             lo = (t - hi.float()).to(torch.bfloat16)
-            return torch.cat([hi, hi, lo], 2).contiguous()
-        self._enc_split_w = [split3(f32(w[f"enc.conv{i}.w"]).permute(2, 0, 1)) for i in range(3)]
-        self._enc_split_w.append(split3(wih.to(d).float()[None]))
+            return torch.cat([hi, hi] + ([lo] if self.enc_parts == 3 else []), 2).contiguous()
+        self._enc_split_w = [split(t) for t in enc_src]
         self.WmT = f32(w["att.memory_layer"].T)                                          # [512][128]
         # decoder
         self.W0T, self.W1T = f32(w["prenet.0"].T), f32(w["prenet.1"].T)
@@ -564,7 +568,7 @@ class TierREngine:
                     f32 = self._buf("enc_f32", lay.total * W.EMB, torch.float32)
                     self._call("itts_r_encode_split", d_pack.data_ptr(), total, n, max_len, lay.total, span,
                                self._enc_ptrs3, ENC_TAPS, x3.data_ptr(), f32.data_ptr(), pre.data_ptr(),
-                               rm.data_ptr(), self._st())
+                               rm.data_ptr(), self.enc_parts, self._st())
                     self.launches += 13  # embed, 4 splits, row map, 3 convs, input projection, BiLSTM, memory, zero
                 else:
                     xa = self._buf("enc_xa", lay.total * W.EMB)
