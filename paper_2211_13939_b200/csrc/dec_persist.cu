@@ -100,6 +100,9 @@ constexpr int HALO = (KLOC - 1) / 2;
 __device__ __forceinline__ int att_off(int bank) { return 768 + bank * 2048; }
 __device__ __forceinline__ int dec_off(int bank) { return 1792 + bank * 2048; }
 __device__ __forceinline__ float sigm(float x) { return 1.0f / (1.0f + expf(-x)); }
+// LSTM cell nonlinearities with one ex2 + one fast reciprocal each (relative error ~1e-7, the fp32
+// rounding level; the accurate expf / tanhf / IEEE division cost ~5x the instructions)
+__device__ __forceinline__ float sigm_fast(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 // tanh via one exp2 and one reciprocal: absolute error ~1e-7 (the energies only sum it)
 __device__ __forceinline__ float tanh_fast(float x) { return 1.0f - __fdividef(2.0f, 1.0f + __expf(2.0f * x)); }
 
@@ -501,8 +504,8 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
         const int b = ks + KSPLIT * (e >> 5), ul = e & 31, j = ug * 32 + ul;
         float hn = 0.f;
         if (live[z]) {
-          const float cn = sigm(gs4[z].y) * cold[z] + sigm(gs4[z].x) * tanhf(gs4[z].z);
-          hn = sigm(gs4[z].w) * tanhf(cn);
+          const float cn = sigm_fast(gs4[z].y) * cold[z] + sigm_fast(gs4[z].x) * tanh_fast(gs4[z].z);
+          hn = sigm_fast(gs4[z].w) * tanh_fast(cn);
           float* st = a.work + (int64_t)b * ROW;
           st[c_off + j] = cn;
           st[h_off + j] = hn;
