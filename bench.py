@@ -446,9 +446,10 @@ def run_ours(args) -> None:
             "frac": round(dec_gbs / peaks["hbm_gbs"], 4) if dec_gbs else None,
             "traffic": traffic.get("k_dec_persist_dram_bytes_per_launch"),
             "peak_source": peaks["source"] + " copy bandwidth",
-            "algorithmic": "per step: gate + GEMV weights (36.7 MB bf16 / 73 MB in the split-bf16 parity mode) + per "
-                           "item 20 KB state + L x 2.5 KB memory/processed memory; achieved = those bytes / CUDA-event "
-                           "time of the decoder call on the engine stream",
+            "algorithmic": "per step: gate + GEMV weights (36.7 MB: bf16, also in the parity mode, whose bf16-grid "
+                           "weights need no low parts; 73 MB for off-grid weights) + per item 20 KB state + L x 2.5 KB "
+                           "memory/processed memory; achieved = those bytes / CUDA-event time of the decoder call on "
+                           "the engine stream",
             "traffic_note": traffic.get("note")}
         line["roofline_vocoder"] = {
             "kernel": "HiFi-GAN V1 chunk vocoder (k_resblock_tc fused MRF layers + k_conv_tc)", "bound": "tensor",
