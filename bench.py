@@ -515,6 +515,38 @@ def side_configs(mods, cfg, lex, args) -> dict:
     if hasattr(mods, "decoder_steps"):
         out["step_admission"] = step_admission_compare(mods, cfg, lex, args)
         log("step-granular admission done")
+    eng = getattr(mods, "engine", None)
+    if eng is not None and hasattr(eng, "set_precision"):
+        out["precision_modes"] = precision_compare(mods, cfg, lex, args)
+        log("precision modes done")
+    return out
+
+
+def precision_compare(mods, cfg, lex, args) -> dict:
+    """north_star: "any bf16 mode reported separately" -- the same 100 QPS Poisson trace with the
+    parity arithmetic (the headline) and with single bf16 gate products, 10 s windows each, plus
+    each mode's decoder device time per iteration."""
+    from paper_2211_13939_b200.harness import poisson_trace, serve
+    eng = mods.engine
+    out, mode0 = {}, eng.precision
+    try:
+        for mode in ("parity", "bf16"):
+            eng.set_precision(mode)
+            eng.prepare_graphs(max_batch=512)
+            eng.timers = []
+            run = serve(mods, cfg, poisson_trace(args.qps, 3600.0, seed=args.seed + 66, lexicon=lex), warmup_iters=3,
+                        warmup_seconds=2.0, timed_iters=None, timed_seconds=10.0, drain_seconds=2.0)
+            import torch
+            torch.cuda.synchronize()
+            dec = [e0.elapsed_time(e1) for kind, e0, e1, _ in eng.timers if kind == "decoder"]
+            eng.timers = None
+            st = _window_stats(run)
+            out[mode] = {"p50_ms": st["p50"], "p99_ms": st["p99"], "requests": st["requests"], "failed": st["failed"],
+                         "decoder_ms_per_call": round(sum(dec) / max(len(dec), 1), 3),
+                         "label": eng.precision_label()}
+    finally:
+        eng.set_precision(mode0)
+        eng.prepare_graphs(max_batch=512)
     return out
 
 
