@@ -228,6 +228,11 @@ int itts_r_mrf_combine(const void* y0, const void* y1, const void* y2, int64_t n
  * pcm16_encode (src/vocoder.py:146-149), produced in the same pass.
  * nonfinite (optional): int32 [n], zeroed here, item i's count of non-finite emitted samples
  * (the finite-audio guard of AudioChunk, domain.py:_frozen_array, without a host scan). */
+/* f1 wire format: per chunk i, base64 (RFC 4648, '=' padded) of the little-endian bytes of
+ * pcm16[plan[3i] .. plan[3i] + plan[3i+1]) into out + plan[3i+2] (4 * ceil(2 count / 3) chars):
+ * the reference server's encode_samples (src/server.py:78-79) on device. */
+int itts_r_pcm16_b64(const void* pcm16, const int64_t* plan, int32_t n, int64_t max_samples, void* out,
+                     void* stream);
 int itts_r_post_splice(const void* X4, const int64_t* plan, int32_t n, int64_t max_g, const float* wpost,
                        float bpost, const float* fade, int32_t overlap_frames, int32_t overlap_samples,
                        float* audio, void* pcm16, int32_t* nonfinite, void* stream);

@@ -57,6 +57,7 @@ SIGNATURES: dict[str, list] = {
     "itts_r_voc_reserve": [_p, _i32, _i32, _p],
     "itts_r_voc_run": [_p, _i32, _p, _p, _i32, _p, _p],
     "itts_r_voc_destroy": [_p],
+    "itts_r_pcm16_b64": [_p, _p, _i32, _i64, _p, _p],
     "itts_r_post_splice": [_p, _p, _i32, _i64, _p, ctypes.c_float, _p, _i32, _i32, _p, _p, _p, _p],
 }
 

@@ -781,6 +781,27 @@ __global__ void __launch_bounds__(256) k_post_splice(const __nv_bfloat16* __rest
   }
 }
 
+// f1 wire format: base64 of each chunk's little-endian PCM16 bytes (the reference server's
+// encode_samples, src/server.py:78-79 + pcm16_encode, src/vocoder.py:146-149).  plan[i] =
+// {first sample, sample count, first output char}; thread = one 3-byte group -> 4 ASCII chars,
+// '=' padding at the chunk's end.
+__global__ void k_pcm16_b64(const int16_t* __restrict__ pcm, const int64_t* __restrict__ plan, char* __restrict__ out) {
+  const int64_t* p = plan + blockIdx.y * 3;
+  const int64_t nbytes = 2 * p[1];
+  const int64_t grp = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (3 * grp >= nbytes) return;
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(pcm + p[0]);
+  const int64_t b = 3 * grp;
+  const int nb = (int)min((int64_t)3, nbytes - b);
+  const uint32_t v = ((uint32_t)src[b] << 16) | (nb > 1 ? (uint32_t)src[b + 1] << 8 : 0u) | (nb > 2 ? src[b + 2] : 0u);
+  const char* tab = "ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz0123456789+/";
+  char* o = out + p[2] + 4 * grp;
+  o[0] = tab[(v >> 18) & 63];
+  o[1] = tab[(v >> 12) & 63];
+  o[2] = nb > 1 ? tab[(v >> 6) & 63] : '=';
+  o[3] = nb > 2 ? tab[v & 63] : '=';
+}
+
 dim3 grid2(int64_t work, int n) { return dim3((unsigned)((work + 255) / 256), (unsigned)n); }
 
 }  // namespace
@@ -1126,6 +1147,16 @@ ITTS_API int itts_r_zero_halo(const int64_t* plan, int32_t n, int64_t max_halo, 
   const cudaError_t le_ = itts::launch_pdl(k_zero_halo, dim3(grid2(2 * max_halo * C, n)), dim3(256), 0, (cudaStream_t)stream,
                                            plan, (__nv_bfloat16*)X, C);
   if (le_ != cudaSuccess) return (int)le_;
+  ITTS_RETURN_LAUNCH();
+}
+
+ITTS_API int itts_r_pcm16_b64(const void* pcm16, const int64_t* plan, int32_t n, int64_t max_samples, void* out,
+                              void* stream) {
+  if (n <= 0) return n == 0 ? ITTS_OK : ITTS_EINVAL;
+  if (!pcm16 || !plan || !out) return ITTS_EINVAL;
+  const int64_t groups = (2 * max_samples + 2) / 3;
+  k_pcm16_b64<<<grid2(max(groups, (int64_t)1), n), 256, 0, (cudaStream_t)stream>>>((const int16_t*)pcm16, plan,
+                                                                                  (char*)out);
   ITTS_RETURN_LAUNCH();
 }
 

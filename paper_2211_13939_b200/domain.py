@@ -195,3 +195,13 @@ class AudioChunk:
             return pre
         from .audio import pcm16_encode
         return pcm16_encode(self.samples)
+
+    def wire_samples(self) -> str:
+        """The reference server's ``"samples"`` field of a chunk frame: base64 of the 16-bit PCM
+        (``encode_samples``, ``src/server.py:78-79``).  GPU modules built with ``wire_b64=True``
+        produce it on device; otherwise it is computed here."""
+        pre = self.__dict__.get("_b64")
+        if pre is not None:
+            return pre
+        import base64
+        return base64.b64encode(self.pcm16()).decode("ascii")

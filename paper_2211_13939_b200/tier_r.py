@@ -189,6 +189,7 @@ class TierREngine:
         # mel, north_star's parity mode); "bf16" = single bf16 products (reported separately)
         self.precision = "parity"
         self.pcm16 = False               # also produce 16-bit PCM on device in the splice pass (f1)
+        self.wire_b64 = False            # and its base64 wire text (server.encode_samples) on device (f1)
         self.mrf_streams = True          # run the 3 MRF branches of a stage on 3 streams (fused path)
         self.native_vocoder = True       # issue the fused HiFi-GAN stack from C++ (voc_run.cu)
         self.native_encoder = True       # issue the encoder launch sequence from C++ (itts_r_encode)
@@ -894,14 +895,23 @@ class TierREngine:
             audio = self._buf("audio", max(int(out_off[-1]), 1), torch.float32)
             with self._mark("vocoder", 2.0 * HIFIGAN_MACS_PER_FRAME * sum(Ts)):
                 x4 = self._hifigan(Ts, lay0, d_mplan)
-            pcm = self._buf("pcm16", max(int(out_off[-1]), 1), torch.int16) if self.pcm16 else None
+            want_pcm = self.pcm16 or self.wire_b64
+            pcm = self._buf("pcm16", max(int(out_off[-1]), 1), torch.int16) if want_pcm else None
             nonfinite = self._buf("voc_nonfinite", n, torch.int32)
             self._call("itts_r_post_splice", x4 if isinstance(x4, int) else x4.data_ptr(), d_pplan.data_ptr(), n, max(mt[4] for mt in metas),
                        self.wpost.data_ptr(), self.bpost, self.fade.data_ptr(), O, S, audio.data_ptr(),
                        0 if pcm is None else pcm.data_ptr(), nonfinite.data_ptr(), st)
-            if pcm is not None:
+            if pcm is not None and self.pcm16:
                 host_pcm = torch.empty(pcm.numel(), dtype=torch.int16, pin_memory=True)
                 host_pcm.copy_(pcm, non_blocking=True)
+            if self.wire_b64:   # base64 text of every chunk's PCM16, one kernel + one D2H
+                b64_len = 4 * ((2 * np.asarray(counts, np.int64) + 2) // 3)
+                b64_off = np.concatenate([[0], np.cumsum(b64_len)]).astype(np.int64)
+                bplan = self._up(np.stack([out_off[:-1], np.asarray(counts, np.int64), b64_off[:-1]], 1))
+                b64 = self._buf("b64", max(int(b64_off[-1]), 1), torch.uint8)
+                self._call("itts_r_pcm16_b64", pcm.data_ptr(), bplan.data_ptr(), n, max(counts), b64.data_ptr(), st)
+                host_b64 = torch.empty(max(int(b64_off[-1]), 1), dtype=torch.uint8, pin_memory=True)
+                host_b64.copy_(b64[:host_b64.numel()], non_blocking=True)
             total = int(out_off[-1])
             # D2H straight into a pinned ring slot whose earlier chunks are all gone; the new chunks
             # are read-only views of it (no host copy).  No free slot (a client holding chunks of
@@ -937,6 +947,11 @@ class TierREngine:
             if self.diagnose:
                 self._diagnose_nonfinite(triples, flat, out_off)
             raise ValueError("array contains non-finite values")
+        if self.wire_b64:
+            raw = host_b64.numpy().tobytes()
+            for i, (chunk, _) in enumerate(out):
+                object.__setattr__(chunk, "_b64", raw[b64_off[i]:b64_off[i + 1]].decode("ascii"))
+            self.d2h_bytes += int(b64_off[-1])
         if self.pcm16:
             pcm_np = host_pcm.numpy()
             for i, (chunk, _) in enumerate(out):

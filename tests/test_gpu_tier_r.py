@@ -212,6 +212,33 @@ def test_device_pcm16_matches_reference_encoding(engine, lexicon):
         engine.pcm16 = False
 
 
+def test_device_wire_base64_matches_reference_server(engine, lexicon):
+    """f1 wire format: the base64 text of each chunk's PCM16, produced on device, equals the
+    reference server's encode_samples (src/server.py:78-79) of the float chunk -- for ragged
+    chunk lengths, including the final short chunks (all three '=' padding cases occur)."""
+    import base64
+
+    from paper_2211_13939_b200.audio import pcm16_encode
+    engine.wire_b64 = True
+    pads = set()
+    try:
+        fos = [run_frontend(t, lexicon) for t in random_texts(lexicon, 5, 12, 3, 40)]
+        encs = engine.encoder_batch(fos)
+        live = [(enc, st, VocoderState.initial()) for enc, st in encs]
+        while live:
+            res = engine.decoder_batch([(st, enc) for enc, st, _ in live])
+            outs = engine.vocoder_batch([(vs, r.mel, r.stop) for (_, _, vs), r in zip(live, res)])
+            for chunk, _ in outs:
+                assert "_b64" in chunk.__dict__
+                want = base64.b64encode(pcm16_encode(chunk.samples)).decode("ascii")
+                assert chunk.wire_samples() == want
+                pads.add((2 * chunk.sample_count) % 3)
+            live = [(enc, r.state, vs) for (enc, _, _), r, (_, vs) in zip(live, res, outs) if not r.stop]
+    finally:
+        engine.wire_b64 = False
+    assert len(pads) >= 2, pads
+
+
 @pytest.mark.parametrize("sizes", [(1,), (5, 3, 40), (24,)])
 def test_native_vocoder_sequence_equals_python_launches(engine, sizes):
     """voc_run.cu (C++ launch sequence, 1 or 3 streams) == the per-layer Python launch loop, bit-exact."""
