@@ -12,8 +12,9 @@
 //   ATT    gates = [p|ctx|att_h] . Wa^T on the tensor cores (tcgen05, weights as M), 4-way
 //          K-split per 32-unit group; the LSTM cell is the fixup epilogue, which also emits the
 //          group's query partial q_g = Wq[:, group] . att_h[group]  (no separate query phase)
-//   ATT-A  per (item, position chunk): q = sum of the 32 group partials, location features,
-//          energies, chunk max, exp, chunk sum, unnormalised context partial
+//   ATT-A  per (item, 32-position chunk), two chunks at a time per CTA (half-CTA streams): q = sum
+//          of the 32 group partials, location features as one tcgen05 MMA chain, energies,
+//          chunk max, exp, chunk sum, unnormalised context partial
 //   ATT-B  per item: combine chunks (max / rescale / sum, chunk order) -> context, W, W_acc
 //   DEC    gates = [ctx|att_h|dec_h] . Wd^T + cell (as ATT); the fixup emits the group's
 //          mel/gate projection partial of dec_h while the CTAs without a gate group project the
@@ -42,9 +43,6 @@
 #ifndef DEC_MERGE_B
 #define DEC_MERGE_B 96
 #endif
-#ifndef DEC_ADAPTIVE_CHUNK
-#define DEC_ADAPTIVE_CHUNK 0  // 1: batch-dependent chunk sizes (not batch-invariant; A/B only)
-#endif
 #ifndef DEC_WFENCE
 #define DEC_WFENCE 0
 #endif
@@ -59,7 +57,7 @@
 
 namespace {
 
-constexpr int NMEL = 80, EMB = 512, HID = 1024, PRE = 256, ATT = 128, NF = 32, KLOC = 31;
+constexpr int NMEL = 80, EMB = 512, HID = 1024, PRE = 256, ATT = 128, KLOC = 31;
 constexpr int P_OFF = 0, CTX_OFF = 256, ATTH_OFF = 768, DECH_OFF = 1792, ATTC_OFF = 2816, DECC_OFF = 3840,
               LAST_OFF = 4864, ROW = 4944;
 constexpr int XB2 = 4864;        // bf16 mirror row: [p | ctx | att_h b0 | dec_h b0 | att_h b1 | dec_h b1]
@@ -94,12 +92,10 @@ constexpr int ACH = 64;          // max positions per attention chunk (pm + memo
 // at most one chunk): chunks up to 64 positions in one 160 KB buffer.  Several rounds: 32-position
 // chunks double-buffered (the next chunk streams in while this one computes).
 constexpr uint32_t ASTAGE = 32 * (ATT + EMB) * 4;
-constexpr int LT = 128;          // positions per location-feature tile
 constexpr int HALO = (KLOC - 1) / 2;
 
 __device__ __forceinline__ int att_off(int bank) { return 768 + bank * 2048; }
 __device__ __forceinline__ int dec_off(int bank) { return 1792 + bank * 2048; }
-__device__ __forceinline__ float sigm(float x) { return 1.0f / (1.0f + expf(-x)); }
 // LSTM cell nonlinearities with one ex2 + one fast reciprocal each (relative error ~1e-7, the fp32
 // rounding level; the accurate expf / tanhf / IEEE division cost ~5x the instructions)
 __device__ __forceinline__ float sigm_fast(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
@@ -157,15 +153,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 // ------------------------------------------------------------------ grid barrier
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& gen) {
   __syncthreads();
   if (threadIdx.x == 0) {  // arrive (release) on one counter, spin (acquire) until all CTAs arrived
@@ -191,7 +178,6 @@ __device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
 
 // L2-coherent loads for data produced inside this kernel by other CTAs (never cached in L1).
 __device__ __forceinline__ float ldf(const float* p) { return __ldcg(p); }
-__device__ __forceinline__ uint32_t ldu(const void* p) { return __ldcg(reinterpret_cast<const unsigned int*>(p)); }
 
 // per-item L and step counts, cached in shared memory at kernel start (B <= MAXB)
 struct PlanCache {
@@ -877,28 +863,10 @@ __global__ void __launch_bounds__(NT, 1)
   WFENCE();
   grid_sync(a.bar, gen);
 
-  // position chunking of the attention: the smallest multiple of 16 (<= 64) that gives every CTA
-  // at most one chunk; if none does, 32-position chunks in several double-buffered rounds
-  int maxL = 1;
-  for (int b = 0; b < a.B; ++b) maxL = max(maxL, pc.L[b]);
-  auto ntask_for = [&](int ch) {
-    int nt = 0;
-    for (int b = 0; b < a.B; ++b) nt += (pc.L[b] + ch - 1) / ch;
-    return nt;
-  };
-#if DEC_ADAPTIVE_CHUNK
-  int chunk = 16;
-  while (chunk < ACH && ntask_for(chunk) > G) chunk += 16;
-  if (ntask_for(chunk) > G) chunk = 32;
-  if ((maxL + chunk - 1) / chunk > MAXCH) chunk = (maxL + MAXCH - 1) / MAXCH;  // <= 32 for L <= 8192
-#else
-  // Fixed 32-position chunks: an item's softmax / context reduction order then depends on its own
-  // L only, so a request decodes to the same bits in any pooled batch (batch transparency,
-  // reference SPEC.md:232); 32 positions = 8 warps x 4 in the energy pass.
+  // Fixed 32-position attention chunks: an item's softmax / context reduction order then depends on
+  // its own L only, so a request decodes to the same bits in any pooled batch (batch transparency,
+  // reference SPEC.md:232); one chunk = the N of one location-term MMA chain.
   constexpr int chunk = 32;
-  (void)maxL;
-  (void)ntask_for;
-#endif
   const int nb8 = (a.B + 7) / 8;
   // PRE tasks: column blocks per task minimising rounds x (mel + H1 + cpt x p-block) (~5 + 3 cpt us);
   // the arithmetic of every value is the same for any choice
