@@ -865,12 +865,12 @@ class TierREngine:
                 hm = self._up(np.concatenate([f.reshape(-1) for f in host_mels]))
             hpos = 0
             lay0 = _Layout(Ts, MEL_HALO)
-            mplan = np.zeros((n, 5), dtype=np.int64)
-            pplan = np.zeros((n, 8), dtype=np.int64)
             stage4 = _Layout([T * 256 for T in Ts], MRF_HALO)
             owners = self._claim_voc(triples, [mt[2] for mt in metas], taken)  # before any a.ptr()
-            for i, ((vstate, mel, is_last), (m, has_tail, last, T, G, cnt)) in enumerate(zip(triples, metas)):
-                req, dst = owners[i]
+            # plan columns gathered per item, arrays built once (a numpy row store per item costs
+            # more than the rest of the loop)
+            tail_c, mel_c, dst_c = [], [], []
+            for (vstate, mel, is_last), (m, has_tail, last, T, G, cnt), (req, dst) in zip(triples, metas, owners):
                 if isinstance(mel, DeviceMelChunk):
                     mel_ptr = mel.ptr
                 else:
@@ -885,11 +885,17 @@ class TierREngine:
                                                      np.asarray(vstate.held_tail, np.float32).reshape(-1)]))
                         keep.append(t)
                         tail_ptr = t.data_ptr()
-                mplan[i] = (tail_ptr, mel_ptr, m, O if has_tail else 0, lay0.first[i])
-                pplan[i] = (stage4.first[i], G, int(has_tail) | 2 * int(last),
-                            tail_ptr + 4 * O * W.N_MEL if has_tail else 0,
-                            0 if dst is None else a.ptr(dst.off), out_off[i], mel_ptr, m)
+                tail_c.append(tail_ptr)
+                mel_c.append(mel_ptr)
+                dst_c.append(0 if dst is None else a.ptr(dst.off))
                 results.append((req, dst, int(vstate.emitted_samples)))
+            mt_arr = np.array(metas, dtype=np.int64)            # m, has_tail, last, T, G, cnt
+            tail_a = np.array(tail_c, dtype=np.int64)
+            mel_a = np.array(mel_c, dtype=np.int64)
+            mplan = np.stack([tail_a, mel_a, mt_arr[:, 0], O * mt_arr[:, 1], lay0.first.astype(np.int64)], 1)
+            pplan = np.stack([stage4.first.astype(np.int64), mt_arr[:, 4], mt_arr[:, 1] | 2 * mt_arr[:, 2],
+                              np.where(mt_arr[:, 1] != 0, tail_a + 4 * O * W.N_MEL, 0),
+                              np.array(dst_c, dtype=np.int64), out_off[:-1], mel_a, mt_arr[:, 0]], 1)
             d_mplan = self._up(mplan)
             d_pplan = self._up(pplan)
             audio = self._buf("audio", max(int(out_off[-1]), 1), torch.float32)
@@ -931,8 +937,9 @@ class TierREngine:
         # result objects are built while the GPU works: the chunks are read-only views of `flat`
         flat = slot[1][:total] if slot is not None else np.empty(total, dtype=np.float32)
         out = []
+        oo = out_off.tolist()
         for i, (req, dst, emitted) in enumerate(results):
-            chunk = AudioChunk.trusted(flat[out_off[i]:out_off[i + 1]], emitted)
+            chunk = AudioChunk.trusted(flat[oo[i]:oo[i + 1]], emitted)
             out.append((chunk, DeviceVocoderState(req, dst, emitted + counts[i])))
         self._speculate_next_decoder()
         if self.idle_hook is not None:
