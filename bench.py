@@ -337,10 +337,27 @@ def run_single(args) -> dict:
     if args.side_configs:
         out["side_configs"] = side_configs(mods, cfg, lex, args)
     if args.sweep:
-        out["sweep"] = qps_sweep(lambda q, secs: serve(
-            mods, cfg, poisson_trace(q, 3600.0, seed=args.seed + int(q), lexicon=lex), warmup_iters=3,
-            warmup_seconds=3.0, timed_iters=None, timed_seconds=secs, drain_seconds=2.0),
-            [float(x) for x in args.sweep.split(",") if x], args.sweep_seconds, args.qps, st["p99"])
+        def serve_at(q, secs):
+            # module CUDA events over the whole run: each level's roofline fractions (the decoder's
+            # achieved bytes/s grow with the pooled batch; the 100 QPS headline is its small-B point)
+            engine.timers = []
+            run = serve(mods, cfg, poisson_trace(q, 3600.0, seed=args.seed + int(q), lexicon=lex), warmup_iters=3,
+                        warmup_seconds=3.0, timed_iters=None, timed_seconds=secs, drain_seconds=2.0)
+            torch.cuda.synchronize()
+            agg_q = {}
+            for kind, e0, e1, units in engine.timers:
+                a_ = agg_q.setdefault(kind, [0.0, 0.0])
+                a_[0] += e0.elapsed_time(e1)
+                a_[1] += units
+            engine.timers = None
+            dec_q, voc_q = agg_q.get("decoder"), agg_q.get("vocoder")
+            run.roofline = {
+                "decoder_frac_hbm": round(dec_q[1] / (dec_q[0] * 1e-3) / 1e9 / peaks["hbm_gbs"], 4) if dec_q else None,
+                "vocoder_frac_bf16": (round(voc_q[1] / (voc_q[0] * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"], 4)
+                                      if voc_q else None)}
+            return run
+        out["sweep"] = qps_sweep(serve_at, [float(x) for x in args.sweep.split(",") if x], args.sweep_seconds,
+                                 args.qps, st["p99"])
     out["n_steps"] = n_steps
     out["engine"] = engine
     return out
@@ -606,6 +623,8 @@ def qps_sweep(serve_at, levels, seconds: float, base_qps: float, base_p99: float
         row = {"qps": q, "p50_ms": st["p50"], "p99_ms": st["p99"], "requests": st["requests"],
                "censored": st["censored"], "failed": st["failed"], "p99_ms_by_third_of_window": st["p99_by_third"],
                "window_s": round(st["window_s"], 2)}
+        if getattr(run, "roofline", None):
+            row["roofline"] = run.roofline
         if hasattr(run, "reports") and run.reports:
             t0, t1 = run.window
             win = [len(r.decoder_ids) for r, e in zip(run.reports, run.iteration_end) if t0 < e <= t1]
