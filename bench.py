@@ -613,7 +613,7 @@ def incr_vs_non_incr(mods, cfg, lex, args) -> dict:
 
 def qps_sweep(serve_at, levels, seconds: float, base_qps: float, base_p99: float | None) -> dict:
     """Max QPS at p99 FCL < 80 ms: windows of `seconds` (3 s warm-up each) at increasing levels until
-    one misses the SLO, then one bisection step between the last pass and the first miss.
+    one misses the SLO, then up to two bisection steps between the last pass and the first miss.
     Requests with no first chunk 2 s after the window count as censored at that time."""
     rows = []
 
@@ -641,10 +641,14 @@ def qps_sweep(serve_at, levels, seconds: float, base_qps: float, base_p99: float
         else:
             first_bad = q
             break
-    if last_ok is not None and first_bad is not None and first_bad - last_ok > 20:
+    for _ in range(2):   # two bisection steps between the last pass and the first miss
+        if last_ok is None or first_bad is None or first_bad - last_ok <= 20:
+            break
         mid = round((last_ok + first_bad) / 2 / 5) * 5
         if level(mid):
             last_ok = mid
+        else:
+            first_bad = mid
     return {"rows": rows, "max_qps": last_ok}
 
 
