@@ -666,7 +666,7 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sweep", default="200,275,350,425",
                     help="QPS levels per GPU for max QPS at p99 < 80 ms (empty: off); stops at the first miss, "
-                         "then one bisection step")
+                         "then up to two bisection steps")
     ap.add_argument("--sweep-seconds", type=float, default=30.0)
     ap.add_argument("--side-configs", type=int, default=1, help="also run C1, C2, C5, INCR vs Non-INCR (1 = on)")
     ap.add_argument("--c5-qps", type=float, default=50.0)
