@@ -208,6 +208,13 @@ class TierREngine:
         self.speculate = True            # precompute the next decoder call's item fields during V waits
         self._spec_src = None            # continuing (state, features) of the last decoder call
         self._spec = None                # their precomputed plan fields (see _speculate_next_decoder)
+        # pools of at least spec_launch_min continuing items launch their next decoder chunk during
+        # the vocoder wait (0: off); small pools only precompute plan fields (a separate launch
+        # for new items would cost their first chunk ~1.4 ms)
+        self.spec_launch_min = 128
+        self._spec_out = None
+        self._last_full_decode = True
+        self.spec_hits = 0
         # f3: chunk-local Tacotron2 PostNet on the decoder's mel output (off: the reference's no-op)
         self.postnet = bool(postnet or postnet_weights is not None)
         if self.postnet:
@@ -624,7 +631,19 @@ class TierREngine:
         states are gone by now, so the free ping-pong buffer is determined)."""
         src, self._spec_src = self._spec_src, None
         self._spec = None
+        self._spec_out = None
         if not src or not self.speculate:
+            return
+        if self.spec_launch_min and len(src) >= self.spec_launch_min and self._last_full_decode:
+            # large pools: LAUNCH the continuing items' next chunk now, behind this vocoder call on
+            # the engine stream, so the GPU does not idle while the host finishes this iteration
+            # and prepares the next; decoder_batch returns these results for the matching pairs
+            # (bit-identical: batch transparency) and decodes only the newly admitted items
+            try:
+                out = self._decode(src)
+            except Exception:  # noqa: BLE001 -- the real call redoes (and retries) it
+                return
+            self._spec_out = (src, out)
             return
         taken: set = set()
         try:
@@ -637,6 +656,8 @@ class TierREngine:
     def decoder_steps(self, triples) -> list:
         """Step-granular decoding (the opt-in admission mode, ``scheduler.run_iteration_steps``):
         (state, features, limit) -> DecodeChunkResult of min(limit, frames left in the chunk) steps."""
+        self._spec_out = None
+        self._last_full_decode = False
         return self._decode([(s, e) for s, e, _ in triples], [lim for _, _, lim in triples])
 
     @_on_device
@@ -649,7 +670,20 @@ class TierREngine:
 
     @_on_device
     def decoder_batch(self, pairs) -> list:
-        return self._decode(pairs)
+        self._last_full_decode = True
+        so, self._spec_out = self._spec_out, None
+        if so is None:
+            return self._decode(pairs)
+        # items whose next chunk was launched during the last vocoder wait (same state / feature
+        # objects); the others -- normally just the newly admitted ones -- decode now
+        done = {(id(st), id(enc)): r for (st, enc), r in zip(*so)}
+        hit = [done.get((id(st), id(enc))) for st, enc in pairs]
+        rest = [p for p, h in zip(pairs, hit) if h is None]
+        fresh = iter(self._decode(rest) if rest else [])
+        out = [h if h is not None else next(fresh) for h in hit]
+        self._spec_src = [(r.state, enc) for r, (_, enc) in zip(out, pairs) if not r.stop]
+        self.spec_hits += len(pairs) - len(rest)
+        return out
 
     def _decode(self, pairs, limits=None) -> list:
         n = len(pairs)
@@ -941,12 +975,12 @@ class TierREngine:
         for i, (req, dst, emitted) in enumerate(results):
             chunk = AudioChunk.trusted(flat[oo[i]:oo[i + 1]], emitted)
             out.append((chunk, DeviceVocoderState(req, dst, emitted + counts[i])))
-        self._speculate_next_decoder()
+        v_done = torch.cuda.Event()
+        v_done.record(self.stream)        # this call's D2H copies are queued before this point
+        self._speculate_next_decoder()    # may enqueue the next decoder chunk behind it
         if self.idle_hook is not None:
-            done = torch.cuda.Event()
-            done.record(self.stream)
-            self.idle_hook(done.query)
-        self.stream.synchronize()
+            self.idle_hook(v_done.query)
+        v_done.synchronize()
         self.d2h_bytes += 4 * total + 4 * n
         if slot is None:
             np.copyto(flat, host.numpy())

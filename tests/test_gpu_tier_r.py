@@ -318,6 +318,30 @@ def test_serving_replay_matches_serialized_launches():
     assert outs[0] == outs[1], outs
 
 
+def test_decoder_launch_speculation_is_transparent():
+    """Large pools launch the continuing items' next decoder chunk during the vocoder wait
+    (engine.spec_launch_min); with the threshold lowered so every iteration speculates, the
+    deterministic serving replay gives the same chunk digest as fully serialised launches."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    outs = []
+    for extra in (["--spec-launch-min", "4"], ["--serial"]):
+        env = dict(os.environ, ITTS_NO_PDL="1")
+        out = subprocess.run([sys.executable, str(root / "tools" / "race_check.py"), "--iters", "120", "--heavy",
+                              *extra], env=env, cwd=root, capture_output=True, text=True, timeout=900)
+        assert out.returncode == 0, out.stderr[-2000:]
+        lines = out.stdout.strip().splitlines()
+        outs.append(lines[-1])
+        if extra[0] == "--spec-launch-min":
+            hits = int(lines[-2].split()[-1])
+            assert hits > 0, lines[-2]
+    assert outs[0].startswith("failed/non-finite 0;"), outs
+    assert outs[0] == outs[1], outs
+
+
 def test_chunk_postnet_matches_oracle(engine, lexicon):
     """f3: mel + PostNet(mel) per chunk (tensor-core convs, bf16 activations) vs the fp32 oracle."""
     from paper_2211_13939_b200.weights import postnet_weights

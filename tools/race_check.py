@@ -31,6 +31,7 @@ ap.add_argument("--spec", action="store_true")
 ap.add_argument("--no-graphs", action="store_true")
 ap.add_argument("--iters", type=int, default=300)
 ap.add_argument("--heavy", action="store_true", help="~2.5 arrivals per iteration (pooled batch ~100)")
+ap.add_argument("--spec-launch-min", type=int, default=None, help="engine.spec_launch_min (decoder launch speculation)")
 args = ap.parse_args()
 cfg, lex = PipelineConfig(), default_lexicon()
 eng = build_engine(cfg, "r", "cuda:0")
@@ -43,6 +44,8 @@ if args.spec:
     eng.speculate = True
 if args.no_graphs:
     eng.use_graphs = False
+if args.spec_launch_min is not None:
+    eng.spec_launch_min = args.spec_launch_min
 mods = modules_for(eng, lex)
 rng = random.Random(1234)
 pool = RequestPool()
@@ -67,4 +70,5 @@ for it in range(args.iters):
                 bad += 1
             h.update(np.ascontiguousarray(c.samples).tobytes())
 torch.cuda.synchronize()
+print(f"spec hits {eng.spec_hits}")
 print(f"failed/non-finite {bad}; digest {h.hexdigest()}")
