@@ -279,7 +279,9 @@ __device__ __forceinline__ void gate_prefetch_w(const DecArgs& a, uint8_t* ring,
 template <int MODE>
 __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy, uint32_t x_stage_bytes, int nst,
                            uint32_t& g_ring, uint32_t& lt_tile, const PlanCache& pc, unsigned& grp_gen, float* hs,
-                           bool merged = false, unsigned ctx_target = 0) {
+                           bool merged = false, unsigned ctx_target = 0, unsigned p_target = 0) {
+  // p_target (attention gates, PRE overlapped with this phase): split 0 loads its prenet chunks
+  // once that many PRE tasks have been counted in
   constexpr int K = MODE == 0 ? KA : KD;
   constexpr int NKC = K / 64;
   constexpr int KCS = NKC / KSPLIT;
@@ -342,16 +344,25 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       // which schedule the batch size selects.
       const bool ctx_last = MODE == 1 && ks == 0;
       bool ctx_ready = !(ctx_last && merged);
+      // attention gates, split 0: the prenet columns (chunks 0..3) go last, in both schedules
+      // (PRE before this phase or overlapped with it), so the accumulation order is the same
+      const bool p_last = MODE == 0 && ks == 0;
+      bool p_ready = !(p_last && p_target);
       for (int v = 0; v < KCS * nsub; ++v, ++g) {
         if ((int)(g % np) != (int)pi) continue;
         const int i = v / nsub, sub = v - i * nsub;
         const uint32_t st = g % nst, ph = (g / nst) & 1;
         if (i >= npre) tcg::mbar_wait(&gsy.empty[st], ph ^ 1);
-        const int kc = ks * KCS + (ctx_last ? (i + 8) % KCS : i), k0 = kc * 64;
+        const int kc = ks * KCS + (ctx_last ? (i + 8) % KCS : p_last ? (i + 4) % KCS : i), k0 = kc * 64;
         if (!ctx_ready && k0 < EMB) {
           wait_count(a.bar + 2 + NGRP, ctx_target);
           asm volatile("fence.proxy.async.global;" ::: "memory");  // contexts written by generic stores
           ctx_ready = true;
+        }
+        if (!p_ready && k0 < PRE) {
+          wait_count(a.bar + 3 + NGRP, p_target);
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // prenet outputs written by generic stores
+          p_ready = true;
         }
         int col;
         if (MODE == 0) col = k0 < 768 ? k0 : att_off(oldb) + (k0 - 768);
@@ -868,10 +879,17 @@ __global__ void __launch_bounds__(NT, 1)
   // reference SPEC.md:232); one chunk = the N of one location-term MMA chain.
   constexpr int chunk = 32;
   const int nb8 = (a.B + 7) / 8;
+  // Small batches: PRE runs on the CTAs without a gate group, overlapped with the attention-gate
+  // phase (splits 1..3 need no prenet columns; split 0 takes its prenet chunks last and waits on a
+  // counter) -- one grid barrier and one latency-bound phase fewer per step
+  const int n_aux = G - GEMM_CTAS;
+  const bool prem = n_aux > 0 && nb8 * 4 <= n_aux;
   // PRE tasks: column blocks per task minimising rounds x (mel + H1 + cpt x p-block) (~5 + 3 cpt us);
   // the arithmetic of every value is the same for any choice
   int pre_cpt = 1;
-  {
+  if (prem) {
+    pre_cpt = nb8 * 8 <= n_aux ? 1 : 2;
+  } else {
     int best = 1 << 30;
     for (int cpt = 1; cpt <= 8; cpt *= 2) {
       const int cost = ((nb8 * (8 / cpt) + G - 1) / G) * (5 + 3 * cpt);
@@ -889,7 +907,7 @@ __global__ void __launch_bounds__(NT, 1)
       tacc[ph_i] += now - tph;
       tph = now;
     }
-    ph_i = ph_i == (merged ? 3 : 4) ? 0 : ph_i + 1;
+    ph_i = ph_i == (merged ? 3 : 4) - (prem ? 1 : 0) ? 0 : ph_i + 1;
   };
   // mel / gate value k of item b for the step whose projection partials are in Pp (group order, ctx last)
   auto mel_value = [&](int b, int k) {
@@ -903,12 +921,17 @@ __global__ void __launch_bounds__(NT, 1)
   };
   float* ringf = reinterpret_cast<float*>(ring);  // generic scratch outside the gate / staging uses
   unsigned ctx_target = 0;                         // combined contexts so far (merged ATT-B)
+  unsigned pre_target = 0;                         // PRE tasks so far (overlapped schedule)
   for (int s = 0; s < a.nsteps; ++s) {
     const int gs = a.step0 + s;
     // ---- PRE: finish mel(s-1); H1 = relu(W0 . last) for the task's 8 items; p = relu(W1 . H1)
     if ((DEC_PREFETCH & 1) && gemm_cta && tid == 0) gate_prefetch_w<0>(a, ring, gsy, nst, g_ring);
     // task = (8 items, pre_cpt blocks of 32 prenet columns): mel and H1 are computed once per task
-    for (int task = c; task < nb8 * (8 / pre_cpt); task += G) {
+    const int n_pre = nb8 * (8 / pre_cpt);
+    unsigned pre_done = 0;
+    for (int task = prem ? c - GEMM_CTAS : c; task < n_pre; task += prem ? n_aux : G) {
+      if (task < 0) break;   // gate CTAs in the overlapped schedule
+      ++pre_done;
       const int b0 = (task / (8 / pre_cpt)) * 8, cb0 = (task % (8 / pre_cpt)) * pre_cpt, nb = min(8, a.B - b0);
       const int n0 = cb0 * 32;
       const bool trp = a.trace && c == 0 && tid == 0;
@@ -1001,10 +1024,19 @@ __global__ void __launch_bounds__(NT, 1)
       WFENCE();
       pmark(7);
     }
-    phase_end();
-    // ---- ATT gates + cell + query partials
-    if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen, ringf);
-    phase_end();
+    if (prem) {   // ---- overlapped: count the finished PRE tasks in, run the attention gates
+      pre_target += (unsigned)n_pre;
+      if (tid == 0 && pre_done)
+        asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.bar + 3 + NGRP), "r"(pre_done) : "memory");
+      if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen, ringf, false, 0,
+                                  pre_target);
+      phase_end();
+    } else {
+      phase_end();
+      // ---- ATT gates + cell + query partials
+      if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen, ringf);
+      phase_end();
+    }
     // ---- ATT-A: the non-empty (item, chunk) tasks of the live items, dealt round-robin
     if (tid < 32) {  // task prefix over items: 16 items per lane, then a warp scan
       constexpr int PL = MAXB / 32;
@@ -1157,7 +1189,7 @@ ITTS_API int itts_r_decode_persistent(int32_t B, int32_t nsteps, const int64_t* 
     if (e != cudaSuccess) return (int)e;
     configured |= itts::device_bit();
   }
-  cudaError_t e = cudaMemsetAsync(bar, 0, (2 + NGRP + 1) * sizeof(unsigned), st);
+  cudaError_t e = cudaMemsetAsync(bar, 0, (2 + NGRP + 2) * sizeof(unsigned), st);
   if (e != cudaSuccess) return (int)e;
   const int G = tcg::num_sms();
   void* args[] = {&a, &a_box_bytes};

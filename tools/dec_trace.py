@@ -43,8 +43,9 @@ for B in [int(x) for x in args.batches.split(",")]:
     _native.call("itts_r_decode_debug_trace", None)
     raw = buf.cpu().tolist()
     t = raw[:5] + [v / REPS for v in raw[5:]]   # phase totals are per launch (last one); the rest accumulate
+    nm = names if t[3] else ["PRE || ATT gates+q", "ATT-A", "DEC gates+combine+proj", "-", "-"]  # overlapped PRE
     print(f"B={B}: chunk {e0.elapsed_time(e1) / REPS:.3f} ms; per step (us): " +
-          ", ".join(f"{n} {t[i] / 32e3:.1f}" for i, n in enumerate(names) if t[i]))
+          ", ".join(f"{n} {t[i] / 32e3:.1f}" for i, n in enumerate(nm) if t[i]))
     print(f"   PRE CTA0 (us): mel partials {t[5] / 32e3:.2f}, H1 {t[6] / 32e3:.2f}, p gemv {t[7] / 32e3:.2f}")
     for m, nm in ((0, "ATT"), (1, "DEC")):
         g = [t[16 + 8 * m + i] / 32e3 for i in range(7)]
