@@ -193,6 +193,12 @@ int itts_r_encode_split(const void* pack, int64_t total, int32_t n, int64_t max_
                         int64_t max_span, const int64_t* weights3, int32_t conv_taps, void* x3, float* f32,
                         float* pre, int32_t* rowmap, int32_t parts, void* stream);
 int itts_r_pmem(const int64_t* plan, int32_t n, int64_t max_len, const float* WmT, void* stream);
+/* The same BiLSTM on the tensor cores (csrc/bilstm_tc.cu): one 8-CTA cluster per (direction,
+ * group of <= 32 items), gates = W_hh . h as one tcgen05 MMA chain per step with h split into bf16
+ * hi + lo parts (fp32-level for bf16-exact W_hh).  Wt = bf16 [2 dir][8 rank][4][128][64]: rank r's
+ * 128 gate rows (unit 32 r + u, gate g at row 4 u + g) x 256 inputs as 128B-swizzled K-major tiles.
+ * The encoder weight tables of itts_r_encode / itts_r_encode_split take it as entry 14 (0: SIMT). */
+int itts_r_bilstm_tc(const float* PRE, const int64_t* plan, int32_t n, const void* Wt, void* stream);
 
 /* K7 helpers around the HiFi-GAN conv stack (replaces vocode_batch,
  * vocoder.py:92-143): spliced-mel assembly, per-stage row maps, halo

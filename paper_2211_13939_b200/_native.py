@@ -44,6 +44,7 @@ SIGNATURES: dict[str, list] = {
     "itts_r_proj": [_p, _p, _i32, _p, _p, _p, _i32, _p],
     "itts_r_enc_embed": [_p, _i64, _p, _i32, _i64, _p, _p, _p, _p, _p, _p],
     "itts_r_bilstm": [_p, _p, _i32, _p, _p],
+    "itts_r_bilstm_tc": [_p, _p, _i32, _p, _p],
     "itts_r_pmem": [_p, _i32, _i64, _p, _p],
     "itts_r_mel_assemble": [_p, _i32, _i64, _p, _i32, _p],
     "itts_r_rowmap": [_p, _i32, _i64, _p, _p],

@@ -14,6 +14,9 @@
 // detected before any launch (so nothing is enqueued on failure).
 #include "incrtts_b200.h"
 
+// bilstm_tc.cu: the encoder BiLSTM on the tensor cores (bf16-exact W_hh tiles), see itts_r_bilstm_tc.
+int bilstm_tc_launch(const float* PRE, const int64_t* plan, int32_t n, const void* Wt, void* stream);
+
 // tier_r.cu: several row maps (as itts_r_rowmap) in one launch (vocoder call setup, voc_run.cu).
 int itts_r_rowmaps(int32_t count, const int64_t* const* plans, int32_t* const* outs, const int64_t* spans, int32_t n,
                    void* stream);

@@ -455,6 +455,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(AT_WARPS * 32, 3)
 // ----------------------------------------------------------------- encoder
 // plan[i] = {tok_off, L, row_base (first valid row), mem_ptr, pm_ptr, 0}
 constexpr int EPLAN = 6;
+#ifndef BILSTM_TC_MIN
+#define BILSTM_TC_MIN 96   // pooled encoder batches from which the tensor-core BiLSTM wins (measured crossover)
+#endif
 
 template <typename OutT>
 __global__ void k_enc_embed(const int32_t* __restrict__ tok4, int64_t total, const int64_t* __restrict__ plan,
@@ -947,7 +950,13 @@ ITTS_API int itts_r_encode(const void* pack, int64_t total, int32_t n, int64_t m
   if ((r = itts_conv1d_tc(xb, rows, EMB, EMB, W(10), 8 * EH, 1, &off0, (const float*)W(11), 8 * EH, rowmap, nullptr,
                           1.0f, pre, 1, nullptr, 0, nullptr, 1.0f, 1, 128, stream)))
     return r;
-  if ((r = itts_r_bilstm(pre, plan, n, (const float*)W(12), stream))) return r;
+  // BiLSTM: one SIMT cluster per (item, direction) (k_bilstm, ~0.85 us per step); pooled batches
+  // of >= BILSTM_TC_MIN items (more than ~10 waves of clusters) run the tensor-core recurrence
+  // instead when the weight table carries W_hh tiles (entry 14, bf16-exact weights): ~2-5 us per
+  // step but 32 items per cluster
+  if ((r = (W(14) && n >= BILSTM_TC_MIN) ? bilstm_tc_launch(pre, plan, n, W(14), stream)
+                                         : itts_r_bilstm(pre, plan, n, (const float*)W(12), stream)))
+    return r;
   if ((r = itts_r_pmem(plan, n, max_len, (const float*)W(13), stream))) return r;
   const cudaError_t le_ = itts::launch_pdl(k_zero_spans, dim3(dim3(8, n)), dim3(256), 0, st, spans);
   if (le_ != cudaSuccess) return (int)le_;
@@ -997,7 +1006,13 @@ ITTS_API int itts_r_encode_split(const void* pack, int64_t total, int32_t n, int
   if ((r = itts_conv1d_tc(x3, rows, kin, 3 * EMB, W(10), 8 * EH, 1, &off0, (const float*)W(11), 8 * EH, rowmap,
                           nullptr, 1.0f, pre, 1, nullptr, 0, nullptr, 1.0f, 1, 128, stream)))
     return r;
-  if ((r = itts_r_bilstm(pre, plan, n, (const float*)W(12), stream))) return r;
+  // BiLSTM: one SIMT cluster per (item, direction) (k_bilstm, ~0.85 us per step); pooled batches
+  // of >= BILSTM_TC_MIN items (more than ~10 waves of clusters) run the tensor-core recurrence
+  // instead when the weight table carries W_hh tiles (entry 14, bf16-exact weights): ~2-5 us per
+  // step but 32 items per cluster
+  if ((r = (W(14) && n >= BILSTM_TC_MIN) ? bilstm_tc_launch(pre, plan, n, W(14), stream)
+                                         : itts_r_bilstm(pre, plan, n, (const float*)W(12), stream)))
+    return r;
   if ((r = itts_r_pmem(plan, n, max_len, (const float*)W(13), stream))) return r;
   const cudaError_t le_ = itts::launch_pdl(k_zero_spans, dim3(dim3(8, n)), dim3(256), 0, st, spans);
   if (le_ != cudaSuccess) return (int)le_;

@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes
 import functools
+import os
 import sys
 import weakref
 
@@ -223,12 +224,13 @@ class TierREngine:
         for wt, _, bias in self.enc_conv:
             enc_w += [wt, bias]
         enc_w += [self.enc_ih[0], self.enc_ih[2], self.enc_whhT, self.WmT]
-        self._enc_ptrs = (ctypes.c_int64 * len(enc_w))(*[t.data_ptr() for t in enc_w])
+        enc_p = [t.data_ptr() for t in enc_w] + [0 if self.enc_whh_tc is None else self.enc_whh_tc.data_ptr()]
+        self._enc_ptrs = (ctypes.c_int64 * len(enc_p))(*enc_p)
         # parity mode: conv / input-projection weights as [Wh | Wh | Wl] along C_in (itts_r_encode_split)
-        enc_w3 = list(enc_w)
+        enc_p3 = list(enc_p)
         for i, t in enumerate(self._enc_split_w):
-            enc_w3[4 + 2 * i] = t
-        self._enc_ptrs3 = (ctypes.c_int64 * len(enc_w3))(*[t.data_ptr() for t in enc_w3])
+            enc_p3[4 + 2 * i] = t.data_ptr()
+        self._enc_ptrs3 = (ctypes.c_int64 * len(enc_p3))(*enc_p3)
         self._voc = self._create_native_vocoder()
         self._side = [torch.cuda.Stream(self.device) for _ in range(2)]
         self._ev = [torch.cuda.Event() for _ in range(3)]
@@ -284,6 +286,20 @@ class TierREngine:
                        f32(torch.cat([w["enc.lstm_fwd.b_ih"] + w["enc.lstm_fwd.b_hh"],
                                       w["enc.lstm_bwd.b_ih"] + w["enc.lstm_bwd.b_hh"]])))
         self.enc_whhT = f32(torch.stack([w["enc.lstm_fwd.w_hh"].T, w["enc.lstm_bwd.w_hh"].T]))  # [2][256][1024]
+        # tensor-core BiLSTM (bilstm_tc.cu), OPT-IN (ITTS_BILSTM_TC=1): pooled encoder batches of >= 96
+        # items then run the recurrence as tcgen05 MMAs (32 items per cluster; 2.05 vs 3.3 ms at 128
+        # ragged items) but ~2x slower per step below that, and its arithmetic differs from the SIMT
+        # recurrence, so a request's encoder bits would depend on the batch crossing the threshold
+        # (batch transparency).  Needs bf16-exact W_hh; rows regrouped per direction as [rank r][unit u]
+        # [gate g] (row g*256 + 32r + u), 128B-swizzled 128-row tiles.
+        self.enc_whh_tc = None
+        whh = [w["enc.lstm_fwd.w_hh"], w["enc.lstm_bwd.w_hh"]]
+        if (os.environ.get("ITTS_BILSTM_TC") == "1"
+                and all(bool((t.to(torch.bfloat16).float() == t).all()) for t in whh)):
+            rows = (torch.arange(4)[None, None, :] * 256 + torch.arange(8)[:, None, None] * 32
+                    + torch.arange(32)[None, :, None]).reshape(-1)
+            self.enc_whh_tc = torch.stack([_swizzle_tiles(t.to(d).float()[rows.to(d)].to(torch.bfloat16), 128)
+                                           for t in whh]).contiguous()
 
         # fp32 [k][C_out][C_in] -> bf16 [k][C_out][3 C_in] = [Wh | Wh | Wl], or [Wh | Wh] when every
         # encoder weight is exact in bf16 (Wl = 0: two products instead of three)

@@ -81,6 +81,22 @@ def test_encoder_matches_oracle(engine, weights, lexicon):
         assert st.frames_emitted == 0 and st.target_frames == 8 * fo.seq_len
 
 
+def test_tensor_core_bilstm_matches_oracle(weights, lexicon, monkeypatch):
+    """Opt-in tensor-core BiLSTM (ITTS_BILSTM_TC=1, pooled encoder batches >= 96 items): encoder
+    memory within the same fp32-level tolerance of the oracle as the SIMT recurrence."""
+    from paper_2211_13939_b200.tier_r import TierREngine
+    monkeypatch.setenv("ITTS_BILSTM_TC", "1")
+    eng = TierREngine(PipelineConfig(), "cuda:0", weights=weights)
+    assert eng.enc_whh_tc is not None
+    texts = random_texts(lexicon, 100, 77, 5, 40)
+    fos = [run_frontend(t, lexicon) for t in texts]
+    encs = eng.encoder_batch(fos)
+    for i in (0, 37, 99):
+        mem, _ = orc.encode(weights, fos[i].phonemes, fos[i].pw, fos[i].pph, fos[i].iph)
+        err = np.abs(encs[i][0].rows - mem.numpy()).max()
+        assert err <= 5e-5, (i, err)
+
+
 @pytest.mark.parametrize("n", [12, 40, 128])
 def test_pooled_encoder_is_bitwise_transparent(engine, lexicon, n):
     """Each item's encoder memory in a pooled ragged batch (packed rows, shared convs, one BiLSTM
