@@ -49,12 +49,14 @@ class PrefetchingFrontend:
             out.append(fo)
         return out
 
-    def prefetch(self, texts: list[str], done=lambda: False) -> None:
-        """Frontend outputs for `texts` until `done()` (the GPU work being waited on finished)."""
+    def prefetch(self, texts: list[str], done=lambda: False) -> list:
+        """Frontend outputs for `texts` until `done()` (the GPU work being waited on finished);
+        returns the outputs computed by this call (the engine may pre-encode them)."""
         consumed, self._consumed = self._consumed, set()
+        new = []
         for text in texts:
             if done():
-                return
+                return new
             if text in consumed or text in self._memo:
                 continue
             try:
@@ -64,6 +66,8 @@ class PrefetchingFrontend:
             if len(self._memo) >= self.cap:
                 self._memo.pop(next(iter(self._memo)))
             self._memo[text] = fo
+            new.append(fo)
+        return new
 
 
 def modules_for(engine, lexicon: Lexicon) -> PipelineModules:

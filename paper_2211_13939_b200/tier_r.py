@@ -213,6 +213,10 @@ class TierREngine:
         # the vocoder wait (0: off); small pools only precompute plan fields (a separate launch
         # for new items would cost their first chunk ~1.4 ms)
         self.spec_launch_min = 128
+        # frontend outputs prefetched during a vocoder wait are encoded right then (pre_encode)
+        self.pre_encode_enabled = True
+        self._pre_enc: dict = {}
+        self.pre_enc_hits = 0
         self._spec_out = None
         self._last_full_decode = True
         self.spec_hits = 0
@@ -513,7 +517,38 @@ class TierREngine:
 
     # ------------------------------------------------------------ encoder
     @_on_device
+    def pre_encode(self, fos) -> None:
+        """Encode just-submitted requests' frontend outputs now (queued on the engine stream behind
+        the vocoder call being waited on, so the work runs in the host gap between iterations);
+        encoder_batch returns these results when the admitting iteration passes the same
+        FrontendOutput objects.  Per-request results are independent of the batch they were
+        computed in (batch transparency), so admission and outputs are unchanged."""
+        if not self.pre_encode_enabled or not fos:
+            return
+        try:
+            res = self._encode(list(fos))
+        except Exception:  # noqa: BLE001 -- the admitting iteration encodes (and reports) itself
+            return
+        for fo, r in zip(fos, res):
+            self._pre_enc[id(fo)] = (fo, r)
+        while len(self._pre_enc) > 1024:   # requests never admitted (shutdown): forget the oldest
+            self._pre_enc.pop(next(iter(self._pre_enc)))
+
+    @_on_device
     def encoder_batch(self, fos) -> list:
+        if self._pre_enc:
+            hit = []
+            for fo in fos:
+                e = self._pre_enc.pop(id(fo), None)
+                hit.append(e[1] if e is not None and e[0] is fo else None)
+            if any(h is not None for h in hit):
+                rest = [fo for fo, h in zip(fos, hit) if h is None]
+                fresh = iter(self._encode(rest) if rest else [])
+                self.pre_enc_hits += sum(h is not None for h in hit)
+                return [h if h is not None else next(fresh) for h in hit]
+        return self._encode(fos)
+
+    def _encode(self, fos) -> list:
         n = len(fos)
         if n == 0:
             return []

@@ -81,6 +81,25 @@ def test_encoder_matches_oracle(engine, weights, lexicon):
         assert st.frames_emitted == 0 and st.target_frames == 8 * fo.seq_len
 
 
+def test_pre_encoded_requests_decode_identically(engine, lexicon):
+    """pre_encode (frontend outputs prefetched during a vocoder wait, encoded right then): the
+    admitting encoder_batch returns those results, and decoding / vocoding them gives the same
+    bits as encoding at admission."""
+    fos = [run_frontend(t, lexicon) for t in random_texts(lexicon, 5, 321, 10, 60)]
+    outs = []
+    for pre in (False, True):
+        if pre:
+            engine.pre_encode(fos[1:4])
+        hits = engine.pre_enc_hits
+        encs = engine.encoder_batch(fos)
+        assert engine.pre_enc_hits - hits == (3 if pre else 0)
+        res = engine.decoder_batch([(st, enc) for enc, st in encs])
+        audio = engine.vocoder_batch([(VocoderState.initial(), r.mel, r.stop) for r in res])
+        outs.append([(np.asarray(r.mel.frames), a.samples.copy()) for r, (a, _) in zip(res, audio)])
+    for (m0, a0), (m1, a1) in zip(*outs):
+        assert np.array_equal(m0, m1) and np.array_equal(a0, a1)
+
+
 def test_tensor_core_bilstm_matches_oracle(weights, lexicon, monkeypatch):
     """Opt-in tensor-core BiLSTM (ITTS_BILSTM_TC=1, pooled encoder batches >= 96 items): encoder
     memory within the same fp32-level tolerance of the oracle as the SIMT recurrence."""
