@@ -80,6 +80,29 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(tcg::smem_u32(bar))
                : "memory");
 }
+// L2 residency: the decoder's weights are re-read every step (evict_last) while the attention's
+// memory / processed-memory rows stream once per step (evict_first), so at large pooled batches the
+// rows (B x L x 2.5 KB per step) do not push the 37 MB of gate weights out of L2
+#ifndef DEC_L2_HINTS
+#define DEC_L2_HINTS 1
+#endif
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+  uint64_t p;
+  if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, bool keep) {
+#if DEC_L2_HINTS
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          tcg::smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(tcg::smem_u32(bar)), "l"(l2_policy(keep))
+      : "memory");
+#else
+  bulk_g2s(dst, src, bytes, bar);
+#endif
+}
 constexpr int DPLAN = 8;
 constexpr int NT = 256, NW = 8;  // threads / warps per CTA
 constexpr int NGRP = HID / 32;   // 32-unit gate groups: query partials, projection partials (+1 ctx)
@@ -370,8 +393,8 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
         const int64_t wofs = ((int64_t)ug * NKC + kc) * 128 * 64, xofs = (int64_t)(col >> 6) * 128 * 64;
         if (comb) {   // [Wh | Wl | Xh | Xl]  (split 2: [Wh | Xh | Xl])
           tcg::mbar_expect_tx(&gsy.full[st], sbytes);
-          bulk_g2s(sW(st), (MODE == 0 ? a.Wa : a.Wd) + wofs, GW_TILE, &gsy.full[st]);
-          if (nw == 2) bulk_g2s(sW(st) + GW_TILE, (MODE == 0 ? a.Wal : a.Wdl) + wofs, GW_TILE, &gsy.full[st]);
+          bulk_g2s_hint(sW(st), (MODE == 0 ? a.Wa : a.Wd) + wofs, GW_TILE, &gsy.full[st], true);
+          if (nw == 2) bulk_g2s_hint(sW(st) + GW_TILE, (MODE == 0 ? a.Wal : a.Wdl) + wofs, GW_TILE, &gsy.full[st], true);
           bulk_g2s(sX(st), a.xb + xofs, n16 * 128, &gsy.full[st]);
           bulk_g2s(sX(st) + n16 * 128, a.xbl + xofs, n16 * 128, &gsy.full[st]);
           continue;
@@ -382,7 +405,7 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
           tcg::mbar_expect_tx(&gsy.full[st], n16 * 128);
         } else {
           tcg::mbar_expect_tx(&gsy.full[st], GW_TILE + n16 * 128);
-          bulk_g2s(sW(st), wsrc + wofs, GW_TILE, &gsy.full[st]);
+          bulk_g2s_hint(sW(st), wsrc + wofs, GW_TILE, &gsy.full[st], true);
         }
         for (int blk = 0; blk * 128 < n16; ++blk)  // items 128 blk.. live in 128-row block blk of the mirror
           bulk_g2s(sX(st) + blk * 128 * 128, xsrc + xofs + (int64_t)blk * NCC * 128 * 64,
@@ -605,14 +628,8 @@ __device__ __forceinline__ void att_prefetch(const DecArgs& a, int b, int ta, in
   float* sMem = sPm + n * ATT;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tcg::mbar_expect_tx(bar, (uint32_t)n * (ATT + EMB) * 4);
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   tcg::smem_u32(sPm)),
-               "l"(reinterpret_cast<const float*>(p[1]) + (int64_t)ta * ATT), "r"(n * ATT * 4), "r"(tcg::smem_u32(bar))
-               : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   tcg::smem_u32(sMem)),
-               "l"(reinterpret_cast<const float*>(p[0]) + (int64_t)ta * EMB), "r"(n * EMB * 4), "r"(tcg::smem_u32(bar))
-               : "memory");
+  bulk_g2s_hint(sPm, reinterpret_cast<const float*>(p[1]) + (int64_t)ta * ATT, n * ATT * 4, bar, false);
+  bulk_g2s_hint(sMem, reinterpret_cast<const float*>(p[0]) + (int64_t)ta * EMB, n * EMB * 4, bar, false);
 }
 
 // 128B-swizzled K-major UMMA tile element (row r, k < 64) of a [rows][64] bf16 tile
