@@ -43,6 +43,9 @@
 #ifndef DEC_MERGE_B
 #define DEC_MERGE_B 96
 #endif
+#ifndef DEC_SPREAD
+#define DEC_SPREAD 1   // context / prenet K-chunks spread over the four K-splits (chunk_of)
+#endif
 #ifndef DEC_WFENCE
 #define DEC_WFENCE 0
 #endif
@@ -299,6 +302,21 @@ __device__ __forceinline__ void gate_prefetch_w(const DecArgs& a, uint8_t* ring,
   }
 }
 
+// K-chunk (64 columns) taken i-th by K-split ks.  X columns: attention gates [p 0..3 | ctx 4..11 |
+// att_h 12..27], decoder gates [ctx 0..7 | att_h 8..23 | dec_h 24..39].  The chunks that depend on
+// this step's prenet / context go last; the map is fixed, so the fp32 accumulation order (and the
+// bits) do not depend on the pooled batch.
+template <int MODE>
+__device__ __forceinline__ int chunk_of(int ks, int i) {
+#if DEC_SPREAD
+  if (MODE == 0) return i < 6 ? 4 + ks * 6 + i : ks;                  // 6 others, then prenet chunk ks
+  return i < 8 ? 8 + ks * 8 + i : 2 * ks + (i - 8);                   // 8 others, then context 2ks, 2ks+1
+#else
+  if (MODE == 0) return ks * 7 + (ks == 0 ? (i + 4) % 7 : i);
+  return ks * 10 + (ks == 0 ? (i + 8) % 10 : i);
+#endif
+}
+
 template <int MODE>
 __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy, uint32_t x_stage_bytes, int nst,
                            uint32_t& g_ring, uint32_t& lt_tile, const PlanCache& pc, unsigned& grp_gen, float* hs,
@@ -365,18 +383,25 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       // schedule after the combined contexts of every live item are counted in.  The order is the
       // same in both schedules, so the fp32 accumulation (and the result bits) do not depend on
       // which schedule the batch size selects.
+#if DEC_SPREAD
+      // the chunks that wait on another CTA's output (context / prenet) are spread over the four
+      // splits (2 context / 1 prenet chunk each, taken last), so after the wait each split loads
+      // and multiplies 1-2 stages instead of split 0 alone loading 8 / 4
+      const bool ctx_last = MODE == 1, p_last = MODE == 0;
+#else
       const bool ctx_last = MODE == 1 && ks == 0;
-      bool ctx_ready = !(ctx_last && merged);
       // attention gates, split 0: the prenet columns (chunks 0..3) go last, in both schedules
       // (PRE before this phase or overlapped with it), so the accumulation order is the same
       const bool p_last = MODE == 0 && ks == 0;
+#endif
+      bool ctx_ready = !(ctx_last && merged);
       bool p_ready = !(p_last && p_target);
       for (int v = 0; v < KCS * nsub; ++v, ++g) {
         if ((int)(g % np) != (int)pi) continue;
         const int i = v / nsub, sub = v - i * nsub;
         const uint32_t st = g % nst, ph = (g / nst) & 1;
         if (i >= npre) tcg::mbar_wait(&gsy.empty[st], ph ^ 1);
-        const int kc = ks * KCS + (ctx_last ? (i + 8) % KCS : p_last ? (i + 4) % KCS : i), k0 = kc * 64;
+        const int kc = chunk_of<MODE>(ks, i), k0 = kc * 64;
         if (!ctx_ready && k0 < EMB) {
           wait_count(a.bar + 2 + NGRP, ctx_target);
           asm volatile("fence.proxy.async.global;" ::: "memory");  // contexts written by generic stores
@@ -825,6 +850,81 @@ __device__ void att_combine(const DecArgs& a, AttSmem& sm, int s, int b, int chu
   __syncthreads();
 }
 
+// att_combine for the merged schedule (the decoder-gate CTAs wait for these contexts): the chunk
+// statistics, the first CPF context partials and the first attention positions are loaded together
+// (one L2 round trip before the reductions), and `ctx_cnt` is released as soon as the context is
+// stored, before W / W_acc, which only the next step's attention reads.  Same arithmetic and order
+// as att_combine.  (Kept separate: the same early loads in the separate ATT-B phase of larger
+// batches, or one templated body for both, measured 1.5-2 % slower decoder chunks at B >= 128.)
+constexpr int CPF = 8;
+__device__ void att_combine_early(const DecArgs& a, AttSmem& sm, int s, int b, int chunk, int part, int nparts,
+                                  unsigned* ctx_cnt) {
+  const int tid = threadIdx.x;
+  const int64_t* p = a.plan + b * DPLAN;
+  const int L = (int)p[2];
+  const int nch = (L + chunk - 1) / chunk;
+  const float* wsrc = reinterpret_cast<const float*>(a.step0 + s == 0 ? p[3] : p[4]);
+  float* wdst = reinterpret_cast<float*>(p[4]);
+  const float* ap = a.AP + (int64_t)b * MAXCH * (2 + EMB);
+  float* scale = sm.scale;  // [MAXCH]
+  const int d0 = part * (EMB / nparts), d1 = d0 + EMB / nparts;
+  const int lp = (L + nparts - 1) / nparts, t1 = min(L, (part + 1) * lp);
+  const float mc = tid < nch ? ldf(ap + tid * (2 + EMB)) : -INFINITY;
+  const float sc = tid < nch ? ldf(ap + tid * (2 + EMB) + 1) : 0.f;
+  float pv[EMB / NT][CPF];
+#pragma unroll
+  for (int r = 0; r < EMB / NT; ++r)
+#pragma unroll
+    for (int k = 0; k < CPF; ++k) {
+      const int d = d0 + tid + r * NT;
+      pv[r][k] = (d < d1 && k < nch) ? ldf(ap + k * (2 + EMB) + 2 + d) : 0.f;
+    }
+  const int tw = part * lp + tid;
+  const float u0 = tw < t1 ? ldf(a.U + (int64_t)b * a.u_ld + tw) : 0.f;
+  const float acc0 = tw < t1 ? ldf(wsrc + L + tw) : 0.f;
+  const float M = block_max(mc, sm.red);
+  const float ec = tid < nch ? expf(mc - M) : 0.f;
+  const float Z = block_sum(sc * ec, sm.red);  // chunk order within a warp, then warp order
+  if (tid < nch) scale[tid] = ec / Z;
+  __syncthreads();
+  float* st = a.work + (int64_t)b * ROW;
+#pragma unroll
+  for (int r = 0; r < EMB / NT; ++r) {
+    const int d = d0 + tid + r * NT;
+    if (d >= d1) continue;
+    float c = 0.f;
+#pragma unroll
+    for (int k = 0; k < CPF; ++k)
+      if (k < nch) c = fmaf(scale[k], pv[r][k], c);
+    int k = CPF;
+    for (; k + 4 <= nch; k += 4) {  // 4 partial loads in flight, summed in chunk order
+      float v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = ldf(ap + (k + j) * (2 + EMB) + 2 + d);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c = fmaf(scale[k + j], v[j], c);
+    }
+    for (; k < nch; ++k) c = fmaf(scale[k], ldf(ap + k * (2 + EMB) + 2 + d), c);
+    st[CTX_OFF + d] = c;
+    xb_store(a, b, CTX_OFF + d, c);
+  }
+  WFENCE();
+  __syncthreads();
+  if (tid == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctx_cnt) : "memory");
+  if (tw < t1) {
+    const float w = u0 * scale[tw / chunk];
+    wdst[tw] = w;
+    wdst[L + tw] = acc0 + w;
+  }
+  for (int t = tw + NT; t < t1; t += NT) {
+    const float w = ldf(a.U + (int64_t)b * a.u_ld + t) * scale[t / chunk];
+    const float acc = ldf(wsrc + L + t);
+    wdst[t] = w;
+    wdst[L + t] = acc + w;
+  }
+  __syncthreads();
+}
+
 // ------------------------------------------------------------------ the kernel
 __global__ void __launch_bounds__(NT, 1)
     k_dec_persist(DecArgs a, uint32_t a_box_bytes) {
@@ -1106,16 +1206,11 @@ __global__ void __launch_bounds__(NT, 1)
       const bool owner = gemm_cta && (c & 3) == 0;
       if (!owner) {
         const int ci = gemm_cta ? (c >> 2) * 3 + (c & 3) - 1 : 3 * (GEMM_CTAS / 4) + (c - GEMM_CTAS);
-        unsigned done = 0;
         for (int task = ci; task < a.B * nparts; task += ncomb) {
           const int b = task / nparts;
-          if (active(pc, b, gs)) {
-            att_combine(a, sm, gs, b, chunk, task % nparts, nparts);  // ends with __syncthreads
-            ++done;
-          }
+          if (active(pc, b, gs))   // releases one count on the context counter, ends with __syncthreads
+            att_combine_early(a, sm, gs, b, chunk, task % nparts, nparts, a.bar + 2 + NGRP);
         }
-        if (tid == 0 && done)
-          asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.bar + 2 + NGRP), "r"(done) : "memory");
       }
     }
     // ---- DEC gates + cell + projection partials of dec_h; the other CTAs project the context
