@@ -1198,14 +1198,17 @@ __global__ void __launch_bounds__(NT, 1)
         if (active(pc, b, gs)) att_combine(a, sm, gs, b, chunk);
       phase_end();
     } else {
-      // on every CTA but the context-column owners (split 0 of each gate group), before their
-      // GEMM; small batches split each item's combine into up to 4 parts so more CTAs share it
-      const int ncomb = 3 * (GEMM_CTAS / 4) + (G - GEMM_CTAS);
+      // At most n_aux items: on the CTAs without a gate group only, so every gate CTA starts its
+      // GEMM at once (the context chunks are the last two of each split).  Otherwise on every CTA
+      // but split 0 of each gate group, before their GEMM.  Small batches split each item's
+      // combine into up to 4 parts so more CTAs share it (the values do not depend on the split).
+      const bool aux_only = n_aux > 0 && a.B <= n_aux;
+      const int ncomb = aux_only ? n_aux : 3 * (GEMM_CTAS / 4) + n_aux;
       const int nparts = a.B * 4 <= ncomb ? 4 : a.B * 2 <= ncomb ? 2 : 1;
       for (int b = 0; b < a.B; ++b) ctx_target += active(pc, b, gs) ? (unsigned)nparts : 0u;
-      const bool owner = gemm_cta && (c & 3) == 0;
-      if (!owner) {
-        const int ci = gemm_cta ? (c >> 2) * 3 + (c & 3) - 1 : 3 * (GEMM_CTAS / 4) + (c - GEMM_CTAS);
+      const bool combiner = aux_only ? !gemm_cta : !(gemm_cta && (c & 3) == 0);
+      if (combiner) {
+        const int ci = !gemm_cta ? (aux_only ? 0 : 3 * (GEMM_CTAS / 4)) + (c - GEMM_CTAS) : (c >> 2) * 3 + (c & 3) - 1;
         for (int task = ci; task < a.B * nparts; task += ncomb) {
           const int b = task / nparts;
           if (active(pc, b, gs))   // releases one count on the context counter, ends with __syncthreads
