@@ -21,6 +21,11 @@ int bilstm_tc_launch(const float* PRE, const int64_t* plan, int32_t n, const voi
 int itts_r_rowmaps(int32_t count, const int64_t* const* plans, int32_t* const* outs, const int64_t* spans, int32_t n,
                    void* stream);
 
+// tier_r.cu: itts_r_mrf_combine that also re-zeroes the halo rows of the NEXT stage's operand buffer
+// (itts_r_zero_halo(zplan, zn, zhalo, zX, zC)) in the same launch (vocoder call, voc_run.cu).
+int mrf_combine_zero_halo(const void* y0, const void* y1, const void* y2, int64_t n, float slope, void* out,
+                          const int64_t* zplan, int32_t zn, int64_t zhalo, void* zX, int32_t zC, void* stream);
+
 // tc_conv.cu: itts_conv1d_tc with a choice of act_out activation: 0 leaky ReLU (slope), 1 tanh
 // (PostNet), 2 GELU tanh form (BERT frontend).
 int conv1d_tc_impl(const void* x, int64_t rows, int32_t c_in, int64_t x_ld, const void* w, int32_t n_total,

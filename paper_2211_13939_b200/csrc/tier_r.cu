@@ -1118,11 +1118,26 @@ ITTS_API int itts_r_rowmap(const int64_t* plan, int32_t n, int64_t max_span, int
 // MRF branch merge: out = bf16(lrelu((y0 + y1 + y2) / 3, slope)), 8 bf16 per thread (16-byte
 // accesses).  The three branches' last ResBlock1 layers write their y independently, so they can
 // run concurrently; halo rows are zero in every input and stay zero.
+// Optionally (zplan != null) the same launch zeroes the halo rows of the next stage's operand
+// buffer zX (k_zero_halo's plan format, zn items of zhalo rows each side): that buffer's previous
+// contents were last read by this stage's first ResBlock layers, which all finished before this
+// kernel, and the next transposed conv writes only valid rows.
 __global__ void __launch_bounds__(256) k_mrf_combine(const uint4* __restrict__ y0, const uint4* __restrict__ y1,
                                                      const uint4* __restrict__ y2, int64_t n8, float slope,
-                                                     uint4* __restrict__ out) {
+                                                     uint4* __restrict__ out, const int64_t* __restrict__ zplan,
+                                                     int zn, int64_t zhalo, __nv_bfloat16* __restrict__ zX, int zC) {
   itts::pdl_trigger();
   itts::pdl_wait();
+  if (zplan) {
+    const int64_t per = 2 * zhalo * zC, tot = per * zn;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < tot; g += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t* p = zplan + (g / per) * 3;
+      const int64_t e = g % per, r0 = e / zC, halo = p[2];
+      if (r0 >= 2 * halo) continue;
+      const int64_t r = r0 < halo ? p[0] + r0 : p[0] + p[1] + r0;
+      zX[r * zC + e % zC] = __float2bfloat16_rn(0.f);
+    }
+  }
   const float third = 1.0f / 3.0f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     const uint4 a = __ldcs(y0 + i), b = __ldcs(y1 + i), c = __ldcs(y2 + i);
@@ -1143,17 +1158,23 @@ __global__ void __launch_bounds__(256) k_mrf_combine(const uint4* __restrict__ y
   }
 }
 
-ITTS_API int itts_r_mrf_combine(const void* y0, const void* y1, const void* y2, int64_t n, float slope, void* out,
-                                void* stream) {
+int mrf_combine_zero_halo(const void* y0, const void* y1, const void* y2, int64_t n, float slope, void* out,
+                          const int64_t* zplan, int32_t zn, int64_t zhalo, void* zX, int32_t zC, void* stream) {
   if (n < 0 || n % 8) return ITTS_EINVAL;
-  if (n == 0) return ITTS_OK;
-  const int64_t n8 = n / 8;
-  const int blocks = (int)std::min<int64_t>((n8 + 255) / 256, 148 * 8);
+  if (zplan && (zn <= 0 || zhalo < 0 || zC <= 0 || !zX)) return ITTS_EINVAL;
+  if (n == 0 && !zplan) return ITTS_OK;
+  const int64_t n8 = n / 8, work = std::max<int64_t>(n8, zplan ? 2 * zhalo * zC * zn : 0);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 148 * 8));
   const cudaError_t le_ = itts::launch_pdl(k_mrf_combine, dim3(blocks), dim3(256), 0, (cudaStream_t)stream,
                                            (const uint4*)y0, (const uint4*)y1, (const uint4*)y2, n8,
-                                                          slope, (uint4*)out);
+                                           slope, (uint4*)out, zplan, (int)zn, zhalo, (__nv_bfloat16*)zX, (int)zC);
   if (le_ != cudaSuccess) return (int)le_;
   ITTS_RETURN_LAUNCH();
+}
+
+ITTS_API int itts_r_mrf_combine(const void* y0, const void* y1, const void* y2, int64_t n, float slope, void* out,
+                                void* stream) {
+  return mrf_combine_zero_halo(y0, y1, y2, n, slope, out, nullptr, 0, 0, nullptr, 0, stream);
 }
 
 ITTS_API int itts_r_zero_halo(const int64_t* plan, int32_t n, int64_t max_halo, void* X, int32_t C,

@@ -253,7 +253,8 @@ struct Vocoder {
       // transposed conv: each input row -> u output rows, then re-zero the output halos
       if ((st = conv(act, lay[s].total, c_prev, 1 + s, u * C, 3, 1, C, rm[1 + 2 * s], XA, 0.1f, 0, stream)))
         return FAIL_AT(st);
-      if ((st = itts_r_zero_halo(z_plan[s], n, kMrfHalo, XA, C, stream))) return FAIL_AT(st);
+      // (stages 1..3: re-zeroed by the previous stage's MRF merge launch)
+      if (s == 0 && (st = itts_r_zero_halo(z_plan[s], n, kMrfHalo, XA, C, stream))) return FAIL_AT(st);
       const int32_t* rms = rm[2 + 2 * s];
       const float slope_out = s < 3 ? 0.1f : 0.01f;
       // MRF: three ResBlock1 branches, each writing its own y; one merge pass averages them.
@@ -273,7 +274,10 @@ struct Vocoder {
       if (multi_stream)
         for (int j = 0; j < 2; ++j)
           if ((e = cudaStreamWaitEvent(stream, ev_side[j], 0)) != cudaSuccess) return FAIL_AT((int)e);
-      if ((st = itts_r_mrf_combine(yo[0], yo[1], yo[2], L.total * C, slope_out, OA, stream))) return FAIL_AT(st);
+      const bool more = s + 1 < kStages;   // the merge also re-zeroes the next stage's XA halos
+      if ((st = mrf_combine_zero_halo(yo[0], yo[1], yo[2], L.total * C, slope_out, OA, more ? z_plan[s + 1] : nullptr,
+                                      n, kMrfHalo, XA, more ? kStageC[s + 1] : 0, stream)))
+        return FAIL_AT(st);
       act = OA;
       c_prev = C;
     }

@@ -1233,7 +1233,7 @@ class TierREngine:
             frames = np.ascontiguousarray(Ts, np.int32)   # must outlive the call (raw pointer below)
             self._call("itts_r_voc_run", self._voc, n, frames.ctypes.data, d_mplan.data_ptr(),
                        int(self.mrf_streams), ctypes.byref(x4), st)
-            self.launches += 58   # 9 row maps, mel assembly, conv_pre, 4 x (convT, halo, 9 ResBlock layers, merge)
+            self.launches += 55   # row maps, mel assembly, conv_pre, 4 x (convT, 9 ResBlock layers, merge), 1 halo pass
             return x4.value
         with torch.cuda.stream(self.stream):
             x0 = self._buf("x0", lay0.total * 128, zero=True).view(lay0.total, 128)
