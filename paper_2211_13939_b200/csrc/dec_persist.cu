@@ -28,13 +28,17 @@
 
 #include "tcgen05.cuh"
 
-// Gate-weight prefetch into the ring during the preceding phase (bit 0: attention-gate weights
-// during PRE; bit 1: decoder-gate weights during ATT-B).  Measured slower on B200 (the issuing
-// thread and the extra L2 traffic delay the latency-bound phases more than the gate GEMMs gain:
-// B=1 +8%, B=24 +8%), so off by default; tools/build_variant.py -DDEC_PREFETCH=n for A/B runs.
-#ifndef DEC_PREFETCH
-#define DEC_PREFETCH 0
+// Gate weights resident in TMEM as the MMA A operand (pooled batches <= 128, weights exact in bf16
+// or bf16 products): DEC_WRES = 1 the decoder gates (10 K-chunks x [128 rows][64] bf16 = 160 KB
+// per gate CTA, TMEM columns [192, 512)), 2 the attention gates (7 K-chunks, 112 KB, [192, 416)),
+// 0 off.  Written once per launch; that phase then streams only the operand tiles
+// (tools/probe_tmem_a.cu: TMEM-A products are bit-identical to smem-A products).  Measured (same box,
+// B = 1..128): no gain for either phase -- their MMAs wait on the prenet / combined-context operand
+// chunks (PRE and ATT-B chains on other CTAs), not on the weight stream -- hence off by default.
+#ifndef DEC_WRES
+#define DEC_WRES 0
 #endif
+constexpr uint32_t WRES_COL = 192;
 // Pooled batches up to DEC_MERGE_B: the chunk combine (ATT-B) runs at the start of the
 // decoder-gate phase on the CTAs that do not own the context columns of that GEMM; the owners
 // start with their att_h columns and wait for the combined contexts on a counter (one grid
@@ -281,25 +285,22 @@ static_assert(2 * ASTAGE <= RING_BYTES && ACH * (ATT + EMB) * 4 <= RING_BYTES, "
 constexpr int KSPLIT = 4;
 constexpr uint32_t GW_TILE = 128 * 128;  // weight stage: 128 rows x 64 bf16
 
-// Weight half of the first min(KCS, nst) stages of the next gate phase, issued by one thread
-// during the phase before it (the weights do not depend on the step): the full barrier gets the
-// weight bytes as a pending transaction now and its arrival with the operand tile later.
-template <int MODE>
-__device__ __forceinline__ void gate_prefetch_w(const DecArgs& a, uint8_t* ring, GateSync& gsy, int nst,
-                                                uint32_t g_ring) {
-  constexpr int NKC = (MODE == 0 ? KA : KD) / 64, KCS = NKC / KSPLIT;
-  const int c = blockIdx.x, ug = c >> 2, ks = c & 3;
-  const int npre = min(KCS, nst);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  for (int i = 0; i < npre; ++i) {
-    const uint32_t g = g_ring + i, st = g % nst, ph = (g / nst) & 1;
-    tcg::mbar_wait(&gsy.empty[st], ph ^ 1);
-    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(tcg::smem_u32(&gsy.full[st])),
-                 "r"(GW_TILE)
-                 : "memory");
-    bulk_g2s(ring + st * GW_TILE, (MODE == 0 ? a.Wa : a.Wd) + ((int64_t)ug * NKC + ks * KCS + i) * 128 * 64,
-             GW_TILE, &gsy.full[st]);
-  }
+// tcgen05.mma kind::f16 with A (M = 128 rows, K = 16: 8 TMEM columns of bf16 pairs, low half = even
+// k, lane = row) read from TMEM and B from shared memory
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t a_tmem, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(a_tmem), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
 }
 
 // K-chunk (64 columns) taken i-th by K-split ks.  X columns: attention gates [p 0..3 | ctx 4..11 |
@@ -319,8 +320,8 @@ __device__ __forceinline__ int chunk_of(int ks, int i) {
 
 template <int MODE>
 __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy, uint32_t x_stage_bytes, int nst,
-                           uint32_t& g_ring, uint32_t& lt_tile, const PlanCache& pc, unsigned& grp_gen, float* hs,
-                           bool merged = false, unsigned ctx_target = 0, unsigned p_target = 0) {
+                           uint32_t& ring_par, uint32_t& lt_tile, const PlanCache& pc, unsigned& grp_gen, float* hs,
+                           bool wres_cta, bool merged = false, unsigned ctx_target = 0, unsigned p_target = 0) {
   // p_target (attention gates, PRE overlapped with this phase): split 0 loads its prenet chunks
   // once that many PRE tasks have been counted in
   constexpr int K = MODE == 0 ? KA : KD;
@@ -337,17 +338,26 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
   };
   const bool comb = a.split && n16 <= 128;   // combined split stages (see k_dec_persist)
   const int nw = a.split == 1 ? 2 : 1;       // weight tiles per combined stage (Wh [, Wl])
-  const uint32_t sbytes = nw * GW_TILE + 2 * (uint32_t)n16 * 128;
+  // decoder gates with the weights resident in TMEM (see DEC_WRES): a stage is the operand tile
+  // only ([Xh | Xl] in the x2 split mode, [Xh] for bf16 products), so up to MAXGS stages are in flight
+  const bool wres = MODE == DEC_WRES - 1 && wres_cta;
+  const uint32_t xres_bytes = (a.split ? 2u : 1u) * (uint32_t)n16 * 128;
+  const uint32_t sbytes = wres ? xres_bytes : nw * GW_TILE + 2 * (uint32_t)n16 * 128;
+  if (wres) nst = min(MAXGS, (int)(RING_BYTES / xres_bytes));
   // stage st: the weight tile and the operand tile (combined split stages: Wh, [Wl,] Xh, Xl)
   auto sW = [&](uint32_t st) { return comb ? ring + st * sbytes : ring + st * GW_TILE; };
   auto sX = [&](uint32_t st) {
-    return comb ? ring + st * sbytes + nw * GW_TILE : ring + nst * GW_TILE + st * x_stage_bytes;
+    return wres ? ring + st * sbytes
+                : comb ? ring + st * sbytes + nw * GW_TILE : ring + nst * GW_TILE + st * x_stage_bytes;
   };
   // virtual stages per K-chunk when the split products do not share one stage: (Wh, Xh), (Wh, Xl)
   // [, (Wl, Xh)] -- the same product order as a combined stage
   const int nsub = (a.split && !comb) ? (a.split == 1 ? 3 : 2) : 1;
-  // producer lanes: stage g goes to lane g % np; np <= nst keeps the empty-barrier parity unambiguous
+  // Ring slots: use v of this phase takes slot v % nst; the mbarrier parity of every slot is
+  // tracked in the bit mask `ring_par` (flipped once per use), so phases may use different nst.
+  // Producer lanes: use v goes to lane v % np; np <= nst keeps the empty-barrier parity unambiguous
   const int np = min(3, nst);
+  const int nv = KCS * nsub;
   ++grp_gen;
   // Loads that do not depend on this phase's GEMM, issued now so their latency hides behind the
   // GEMM and the group sync: the group's slice of the next linear layer (query / projection)
@@ -377,8 +387,7 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       const uint32_t pi = warp == 0 ? 0 : warp - 1;
       asm volatile("fence.proxy.async.global;" ::: "memory");  // xb tiles written by generic stores
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the ring doubles as PRE scratch
-      uint32_t g = g_ring;
-      const int npre = (!a.split && (DEC_PREFETCH & (1 << MODE))) ? min(KCS, nst) : 0;  // weights prefetched
+      uint32_t par = ring_par;
       // decoder gates, split 0: the context columns (chunks 0..7) go last -- in the merged-combine
       // schedule after the combined contexts of every live item are counted in.  The order is the
       // same in both schedules, so the fp32 accumulation (and the result bits) do not depend on
@@ -396,11 +405,12 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
 #endif
       bool ctx_ready = !(ctx_last && merged);
       bool p_ready = !(p_last && p_target);
-      for (int v = 0; v < KCS * nsub; ++v, ++g) {
-        if ((int)(g % np) != (int)pi) continue;
+      for (int v = 0; v < nv; ++v) {
+        const uint32_t st = v % nst, ph = (par >> st) & 1;
+        par ^= 1u << st;
+        if (v % np != (int)pi) continue;
         const int i = v / nsub, sub = v - i * nsub;
-        const uint32_t st = g % nst, ph = (g / nst) & 1;
-        if (i >= npre) tcg::mbar_wait(&gsy.empty[st], ph ^ 1);
+        tcg::mbar_wait(&gsy.empty[st], ph ^ 1);
         const int kc = chunk_of<MODE>(ks, i), k0 = kc * 64;
         if (!ctx_ready && k0 < EMB) {
           wait_count(a.bar + 2 + NGRP, ctx_target);
@@ -416,6 +426,12 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
         if (MODE == 0) col = k0 < 768 ? k0 : att_off(oldb) + (k0 - 768);
         else col = k0 < 512 ? CTX_OFF + k0 : (k0 < 1536 ? att_off(newb) + (k0 - 512) : dec_off(oldb) + (k0 - 1536));
         const int64_t wofs = ((int64_t)ug * NKC + kc) * 128 * 64, xofs = (int64_t)(col >> 6) * 128 * 64;
+        if (wres) {   // [Xh | Xl] or [Xh]: the weights are in TMEM
+          tcg::mbar_expect_tx(&gsy.full[st], sbytes);
+          bulk_g2s(sX(st), a.xb + xofs, n16 * 128, &gsy.full[st]);
+          if (a.split) bulk_g2s(sX(st) + n16 * 128, a.xbl + xofs, n16 * 128, &gsy.full[st]);
+          continue;
+        }
         if (comb) {   // [Wh | Wl | Xh | Xl]  (split 2: [Wh | Xh | Xl])
           tcg::mbar_expect_tx(&gsy.full[st], sbytes);
           bulk_g2s_hint(sW(st), (MODE == 0 ? a.Wa : a.Wd) + wofs, GW_TILE, &gsy.full[st], true);
@@ -426,12 +442,8 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
         }
         const __nv_bfloat16* wsrc = sub == 2 ? (MODE == 0 ? a.Wal : a.Wdl) : (MODE == 0 ? a.Wa : a.Wd);
         const __nv_bfloat16* xsrc = sub == 1 ? a.xbl : a.xb;
-        if (i < npre) {
-          tcg::mbar_expect_tx(&gsy.full[st], n16 * 128);
-        } else {
-          tcg::mbar_expect_tx(&gsy.full[st], GW_TILE + n16 * 128);
-          bulk_g2s_hint(sW(st), wsrc + wofs, GW_TILE, &gsy.full[st], true);
-        }
+        tcg::mbar_expect_tx(&gsy.full[st], GW_TILE + n16 * 128);
+        bulk_g2s_hint(sW(st), wsrc + wofs, GW_TILE, &gsy.full[st], true);
         for (int blk = 0; blk * 128 < n16; ++blk)  // items 128 blk.. live in 128-row block blk of the mirror
           bulk_g2s(sX(st) + blk * 128 * 128, xsrc + xofs + (int64_t)blk * NCC * 128 * 64,
                    min(128, n16 - 128 * blk) * 128, &gsy.full[st]);
@@ -447,17 +459,29 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nA >> 3) << 17) | ((128u >> 4) << 24);
       const uint32_t idescB = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nB >> 3) << 17) | ((128u >> 4) << 24);
       constexpr uint32_t XB_OFF = 256 * 128;  // bytes to the second N tile of an operand tile
-      uint32_t g = g_ring;
+      uint32_t par = ring_par;
       tcg::mbar_wait(&gsy.acce, (lt_tile & 1) ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int nv = KCS * nsub;
-      for (int i = 0; i < nv; ++i, ++g) {
-        const uint32_t st = g % nst, ph = (g / nst) & 1;
+      for (int i = 0; i < nv; ++i) {
+        const uint32_t st = i % nst, ph = (par >> st) & 1;
+        par ^= 1u << st;
         tcg::mbar_wait(&gsy.full[st], ph);
         if (i == 0) mark(1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t dw = tcg::make_desc<128>(tcg::smem_u32(sW(st)));
         const uint64_t dx = tcg::make_desc<128>(tcg::smem_u32(sX(st)));
+        if (wres) {   // A = this K-chunk's weight rows in TMEM (same product order as the smem path)
+          const uint32_t wa = gsy.tmem + WRES_COL + 32 * i;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) umma_ts(gsy.tmem, wa + 8 * kk, dx + 2 * kk, idesc, (i | kk) != 0);
+          if (a.split) {
+            const uint64_t dxl = tcg::make_desc<128>(tcg::smem_u32(sX(st) + n16 * 128));
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) umma_ts(gsy.tmem, wa + 8 * kk, dxl + 2 * kk, idesc, 1);
+          }
+          tcg::umma_commit(&gsy.empty[st]);
+          continue;
+        }
+        const uint64_t dw = tcg::make_desc<128>(tcg::smem_u32(sW(st)));
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) tcg::umma_bf16(gsy.tmem, dw + 2 * kk, dx + 2 * kk, idesc, (i | kk) != 0);
         if (nB) {  // no combined stages above 128 rows: every product has its own (W, X) stage
@@ -598,7 +622,7 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
     __syncthreads();
     if (threadIdx.x == 0) mark(5);
   }
-  g_ring += KCS * nsub;
+  for (int v = 0; v < nv; ++v) ring_par ^= 1u << (v % nst);
   lt_tile += 1;
 }
 
@@ -620,7 +644,6 @@ struct AttSmem {
 // h values [32 x B/4] and PRE's last frame [8][80] + H1 [8][256] + gemv partials [8 warps][8][32]
 constexpr int SCRATCH_F = 8 * NMEL + 8 * PRE + NW * 8 * 32;
 static_assert(SCRATCH_F * 4 <= RING_BYTES && 32 * (MAXB / 4) * 4 <= RING_BYTES, "ring scratch");
-static_assert(DEC_PREFETCH == 0, "gate-weight prefetch would overwrite the PRE scratch in the ring");
 
 
 __device__ __forceinline__ float block_max(float v, float* red) {
@@ -941,7 +964,7 @@ __global__ void __launch_bounds__(NT, 1)
   const int tid = threadIdx.x, G = gridDim.x, c = blockIdx.x;
   const bool gemm_cta = c < GEMM_CTAS;
   unsigned gen = 0;
-  uint32_t g_ring = 0, lt_tile = 0, aphase[2] = {0, 0}, mphase[2] = {0, 0};
+  uint32_t ring_par = 0, lt_tile = 0, aphase[2] = {0, 0}, mphase[2] = {0, 0};
   unsigned grp_gen = 0;
 
   if (tid == 0) {
@@ -959,7 +982,9 @@ __global__ void __launch_bounds__(NT, 1)
   }
   // gate CTAs: accumulator columns = rows (2 N tiles above 256); every CTA: ATT-A location features
   // in columns [0, 64) (two pipeline buffers; free between gate phases)
-  const uint32_t tcols = !gemm_cta ? 64u : a_box_bytes > 256u * 128u ? 512u : 256u;
+  // gate CTAs with the decoder-gate weights resident: columns [WRES_COL, 512) hold them (n16 <= 128)
+  const bool wres = DEC_WRES && gemm_cta && a.split != 1 && a_box_bytes <= 128u * 128u;
+  const uint32_t tcols = !gemm_cta ? 64u : (wres || a_box_bytes > 256u * 128u) ? 512u : 256u;
   if ((tid >> 5) == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tcg::smem_u32(&gsy.tmem)),
                  "r"(tcols));
@@ -968,6 +993,27 @@ __global__ void __launch_bounds__(NT, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if constexpr (DEC_WRES > 0) if (wres) {
+    // this CTA's resident gate-weight rows (unit group c / 4, K-split c % 4, chunks in chunk_of
+    // order) -> TMEM: warps w and w + 4 own lane quarter w % 4 (row r = lane of the quarter) and
+    // take alternate chunks; the swizzled 16-byte pieces of a row are read in k order
+    constexpr int WM = DEC_WRES - 1, NKC = (WM == 0 ? KA : KD) / 64, KCS = NKC / KSPLIT;
+    const int q = (tid >> 5) & 3, r = q * 32 + (tid & 31);
+    for (int i = tid >> 7; i < KCS; i += 2) {
+      const __nv_bfloat16* src = (WM == 0 ? a.Wa : a.Wd) + (((int64_t)(c >> 2) * NKC + chunk_of<WM>(c & 3, i)) * 128 + r) * 64;
+      uint32_t w[32];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(src) + (j ^ (r & 7)));
+        w[4 * j] = u.x, w[4 * j + 1] = u.y, w[4 * j + 2] = u.z, w[4 * j + 3] = u.w;
+      }
+      tmem_st32(gsy.tmem + ((uint32_t)(q * 32) << 16) + WRES_COL + 32 * i, w);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
   for (int b = tid; b < a.B; b += NT) {
     pc.L[b] = (int)a.plan[b * DPLAN + 2];
     pc.steps[b] = (int)a.plan[b * DPLAN + 5];
@@ -1017,8 +1063,10 @@ __global__ void __launch_bounds__(NT, 1)
 
   unsigned long long tph = gtimer(), tacc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   int ph_i = 0;
+  unsigned long long t_sync = 0;   // trace: when this CTA left its last grid barrier
   auto phase_end = [&]() {
     grid_sync(a.bar, gen);
+    if (a.trace && tid == 0) t_sync = gtimer();
     if (a.trace && c == 0 && tid == 0) {
       const unsigned long long now = gtimer();
       tacc[ph_i] += now - tph;
@@ -1042,7 +1090,6 @@ __global__ void __launch_bounds__(NT, 1)
   for (int s = 0; s < a.nsteps; ++s) {
     const int gs = a.step0 + s;
     // ---- PRE: finish mel(s-1); H1 = relu(W0 . last) for the task's 8 items; p = relu(W1 . H1)
-    if ((DEC_PREFETCH & 1) && gemm_cta && tid == 0) gate_prefetch_w<0>(a, ring, gsy, nst, g_ring);
     // task = (8 items, pre_cpt blocks of 32 prenet columns): mel and H1 are computed once per task
     const int n_pre = nb8 * (8 / pre_cpt);
     unsigned pre_done = 0;
@@ -1051,8 +1098,9 @@ __global__ void __launch_bounds__(NT, 1)
       ++pre_done;
       const int b0 = (task / (8 / pre_cpt)) * 8, cb0 = (task % (8 / pre_cpt)) * pre_cpt, nb = min(8, a.B - b0);
       const int n0 = cb0 * 32;
-      const bool trp = a.trace && c == 0 && tid == 0;
+      const bool trp = a.trace && c == (prem ? GEMM_CTAS : 0) && tid == 0;   // first PRE CTA
       unsigned long long tp0 = trp ? gtimer() : 0;
+      if (trp && s > 0) a.trace[15] += tp0 - t_sync;
       auto pmark = [&](int slot) {
         if (trp) {
           const unsigned long long t1 = gtimer();
@@ -1145,13 +1193,14 @@ __global__ void __launch_bounds__(NT, 1)
       pre_target += (unsigned)n_pre;
       if (tid == 0 && pre_done)
         asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.bar + 3 + NGRP), "r"(pre_done) : "memory");
-      if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen, ringf, false, 0,
+      if (a.trace && c == GEMM_CTAS && tid == 0 && s > 0) a.trace[14] += gtimer() - t_sync;
+      if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, ring_par, lt_tile, pc, grp_gen, ringf, wres, false, 0,
                                   pre_target);
       phase_end();
     } else {
       phase_end();
       // ---- ATT gates + cell + query partials
-      if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen, ringf);
+      if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, ring_par, lt_tile, pc, grp_gen, ringf, wres);
       phase_end();
     }
     // ---- ATT-A: the non-empty (item, chunk) tasks of the live items, dealt round-robin
@@ -1192,7 +1241,6 @@ __global__ void __launch_bounds__(NT, 1)
     }
     phase_end();
     // ---- ATT-B: combine the chunks of every live item -> context, W, W_acc
-    if ((DEC_PREFETCH & 2) && gemm_cta && tid == 0) gate_prefetch_w<1>(a, ring, gsy, nst, g_ring);
     if (!merged) {
       for (int b = c; b < a.B; b += G)
         if (active(pc, b, gs)) att_combine(a, sm, gs, b, chunk);
@@ -1217,7 +1265,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
     // ---- DEC gates + cell + projection partials of dec_h; the other CTAs project the context
-    if (gemm_cta) gate_phase<1>(a, gs, ring, gsy, a_box_bytes, nst, g_ring, lt_tile, pc, grp_gen, ringf,
+    if (gemm_cta) gate_phase<1>(a, gs, ring, gsy, a_box_bytes, nst, ring_par, lt_tile, pc, grp_gen, ringf, wres,
                                 merged, ctx_target);
     {
       const int c0 = G > GEMM_CTAS ? GEMM_CTAS : 0, nsp = G - c0;

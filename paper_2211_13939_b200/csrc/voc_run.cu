@@ -68,6 +68,10 @@ struct DevBuf {
     size_t want = std::max<size_t>(n + n / 4, 1024);
     cudaError_t e = cudaMalloc(&p, want * sizeof(T));
     if (e != cudaSuccess) return (int)e;
+    // debug / test: ITTS_VOC_POISON=1 fills fresh work buffers with 0xFF bytes (bf16 NaN), so a test
+    // can show that no output depends on a row (e.g. a halo) the launch sequence did not write
+    const char* poison = getenv("ITTS_VOC_POISON");
+    if (poison && poison[0] == '1' && (e = cudaMemset(p, 0xFF, want * sizeof(T))) != cudaSuccess) return (int)e;
     cap = want;
     return ITTS_OK;
   }

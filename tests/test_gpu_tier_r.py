@@ -307,6 +307,23 @@ def test_native_vocoder_large_pool(engine):
         assert np.array_equal(batched[i][0].samples, solo.samples)
 
 
+def test_vocoder_ignores_unwritten_buffer_contents(engine, weights, monkeypatch):
+    """Every row the HiFi-GAN sequence reads (halos included) is written inside the same call:
+    work buffers filled with bf16 NaN at allocation (ITTS_VOC_POISON=1) give the same bits.
+    (compute-sanitizer initcheck cannot show this: it does not track TMA tensor stores.)"""
+    from paper_2211_13939_b200.tier_r import TierREngine
+    rng = np.random.default_rng(21)
+    triples = [(VocoderState.initial(), MelChunk(rng.uniform(-0.2, 0.2, (m, 80))), m < 32)
+               for m in (32, 5, 32, 17, 32, 1, 32, 32)]
+    want = [a.samples for a, _ in engine.vocoder_batch(triples)]
+    monkeypatch.setenv("ITTS_VOC_POISON", "1")
+    poisoned = TierREngine(PipelineConfig(), "cuda:0", weights=weights)
+    for sub in (triples, triples[:3], triples):   # fresh buffers, then reuse after a smaller call
+        got = [a.samples for a, _ in poisoned.vocoder_batch(sub)]
+        for g, w in zip(got, want):
+            assert np.array_equal(g, w)
+
+
 def test_nonfinite_audio_is_caught_on_device(engine):
     """The finite-audio guard (reference _frozen_array, domain.py:170-178) now counts non-finite
     samples per chunk in the splice kernel: an overflowing mel chunk fails its batch (the

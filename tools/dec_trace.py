@@ -46,7 +46,8 @@ for B in [int(x) for x in args.batches.split(",")]:
     nm = names if t[3] else ["PRE || ATT gates+q", "ATT-A", "DEC gates+combine+proj", "-", "-"]  # overlapped PRE
     print(f"B={B}: chunk {e0.elapsed_time(e1) / REPS:.3f} ms; per step (us): " +
           ", ".join(f"{n} {t[i] / 32e3:.1f}" for i, n in enumerate(nm) if t[i]))
-    print(f"   PRE CTA0 (us): mel partials {t[5] / 32e3:.2f}, H1 {t[6] / 32e3:.2f}, p gemv {t[7] / 32e3:.2f}")
+    print(f"   PRE first PRE CTA (us): mel partials {t[5] / 32e3:.2f}, H1 {t[6] / 32e3:.2f}, p gemv {t[7] / 32e3:.2f}"
+          + (f"; overlapped: start {t[15] / 31e3:.2f}, released {t[14] / 31e3:.2f} after the CTA's barrier" if t[14] else ""))
     for m, nm in ((0, "ATT"), (1, "DEC")):
         g = [t[16 + 8 * m + i] / 32e3 for i in range(7)]
         print(f"   {nm} gates CTA0 (us from phase start): producer issued {g[0]:.1f}, first stage {g[1]:.1f}, "

@@ -35,7 +35,8 @@ ap.add_argument("--spec-launch-min", type=int, default=None, help="engine.spec_l
 args = ap.parse_args()
 cfg, lex = PipelineConfig(), default_lexicon()
 eng = build_engine(cfg, "r", "cuda:0")
-eng.prepare_graphs(max_batch=256)
+if not args.no_graphs:
+    eng.prepare_graphs(max_batch=256)
 if args.serial or args.no_streams:
     eng.mrf_streams = False
 if args.serial or args.no_spec:
