@@ -135,7 +135,7 @@ int itts_resblock_debug_trace(void* buf);
  * W0T [80][256], W1T [256][256], WqT [1024][128], v [128], WpT [1536][81], bp [81] fp32;
  * WlocD [2][31][128] = the location conv composed with the location dense layer
  * (sum_f Wloc[f][c][k] WdT[f][a]).  Scratch: H1 [B][256], Q [32][B][128], P [33][B][81],
- * U [B][u_ld >= max L], AP [B][256][514], bar = 36 x u32.  B <= 512, texts <= 8192 phonemes.
+ * U [B][u_ld >= max L], AP [B][256][514], bar = 64 + B x u32 (zeroed by the call).  B <= 512, texts <= 8192 phonemes.
  * Split-bf16 parity mode: Wa_lo / Wd_lo = the low bf16 parts (W - bf16(W)) in the same layout;
  * the gate products are then Wh.Xh + Wh.Xl + Wl.Xh with fp32 accumulation (about 16 significant
  * bits per operand) and xb must hold 2 x the mirror (high parts, then low parts).  Both null: plain

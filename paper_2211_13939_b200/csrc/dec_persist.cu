@@ -47,6 +47,14 @@ constexpr uint32_t WRES_COL = 192;
 #ifndef DEC_MERGE_B
 #define DEC_MERGE_B 96
 #endif
+// Merged schedule: no grid barrier between ATT-A and the decoder-gate phase.  Every ATT-A task
+// releases its item's chunk counter (bar + ITEM_CNT + b) after its U / AP stores; a combiner waits
+// for that item's chunks only, and the gate CTAs go from their own attention tasks straight into
+// the decoder-gate GEMM (its context chunks already wait on the combined-context counter).
+#ifndef DEC_ITEM_CNT
+#define DEC_ITEM_CNT 1
+#endif
+constexpr int ITEM_CNT = 64;     // bar[64 + b]: ATT-A chunks of item b done (monotonic over the launch)
 #ifndef DEC_SPREAD
 #define DEC_SPREAD 1   // context / prenet K-chunks spread over the four K-splits (chunk_of)
 #endif
@@ -702,7 +710,7 @@ __device__ __forceinline__ void half_sync(int h) { asm volatile("bar.sync %0, 12
 
 __device__ __forceinline__ void att_task(const DecArgs& a, AttSmem& sm, GateSync& gsy, uint8_t* ring, int s, int h,
                                          int b, int L, int ch, bool load_q, uint32_t& aph, uint32_t& mph,
-                                         unsigned long long* tr_t) {
+                                         unsigned long long* tr_t, unsigned* item_cnt) {
   const int tid = threadIdx.x & 127, lane = tid & 31, qd = tid >> 5;
   const int ta = ch * 32, n = min(L, ta + 32) - ta;
   auto mark = [&](int slot) {
@@ -822,6 +830,8 @@ __device__ __forceinline__ void att_task(const DecArgs& a, AttSmem& sm, GateSync
     for (int j = 0; j < 4; ++j) ap[2 + tid + 128 * j] = c[j];
   }
   half_sync(h);   // ring half / e / q reuse
+  if (item_cnt && tid == 0)  // this chunk's U / AP stores (ordered by the half barrier) are visible
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(item_cnt) : "memory");
   mark(12);
   if (tr_t) a.trace[13] += 1;
 }
@@ -881,11 +891,15 @@ __device__ void att_combine(const DecArgs& a, AttSmem& sm, int s, int b, int chu
 // batches, or one templated body for both, measured 1.5-2 % slower decoder chunks at B >= 128.)
 constexpr int CPF = 8;
 __device__ void att_combine_early(const DecArgs& a, AttSmem& sm, int s, int b, int chunk, int part, int nparts,
-                                  unsigned* ctx_cnt) {
+                                  unsigned* ctx_cnt, unsigned chunks_target) {
   const int tid = threadIdx.x;
   const int64_t* p = a.plan + b * DPLAN;
   const int L = (int)p[2];
   const int nch = (L + chunk - 1) / chunk;
+  if (chunks_target) {  // no barrier after ATT-A: wait for this item's chunk tasks of step s
+    if (tid == 0) wait_count(a.bar + ITEM_CNT + b, chunks_target);
+    __syncthreads();
+  }
   const float* wsrc = reinterpret_cast<const float*>(a.step0 + s == 0 ? p[3] : p[4]);
   float* wdst = reinterpret_cast<float*>(p[4]);
   const float* ap = a.AP + (int64_t)b * MAXCH * (2 + EMB);
@@ -1060,6 +1074,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
   }
   const bool merged = a.B <= DEC_MERGE_B;  // ATT-B folded into the decoder-gate phase
+  const bool icnt = DEC_ITEM_CNT && merged;  // per-item chunk counters instead of the ATT-A barrier
 
   unsigned long long tph = gtimer(), tacc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   int ph_i = 0;
@@ -1072,7 +1087,7 @@ __global__ void __launch_bounds__(NT, 1)
       tacc[ph_i] += now - tph;
       tph = now;
     }
-    ph_i = ph_i == (merged ? 3 : 4) - (prem ? 1 : 0) ? 0 : ph_i + 1;
+    ph_i = ph_i == (merged ? 3 : 4) - (prem ? 1 : 0) - (icnt ? 1 : 0) ? 0 : ph_i + 1;
   };
   // mel / gate value k of item b for the step whose projection partials are in Pp (group order, ctx last)
   auto mel_value = [&](int b, int k) {
@@ -1235,11 +1250,12 @@ __global__ void __launch_bounds__(NT, 1)
       for (int task = t0 + h; task < t1; task += 2) {
         while (sm.tstart[bi + 1] <= task) ++bi;
         att_task(a, sm, gsy, ring, gs, h, bi, pc.L[bi], task - sm.tstart[bi], bi != bprev, aphase[h], mphase[h],
-                 (a.trace && c == 0 && tid == 0) ? &tq : nullptr);
+                 (a.trace && c == 0 && tid == 0) ? &tq : nullptr, icnt ? a.bar + ITEM_CNT + bi : nullptr);
         bprev = bi;
       }
     }
-    phase_end();
+    if (icnt) __syncthreads();   // this CTA's attention work (TMEM columns, ring) is done
+    else phase_end();
     // ---- ATT-B: combine the chunks of every live item -> context, W, W_acc
     if (!merged) {
       for (int b = c; b < a.B; b += G)
@@ -1260,7 +1276,8 @@ __global__ void __launch_bounds__(NT, 1)
         for (int task = ci; task < a.B * nparts; task += ncomb) {
           const int b = task / nparts;
           if (active(pc, b, gs))   // releases one count on the context counter, ends with __syncthreads
-            att_combine_early(a, sm, gs, b, chunk, task % nparts, nparts, a.bar + 2 + NGRP);
+            att_combine_early(a, sm, gs, b, chunk, task % nparts, nparts, a.bar + 2 + NGRP,
+                              icnt ? (unsigned)(((pc.L[b] + chunk - 1) / chunk) * (s + 1)) : 0u);
         }
       }
     }
@@ -1352,7 +1369,8 @@ ITTS_API int itts_r_decode_persistent(int32_t B, int32_t nsteps, const int64_t* 
     if (e != cudaSuccess) return (int)e;
     configured |= itts::device_bit();
   }
-  cudaError_t e = cudaMemsetAsync(bar, 0, (2 + NGRP + 2) * sizeof(unsigned), st);
+  static_assert(ITEM_CNT >= 2 + NGRP + 2, "item counters overlap the phase counters");
+  cudaError_t e = cudaMemsetAsync(bar, 0, (ITEM_CNT + B) * sizeof(unsigned), st);
   if (e != cudaSuccess) return (int)e;
   const int G = tcg::num_sms();
   void* args[] = {&a, &a_box_bytes};

@@ -59,6 +59,7 @@ HID = 1024
 XB2 = 4864          # persistent decoder's bf16 mirror row (two banks of att_h / dec_h)
 PERSIST_MAX_L = 8192  # 256 attention chunks of <= 32 positions
 PERSIST_MAX_B = 512   # kernel limit (2 MMA N tiles, plan cache); larger pools decode in slices of <= 512
+DEC_BAR_WORDS = 64 + PERSIST_MAX_B   # persistent-decoder counters: barrier / groups / contexts, then one per item
 
 
 def _hifigan_macs_per_frame() -> int:
@@ -1394,7 +1395,7 @@ class _DecBuffers:
                                      2 * (-(-self._POOL_ROWS // 128)) * (XB2 // 64) * 128 * 64)
             self.U = self.pool.get("U", (self.n, GRAPH_MAX_L), torch.float32, self._POOL_ROWS * GRAPH_MAX_L)
             self.AP = self.pool.get("AP", (self.n, 256, 2 + 512), torch.float32, self._POOL_ROWS * 256 * 514)
-            self.bar = self.pool.get("bar", (64,), torch.int32, 64)
+            self.bar = self.pool.get("bar", (DEC_BAR_WORDS,), torch.int32, DEC_BAR_WORDS)
             self.Gp = self.pool.get("Gp", (4 * 32 * (-(-self.n // 16) * 16) * 128,), torch.float32,
                                     4 * 32 * self._POOL_ROWS * 128)
             return
@@ -1403,7 +1404,7 @@ class _DecBuffers:
             self.xb2.zero_()
         self.U = self._empty((self.n, max(max_L, 256)), torch.float32, "U")
         self.AP = self._empty((self.n, 256, 2 + 512), torch.float32, "AP")
-        self.bar = torch.zeros(64, dtype=torch.int32, device=self.dev)
+        self.bar = torch.zeros(DEC_BAR_WORDS, dtype=torch.int32, device=self.dev)
         self.Gp = self._empty((4 * 32 * (-(-self.n // 16) * 16) * 128,), torch.float32, "Gp")
 
 

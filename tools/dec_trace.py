@@ -43,7 +43,12 @@ for B in [int(x) for x in args.batches.split(",")]:
     _native.call("itts_r_decode_debug_trace", None)
     raw = buf.cpu().tolist()
     t = raw[:5] + [v / REPS for v in raw[5:]]   # phase totals are per launch (last one); the rest accumulate
-    nm = names if t[3] else ["PRE || ATT gates+q", "ATT-A", "DEC gates+combine+proj", "-", "-"]  # overlapped PRE
+    # phases per step: PRE overlapped with the attention gates for B <= 40 (148 SMs), no barrier
+    # between ATT-A and the decoder gates for B <= 96 (merged combine, per-item chunk counters)
+    prem, merged = B <= 40, B <= 96
+    nm = (["PRE || ATT gates+q"] if prem else ["PRE", "ATT gates+q"]) + (
+        ["ATT-A + DEC gates+combine+proj (no barrier)"] if merged else ["ATT-A", "ATT-B", "DEC gates+proj"])
+    nm += ["-"] * (5 - len(nm))
     print(f"B={B}: chunk {e0.elapsed_time(e1) / REPS:.3f} ms; per step (us): " +
           ", ".join(f"{n} {t[i] / 32e3:.1f}" for i, n in enumerate(nm) if t[i]))
     print(f"   PRE first PRE CTA (us): mel partials {t[5] / 32e3:.2f}, H1 {t[6] / 32e3:.2f}, p gemv {t[7] / 32e3:.2f}"
