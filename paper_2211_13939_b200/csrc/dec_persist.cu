@@ -55,6 +55,10 @@ constexpr uint32_t WRES_COL = 192;
 #define DEC_ITEM_CNT 1
 #endif
 constexpr int ITEM_CNT = 64;     // bar[64 + b]: ATT-A chunks of item b done (monotonic over the launch)
+// With DEC_ITEM_CNT, also no grid barrier between the attention-gate phase and ATT-A: every gate CTA
+// releases bar[QCNT + ks] once per step after its query partials (items b = ks mod 4), and an
+// attention task loads an item's q once the 32 unit groups of that split have released.
+constexpr int QCNT = 36;
 #ifndef DEC_SPREAD
 #define DEC_SPREAD 1   // context / prenet K-chunks spread over the four K-splits (chunk_of)
 #endif
@@ -329,7 +333,8 @@ __device__ __forceinline__ int chunk_of(int ks, int i) {
 template <int MODE>
 __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy, uint32_t x_stage_bytes, int nst,
                            uint32_t& ring_par, uint32_t& lt_tile, const PlanCache& pc, unsigned& grp_gen, float* hs,
-                           bool wres_cta, bool merged = false, unsigned ctx_target = 0, unsigned p_target = 0) {
+                           bool wres_cta, bool merged = false, unsigned ctx_target = 0, unsigned p_target = 0,
+                           bool q_release = false) {
   // p_target (attention gates, PRE overlapped with this phase): split 0 loads its prenet chunks
   // once that many PRE tasks have been counted in
   constexpr int K = MODE == 0 ? KA : KD;
@@ -628,6 +633,8 @@ __device__ void gate_phase(const DecArgs& a, int s, uint8_t* ring, GateSync& gsy
       }
     }
     __syncthreads();
+    if (MODE == 0 && q_release && threadIdx.x == 0)   // the query partials above (ordered by the barrier)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar + QCNT + ks) : "memory");
     if (threadIdx.x == 0) mark(5);
   }
   for (int v = 0; v < nv; ++v) ring_par ^= 1u << (v % nst);
@@ -710,7 +717,7 @@ __device__ __forceinline__ void half_sync(int h) { asm volatile("bar.sync %0, 12
 
 __device__ __forceinline__ void att_task(const DecArgs& a, AttSmem& sm, GateSync& gsy, uint8_t* ring, int s, int h,
                                          int b, int L, int ch, bool load_q, uint32_t& aph, uint32_t& mph,
-                                         unsigned long long* tr_t, unsigned* item_cnt) {
+                                         unsigned long long* tr_t, unsigned* item_cnt, unsigned q_target) {
   const int tid = threadIdx.x & 127, lane = tid & 31, qd = tid >> 5;
   const int ta = ch * 32, n = min(L, ta + 32) - ta;
   auto mark = [&](int slot) {
@@ -722,6 +729,10 @@ __device__ __forceinline__ void att_task(const DecArgs& a, AttSmem& sm, GateSync
   };
   uint8_t* stage = ring + h * ASTAGE;
   if (tid == 0) att_prefetch(a, b, ta, ta + n, stage, &gsy.abar[h]);
+  if (load_q && q_target) {  // no barrier after the attention gates: the 32 groups' partials of b
+    if (tid == 0) wait_count(a.bar + QCNT + (b & 3), q_target);
+    half_sync(h);
+  }
   if (load_q) {  // q = sum of the 32 unit-group partials, group order (kept for the item's next chunk)
     float qv[NGRP];
 #pragma unroll
@@ -1087,7 +1098,7 @@ __global__ void __launch_bounds__(NT, 1)
       tacc[ph_i] += now - tph;
       tph = now;
     }
-    ph_i = ph_i == (merged ? 3 : 4) - (prem ? 1 : 0) - (icnt ? 1 : 0) ? 0 : ph_i + 1;
+    ph_i = ph_i == (merged ? 3 : 4) - (prem ? 1 : 0) - (icnt ? 2 : 0) ? 0 : ph_i + 1;
   };
   // mel / gate value k of item b for the step whose projection partials are in Pp (group order, ctx last)
   auto mel_value = [&](int b, int k) {
@@ -1210,14 +1221,15 @@ __global__ void __launch_bounds__(NT, 1)
         asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.bar + 3 + NGRP), "r"(pre_done) : "memory");
       if (a.trace && c == GEMM_CTAS && tid == 0 && s > 0) a.trace[14] += gtimer() - t_sync;
       if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, ring_par, lt_tile, pc, grp_gen, ringf, wres, false, 0,
-                                  pre_target);
-      phase_end();
+                                  pre_target, icnt);
     } else {
       phase_end();
       // ---- ATT gates + cell + query partials
-      if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, ring_par, lt_tile, pc, grp_gen, ringf, wres);
-      phase_end();
+      if (gemm_cta) gate_phase<0>(a, gs, ring, gsy, a_box_bytes, nst, ring_par, lt_tile, pc, grp_gen, ringf, wres, false, 0,
+                                  0, icnt);
     }
+    if (icnt) __syncthreads();   // this CTA's gate / PRE work (TMEM columns, ring scratch) is done
+    else phase_end();
     // ---- ATT-A: the non-empty (item, chunk) tasks of the live items, dealt round-robin
     if (tid < 32) {  // task prefix over items: 16 items per lane, then a warp scan
       constexpr int PL = MAXB / 32;
@@ -1250,7 +1262,8 @@ __global__ void __launch_bounds__(NT, 1)
       for (int task = t0 + h; task < t1; task += 2) {
         while (sm.tstart[bi + 1] <= task) ++bi;
         att_task(a, sm, gsy, ring, gs, h, bi, pc.L[bi], task - sm.tstart[bi], bi != bprev, aphase[h], mphase[h],
-                 (a.trace && c == 0 && tid == 0) ? &tq : nullptr, icnt ? a.bar + ITEM_CNT + bi : nullptr);
+                 (a.trace && c == 0 && tid == 0) ? &tq : nullptr, icnt ? a.bar + ITEM_CNT + bi : nullptr,
+                 icnt ? (unsigned)(NGRP * (s + 1)) : 0u);
         bprev = bi;
       }
     }
@@ -1369,7 +1382,7 @@ ITTS_API int itts_r_decode_persistent(int32_t B, int32_t nsteps, const int64_t* 
     if (e != cudaSuccess) return (int)e;
     configured |= itts::device_bit();
   }
-  static_assert(ITEM_CNT >= 2 + NGRP + 2, "item counters overlap the phase counters");
+  static_assert(QCNT >= 2 + NGRP + 2 && ITEM_CNT >= QCNT + 4, "counter ranges overlap");
   cudaError_t e = cudaMemsetAsync(bar, 0, (ITEM_CNT + B) * sizeof(unsigned), st);
   if (e != cudaSuccess) return (int)e;
   const int G = tcg::num_sms();

@@ -46,8 +46,10 @@ for B in [int(x) for x in args.batches.split(",")]:
     # phases per step: PRE overlapped with the attention gates for B <= 40 (148 SMs), no barrier
     # between ATT-A and the decoder gates for B <= 96 (merged combine, per-item chunk counters)
     prem, merged = B <= 40, B <= 96
-    nm = (["PRE || ATT gates+q"] if prem else ["PRE", "ATT gates+q"]) + (
-        ["ATT-A + DEC gates+combine+proj (no barrier)"] if merged else ["ATT-A", "ATT-B", "DEC gates+proj"])
+    if merged:   # one grid barrier per step after the decoder gates (+ one after PRE if not overlapped)
+        nm = (["whole step"] if prem else ["PRE", "ATT gates + ATT-A + DEC gates"])
+    else:
+        nm = ["PRE", "ATT gates+q", "ATT-A", "ATT-B", "DEC gates+proj"]
     nm += ["-"] * (5 - len(nm))
     print(f"B={B}: chunk {e0.elapsed_time(e1) / REPS:.3f} ms; per step (us): " +
           ", ".join(f"{n} {t[i] / 32e3:.1f}" for i, n in enumerate(nm) if t[i]))
