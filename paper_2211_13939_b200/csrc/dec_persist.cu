@@ -2,9 +2,11 @@
 //
 // Replaces the per-step chain of ~10 launches (tier_r.cu k_gemv / k_lstm_cell / k_attention +
 // two tc_conv gate GEMMs) for decode_chunk_batch (reference acoustic.py:191-219, :234-238;
-// Tacotron2 decoder step = paper Eq. 2).  One CTA per SM; the five phases of
-// a step are separated by a grid-wide barrier, and everything that is constant across steps
-// stays on chip:
+// Tacotron2 decoder step = paper Eq. 2).  One CTA per SM; everything that is
+// constant across steps stays on chip.  The five phases of a step are separated by grid-wide
+// barriers for pooled batches > 96; up to 96 rows only the decoder-gate phase ends in one (and
+// PRE above 40 rows), the other hand-offs are monotonic counters in global memory (PRE tasks,
+// query partials per K-split, attention chunks per item, combined contexts):
 //
 //   PRE    mel(s-1) = bp + the 33 projection partials (fixed order) -> mel / gate outputs,
 //          last_frame; H1 = relu(W0 . last_frame) (in shared memory); p = relu(W1 . H1)
