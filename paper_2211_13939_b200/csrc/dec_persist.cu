@@ -274,6 +274,53 @@ __device__ __forceinline__ void gemv_task(int b0, int nb, int n0, int N, int k0,
   __syncthreads();
 }
 
+// gemv_task over NCB column blocks in one pass (X staged in sx[8][KL], K range [0, KL)): every weight
+// load of the NCB blocks is in flight together; each output keeps gemv_task's summation order
+// (the warp's K slice in k order, then the warps in order), so the values are the same.
+template <int KWM, int NCB, typename OUT>
+__device__ __forceinline__ void gemv_staged_blocks(int b0, int nb, int n0, int N, int KL, const float* __restrict__ wT,
+                                                   const float* sx, float* spart, OUT out) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kw = (KL + NW - 1) / NW, ka = warp * kw, kb = min(KL, ka + kw);
+  float w[NCB][KWM];
+#pragma unroll
+  for (int j = 0; j < NCB; ++j)
+#pragma unroll
+    for (int u = 0; u < KWM; ++u) {
+      const int n = n0 + 32 * j + lane;
+      w[j][u] = (ka + u < kb && n < N) ? __ldg(wT + (int64_t)(ka + u) * N + n) : 0.f;
+    }
+  float acc[NCB][8];
+#pragma unroll
+  for (int j = 0; j < NCB; ++j)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[j][i] = 0.f;
+#pragma unroll
+  for (int u = 0; u < KWM; ++u)
+    if (ka + u < kb)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float x = sx[i * KL + ka + u];
+#pragma unroll
+        for (int j = 0; j < NCB; ++j) acc[j][i] = fmaf(w[j][u], x, acc[j][i]);
+      }
+#pragma unroll
+  for (int j = 0; j < NCB; ++j)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) spart[((warp * 8 + i) * NCB + j) * 32 + lane] = acc[j][i];
+  __syncthreads();
+  for (int e = tid; e < 8 * 32 * NCB; e += NT) {
+    const int it = e / (32 * NCB), j = (e / 32) % NCB, cc = e % 32, n = n0 + 32 * j + cc;
+    if (it < nb && n < N) {
+      float vsum = spart[(it * NCB + j) * 32 + cc];
+#pragma unroll
+      for (int w2 = 1; w2 < NW; ++w2) vsum += spart[((w2 * 8 + it) * NCB + j) * 32 + cc];
+      out(b0 + it, n, vsum);
+    }
+  }
+  __syncthreads();
+}
+
 // ------------------------------------------------------------------ tensor-core gate GEMM + LSTM cell
 // tcgen05: D[128 rows = items][32 gate columns] in TMEM; A (the bf16 operand mirror, 64-column
 // boxes of up to 128 item rows) and this CTA's 32 weight rows stream through a TMA ring; the
@@ -659,7 +706,7 @@ struct AttSmem {
 };
 // Generic scratch in the ring (free outside the gate pipeline / attention staging): the gate fixup's
 // h values [32 x B/4] and PRE's last frame [8][80] + H1 [8][256] + gemv partials [8 warps][8][32]
-constexpr int SCRATCH_F = 8 * NMEL + 8 * PRE + NW * 8 * 32;
+constexpr int SCRATCH_F = 8 * NMEL + 8 * PRE + NW * 8 * 32 * 2;   // (gemv partials of 2 column blocks)
 static_assert(SCRATCH_F * 4 <= RING_BYTES && 32 * (MAXB / 4) * 4 <= RING_BYTES, "ring scratch");
 
 
@@ -1205,15 +1252,17 @@ __global__ void __launch_bounds__(NT, 1)
       }
       __syncthreads();
       pmark(6);
-      for (int cb = cb0; cb < cb0 + pre_cpt; ++cb)
-        gemv_task<32, true>(b0, nb, cb * 32, PRE, 0, PRE, a.W1T, sh, gsc,
-                      [&](int b, int k) { return 0.f; },
-                      [&](int b, int n, float y) {
-                        if (!active(pc, b, gs)) return;
-                        y = fmaxf(y, 0.f);
-                        a.work[(int64_t)b * ROW + P_OFF + n] = y;
-                        xb_store(a, b, P_OFF + n, y);
-                      });
+      auto p_out = [&](int b, int n, float y) {
+        if (!active(pc, b, gs)) return;
+        y = fmaxf(y, 0.f);
+        a.work[(int64_t)b * ROW + P_OFF + n] = y;
+        xb_store(a, b, P_OFF + n, y);
+      };
+      if (pre_cpt == 2)   // both column blocks' weight loads in flight together
+        gemv_staged_blocks<32, 2>(b0, nb, n0, PRE, PRE, a.W1T, sh, gsc, p_out);
+      else
+        for (int cb = cb0; cb < cb0 + pre_cpt; ++cb)
+          gemv_task<32, true>(b0, nb, cb * 32, PRE, 0, PRE, a.W1T, sh, gsc, [&](int b, int k) { return 0.f; }, p_out);
       WFENCE();
       pmark(7);
     }
