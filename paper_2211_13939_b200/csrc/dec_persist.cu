@@ -61,6 +61,9 @@ constexpr int ITEM_CNT = 64;     // bar[64 + b]: ATT-A chunks of item b done (mo
 // releases bar[QCNT + ks] once per step after its query partials (items b = ks mod 4), and an
 // attention task loads an item's q once the 32 unit groups of that split have released.
 constexpr int QCNT = 36;
+#ifndef DEC_H1_UNROLL
+#define DEC_H1_UNROLL 5
+#endif
 #ifndef DEC_SPREAD
 #define DEC_SPREAD 1   // context / prenet K-chunks spread over the four K-splits (chunk_of)
 #endif
@@ -949,7 +952,11 @@ __device__ void att_combine(const DecArgs& a, AttSmem& sm, int s, int b, int chu
 // stored, before W / W_acc, which only the next step's attention reads.  Same arithmetic and order
 // as att_combine.  (Kept separate: the same early loads in the separate ATT-B phase of larger
 // batches, or one templated body for both, measured 1.5-2 % slower decoder chunks at B >= 128.)
-constexpr int CPF = 8;
+#ifndef DEC_CPF
+#define DEC_CPF 16
+#endif
+constexpr int CPF = DEC_CPF;   // chunk partials per context dim loaded with the statistics
+constexpr int CPR = 8;         // then CPR partial loads in flight per round
 __device__ void att_combine_early(const DecArgs& a, AttSmem& sm, int s, int b, int chunk, int part, int nparts,
                                   unsigned* ctx_cnt, unsigned chunks_target) {
   const int tid = threadIdx.x;
@@ -994,14 +1001,14 @@ __device__ void att_combine_early(const DecArgs& a, AttSmem& sm, int s, int b, i
     for (int k = 0; k < CPF; ++k)
       if (k < nch) c = fmaf(scale[k], pv[r][k], c);
     int k = CPF;
-    for (; k + 4 <= nch; k += 4) {  // 4 partial loads in flight, summed in chunk order
-      float v[4];
+    for (; k < nch; k += CPR) {  // CPR partial loads in flight, summed in chunk order
+      float v[CPR];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] = ldf(ap + (k + j) * (2 + EMB) + 2 + d);
+      for (int jj = 0; jj < CPR; ++jj) v[jj] = k + jj < nch ? ldf(ap + (k + jj) * (2 + EMB) + 2 + d) : 0.f;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) c = fmaf(scale[k + j], v[j], c);
+      for (int jj = 0; jj < CPR; ++jj)
+        if (k + jj < nch) c = fmaf(scale[k + jj], v[jj], c);
     }
-    for (; k < nch; ++k) c = fmaf(scale[k], ldf(ap + k * (2 + EMB) + 2 + d), c);
     st[CTX_OFF + d] = c;
     xb_store(a, b, CTX_OFF + d, c);
   }
@@ -1233,7 +1240,8 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int it = 0; it < 8; ++it) acc[it] = 0.f;
         const float4* sx4 = reinterpret_cast<const float4*>(sx);
-#pragma unroll 2
+        constexpr int H1U = DEC_H1_UNROLL;   // k4 iterations (4 W0 loads each) unrolled together
+#pragma unroll H1U
         for (int k4 = 0; k4 < NMEL / 4; ++k4) {
           float w[4];
 #pragma unroll
