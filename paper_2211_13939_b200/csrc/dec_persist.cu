@@ -921,19 +921,33 @@ __device__ void att_combine(const DecArgs& a, AttSmem& sm, int s, int b, int chu
   __syncthreads();
   float* st = a.work + (int64_t)b * ROW;
   const int d0 = part * (EMB / nparts), d1 = d0 + EMB / nparts;
-  for (int d = d0 + tid; d < d1; d += NT) {
-    float c = 0.f;
-    int k = 0;
-    for (; k + 4 <= nch; k += 4) {  // 4 partial loads in flight, summed in chunk order
-      float v[4];
+  // both context dims of this thread at once, 8 chunk partials each in flight per round, every dim
+  // summed in chunk order
+  constexpr int ND = EMB / NT, CR = 8;
+  float c[ND];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] = ldf(ap + (k + j) * (2 + EMB) + 2 + d);
+  for (int r = 0; r < ND; ++r) c[r] = 0.f;
+  for (int k = 0; k < nch; k += CR) {
+    float v[ND][CR];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) c = fmaf(scale[k + j], v[j], c);
-    }
-    for (; k < nch; ++k) c = fmaf(scale[k], ldf(ap + k * (2 + EMB) + 2 + d), c);
-    st[CTX_OFF + d] = c;
-    xb_store(a, b, CTX_OFF + d, c);
+    for (int r = 0; r < ND; ++r)
+#pragma unroll
+      for (int j = 0; j < CR; ++j) {
+        const int d = d0 + tid + r * NT;
+        v[r][j] = (d < d1 && k + j < nch) ? ldf(ap + (k + j) * (2 + EMB) + 2 + d) : 0.f;
+      }
+#pragma unroll
+    for (int r = 0; r < ND; ++r)
+#pragma unroll
+      for (int j = 0; j < CR; ++j)
+        if (k + j < nch) c[r] = fmaf(scale[k + j], v[r][j], c[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < ND; ++r) {
+    const int d = d0 + tid + r * NT;
+    if (d >= d1) continue;
+    st[CTX_OFF + d] = c[r];
+    xb_store(a, b, CTX_OFF + d, c[r]);
   }
   WFENCE();
   const int lp = (L + nparts - 1) / nparts, t1 = min(L, (part + 1) * lp);
