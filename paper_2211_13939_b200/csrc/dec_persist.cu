@@ -883,7 +883,8 @@ __device__ __forceinline__ void att_task(const DecArgs& a, AttSmem& sm, GateSync
   {  // unnormalised context partial: thread -> dims tid + 128 j, positions in order
     const float* sMem = sPm + n * ATT;
     float c[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int t = 0; t < n; ++t) {
+#pragma unroll 8
+    for (int t = 0; t < n; ++t) {   // (unrolled: the shared-memory loads of 8 positions issue together)
       const float w = sm.e[h][t];
 #pragma unroll
       for (int j = 0; j < 4; ++j) c[j] = fmaf(w, sMem[t * EMB + tid + 128 * j], c[j]);
